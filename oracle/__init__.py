@@ -1,0 +1,177 @@
+"""CPU oracle for the PG-SAG masked rasterizer — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package.  The product path
+(paper_2501_01677_b200) never imports it and shares no code with it.
+
+This module is argument marshalling for oracle/oracle.cpp (a plain,
+single-threaded C++ renderer written from PAPER.md §3.1 Eq. 1-4; see the
+header of that file and DESIGN.md §3 for the readings).  The library is
+compiled on demand with g++ -O2 -ffp-contract=off -fno-fast-math.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_SO = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+N_GRAD_ROWS = 59  # dmean 3, dscale 3, drot 4, dopac 1, dsh 48
+
+F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT = 1, 2, 4, 8
+F_LIVE = 15
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (no -march=native: plain IEEE double/float)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+               _SRC, "-o", _SO + ".tmp"]
+        subprocess.check_call(cmd)
+        os.replace(_SO + ".tmp", _SO)
+    return _SO
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_SO)
+            P = C.c_void_p
+            i32, i64 = C.c_int, C.c_int64
+            L.oracle_tilemask.argtypes = [P, i32, i32, P, P]
+            L.oracle_tilemask.restype = None
+            for nm in ("oracle_project_f32", "oracle_project_f64"):
+                getattr(L, nm).argtypes = [P, P, P, P, P, i32, i32, P, i32, i32, P, P, P, P, P, P, P, P, P, P]
+                getattr(L, nm).restype = None
+            L.oracle_keys.argtypes = [P, P, P, i32, P, i32, i32, i64, P, P, P]
+            L.oracle_keys.restype = i64
+            for nm in ("oracle_render_f32", "oracle_render_f64"):
+                getattr(L, nm).argtypes = [P, P, P, P, P, i32, i32, P, i32, i32, P, P, P, i32, P, P, P, P,
+                                           i32, P, P, P]
+                getattr(L, nm).restype = None
+            L.oracle_sh_basis.argtypes = [C.c_double, C.c_double, C.c_double, P]
+            L.oracle_sh_basis.restype = None
+            L.oracle_lnup_f32.argtypes = [C.c_float]
+            L.oracle_lnup_f32.restype = C.c_float
+            _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def cam_array(cam) -> np.ndarray:
+    """[fx, fy, cx, cy, R(9), C(3), znear] as float64 (values are the float32 ones)."""
+    f32 = lambda v: float(np.float32(v))
+    vals = [f32(cam.fx), f32(cam.fy), f32(cam.cx), f32(cam.cy)]
+    vals += [float(v) for v in np.asarray(cam.R, np.float32).reshape(-1)]
+    vals += [float(v) for v in np.asarray(cam.C, np.float32).reshape(-1)]
+    vals += [f32(cam.znear)]
+    return np.array(vals, np.float64)
+
+
+def _params(g, dtype):
+    a = [np.ascontiguousarray(np.asarray(x), dtype) for x in (g.mean, g.scale, g.rot, g.opacity, g.sh)]
+    return a
+
+
+def tilemask(mask: np.ndarray):
+    H, W = mask.shape
+    TX, TY = (W + 15) // 16, (H + 15) // 16
+    cnt = np.zeros(TY * TX, np.uint32)
+    sat = np.zeros((TY + 1) * (TX + 1), np.int32)
+    m = np.ascontiguousarray(mask, np.uint8)
+    lib().oracle_tilemask(_p(m), W, H, _p(cnt), _p(sat))
+    return cnt.reshape(TY, TX), sat.reshape(TY + 1, TX + 1)
+
+
+def project(g, cam, mask, dtype=np.float32):
+    """O2 for every Gaussian.  Returns dict of numpy arrays (AoS-interleaved as documented)."""
+    n = int(np.asarray(g.opacity).shape[0])
+    prm = _params(g, dtype)
+    m = np.ascontiguousarray(mask, np.uint8)
+    out = dict(mean2d=np.zeros((n, 2), dtype), conic_o=np.zeros((n, 4), dtype), depth=np.zeros(n, dtype),
+               rect=np.zeros((n, 4), np.int32), tiles=np.zeros(n, np.uint32), rgb=np.zeros((n, 3), dtype),
+               ncam=np.zeros((n, 3), dtype), dist=np.zeros(n, dtype), flags=np.zeros(n, np.uint32))
+    fn = lib().oracle_project_f32 if dtype == np.float32 else lib().oracle_project_f64
+    ca = cam_array(cam)
+    fn(*[_p(a) for a in prm], n, int(g.sh_degree), _p(ca), int(cam.width), int(cam.height), _p(m),
+       *[_p(out[k]) for k in ("mean2d", "conic_o", "depth", "rect", "tiles", "rgb", "ncam", "dist", "flags")])
+    return out
+
+
+def keys(proj, mask):
+    """O3: sorted tile ids, Gaussian ids and ranges [TY*TX][2]."""
+    H, W = mask.shape
+    n = proj["depth"].shape[0]
+    TX, TY = (W + 15) // 16, (H + 15) // 16
+    depth = np.ascontiguousarray(proj["depth"], np.float32)
+    rect = np.ascontiguousarray(proj["rect"], np.int32)
+    flags = np.ascontiguousarray(proj["flags"], np.uint32)
+    m = np.ascontiguousarray(mask, np.uint8)
+    ranges = np.zeros((TY * TX, 2), np.uint32)
+    M = lib().oracle_keys(_p(depth), _p(rect), _p(flags), n, _p(m), W, H, 0, None, None, _p(ranges))
+    tiles = np.zeros(M, np.uint32)
+    vals = np.zeros(M, np.uint32)
+    M2 = lib().oracle_keys(_p(depth), _p(rect), _p(flags), n, _p(m), W, H, M, _p(tiles), _p(vals), _p(ranges))
+    assert M2 == M
+    return tiles, vals, ranges
+
+
+def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=False, upstream=None):
+    """O4 (and O5/O6 if upstream is given) for the listed flat pixel indices.
+
+    upstream: (npix, 9) float64 = gC(3), gN(3), gD, gA, gDep per listed pixel.
+    Returns dict: C (npix,3) N (npix,3) D A Dep T (npix,), g, last (Gaussian id), near, n_clamped,
+    id_sum, evaluated, cert_bad, and grads (59, n) float64 if upstream was given.
+    """
+    n = int(np.asarray(g.opacity).shape[0])
+    prm = _params(g, dtype)
+    H, W = mask.shape
+    m = np.ascontiguousarray(mask, np.uint8)
+    pix = np.ascontiguousarray(pixels, np.int64)
+    npix = int(pix.shape[0])
+    out = np.zeros((npix, 10), dtype)
+    iout = np.zeros((npix, 4), np.int32)
+    id_sum = np.zeros(npix, np.float64)
+    evaluated = np.zeros(npix, np.int64)
+    cert = np.zeros(1, np.int64)
+    bgd = np.asarray(bg, np.float64)
+    up = None if upstream is None else np.ascontiguousarray(upstream, np.float64).reshape(npix, 9)
+    grads = None if upstream is None else np.zeros((N_GRAD_ROWS, n), np.float64)
+    fn = lib().oracle_render_f32 if dtype == np.float32 else lib().oracle_render_f64
+    ca = cam_array(cam)
+    fn(*[_p(a) for a in prm], n, int(g.sh_degree), _p(ca), W, H, _p(m), _p(bgd), _p(pix), npix, _p(out),
+       _p(iout), _p(id_sum), _p(evaluated), int(bool(certify)), _p(cert), _p(up), _p(grads))
+    res = dict(C=out[:, 0:3], N=out[:, 3:6], D=out[:, 6], A=out[:, 7], Dep=out[:, 8], T=out[:, 9],
+               g=iout[:, 0], last=iout[:, 1], near=iout[:, 2], n_clamped=iout[:, 3], id_sum=id_sum,
+               evaluated=evaluated, cert_bad=int(cert[0]))
+    if grads is not None:
+        res["grads"] = grads
+    return res
+
+
+def split_grads(grads, n):
+    """(59, n) -> dict of named gradient blocks."""
+    return dict(dmean=grads[0:3], dscale=grads[3:6], drot=grads[6:10], dopacity=grads[10], dsh=grads[11:59])
+
+
+def sh_basis(x, y, z):
+    Y = np.zeros(16, np.float64)
+    lib().oracle_sh_basis(float(x), float(y), float(z), _p(Y))
+    return Y
+
+
+def lnup_f32(y):
+    return float(lib().oracle_lnup_f32(float(y)))

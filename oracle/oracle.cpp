@@ -1,0 +1,797 @@
+// ============================================================================
+// PG-SAG masked rasterizer — CPU ORACLE.  TEST INFRASTRUCTURE, NOT PRODUCT.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+// reference legs may load this library.  It shares no code, header, table or
+// constant generator with the CUDA path (paper_2501_01677_b200/csrc); the two
+// are independent implementations of the readings listed in DESIGN.md §3.
+//
+// What it computes is the PLAIN DEFINITION of the method's render (PAPER.md
+// §3.1, lines 78-96, Eq. 1-4): for every requested masked pixel, every
+// Gaussian, ordered by (camera depth, id), alpha-composited front to back, and
+// the exact reverse-mode gradient of that composite (PAPER.md:82
+// "optimized ... using differentiable rendering").  Tiles appear only through
+// the rect predicate, and `certify` counts pairs the rect excluded that would
+// have contributed (must be 0: tiling is then a pure acceleration).
+//
+// Precision (reading R20): Real = float reproduces the discrete
+// decisions of a float32 renderer (the tile keys are integer decisions made in
+// float32, so both sides take them in float32); Real = double is used for the
+// closed-form pins and the finite-difference pins.  Gradient sums are always
+// accumulated in double.  Compile with -O2 -ffp-contract=off -fno-fast-math:
+// every float expression below is evaluated exactly as written, left to right.
+//
+// Citations: P:n = /root/reference/PAPER.md line n.  Readings Rk = DESIGN.md §3.
+// Parity of every function here is pinned by tests/test_oracle_pins.py.
+// ============================================================================
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+namespace {
+
+// ---------------------------------------------------------------- flags (R*)
+enum : uint32_t {
+  F_VISIBLE = 1u << 0,   // z > znear                                  (R9)
+  F_DET_OK = 1u << 1,    // det(cov2d) > 0                             (R10)
+  F_OPAC_OK = 1u << 2,   // o >= 1/255                                 (R6)
+  F_RECT = 1u << 3,      // tile rect non-empty                        (R8)
+  F_CLAMP_X = 1u << 4,   // x/z clamped inside J                       (R9)
+  F_CLAMP_Y = 1u << 5,
+  F_RGB_CLAMP0 = 1u << 6,  // colour channel c clamped at 0 -> bit 6+c   (R12)
+  F_NFLIP = 1u << 11,      // normal flipped to face the camera          (R4)
+  F_AXIS_SHIFT = 9,        // bits 9-10: index of the minimum-scale axis  (R4)
+};
+constexpr uint32_t F_LIVE = F_VISIBLE | F_DET_OK | F_OPAC_OK | F_RECT;
+
+template <typename R> struct Cam {
+  R fx, fy, cx, cy;
+  int W, H;
+  R Rc[9];  // world -> camera, row-major (P:88 R_c)
+  R C[3];   // camera centre T_C
+  R znear;
+};
+
+template <typename R> Cam<R> load_cam(const double* cf, int W, int H) {
+  // cf = [fx, fy, cx, cy, R0..R8, C0..C2, znear]; values are float32-representable.
+  Cam<R> c;
+  c.fx = (R)cf[0]; c.fy = (R)cf[1]; c.cx = (R)cf[2]; c.cy = (R)cf[3];
+  for (int k = 0; k < 9; ++k) c.Rc[k] = (R)cf[4 + k];
+  for (int k = 0; k < 3; ++k) c.C[k] = (R)cf[13 + k];
+  c.znear = (R)cf[16];
+  c.W = W; c.H = H;
+  return c;
+}
+
+// ------------------------------------------------------------ SH basis (R12)
+// Real spherical harmonics up to degree 3 in the 3DGS convention
+// ("multi-order spherical harmonics"); pinned against scipy's complex
+// Y_l^m (real part sqrt2*Re / sqrt2*Im) in test_oracle_pins.py.
+const double SH_C0 = 0.28209479177387814;
+const double SH_C1 = 0.4886025119029199;
+const double SH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                         -1.0925484305920792, 0.5462742152960396};
+const double SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                         0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                         -0.5900435899266435};
+
+template <typename R> void sh_basis(R x, R y, R z, R* Y) {
+  const R xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  Y[0] = (R)SH_C0;
+  Y[1] = -(R)SH_C1 * y;
+  Y[2] = (R)SH_C1 * z;
+  Y[3] = -(R)SH_C1 * x;
+  Y[4] = (R)SH_C2[0] * xy;
+  Y[5] = (R)SH_C2[1] * yz;
+  Y[6] = (R)SH_C2[2] * (((R)2 * zz - xx) - yy);
+  Y[7] = (R)SH_C2[3] * xz;
+  Y[8] = (R)SH_C2[4] * (xx - yy);
+  Y[9] = ((R)SH_C3[0] * y) * ((R)3 * xx - yy);
+  Y[10] = ((R)SH_C3[1] * xy) * z;
+  Y[11] = ((R)SH_C3[2] * y) * (((R)4 * zz - xx) - yy);
+  Y[12] = ((R)SH_C3[3] * z) * (((R)2 * zz - (R)3 * xx) - (R)3 * yy);
+  Y[13] = ((R)SH_C3[4] * x) * (((R)4 * zz - xx) - yy);
+  Y[14] = ((R)SH_C3[5] * z) * (xx - yy);
+  Y[15] = ((R)SH_C3[6] * x) * (xx - (R)3 * yy);
+}
+
+// gradient of each basis function w.r.t. the (unnormalised-treated) direction
+// components, i.e. the partial derivatives of the polynomials above.
+void sh_basis_grad(double x, double y, double z, double G[16][3]) {
+  const double xx = x * x, yy = y * y, zz = z * z;
+  const double* c2 = SH_C2;
+  const double* c3 = SH_C3;
+  double g[16][3] = {
+      {0, 0, 0},
+      {0, -SH_C1, 0},
+      {0, 0, SH_C1},
+      {-SH_C1, 0, 0},
+      {c2[0] * y, c2[0] * x, 0},
+      {0, c2[1] * z, c2[1] * y},
+      {-2 * c2[2] * x, -2 * c2[2] * y, 4 * c2[2] * z},
+      {c2[3] * z, 0, c2[3] * x},
+      {2 * c2[4] * x, -2 * c2[4] * y, 0},
+      {6 * c3[0] * x * y, c3[0] * (3 * xx - 3 * yy), 0},
+      {c3[1] * y * z, c3[1] * x * z, c3[1] * x * y},
+      {-2 * c3[2] * x * y, c3[2] * (4 * zz - xx - 3 * yy), 8 * c3[2] * y * z},
+      {-6 * c3[3] * x * z, -6 * c3[3] * y * z, c3[3] * (6 * zz - 3 * xx - 3 * yy)},
+      {c3[4] * (4 * zz - 3 * xx - yy), -2 * c3[4] * x * y, 8 * c3[4] * x * z},
+      {2 * c3[5] * x * z, -2 * c3[5] * y * z, c3[5] * (xx - yy)},
+      {c3[6] * (3 * xx - 3 * yy), -6 * c3[6] * x * y, 0},
+  };
+  std::memcpy(G, g, sizeof(g));
+}
+
+// ------------------------------------------------- log upper bound (R8)
+// lnup(y) >= ln(y) for y >= 1 using only exact decomposition y = 2^e (1+f),
+// f in [0,1), the Pade upper bound ln(1+f) <= f(6+f)/(6+4f) (slack f^4/36 for
+// small f) and an absolute 2^-18 that absorbs the float rounding of the sum.
+template <typename R> R lnup(R y) {
+  int ex = 0;
+  R m = std::frexp(y, &ex);         // y = m 2^ex, m in [0.5, 1)  (exact)
+  const R e = (R)(ex - 1);
+  const R f = (R)2 * m - (R)1;      // exact
+  return (e * (R)0.6931471805599453 + (f * ((R)6 + f)) / ((R)6 + (R)4 * f)) + (R)3.814697265625e-06;
+}
+
+// ------------------------------------------------------- per-Gaussian (O2)
+template <typename R> struct Proj {
+  R u, v, ca, cb, cc, o, depth;
+  int rect[4];  // tx0, ty0, tx1, ty1 (inclusive); empty = (0,0,-1,-1)
+  uint32_t tiles;
+  R rgb[3], ncam[3], dist;
+  uint32_t flags;
+};
+
+struct TileMask {
+  int TX, TY;
+  std::vector<uint32_t> cnt;
+  std::vector<int32_t> sat;  // (TY+1) x (TX+1)
+  int rect_count(int tx0, int ty0, int tx1, int ty1) const {
+    const int S = TX + 1;
+    return sat[(ty1 + 1) * S + tx1 + 1] - sat[ty0 * S + tx1 + 1] - sat[(ty1 + 1) * S + tx0] +
+           sat[ty0 * S + tx0];
+  }
+  bool active(int tx, int ty) const { return cnt[ty * TX + tx] > 0; }
+};
+
+// O1: per-16x16-tile mask-pixel counts and the summed-area table of active
+// tiles ("only need to compute a subset of pixels"; reading R14).
+TileMask make_tilemask(const uint8_t* mask, int W, int H) {
+  TileMask tm;
+  tm.TX = (W + 15) / 16;
+  tm.TY = (H + 15) / 16;
+  tm.cnt.assign((size_t)tm.TX * tm.TY, 0);
+  for (int j = 0; j < H; ++j)
+    for (int i = 0; i < W; ++i)
+      if (mask[(size_t)j * W + i]) tm.cnt[(j / 16) * tm.TX + i / 16] += 1;
+  const int S = tm.TX + 1;
+  tm.sat.assign((size_t)(tm.TY + 1) * S, 0);
+  for (int y = 1; y <= tm.TY; ++y)
+    for (int x = 1; x <= tm.TX; ++x)
+      tm.sat[y * S + x] = tm.sat[(y - 1) * S + x] + tm.sat[y * S + x - 1] -
+                          tm.sat[(y - 1) * S + x - 1] +
+                          (tm.cnt[(y - 1) * tm.TX + (x - 1)] > 0 ? 1 : 0);
+  return tm;
+}
+
+template <typename R> struct Params {
+  const R *mean, *scale, *rot, *opac, *sh;
+  int n, deg;
+};
+
+template <typename R> void quat_to_rot(const R q[4], R Rg[3][3], R qn_out[4], R* norm_out) {
+  const R qn = std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+  const R w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
+  Rg[0][0] = (R)1 - (R)2 * (y * y + z * z);
+  Rg[0][1] = (R)2 * (x * y - w * z);
+  Rg[0][2] = (R)2 * (x * z + w * y);
+  Rg[1][0] = (R)2 * (x * y + w * z);
+  Rg[1][1] = (R)1 - (R)2 * (x * x + z * z);
+  Rg[1][2] = (R)2 * (y * z - w * x);
+  Rg[2][0] = (R)2 * (x * z - w * y);
+  Rg[2][1] = (R)2 * (y * z + w * x);
+  Rg[2][2] = (R)1 - (R)2 * (x * x + y * y);
+  if (qn_out) { qn_out[0] = w; qn_out[1] = x; qn_out[2] = y; qn_out[3] = z; }
+  if (norm_out) *norm_out = qn;
+}
+
+// O2: EWA projection, culling, conservative tile rect, normal, distance, colour.
+// P:78 ("transformed into a 2D Gaussian ... projected onto different image
+// tiles"), P:84-92 (Eq. 2-3: n_i, R_c n_i, d_i), readings R2,R4,R5,R8-R13.
+template <typename R>
+Proj<R> project(const Params<R>& P, int i, const Cam<R>& cam, const TileMask& tm) {
+  Proj<R> g;
+  std::memset(&g, 0, sizeof(g));
+  g.rect[0] = 0; g.rect[1] = 0; g.rect[2] = -1; g.rect[3] = -1;
+  const int N = P.n;
+  const R m0 = P.mean[i], m1 = P.mean[N + i], m2 = P.mean[2 * N + i];
+  const R t[3] = {m0 - cam.C[0], m1 - cam.C[1], m2 - cam.C[2]};
+  const R* Rc = cam.Rc;
+  R pc[3];
+  for (int r = 0; r < 3; ++r) pc[r] = (Rc[3 * r] * t[0] + Rc[3 * r + 1] * t[1]) + Rc[3 * r + 2] * t[2];
+  const R x = pc[0], y = pc[1], z = pc[2];
+  uint32_t fl = 0;
+  if (!(z > cam.znear)) { g.flags = fl; return g; }
+  fl |= F_VISIBLE;
+  g.depth = z;
+  const R xz = x / z, yz = y / z;
+  g.u = cam.fx * xz + cam.cx;
+  g.v = cam.fy * yz + cam.cy;
+
+  // 3D covariance Sigma = (Rg S)(Rg S)^T
+  const R q[4] = {P.rot[i], P.rot[N + i], P.rot[2 * N + i], P.rot[3 * N + i]};
+  R Rg[3][3];
+  quat_to_rot(q, Rg, (R*)nullptr, (R*)nullptr);
+  const R s[3] = {P.scale[i], P.scale[N + i], P.scale[2 * N + i]};
+  R Mg[3][3], Sig[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) Mg[a][b] = Rg[a][b] * s[b];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) Sig[a][b] = (Mg[a][0] * Mg[b][0] + Mg[a][1] * Mg[b][1]) + Mg[a][2] * Mg[b][2];
+
+  // perspective Jacobian with the 1.3 x half-FoV clamp (R9)
+  const R lx = (R)1.3 * (((R)0.5 * (R)cam.W) / cam.fx);
+  const R ly = (R)1.3 * (((R)0.5 * (R)cam.H) / cam.fy);
+  R cxz = xz, cyz = yz;
+  if (xz < -lx) { cxz = -lx; fl |= F_CLAMP_X; }
+  if (xz > lx) { cxz = lx; fl |= F_CLAMP_X; }
+  if (yz < -ly) { cyz = -ly; fl |= F_CLAMP_Y; }
+  if (yz > ly) { cyz = ly; fl |= F_CLAMP_Y; }
+  const R J[2][3] = {{cam.fx / z, (R)0, -((cam.fx * cxz) / z)},
+                     {(R)0, cam.fy / z, -((cam.fy * cyz) / z)}};
+  R Tm[2][3], Mt[2][3], cov[2][2];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 3; ++b) Tm[a][b] = (J[a][0] * Rc[b] + J[a][1] * Rc[3 + b]) + J[a][2] * Rc[6 + b];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 3; ++b) Mt[a][b] = (Tm[a][0] * Sig[0][b] + Tm[a][1] * Sig[1][b]) + Tm[a][2] * Sig[2][b];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) cov[a][b] = (Mt[a][0] * Tm[b][0] + Mt[a][1] * Tm[b][1]) + Mt[a][2] * Tm[b][2];
+  const R A = cov[0][0] + (R)0.3, B = cov[0][1], Cc = cov[1][1] + (R)0.3;  // low-pass (R10)
+  const R det = A * Cc - B * B;
+  if (!(det > (R)0)) { g.flags = fl; return g; }
+  fl |= F_DET_OK;
+  g.ca = Cc / det;
+  g.cb = -B / det;
+  g.cc = A / det;
+  const R o = P.opac[i];
+  g.o = o;
+  if (o < (R)1 / (R)255) { g.flags = fl; return g; }
+  fl |= F_OPAC_OK;
+
+  // opacity-aware conservative ellipse AABB (R8): every pixel with
+  // alpha >= 1/255 satisfies d^T conic d <= 2 ln(255 o) <= k2.
+  const R ylog = (R)255 * o;
+  R k2 = ((R)2 * lnup(ylog)) * ((R)1 + (R)0.0009765625);
+  if (k2 < (R)0) k2 = (R)0;
+  const R PAD = (R)0.015625;
+  const R rx = std::sqrt(k2 * A) + PAD, ry = std::sqrt(k2 * Cc) + PAD;
+  auto clampf = [](R v) { return std::min(std::max(v, (R)-1048576), (R)1048576); };
+  const int ix0 = (int)clampf(std::ceil((g.u - rx) - (R)0.5));
+  const int ix1 = (int)clampf(std::floor((g.u + rx) - (R)0.5));
+  const int iy0 = (int)clampf(std::ceil((g.v - ry) - (R)0.5));
+  const int iy1 = (int)clampf(std::floor((g.v + ry) - (R)0.5));
+  auto fdiv16 = [](int a) { return (a >= 0) ? a / 16 : -((-a + 15) / 16); };
+  const int tx0 = std::max(0, fdiv16(ix0)), tx1 = std::min(tm.TX - 1, fdiv16(ix1));
+  const int ty0 = std::max(0, fdiv16(iy0)), ty1 = std::min(tm.TY - 1, fdiv16(iy1));
+  if (tx0 <= tx1 && ty0 <= ty1) {
+    fl |= F_RECT;
+    g.rect[0] = tx0; g.rect[1] = ty0; g.rect[2] = tx1; g.rect[3] = ty1;
+    g.tiles = (uint32_t)tm.rect_count(tx0, ty0, tx1, ty1);
+  }
+
+  // flattened-Gaussian normal (Eq. 2; R4) and plane distance (Eq. 3; R2)
+  int k = 0;
+  if (s[1] < s[k]) k = 1;
+  if (s[2] < s[k]) k = 2;
+  fl |= (uint32_t)k << F_AXIS_SHIFT;
+  R n[3] = {Rg[0][k], Rg[1][k], Rg[2][k]};
+  const R dotv = (n[0] * t[0] + n[1] * t[1]) + n[2] * t[2];
+  if (dotv > (R)0) { n[0] = -n[0]; n[1] = -n[1]; n[2] = -n[2]; fl |= F_NFLIP; }
+  for (int r = 0; r < 3; ++r) g.ncam[r] = (Rc[3 * r] * n[0] + Rc[3 * r + 1] * n[1]) + Rc[3 * r + 2] * n[2];
+  g.dist = (n[0] * t[0] + n[1] * t[1]) + n[2] * t[2];
+
+  // view-dependent colour from SH (R12)
+  const R len = std::sqrt((t[0] * t[0] + t[1] * t[1]) + t[2] * t[2]);
+  const R dx = t[0] / len, dy = t[1] / len, dz = t[2] / len;
+  R Y[16];
+  sh_basis(dx, dy, dz, Y);
+  const int K = (P.deg + 1) * (P.deg + 1);
+  for (int c = 0; c < 3; ++c) {
+    R acc = Y[0] * P.sh[(size_t)c * N + i];
+    for (int l = 1; l < K; ++l) acc = acc + Y[l] * P.sh[(size_t)(l * 3 + c) * N + i];
+    acc = acc + (R)0.5;
+    if (acc < (R)0) { acc = (R)0; fl |= F_RGB_CLAMP0 << c; }
+    g.rgb[c] = acc;
+  }
+  g.flags = fl;
+  return g;
+}
+
+// ------------------------------------------------------ compositing (O4)
+template <typename R> struct PixOut {
+  R C[3], N[3], D, A, Dep, T;
+  int g;
+  int last;       // Gaussian id of the last blended, -1 if none
+  int near_flag;  // some decision was within the reading-R18 margin
+  long long evaluated;  // list entries visited (E counter)
+  double id_sum;        // checksum of blended ids (FD validity)
+  int n_clamped;        // blended pairs with o*rho > 0.99
+};
+
+template <typename R> struct Blend {
+  int id;
+  R alpha, T, rho, orho, dx, dy;
+};
+
+template <typename R> struct Renderer {
+  const Params<R>& P;
+  const Cam<R>& cam;
+  const TileMask& tm;
+  std::vector<Proj<R>> proj;
+  Renderer(const Params<R>& P_, const Cam<R>& cam_, const TileMask& tm_) : P(P_), cam(cam_), tm(tm_) {
+    proj.resize(P.n);
+    for (int i = 0; i < P.n; ++i) proj[i] = project(P, i, cam, tm);
+  }
+
+  // Candidates of tile (tx,ty): live Gaussians whose rect contains it, in
+  // (depth, id) order ("sorted"; R11).
+  void candidates(int tx, int ty, std::vector<int>& out) const {
+    out.clear();
+    for (int i = 0; i < P.n; ++i) {
+      const Proj<R>& g = proj[i];
+      if ((g.flags & F_LIVE) != F_LIVE) continue;
+      if (tx < g.rect[0] || tx > g.rect[2] || ty < g.rect[1] || ty > g.rect[3]) continue;
+      out.push_back(i);
+    }
+    std::stable_sort(out.begin(), out.end(), [&](int a, int b) {
+      if (proj[a].depth != proj[b].depth) return proj[a].depth < proj[b].depth;
+      return a < b;
+    });
+  }
+
+  static bool near_rel(R a, R b, double tol) {
+    return std::fabs((double)a - (double)b) <= tol * std::fabs((double)b);
+  }
+
+  // Eq. 1-3 front to back for pixel (i,j), then Eq. 4 (R1, R3, R5, R6, R15).
+  PixOut<R> pixel(int i, int j, const std::vector<int>& cand, const R bg[3],
+                  std::vector<Blend<R>>* blends) const {
+    PixOut<R> o;
+    std::memset(&o, 0, sizeof(o));
+    o.last = -1;
+    R T = (R)1;
+    const R px = (R)i + (R)0.5, py = (R)j + (R)0.5;
+    const R a_min = (R)1 / (R)255;
+    const R t_min = (R)0.0001;
+    if (blends) blends->clear();
+    for (int id : cand) {
+      const Proj<R>& g = proj[id];
+      o.evaluated += 1;
+      const R dx = px - g.u, dy = py - g.v;
+      const R power = (R)-0.5 * ((g.ca * dx) * dx + (g.cc * dy) * dy) - (g.cb * dx) * dy;
+      if (std::fabs((double)power) < 1e-5) o.near_flag = 1;
+      if (power > (R)0) continue;
+      const R rho = std::exp(power);
+      const R orho = g.o * rho;
+      const R alpha = std::min((R)0.99, orho);
+      if (near_rel(orho, a_min, 1e-5) || near_rel(orho, (R)0.99, 1e-5)) o.near_flag = 1;
+      if (alpha < a_min) continue;
+      const R Tn = T * ((R)1 - alpha);
+      if (near_rel(Tn, t_min, 1e-3)) o.near_flag = 1;
+      if (Tn < t_min) break;  // R6: the crossing Gaussian is not blended
+      const R w = alpha * T;
+      for (int c = 0; c < 3; ++c) o.C[c] = o.C[c] + w * g.rgb[c];
+      for (int c = 0; c < 3; ++c) o.N[c] = o.N[c] + w * g.ncam[c];
+      o.D = o.D + w * g.dist;
+      if (blends) blends->push_back(Blend<R>{id, alpha, T, rho, orho, dx, dy});
+      o.g += 1;
+      o.last = id;
+      o.id_sum += (double)id;
+      if (orho > (R)0.99) o.n_clamped += 1;
+      T = Tn;
+    }
+    for (int c = 0; c < 3; ++c) o.C[c] = o.C[c] + T * bg[c];
+    o.A = (R)1 - T;
+    o.T = T;
+    const R r0 = (px - cam.cx) / cam.fx, r1 = (py - cam.cy) / cam.fy;
+    const R den = (o.N[0] * r0 + o.N[1] * r1) + o.N[2];
+    o.Dep = (o.g > 0 && std::fabs(den) > (R)1e-6) ? o.D / den : (R)0;  // Eq. 4, R3
+    return o;
+  }
+
+  // Certificate: pairs excluded by the rect that would have alpha >= 1/255.
+  long long certify(int i, int j) const {
+    long long bad = 0;
+    const int tx = i / 16, ty = j / 16;
+    const R px = (R)i + (R)0.5, py = (R)j + (R)0.5;
+    for (int id = 0; id < P.n; ++id) {
+      const Proj<R>& g = proj[id];
+      const uint32_t need = F_VISIBLE | F_DET_OK | F_OPAC_OK;
+      if ((g.flags & need) != need) continue;
+      const bool inrect = (g.flags & F_RECT) && tx >= g.rect[0] && tx <= g.rect[2] &&
+                          ty >= g.rect[1] && ty <= g.rect[3];
+      if (inrect) continue;
+      const R dx = px - g.u, dy = py - g.v;
+      const R power = (R)-0.5 * ((g.ca * dx) * dx + (g.cc * dy) * dy) - (g.cb * dx) * dy;
+      if (power > (R)0) continue;
+      const R alpha = std::min((R)0.99, g.o * std::exp(power));
+      if (alpha >= (R)1 / (R)255) ++bad;
+    }
+    return bad;
+  }
+};
+
+// -------------------------------------------------- per-Gaussian 2D grads
+struct G2 {
+  double du, dv, dca, dcb, dcc, dop, drgb[3], dncam[3], ddist;
+};
+
+// O5: reverse-order backward of one pixel (exact reverse mode of Eq. 1-4,
+// P:82; decisions frozen per R17; clamp gradient per R16).
+template <typename R>
+void pixel_backward(const Renderer<R>& rd, int i, int j, const PixOut<R>& fw,
+                    const std::vector<Blend<R>>& bl, const R bg[3], const double up[9],
+                    std::vector<G2>& g2) {
+  // up = (gC0,gC1,gC2, gN0,gN1,gN2, gD, gA, gDep)
+  double G[8] = {up[0], up[1], up[2], up[3], up[4], up[5], up[6], up[7]};
+  const double gDep = up[8];
+  const double px = i + 0.5, py = j + 0.5;
+  const double r[3] = {(px - (double)rd.cam.cx) / (double)rd.cam.fx,
+                       (py - (double)rd.cam.cy) / (double)rd.cam.fy, 1.0};
+  const double den = (double)fw.N[0] * r[0] + (double)fw.N[1] * r[1] + (double)fw.N[2];
+  // validity decided exactly as the forward decided it (in R)
+  const R r0R = (((R)i + (R)0.5) - rd.cam.cx) / rd.cam.fx, r1R = (((R)j + (R)0.5) - rd.cam.cy) / rd.cam.fy;
+  const bool dep_valid = fw.g > 0 && std::fabs((fw.N[0] * r0R + fw.N[1] * r1R) + fw.N[2]) > (R)1e-6;
+  if (dep_valid) {  // Eq. 4: Dep = D / (N . r)
+    G[6] += gDep / den;
+    for (int c = 0; c < 3; ++c) G[3 + c] -= gDep * (double)fw.D / (den * den) * r[c];
+  }
+  const double bgdot = (double)bg[0] * G[0] + (double)bg[1] * G[1] + (double)bg[2] * G[2];
+  double S[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double Pp = 1.0;
+  for (int k = (int)bl.size() - 1; k >= 0; --k) {
+    const Blend<R>& b = bl[k];
+    const Proj<R>& g = rd.proj[b.id];
+    const double F[8] = {(double)g.rgb[0], (double)g.rgb[1], (double)g.rgb[2], (double)g.ncam[0],
+                         (double)g.ncam[1], (double)g.ncam[2], (double)g.dist, 1.0};
+    const double a = (double)b.alpha, T = (double)b.T;
+    double dot = 0.0;
+    for (int c = 0; c < 8; ++c) dot += G[c] * (F[c] - S[c]);
+    const double dalpha = T * (dot - Pp * bgdot);
+    const double w = a * T;
+    G2& o = g2[b.id];
+    for (int c = 0; c < 3; ++c) o.drgb[c] += w * G[c];
+    for (int c = 0; c < 3; ++c) o.dncam[c] += w * G[3 + c];
+    o.ddist += w * G[6];
+    for (int c = 0; c < 8; ++c) S[c] = a * F[c] + (1.0 - a) * S[c];
+    Pp *= (1.0 - a);
+    double dpow = 0.0;
+    if (b.orho <= (R)0.99) {
+      o.dop += (double)b.rho * dalpha;
+      dpow = a * dalpha;
+    }
+    const double dx = (double)b.dx, dy = (double)b.dy;
+    o.dca += -0.5 * dx * dx * dpow;
+    o.dcb += -dx * dy * dpow;
+    o.dcc += -0.5 * dy * dy * dpow;
+    o.du += ((double)g.ca * dx + (double)g.cb * dy) * dpow;
+    o.dv += ((double)g.cb * dx + (double)g.cc * dy) * dpow;
+  }
+}
+
+// O6: chain rule from the 2D/per-Gaussian gradients to the 3D parameters
+// (P:82), through O2 in double; decisions (clamps, axis, flip) from flags.
+template <typename R>
+void gaussian_backward(const Params<R>& P, int i, const Cam<R>& camR, uint32_t fl, const G2& g,
+                       double* dmean, double* dscale, double* drot, double* dopac, double* dsh) {
+  const int N = P.n;
+  if ((fl & F_LIVE) != F_LIVE) return;
+  Cam<double> cam;
+  cam.fx = camR.fx; cam.fy = camR.fy; cam.cx = camR.cx; cam.cy = camR.cy;
+  for (int k = 0; k < 9; ++k) cam.Rc[k] = camR.Rc[k];
+  for (int k = 0; k < 3; ++k) cam.C[k] = camR.C[k];
+  const double* Rc = cam.Rc;
+  const double t[3] = {(double)P.mean[i] - cam.C[0], (double)P.mean[N + i] - cam.C[1],
+                       (double)P.mean[2 * N + i] - cam.C[2]};
+  double pc[3];
+  for (int r = 0; r < 3; ++r) pc[r] = Rc[3 * r] * t[0] + Rc[3 * r + 1] * t[1] + Rc[3 * r + 2] * t[2];
+  const double x = pc[0], y = pc[1], z = pc[2];
+  const double q[4] = {(double)P.rot[i], (double)P.rot[N + i], (double)P.rot[2 * N + i], (double)P.rot[3 * N + i]};
+  double Rg[3][3], qh[4], qn;
+  quat_to_rot(q, Rg, qh, &qn);
+  const double s[3] = {(double)P.scale[i], (double)P.scale[N + i], (double)P.scale[2 * N + i]};
+  double Mg[3][3], Sig[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) Mg[a][b] = Rg[a][b] * s[b];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) Sig[a][b] = Mg[a][0] * Mg[b][0] + Mg[a][1] * Mg[b][1] + Mg[a][2] * Mg[b][2];
+  const bool clx = fl & F_CLAMP_X, cly = fl & F_CLAMP_Y;
+  const double lx = 1.3 * (0.5 * camR.W / cam.fx), ly = 1.3 * (0.5 * camR.H / cam.fy);
+  const double xz = x / z, yz = y / z;
+  const double cxz = clx ? std::min(std::max(xz, -lx), lx) : xz;
+  const double cyz = cly ? std::min(std::max(yz, -ly), ly) : yz;
+  const double J[2][3] = {{cam.fx / z, 0.0, -cam.fx * cxz / z}, {0.0, cam.fy / z, -cam.fy * cyz / z}};
+  double Tm[2][3];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 3; ++b) Tm[a][b] = J[a][0] * Rc[b] + J[a][1] * Rc[3 + b] + J[a][2] * Rc[6 + b];
+  double cov[2][2];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      double acc = 0;
+      for (int k = 0; k < 3; ++k)
+        for (int l = 0; l < 3; ++l) acc += Tm[a][k] * Sig[k][l] * Tm[b][l];
+      cov[a][b] = acc;
+    }
+  const double A = cov[0][0] + 0.3, B = cov[0][1], C = cov[1][1] + 0.3;
+  const double det = A * C - B * B, det2 = det * det;
+  // conic (ca,cb,cc) = (C,-B,A)/det  ->  d(A,B,C)
+  const double dA = (-C * C * g.dca + B * C * g.dcb - B * B * g.dcc) / det2;
+  const double dC = (-B * B * g.dca + A * B * g.dcb - A * A * g.dcc) / det2;
+  const double dB = (2 * B * C * g.dca - (A * C + B * B) * g.dcb + 2 * A * B * g.dcc) / det2;
+  // cov_ab = Tm_a Sig Tm_b^T
+  double dSig[3][3];
+  for (int k = 0; k < 3; ++k)
+    for (int l = 0; l < 3; ++l)
+      dSig[k][l] = dA * Tm[0][k] * Tm[0][l] + dC * Tm[1][k] * Tm[1][l] + dB * Tm[0][k] * Tm[1][l];
+  double STm[2][3];  // Sig Tm_a^T
+  for (int a = 0; a < 2; ++a)
+    for (int k = 0; k < 3; ++k) STm[a][k] = Sig[k][0] * Tm[a][0] + Sig[k][1] * Tm[a][1] + Sig[k][2] * Tm[a][2];
+  double dTm[2][3];
+  for (int k = 0; k < 3; ++k) {
+    dTm[0][k] = 2 * dA * STm[0][k] + dB * STm[1][k];
+    dTm[1][k] = 2 * dC * STm[1][k] + dB * STm[0][k];
+  }
+  // Tm = J Rc
+  double dJ[2][3];
+  for (int a = 0; a < 2; ++a)
+    for (int k = 0; k < 3; ++k) dJ[a][k] = dTm[a][0] * Rc[3 * k] + dTm[a][1] * Rc[3 * k + 1] + dTm[a][2] * Rc[3 * k + 2];
+  double dp[3] = {0, 0, 0};
+  const double z2 = z * z, z3 = z2 * z;
+  dp[2] += -cam.fx / z2 * dJ[0][0] - cam.fy / z2 * dJ[1][1];
+  if (!clx) { dp[0] += -cam.fx / z2 * dJ[0][2]; dp[2] += 2 * cam.fx * x / z3 * dJ[0][2]; }
+  else { dp[2] += cam.fx * cxz / z2 * dJ[0][2]; }
+  if (!cly) { dp[1] += -cam.fy / z2 * dJ[1][2]; dp[2] += 2 * cam.fy * y / z3 * dJ[1][2]; }
+  else { dp[2] += cam.fy * cyz / z2 * dJ[1][2]; }
+  // mean2d
+  dp[0] += cam.fx / z * g.du;
+  dp[2] += -cam.fx * x / z2 * g.du;
+  dp[1] += cam.fy / z * g.dv;
+  dp[2] += -cam.fy * y / z2 * g.dv;
+  double dt[3];
+  for (int k = 0; k < 3; ++k) dt[k] = Rc[k] * dp[0] + Rc[3 + k] * dp[1] + Rc[6 + k] * dp[2];
+  // Sigma = Mg Mg^T
+  double dMg[3][3], dRg[3][3];
+  for (int k = 0; k < 3; ++k)
+    for (int m = 0; m < 3; ++m) {
+      double acc = 0;
+      for (int l = 0; l < 3; ++l) acc += (dSig[k][l] + dSig[l][k]) * Mg[l][m];
+      dMg[k][m] = acc;
+    }
+  double ds[3] = {0, 0, 0};
+  for (int k = 0; k < 3; ++k)
+    for (int m = 0; m < 3; ++m) {
+      ds[m] += dMg[k][m] * Rg[k][m];
+      dRg[k][m] = dMg[k][m] * s[m];
+    }
+  // normal n = sgn Rg[:,k];  ncam = Rc n;  dist = n . t
+  const int ax = (fl >> F_AXIS_SHIFT) & 3;
+  const double sg = (fl & F_NFLIP) ? -1.0 : 1.0;
+  const double n[3] = {sg * Rg[0][ax], sg * Rg[1][ax], sg * Rg[2][ax]};
+  double dn[3];
+  for (int k = 0; k < 3; ++k) dn[k] = Rc[k] * g.dncam[0] + Rc[3 + k] * g.dncam[1] + Rc[6 + k] * g.dncam[2];
+  for (int k = 0; k < 3; ++k) { dn[k] += t[k] * g.ddist; dt[k] += n[k] * g.ddist; }
+  for (int k = 0; k < 3; ++k) dRg[k][ax] += sg * dn[k];
+  // Rg(qh)
+  const double w = qh[0], X = qh[1], Y = qh[2], Z = qh[3];
+  double dq[4] = {0, 0, 0, 0};  // w, x, y, z
+  dq[2] += -4 * Y * dRg[0][0]; dq[3] += -4 * Z * dRg[0][0];
+  dq[1] += 2 * Y * dRg[0][1]; dq[2] += 2 * X * dRg[0][1]; dq[0] += -2 * Z * dRg[0][1]; dq[3] += -2 * w * dRg[0][1];
+  dq[1] += 2 * Z * dRg[0][2]; dq[3] += 2 * X * dRg[0][2]; dq[0] += 2 * Y * dRg[0][2]; dq[2] += 2 * w * dRg[0][2];
+  dq[1] += 2 * Y * dRg[1][0]; dq[2] += 2 * X * dRg[1][0]; dq[0] += 2 * Z * dRg[1][0]; dq[3] += 2 * w * dRg[1][0];
+  dq[1] += -4 * X * dRg[1][1]; dq[3] += -4 * Z * dRg[1][1];
+  dq[2] += 2 * Z * dRg[1][2]; dq[3] += 2 * Y * dRg[1][2]; dq[0] += -2 * X * dRg[1][2]; dq[1] += -2 * w * dRg[1][2];
+  dq[1] += 2 * Z * dRg[2][0]; dq[3] += 2 * X * dRg[2][0]; dq[0] += -2 * Y * dRg[2][0]; dq[2] += -2 * w * dRg[2][0];
+  dq[2] += 2 * Z * dRg[2][1]; dq[3] += 2 * Y * dRg[2][1]; dq[0] += 2 * X * dRg[2][1]; dq[1] += 2 * w * dRg[2][1];
+  dq[1] += -4 * X * dRg[2][2]; dq[2] += -4 * Y * dRg[2][2];
+  const double qdot = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
+  double dqr[4];
+  for (int k = 0; k < 4; ++k) dqr[k] = (dq[k] - qh[k] * qdot) / qn;
+  // SH colour
+  const double len = std::sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
+  const double dir[3] = {t[0] / len, t[1] / len, t[2] / len};
+  double Yb[16], GY[16][3];
+  sh_basis(dir[0], dir[1], dir[2], Yb);
+  sh_basis_grad(dir[0], dir[1], dir[2], GY);
+  const int K = (P.deg + 1) * (P.deg + 1);
+  double ddir[3] = {0, 0, 0};
+  for (int c = 0; c < 3; ++c) {
+    if (fl & (F_RGB_CLAMP0 << c)) continue;
+    const double gc = g.drgb[c];
+    for (int l = 0; l < K; ++l) {
+      const double shv = (double)P.sh[(size_t)(l * 3 + c) * N + i];
+      dsh[(size_t)(l * 3 + c) * N + i] = Yb[l] * gc;
+      for (int k = 0; k < 3; ++k) ddir[k] += GY[l][k] * shv * gc;
+    }
+  }
+  const double dd = dir[0] * ddir[0] + dir[1] * ddir[1] + dir[2] * ddir[2];
+  for (int k = 0; k < 3; ++k) dt[k] += (ddir[k] - dir[k] * dd) / len;
+  for (int k = 0; k < 3; ++k) dmean[(size_t)k * N + i] = dt[k];
+  for (int k = 0; k < 3; ++k) dscale[(size_t)k * N + i] = ds[k];
+  for (int k = 0; k < 4; ++k) drot[(size_t)k * N + i] = dqr[k];
+  dopac[i] = g.dop;
+}
+
+template <typename R>
+Params<R> make_params(const R* mean, const R* scale, const R* rot, const R* opac, const R* sh, int n, int deg) {
+  Params<R> p;
+  p.mean = mean; p.scale = scale; p.rot = rot; p.opac = opac; p.sh = sh; p.n = n; p.deg = deg;
+  return p;
+}
+
+// ----------------------------------------------------------- entry points
+template <typename R>
+void project_all(const R* mean, const R* scale, const R* rot, const R* opac, const R* sh, int n, int deg,
+                 const double* camf, int W, int H, const uint8_t* mask, R* mean2d, R* conic_o, R* depth,
+                 int32_t* rect, uint32_t* tiles, R* rgb, R* ncam, R* dist, uint32_t* flags) {
+  const Params<R> P = make_params(mean, scale, rot, opac, sh, n, deg);
+  const Cam<R> cam = load_cam<R>(camf, W, H);
+  const TileMask tm = make_tilemask(mask, W, H);
+  for (int i = 0; i < n; ++i) {
+    const Proj<R> g = project(P, i, cam, tm);
+    mean2d[2 * i] = g.u; mean2d[2 * i + 1] = g.v;
+    conic_o[4 * i] = g.ca; conic_o[4 * i + 1] = g.cb; conic_o[4 * i + 2] = g.cc; conic_o[4 * i + 3] = g.o;
+    depth[i] = g.depth;
+    for (int k = 0; k < 4; ++k) rect[4 * i + k] = g.rect[k];
+    tiles[i] = g.tiles;
+    for (int c = 0; c < 3; ++c) { rgb[3 * i + c] = g.rgb[c]; ncam[3 * i + c] = g.ncam[c]; }
+    dist[i] = g.dist;
+    flags[i] = g.flags;
+  }
+}
+
+template <typename R>
+void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, const R* sh, int n, int deg,
+                   const double* camf, int W, int H, const uint8_t* mask, const double* bgd,
+                   const int64_t* pix, int npix, R* out /* [npix][10]: C3 N3 D A Dep T */,
+                   int32_t* iout /* [npix][4]: g last near_flag n_clamped */, double* id_sum, int64_t* evaluated,
+                   int certify_flag, int64_t* cert_bad,
+                   const double* upstream /* [npix][9] or null */, double* grads /* 59 x n or null */) {
+  const Params<R> P = make_params(mean, scale, rot, opac, sh, n, deg);
+  const Cam<R> cam = load_cam<R>(camf, W, H);
+  const TileMask tm = make_tilemask(mask, W, H);
+  Renderer<R> rd(P, cam, tm);
+  const R bg[3] = {(R)bgd[0], (R)bgd[1], (R)bgd[2]};
+  // group requested pixels by tile so each tile's candidate list is built once
+  std::vector<int> order(npix);
+  for (int k = 0; k < npix; ++k) order[k] = k;
+  auto tile_of = [&](int k) { const int64_t p = pix[k]; return (int)((p / W) / 16) * tm.TX + (int)((p % W) / 16); };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tile_of(a) < tile_of(b); });
+  std::vector<int> cand;
+  std::vector<Blend<R>> bl;
+  std::vector<G2> g2;
+  if (grads) g2.assign(n, G2{0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, 0});
+  int cur_tile = -1;
+  long long bad = 0;
+  for (int k : order) {
+    const int64_t p = pix[k];
+    const int i = (int)(p % W), j = (int)(p / W);
+    if (!mask[p]) {  // masked-out pixels are not rendered (R14)
+      for (int c = 0; c < 10; ++c) out[(size_t)k * 10 + c] = (R)0;
+      iout[(size_t)k * 4] = 0; iout[(size_t)k * 4 + 1] = -1; iout[(size_t)k * 4 + 2] = 0; iout[(size_t)k * 4 + 3] = 0;
+      continue;
+    }
+    const int t = tile_of(k);
+    if (t != cur_tile) { rd.candidates(i / 16, j / 16, cand); cur_tile = t; }
+    const PixOut<R> o = rd.pixel(i, j, cand, bg, grads ? &bl : nullptr);
+    R* op = out + (size_t)k * 10;
+    op[0] = o.C[0]; op[1] = o.C[1]; op[2] = o.C[2];
+    op[3] = o.N[0]; op[4] = o.N[1]; op[5] = o.N[2];
+    op[6] = o.D; op[7] = o.A; op[8] = o.Dep; op[9] = o.T;
+    iout[(size_t)k * 4] = o.g; iout[(size_t)k * 4 + 1] = o.last;
+    iout[(size_t)k * 4 + 2] = o.near_flag; iout[(size_t)k * 4 + 3] = o.n_clamped;
+    if (id_sum) id_sum[k] = o.id_sum;
+    if (evaluated) evaluated[k] = o.evaluated;
+    if (certify_flag) bad += rd.certify(i, j);
+    if (grads) pixel_backward(rd, i, j, o, bl, bg, upstream + (size_t)k * 9, g2);
+  }
+  if (cert_bad) *cert_bad = bad;
+  if (grads) {
+    double* dmean = grads;
+    double* dscale = grads + (size_t)3 * n;
+    double* drot = grads + (size_t)6 * n;
+    double* dop = grads + (size_t)10 * n;
+    double* dsh = grads + (size_t)11 * n;
+    std::memset(grads, 0, sizeof(double) * (size_t)59 * n);
+    for (int i = 0; i < n; ++i) gaussian_backward(P, i, cam, rd.proj[i].flags, g2[i], dmean, dscale, drot, dop, dsh);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// O1: tile occupancy counts [TY*TX] and SAT [(TY+1)*(TX+1)].
+void oracle_tilemask(const uint8_t* mask, int W, int H, uint32_t* cnt, int32_t* sat) {
+  const TileMask tm = make_tilemask(mask, W, H);
+  std::memcpy(cnt, tm.cnt.data(), tm.cnt.size() * sizeof(uint32_t));
+  std::memcpy(sat, tm.sat.data(), tm.sat.size() * sizeof(int32_t));
+}
+
+// O2 in float32 (parity) and float64 (pins).  Interleaved outputs:
+// mean2d[n][2], conic_o[n][4], depth[n], rect[n][4], tiles[n], rgb[n][3], ncam[n][3], dist[n], flags[n].
+void oracle_project_f32(const float* mean, const float* scale, const float* rot, const float* opac,
+                        const float* sh, int n, int deg, const double* cam, int W, int H, const uint8_t* mask,
+                        float* mean2d, float* conic_o, float* depth, int32_t* rect, uint32_t* tiles,
+                        float* rgb, float* ncam, float* dist, uint32_t* flags) {
+  project_all<float>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, mean2d, conic_o, depth, rect, tiles,
+                     rgb, ncam, dist, flags);
+}
+void oracle_project_f64(const double* mean, const double* scale, const double* rot, const double* opac,
+                        const double* sh, int n, int deg, const double* cam, int W, int H, const uint8_t* mask,
+                        double* mean2d, double* conic_o, double* depth, int32_t* rect, uint32_t* tiles,
+                        double* rgb, double* ncam, double* dist, uint32_t* flags) {
+  project_all<double>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, mean2d, conic_o, depth, rect, tiles,
+                      rgb, ncam, dist, flags);
+}
+
+// O3: (tile, depth bits, id) entries for every live Gaussian and active tile in
+// its rect, sorted lexicographically; tile ranges [TX*TY][2].  Returns M, and
+// writes only if M <= capacity.  depth: float32 depths from oracle_project_f32.
+int64_t oracle_keys(const float* depth, const int32_t* rect, const uint32_t* flags, int n, const uint8_t* mask,
+                    int W, int H, int64_t capacity, uint32_t* tile_out, uint32_t* val_out, uint32_t* ranges) {
+  const TileMask tm = make_tilemask(mask, W, H);
+  struct E { uint32_t tile, bits, id; };
+  std::vector<E> ent;
+  for (int i = 0; i < n; ++i) {
+    if ((flags[i] & F_LIVE) != F_LIVE) continue;
+    uint32_t bits;
+    std::memcpy(&bits, &depth[i], 4);
+    for (int ty = rect[4 * i + 1]; ty <= rect[4 * i + 3]; ++ty)
+      for (int tx = rect[4 * i]; tx <= rect[4 * i + 2]; ++tx)
+        if (tm.active(tx, ty)) ent.push_back(E{(uint32_t)(ty * tm.TX + tx), bits, (uint32_t)i});
+  }
+  const int64_t M = (int64_t)ent.size();
+  if (M > capacity) return M;
+  std::sort(ent.begin(), ent.end(), [](const E& a, const E& b) {
+    if (a.tile != b.tile) return a.tile < b.tile;
+    if (a.bits != b.bits) return a.bits < b.bits;
+    return a.id < b.id;
+  });
+  const int T = tm.TX * tm.TY;
+  for (int t = 0; t < 2 * T; ++t) ranges[t] = 0;
+  for (int64_t k = 0; k < M; ++k) {
+    tile_out[k] = ent[k].tile;
+    val_out[k] = ent[k].id;
+    if (k == 0 || ent[k].tile != ent[k - 1].tile) ranges[2 * ent[k].tile] = (uint32_t)k;
+    if (k == M - 1 || ent[k].tile != ent[k + 1].tile) ranges[2 * ent[k].tile + 1] = (uint32_t)(k + 1);
+  }
+  return M;
+}
+
+// O4 (+ O5/O6 when upstream && grads): render the listed pixels.
+// out[npix][10] = C0 C1 C2 N0 N1 N2 D A Dep T; iout[npix][4] = g, last id, near flag, n_clamped.
+// grads (double, 59*n): dmean[3][n] dscale[3][n] drot[4][n] dopac[n] dsh[48][n].
+void oracle_render_f32(const float* mean, const float* scale, const float* rot, const float* opac, const float* sh,
+                       int n, int deg, const double* cam, int W, int H, const uint8_t* mask, const double* bg,
+                       const int64_t* pix, int npix, float* out, int32_t* iout, double* id_sum, int64_t* evaluated,
+                       int certify, int64_t* cert_bad, const double* upstream, double* grads) {
+  render_pixels<float>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, bg, pix, npix, out, iout, id_sum,
+                       evaluated, certify, cert_bad, upstream, grads);
+}
+void oracle_render_f64(const double* mean, const double* scale, const double* rot, const double* opac,
+                       const double* sh, int n, int deg, const double* cam, int W, int H, const uint8_t* mask,
+                       const double* bg, const int64_t* pix, int npix, double* out, int32_t* iout, double* id_sum,
+                       int64_t* evaluated, int certify, int64_t* cert_bad, const double* upstream, double* grads) {
+  render_pixels<double>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, bg, pix, npix, out, iout, id_sum,
+                        evaluated, certify, cert_bad, upstream, grads);
+}
+
+// SH basis in double (for the library pin against scipy).
+void oracle_sh_basis(double x, double y, double z, double* Y) { sh_basis<double>(x, y, z, Y); }
+// log upper bound used by the rect (for the pin that it bounds ln from above).
+float oracle_lnup_f32(float y) { return lnup<float>(y); }
+
+}  // extern "C"

@@ -1,0 +1,454 @@
+"""Pins of the CPU oracle against things other than itself (closed forms,
+library routines, Monte-Carlo, brute force, finite differences).
+
+Each test names the passage it follows (P:n = PAPER.md line n, S:n = SPEC.md
+line n, Rk = DESIGN.md §3 reading k).  None of these calls the CUDA path.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import scenes as S
+from tests.helpers import SH_C0, all_pixels, cam_identity, full_mask, gaussians, quat_axis_angle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def one_pixel(W, i, j):
+    return np.array([j * W + i], np.int64)
+
+
+# ---------------------------------------------------------------- projection
+def test_project_point_closed_form():
+    """S:62 worked example: x=(1,0,5), fx=500, cx=320 -> u=420 (P:78 projection)."""
+    ex = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))["project_point"]
+    cam = cam_identity(W=640, H=480, fx=ex["fx"], cx=ex["cx"], cy=240.0)
+    g = gaussians([ex["x"]], [[0.1, 0.1, 0.1]], opac=[0.9])
+    for dt in (np.float32, np.float64):
+        p = oracle.project(g, cam, full_mask(480, 640), dtype=dt)
+        assert p["mean2d"][0, 0] == ex["u"]
+        assert p["mean2d"][0, 1] == 240.0
+        assert p["depth"][0] == 5.0
+
+
+def test_fx_doubling_doubles_offset():
+    """doubling fx doubles the mean2d offset from the principal point."""
+    g = gaussians([[0.37, -0.21, 3.3]], [[0.1, 0.1, 0.1]], opac=[0.9])
+    p1 = oracle.project(g, cam_identity(fx=64.0), full_mask(64, 64), dtype=np.float64)
+    p2 = oracle.project(g, cam_identity(fx=128.0, fy=64.0), full_mask(64, 64), dtype=np.float64)
+    assert math.isclose(p2["mean2d"][0, 0] - 32.0, 2 * (p1["mean2d"][0, 0] - 32.0), rel_tol=1e-14)
+    assert math.isclose(p2["mean2d"][0, 1], p1["mean2d"][0, 1], rel_tol=1e-14)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_isotropic_on_axis_conic_closed_form(seed):
+    """EWA: an isotropic Gaussian (scale s) on the optical axis at z0
+    projects to cov2d = diag(fx^2 s^2/z0^2 + 0.3, fy^2 s^2/z0^2 + 0.3) whatever its rotation."""
+    rng = np.random.default_rng(seed)
+    s, z0, fx, fy = 0.1, 4.0, 64.0, 80.0
+    q = rng.normal(size=4)
+    g = gaussians([[0, 0, z0]], [[s, s, s]], quats=[q], opac=[0.9])
+    p = oracle.project(g, cam_identity(fx=fx, fy=fy), full_mask(64, 64), dtype=np.float64)
+    a = fx * fx * s * s / z0 ** 2 + 0.3
+    c = fy * fy * s * s / z0 ** 2 + 0.3
+    ca, cb, cc, o = p["conic_o"][0]
+    assert math.isclose(ca, 1 / a, rel_tol=1e-12) and math.isclose(cc, 1 / c, rel_tol=1e-12)
+    assert abs(cb) < 1e-12 and o == 0.9
+
+
+def test_anisotropic_axis_aligned_conic():
+    """Axis-aligned anisotropic Gaussian on axis: cov2d = diag((fx sx/z0)^2+0.3, (fy sy/z0)^2+0.3)."""
+    sx, sy, sz, z0 = 0.1, 0.25, 0.04, 5.0
+    g = gaussians([[0, 0, z0]], [[sx, sy, sz]], opac=[0.9])
+    p = oracle.project(g, cam_identity(fx=100.0), full_mask(64, 64), dtype=np.float64)
+    ca, cb, cc, _ = p["conic_o"][0]
+    assert math.isclose(1 / ca, (100 * sx / z0) ** 2 + 0.3, rel_tol=1e-12)
+    assert math.isclose(1 / cc, (100 * sy / z0) ** 2 + 0.3, rel_tol=1e-12)
+    assert abs(cb) < 1e-12
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_cov2d_monte_carlo(seed):
+    """cov2d - 0.3 I matches the covariance of projected 3D samples within 2% (Frobenius),
+    for a small far anisotropic splat, off-axis, seen by a rotated camera."""
+    rng = np.random.default_rng(seed)
+    cam = S.make_camera([0.3, -0.2, -0.5], [0.5, 0.4, 6.0], 64, 64, 64.0)
+    mu = np.array([0.8, 0.9, 6.0]) + rng.normal(scale=0.2, size=3)
+    q = rng.normal(size=4)
+    sc = np.array([0.06, 0.03, 0.012])
+    g = gaussians([mu], [sc], quats=[q], opac=[0.9])
+    p = oracle.project(g, cam, full_mask(64, 64), dtype=np.float64)
+    ca, cb, cc, _ = p["conic_o"][0]
+    det = ca * cc - cb * cb
+    cov = np.array([[cc, -cb], [-cb, ca]]) / det - 0.3 * np.eye(2)
+    w, x, y, z = q / np.linalg.norm(q)
+    Rg = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                   [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                   [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    X = mu[None] + (rng.normal(size=(1_000_000, 3)) * sc[None]) @ Rg.T
+    Pc = (X - cam.C.astype(float)[None]) @ cam.R.astype(float).T
+    uv = np.stack([cam.fx * Pc[:, 0] / Pc[:, 2] + cam.cx, cam.fy * Pc[:, 1] / Pc[:, 2] + cam.cy], 1)
+    emp = np.cov(uv.T)
+    assert np.linalg.norm(emp - cov) / np.linalg.norm(emp) < 0.02
+
+
+def test_peak_alpha_at_centre_pixel():
+    """S:290 + R5: a Gaussian projected exactly on a pixel centre has alpha = min(0.99, o) there."""
+    cam = cam_identity(cx=32.5, cy=32.5)
+    for o, expect in ((0.7, 0.7), (0.995, 0.99), (0.3, 0.3)):
+        g = gaussians([[0, 0, 4.0]], [[0.2, 0.2, 0.2]], opac=[o], rgb=[[1, 1, 1]])
+        r = oracle.render(g, cam, full_mask(64, 64), one_pixel(64, 32, 32), dtype=np.float64)
+        assert r["g"][0] == 1
+        assert math.isclose(r["A"][0], expect, rel_tol=1e-12)
+        assert math.isclose(r["T"][0], 1 - expect, rel_tol=1e-12)
+
+
+# ------------------------------------------------------------ normal / dist
+@pytest.mark.parametrize("camz,expect", [(10.0, 1.0), (-10.0, -1.0)])
+def test_flatten_normal_faces_camera(camz, expect):
+    """S:275-276 / R4: disk (1,1,0.01), identity rotation: camera on +z gives n=(0,0,1),
+    camera on -z gives n=(0,0,-1); its plane distance is -|z0| (Eq. 3, R2)."""
+    cam = S.make_camera([0.0, 0.0, camz], [0.0, 0.0, 0.0], 64, 64, 64.0)
+    g = gaussians([[0, 0, 0]], [[1, 1, 0.01]], opac=[0.9])
+    p = oracle.project(g, cam, full_mask(64, 64), dtype=np.float64)
+    n_world = cam.R.astype(float).T @ p["ncam"][0]
+    np.testing.assert_allclose(n_world, [0, 0, expect], atol=1e-12)
+    assert math.isclose(p["dist"][0], -10.0, rel_tol=1e-12)
+
+
+def test_normal_is_min_scale_axis():
+    """R4: n is the column of R_g for the smallest scale (ties -> lowest index)."""
+    rng = np.random.default_rng(7)
+    q = rng.normal(size=4)
+    w, x, y, z = q / np.linalg.norm(q)
+    Rg = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                   [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                   [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    for k, sc in ((0, [0.01, 0.2, 0.3]), (1, [0.2, 0.01, 0.3]), (2, [0.2, 0.3, 0.01]), (0, [0.1, 0.1, 0.1])):
+        g = gaussians([[0.1, 0.2, 5.0]], [sc], quats=[q], opac=[0.9])
+        p = oracle.project(g, cam_identity(), full_mask(64, 64), dtype=np.float64)
+        n = p["ncam"][0]
+        col = Rg[:, k]
+        col = -col if col @ np.array([0.1, 0.2, 5.0]) > 0 else col
+        np.testing.assert_allclose(n, col, atol=1e-12)
+        assert (int(p["flags"][0]) >> 9) & 3 == k
+
+
+# ---------------------------------------------------------------- SH basis
+def test_sh_basis_matches_scipy():
+    """P:78 'multi-order spherical harmonics' (R12): the oracle's 16 real basis functions
+    equal sqrt2*Im(Y_l^|m|) (m<0), Y_l^0, sqrt2*Re(Y_l^m) (m>0) of scipy's complex
+    (Condon-Shortley) spherical harmonics."""
+    from scipy.special import sph_harm_y
+    rng = np.random.default_rng(11)
+    for _ in range(50):
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        th, ph = math.acos(d[2]), math.atan2(d[1], d[0])
+        ref = []
+        for l in range(4):
+            for m in range(-l, l + 1):
+                Y = complex(sph_harm_y(l, abs(m), th, ph))
+                ref.append(Y.real if m == 0 else (math.sqrt(2) * (Y.imag if m < 0 else Y.real)))
+        np.testing.assert_allclose(oracle.sh_basis(*d), ref, atol=1e-12)
+
+
+def test_sh_degree0_colour():
+    """Degree 0: colour = C0 sh0 + 0.5 (R12); C0 = Y_0^0 = 1/(2 sqrt(pi))."""
+    assert math.isclose(SH_C0, 0.5 / math.sqrt(math.pi), rel_tol=1e-15)
+    sh = np.array([[0.3], [-0.4], [2.0]])
+    g = gaussians([[0, 0, 4.0]], [[0.1, 0.1, 0.1]], opac=[0.9], sh=sh)
+    p = oracle.project(g, cam_identity(), full_mask(64, 64), dtype=np.float64)
+    np.testing.assert_allclose(p["rgb"][0], np.maximum(0, SH_C0 * sh[:, 0] + 0.5), rtol=1e-14)
+
+
+# ---------------------------------------------------------- compositing
+def test_two_half_alphas():
+    """S:294 worked example (Eq. 1 with T_i = prod_{j<i}(1-alpha_j), R1):
+    two alpha=0.5 -> C = 0.5 c1 + 0.25 c2 + 0.25 bg, T = 0.25."""
+    ex = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))["two_half_alphas"]
+    cam = cam_identity(cx=32.5, cy=32.5)
+    g = gaussians([[0, 0, 3.0], [0, 0, 2.0]], [[0.3] * 3] * 2, opac=[0.5, 0.5],
+                  rgb=[ex["c2"], ex["c1"]])  # id 1 is nearer -> composited first
+    r = oracle.render(g, cam, full_mask(64, 64), one_pixel(64, 32, 32), bg=ex["bg"], dtype=np.float64)
+    np.testing.assert_allclose(r["C"][0], ex["C"], rtol=1e-12)
+    assert math.isclose(r["T"][0], ex["T"], rel_tol=1e-12)
+    assert r["g"][0] == 2 and r["last"][0] == 0
+
+
+@pytest.mark.parametrize("alpha,K", [(0.6, 12), (0.3, 40), (0.6, 5), (0.99, 4)])
+def test_stacked_identical_alphas(alpha, K):
+    """R6 (termination 1e-4, crossing Gaussian not blended): K stacked alpha gives
+    g = min(K, max{k: (1-alpha)^k >= 1e-4}), T = (1-alpha)^g, C = c(1-T) + T bg."""
+    cam = cam_identity(cx=32.5, cy=32.5)
+    c, bg = np.array([0.7, 0.2, 0.9]), np.array([0.1, 0.5, 0.3])
+    g = gaussians([[0, 0, 2.0 + 0.1 * k] for k in range(K)], [[0.3] * 3] * K, opac=[alpha] * K,
+                  rgb=[c] * K)
+    r = oracle.render(g, cam, full_mask(64, 64), one_pixel(64, 32, 32), bg=bg, dtype=np.float64)
+    gk = 0
+    while gk < K and (1 - alpha) ** (gk + 1) >= 1e-4:
+        gk += 1
+    T = (1 - alpha) ** gk
+    assert r["g"][0] == gk
+    assert math.isclose(r["T"][0], T, rel_tol=1e-12)
+    np.testing.assert_allclose(r["C"][0], c * (1 - T) + T * bg, rtol=1e-12)
+
+
+def test_empty_scene_and_behind_camera():
+    """no primitives -> C = bg, g = 0, depth sentinel 0 (R3); Gaussians behind the
+    near plane are culled (R9)."""
+    bg = [0.25, 0.5, 0.75]
+    m = full_mask(16, 16)
+    cam = cam_identity(W=16, H=16, fx=16.0)
+    for g in (gaussians(np.zeros((0, 3)), np.zeros((0, 3))),
+              gaussians([[0, 0, -2.0], [0, 0, 0.001]], [[0.5] * 3] * 2, opac=[0.9, 0.9])):
+        r = oracle.render(g, cam, m, all_pixels(m), bg=bg, dtype=np.float64)
+        assert (r["g"] == 0).all() and (r["last"] == -1).all()
+        np.testing.assert_array_equal(r["C"], np.tile(bg, (256, 1)))
+        assert (r["Dep"] == 0).all() and (r["T"] == 1).all()
+
+
+def test_weights_sum_to_one_minus_T():
+    """sum_i alpha_i T_i + T_final = 1.  With colour == 1 and bg = 0, C = sum w_i,
+    so C + T = 1 at every pixel of a random scene."""
+    sc = S.config1(n=300, sh_degree=0)
+    g = sc.gaussians
+    g.sh[:] = np.float32(0.5 / SH_C0)
+    g64 = gaussians(g.mean.T, g.scale.T, g.rot.T, g.opacity, deg=0,
+                    sh=np.full((3, g.n), 0.5 / SH_C0), dtype=np.float64)
+    r = oracle.render(g64, sc.camera, sc.mask, all_pixels(sc.mask), dtype=np.float64)
+    assert (r["g"] > 0).mean() > 0.5
+    np.testing.assert_allclose(r["C"] + r["T"][:, None], 1.0, atol=1e-12)
+    np.testing.assert_allclose(r["A"], 1 - r["T"], atol=0)
+
+
+def test_unbiased_depth_fronto_parallel():
+    """Eq. 4: fronto-parallel flattened Gaussians at z0 give D_unbiased = z0
+    exactly at every covered pixel, independent of alpha."""
+    z0 = 5.0
+    rng = np.random.default_rng(5)
+    n = 6
+    means = np.c_[rng.uniform(-0.8, 0.8, n), rng.uniform(-0.8, 0.8, n), np.full(n, z0)]
+    g = gaussians(means, [[0.4, 0.3, 0.001]] * n, opac=rng.uniform(0.1, 0.95, n), rgb=[[0.5] * 3] * n)
+    m = full_mask(32, 32)
+    r = oracle.render(g, cam_identity(W=32, H=32, fx=32.0), m, all_pixels(m), dtype=np.float64)
+    cov = r["g"] > 0
+    assert cov.sum() > 200
+    np.testing.assert_allclose(r["Dep"][cov], z0, rtol=1e-12)
+
+
+def test_unbiased_depth_45deg_plane():
+    """Eq. 4 vs the analytic ray-plane intersection: a plane tilted 45 deg about x
+    through (0,0,5) gives depth z = (n.mu)/(n.r), r = ((i+.5-cx)/fx, (j+.5-cy)/fy, 1)."""
+    ang = math.radians(45)
+    q = quat_axis_angle([1, 0, 0], ang)
+    rng = np.random.default_rng(6)
+    n = 5
+    nrm = np.array([0.0, -math.sin(ang), math.cos(ang)])
+    t1 = np.array([1.0, 0, 0])
+    t2 = np.cross(nrm, t1)
+    means = np.array([0, 0, 5.0]) + rng.uniform(-0.6, 0.6, (n, 1)) * t1 + rng.uniform(-0.6, 0.6, (n, 1)) * t2
+    g = gaussians(means, [[0.6, 0.6, 0.001]] * n, quats=[q] * n, opac=rng.uniform(0.2, 0.9, n))
+    W = H = 32
+    cam = cam_identity(W=W, H=H, fx=32.0)
+    m = full_mask(H, W)
+    pix = all_pixels(m)
+    r = oracle.render(g, cam, m, pix, dtype=np.float64)
+    cov = r["g"] > 0
+    i, j = pix % W, pix // W
+    ray = np.stack([(i + 0.5 - cam.cx) / cam.fx, (j + 0.5 - cam.cy) / cam.fy, np.ones_like(i, float)], 1)
+    expect = (nrm @ np.array([0, 0, 5.0])) / (ray @ nrm)
+    assert cov.sum() > 100
+    np.testing.assert_allclose(r["Dep"][cov], expect[cov], rtol=1e-10)
+
+
+def test_permutation_invariance():
+    """rendering is invariant under permutation of the input list (depth sort, id tie-break)."""
+    sc = S.config1(n=400)
+    perm = np.random.default_rng(3).permutation(400)
+    g = sc.gaussians
+    gp = S.Gaussians(g.mean[:, perm], g.scale[:, perm], g.rot[:, perm], g.opacity[perm], g.sh[:, perm], 3)
+    pix = all_pixels(sc.mask)
+    r1 = oracle.render(g, sc.camera, sc.mask, pix)
+    r2 = oracle.render(gp, sc.camera, sc.mask, pix)
+    for k in ("C", "N", "D", "A", "Dep", "T", "g"):
+        np.testing.assert_array_equal(r1[k], r2[k])
+    has = r1["last"] >= 0
+    np.testing.assert_array_equal(perm[r2["last"][has]], r1["last"][has])
+
+
+# --------------------------------------------------- tiles, keys, ranges
+def test_tilemask_matches_numpy():
+    """O1 (R14) vs numpy reshape-sum + cumsum, with a ragged 16-px tail."""
+    rng = np.random.default_rng(2)
+    H, W = 37, 53
+    mask = (rng.uniform(size=(H, W)) < 0.1).astype(np.uint8)
+    cnt, sat = oracle.tilemask(mask)
+    pad = np.zeros((48, 64), np.uint8)
+    pad[:H, :W] = mask
+    ref = pad.reshape(3, 16, 4, 16).sum(axis=(1, 3))
+    np.testing.assert_array_equal(cnt, ref)
+    act = (ref > 0).astype(np.int64)
+    sref = np.zeros((4, 5), np.int64)
+    sref[1:, 1:] = act.cumsum(0).cumsum(1)
+    np.testing.assert_array_equal(sat, sref)
+
+
+def _brute_keys(p, mask):
+    H, W = mask.shape
+    TX = (W + 15) // 16
+    act = oracle.tilemask(mask)[0].reshape(-1) > 0
+    tl, db, ids, touched = [], [], [], np.zeros(len(p["depth"]), np.int64)
+    bits = p["depth"].astype(np.float32).view(np.uint32)
+    for i in np.flatnonzero((p["flags"] & 15) == 15):
+        tx0, ty0, tx1, ty1 = p["rect"][i]
+        tys, txs = np.meshgrid(np.arange(ty0, ty1 + 1), np.arange(tx0, tx1 + 1), indexing="ij")
+        t = (tys * TX + txs).reshape(-1)
+        t = t[act[t]]
+        touched[i] = len(t)
+        tl.append(t)
+        db.append(np.full(len(t), bits[i]))
+        ids.append(np.full(len(t), i))
+    tl, db, ids = (np.concatenate(a) if a else np.zeros(0, np.int64) for a in (tl, db, ids))
+    order = np.lexsort((ids, db, tl))
+    return tl[order], ids[order], touched
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_keys_sort_ranges_vs_lexsort(cfg):
+    """O3 (P:78 'projected onto different image tiles ... sorted'; R11): the oracle's sorted
+    (tile, depth bits, id) list equals an independent rect x active-tile enumeration ordered by
+    numpy.lexsort; ranges partition it; tiles_touched counts active tiles (R14)."""
+    sc = S.config1() if cfg == 1 else S.config2(n=20000)
+    p = oracle.project(sc.gaussians, sc.camera, sc.mask)
+    tl, vl, rg = oracle.keys(p, sc.mask)
+    btl, bids, touched = _brute_keys(p, sc.mask)
+    np.testing.assert_array_equal(tl, btl)
+    np.testing.assert_array_equal(vl, bids)
+    np.testing.assert_array_equal(p["tiles"].astype(np.int64), touched)
+    T = rg.shape[0]
+    lo = np.searchsorted(tl, np.arange(T), "left")
+    hi = np.searchsorted(tl, np.arange(T), "right")
+    empty = lo == hi
+    np.testing.assert_array_equal(rg[~empty, 0], lo[~empty])
+    np.testing.assert_array_equal(rg[~empty, 1], hi[~empty])
+    assert (rg[empty] == 0).all()
+    assert int((rg[:, 1] - rg[:, 0]).sum()) == len(tl)
+
+
+def test_lnup_is_upper_bound():
+    """R8: lnup(y) >= ln(y) on [1, 256) (dense float32 grid), slack < 0.01 + 1e-6 y."""
+    ys = np.unique(np.concatenate([
+        np.linspace(1.0, 255.999, 40001, dtype=np.float32),
+        np.float32(2.0) ** np.arange(0, 8, dtype=np.float32),
+        np.nextafter(np.float32(2.0) ** np.arange(1, 9, dtype=np.float32), np.float32(0)),
+    ]))
+    vals = np.array([oracle.lnup_f32(y) for y in ys])
+    lg = np.log(ys.astype(np.float64))
+    assert (vals >= lg).all()
+    assert (vals - lg).max() < 0.01
+
+
+@pytest.mark.parametrize("opac", [0.99, 0.5, 0.02])
+def test_tiling_is_exact_certificate(opac):
+    """R8: no pixel outside a Gaussian's tile rect can see alpha >= 1/255 (so the tile lists
+    are pure acceleration of the brute-force definition), incl. o = 0.99 where a 3-sigma
+    bound would fail."""
+    sc = S.config1(n=300)
+    sc.gaussians.opacity[:] = np.float32(opac)
+    pix = all_pixels(np.ones_like(sc.mask))
+    r = oracle.render(sc.gaussians, sc.camera, np.ones_like(sc.mask), pix, certify=True)
+    assert r["cert_bad"] == 0
+
+
+# ------------------------------------------------------------- gradients
+def _loss(g, cam, mask, pix, up, bg):
+    r = oracle.render(g, cam, mask, pix, bg=bg, dtype=np.float64)
+    out = np.concatenate([r["C"], r["N"], r["D"][:, None], r["A"][:, None], r["Dep"][:, None]], 1)
+    state = (r["g"].copy(), r["last"].copy(), r["id_sum"].copy(), r["n_clamped"].copy())
+    return float((out * up).sum()), state
+
+
+def _fd_scene(seed, n, deg=3):
+    rng = np.random.default_rng(seed)
+    means = np.c_[rng.uniform(-0.5, 0.5, n), rng.uniform(-0.5, 0.5, n), rng.uniform(3.0, 5.0, n)]
+    scales = np.exp(rng.uniform(np.log(0.08), np.log(0.4), (n, 3)))
+    scales[np.arange(n), rng.integers(0, 3, n)] *= 0.1
+    quats = rng.normal(size=(n, 4))
+    opac = rng.uniform(0.2, 0.9, n)
+    sh = rng.normal(0, 0.3, ((deg + 1) ** 2 * 3, n))
+    sh[0:3] += 1.0
+    return gaussians(means, scales, quats, opac, deg=deg, sh=sh, dtype=np.float64)
+
+
+@pytest.mark.parametrize("seed,n", [(0, 1), (1, 3), (2, 5), (3, 8)])
+def test_gradients_match_finite_differences(seed, n):
+    """P:82 differentiable rendering; every parameter gradient of the double
+    oracle matches central finite differences (h=1e-6) of the double forward, where the
+    contributor sets, clamp states and flags are identical at +-h (else skipped)."""
+    g = _fd_scene(seed, n)
+    W = H = 24
+    cam = cam_identity(W=W, H=H, fx=24.0)
+    mask = full_mask(H, W)
+    mask[::5, ::3] = 0
+    pix = all_pixels(mask)
+    rng = np.random.default_rng(100 + seed)
+    up = rng.normal(size=(len(pix), 9))
+    bg = np.array([0.2, 0.1, 0.3])
+    r = oracle.render(g, cam, mask, pix, bg=bg, dtype=np.float64, upstream=up)
+    grads = r["grads"]
+    assert (r["near"] == 0).all()
+    fields = [("mean", 0, 3), ("scale", 3, 3), ("rot", 6, 4), ("opacity", 10, 1), ("sh", 11, 48)]
+    checked = 0
+    worst = 0.0
+    base_flags = oracle.project(g, cam, mask, dtype=np.float64)["flags"]
+    for name, row0, rows in fields:
+        arr = getattr(g, name)
+        for k in range(rows):
+            for i in range(n):
+                idx = (k, i) if arr.ndim == 2 else (i,)
+                x0 = arr[idx]
+                h = 1e-6 * max(1.0, abs(x0))
+                arr[idx] = x0 + h
+                lp, sp = _loss(g, cam, mask, pix, up, bg)
+                fp = oracle.project(g, cam, mask, dtype=np.float64)["flags"]
+                arr[idx] = x0 - h
+                lm, sm = _loss(g, cam, mask, pix, up, bg)
+                fm = oracle.project(g, cam, mask, dtype=np.float64)["flags"]
+                arr[idx] = x0
+                same = all(np.array_equal(a, b) for a, b in zip(sp, sm))
+                same &= np.array_equal(fp & ~np.uint32(8), base_flags & ~np.uint32(8))
+                same &= np.array_equal(fm & ~np.uint32(8), base_flags & ~np.uint32(8))
+                if not same:
+                    continue
+                fd = (lp - lm) / (2 * h)
+                an = grads[row0 + k, i]
+                err = abs(fd - an) / max(abs(fd), 1e-3)
+                worst = max(worst, err)
+                assert err < 2e-5, (name, k, i, fd, an)
+                checked += 1
+    assert checked >= 0.8 * n * 59
+    assert np.abs(grads[11 + 16 * 3:]).sum() == 0 if g.sh_degree < 3 else True
+
+
+def test_single_gaussian_dC_drgb_closed_form():
+    """single primitive, gradient on C only -> dL/dc = alpha (T = 1), so
+    dL/dsh_0c = C0 * alpha * gC_c."""
+    cam = cam_identity(cx=32.5, cy=32.5)
+    g = gaussians([[0, 0, 4.0]], [[0.2, 0.2, 0.2]], opac=[0.6], rgb=[[0.4, 0.5, 0.6]], dtype=np.float64)
+    up = np.zeros((1, 9))
+    up[0, :3] = [1.0, -2.0, 0.5]
+    r = oracle.render(g, cam, full_mask(64, 64), one_pixel(64, 32, 32), dtype=np.float64, upstream=up)
+    np.testing.assert_allclose(r["grads"][11:14, 0], SH_C0 * 0.6 * up[0, :3], rtol=1e-12)
+
+
+def test_zero_upstream_zero_grads():
+    """zero upstream gradient -> all parameter gradients zero."""
+    sc = S.config1(n=200)
+    pix = all_pixels(sc.mask)
+    r = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=np.zeros((len(pix), 9)))
+    assert np.abs(r["grads"]).max() == 0.0
