@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the PG-SAG masked tile rasterizer (forward + backward) on B200.
+
+One "step" = the whole hot path (A0-A8: preprocess, bin/sort, forward
+compositor, backward compositor, preprocess backward) for one full-resolution
+view of the rank's sub-region (BASELINE.json configs[3], "C4": visibility-
+grouped sub-regions of 1.5M Gaussians with 40 oblique 5472x3648 views, one
+sub-region per GPU; weak scaling, no collective on the data path).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c4|c3|c2|c5]
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "masked Mpix/s fwd+bwd and Gaussian-pixel blends/s at 1/2/4/8 B200; % FP32/HBM roofline"
+UNIT = "Mpix/s"
+
+# algorithmic work per unit (DESIGN.md §5 / SURVEY §8(d))
+FLOP_EVAL = 12      # per evaluated (pixel, Gaussian) pair: dx, dy, quadratic form, o*rho
+FLOP_BLEND_FWD = 17  # per blended pair in A6: 1-a, T(1-a), aT, 7 channel FMAs (x2)
+FLOP_BLEND_BWD = 79  # per blended pair in A7
+BYTES_A1 = {0: 56 + 76, 1: 56 + 36 + 76, 2: 56 + 96 + 76, 3: 56 + 180 + 76}  # params read + 76 B written
+SM_COUNT = 148
+FP32_LANES = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--views", type=int, default=40)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="per-kernel table on stderr")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- workload
+def load_workload(cfg, rank, n_views, device):
+    """Returns (numpy Gaussians, [cameras], [mask tensors on device], name)."""
+    import torch
+    from synth import scenes as S
+    if cfg == "c4":
+        sub = S.subregion(rank % 8, n_views=n_views)
+        cams = sub["cameras"]
+        masks = [torch.from_numpy(S.ray_cast_mask(c, sub["boxes"], device=device)).to(device) for c in cams]
+        return sub["gaussians"], cams, masks, (f"C4 sub-region {rank % 8}: 1.5M Gaussians, {len(cams)} oblique "
+                                               "5472x3648 views, building mask")
+    sc = {"c2": S.config2, "c3": S.config3, "c5": S.config5}[cfg](device=device)
+    mask = torch.from_numpy(sc.mask).to(device)
+    return sc.gaussians, [sc.camera], [mask], f"{cfg.upper()}: {sc.gaussians.n} Gaussians, " \
+                                                 f"{sc.camera.width}x{sc.camera.height}, building mask"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# -------------------------------------------------------------- oracle arm
+def oracle_sample(g, cam, mask_np, n_pix, seed=0):
+    """Time the oracle (single thread, as it stands) fwd+bwd on n_pix sampled masked pixels."""
+    import oracle
+    from synth import scenes as S
+    pix = S.sample_pixels(mask_np, n_pix, seed=seed)
+    up = np.random.default_rng(seed).normal(size=(len(pix), 9))
+    t0 = time.perf_counter()
+    oracle.render(g, cam, mask_np, pix, upstream=up)
+    return len(pix), time.perf_counter() - t0
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (the only reference this paper-tier run has), rank 0 only."""
+    if rank != 0:
+        return
+    import torch
+    from synth import scenes as S
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    g, cams, masks, name = load_workload(args.config, 0, min(args.views, args.steps + args.warmup), dev)
+    mask_np = [m.cpu().numpy() for m in masks]
+    n_pix = 256
+    for s in range(args.warmup):
+        oracle_sample(g, cams[s % len(cams)], mask_np[s % len(cams)], 16, seed=s)
+    tot_pix, tot_t = 0, 0.0
+    for s in range(args.steps):
+        v = (args.warmup + s) % len(cams)
+        p, t = oracle_sample(g, cams[v], mask_np[v], n_pix, seed=100 + s)
+        tot_pix += p
+        tot_t += t
+    val = tot_pix / 1e6 / tot_t
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (CPU oracle)",
+            "data": "synthetic", "config": {"workload": name, "sample": f"{n_pix} sampled masked pixels per step"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{n_pix} sampled masked pixels per step, fwd+bwd, full-scene projection"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    from paper_2501_01677_b200 import _lib as L
+    from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+
+    n_views = min(args.views, args.steps + args.warmup) if args.config == "c4" else 1
+    g_np, cams, masks, wname = load_workload(args.config, rank, n_views, dev)
+    g = GaussianTensors.from_numpy(g_np, dev)
+    H, W = masks[0].shape
+    ccam = [camera_from(c) for c in cams]
+    r = Rasterizer(g.n, W, H, g.sh_degree, capacity=24 * g.n, device=dev, counters=True)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1677 + rank)
+    up = {"dC": torch.randn(3, H, W, device=dev, generator=gen), "dN": torch.randn(3, H, W, device=dev, generator=gen),
+          "dD": torch.randn(H, W, device=dev, generator=gen), "dA": torch.randn(H, W, device=dev, generator=gen),
+          "dDep": torch.randn(H, W, device=dev, generator=gen)}
+    npix = [int(m.count_nonzero().item()) for m in masks]
+
+    def step(v):
+        r.forward(g, ccam[v], masks[v])
+        r.backward(**up)
+
+    # counting pass (untimed): E, B, V and M per view
+    per_view = {}
+    for v in range(len(cams)):
+        r.counters.zero_()
+        step(v)
+        torch.cuda.synchronize()
+        st = r.stats()
+        per_view[v] = st
+    # tile imbalance of view 0: max / mean blends per active tile
+    r.forward(g, ccam[0], masks[0])
+    gt = torch.nn.functional.pad(r.img_g.clamp(min=0).float() * (masks[0] > 0),
+                                 (0, (16 - W % 16) % 16, 0, (16 - H % 16) % 16))
+    tb = gt.reshape(gt.shape[0] // 16, 16, gt.shape[1] // 16, 16).sum(dim=(1, 3))
+    act = tb[tb > 0]
+    imbalance = float(act.max() / act.mean()) if act.numel() else 0.0
+    r._img.counters = None  # timed steps run the non-counting kernels
+
+    views = [(args.warmup + s) % len(cams) for s in range(args.steps)]
+    for s in range(args.warmup):
+        step(s % len(cams))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    L.timing_enable(True)
+    L.timing_collect()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record()
+        for v in views:
+            step(v)
+        ev1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    L.timing_enable(False)
+    ktimes = L.timing_collect()
+    ms = ev0.elapsed_time(ev1)
+    pix = float(sum(npix[v] for v in views))
+    blends = float(sum(per_view[v]["blended"] for v in views))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        agg = torch.tensor([pix, blends], device=dev, dtype=torch.float64)
+        dist.all_reduce(agg)
+        pix_all, blends_all = float(agg[0]), float(agg[1])
+        # per-rank statistics record all-gathered over NVLink (off the timed region)
+        rec = torch.tensor([rank, ms, pix, blends, imbalance] + [0.0] * 11, device=dev, dtype=torch.float32)
+        recs = [torch.zeros_like(rec) for _ in range(world)]
+        dist.all_gather(recs, rec)
+    else:
+        ms_max, pix_all, blends_all = ms, pix, blends
+    value = pix_all / 1e6 / (ms_max / 1e3)
+
+    # ---------------------------------------------------- roofline (dominant kernel)
+    peaks = measured_peaks()
+    ksteps = {k: (v[0] / args.steps, v[1] // max(args.steps, 1)) for k, v in ktimes.items()}
+    launches = int(sum(v[1] for v in ktimes.values()))
+    dom = max(ktimes.items(), key=lambda kv: kv[1][0])[0] if ktimes else None
+    roof = None
+    if dom:
+        tot_ms, nl = ktimes[dom]
+        avg_s = tot_ms / 1e3 / max(nl, 1)
+        E = sum(per_view[v]["evaluated"] for v in views) / len(views)
+        B = sum(per_view[v]["blended"] for v in views) / len(views)
+        V = sum(per_view[v]["bwd_visited"] for v in views) / len(views)
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        fp32_peak = SM_COUNT * FP32_LANES * 2 * sm_mhz * 1e6 / 1e12
+        if dom.startswith("A6"):
+            roof = {"kernel": dom, "bound": "alu", "achieved": (FLOP_EVAL * E + FLOP_BLEND_FWD * B) / avg_s / 1e12,
+                    "peak": fp32_peak, "unit": "TFLOP/s"}
+        elif dom.startswith("A7"):
+            roof = {"kernel": dom, "bound": "alu", "achieved": (FLOP_EVAL * V + FLOP_BLEND_BWD * B) / avg_s / 1e12,
+                    "peak": fp32_peak, "unit": "TFLOP/s"}
+        elif dom.startswith("A1"):
+            roof = {"kernel": dom, "bound": "hbm", "achieved": BYTES_A1[g.sh_degree] * g.n / avg_s / 1e9,
+                    "peak": float(peaks.get("hbm_gbs", 6551.4)), "unit": "GB/s"}
+        else:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": float(peaks.get("hbm_gbs", 6551.4)),
+                    "unit": "GB/s"}
+        if roof["achieved"] is not None:
+            roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["peak_source"] = ("148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"
+                               if roof["bound"] == "alu" else "MEASURED_PEAKS.json hbm_gbs")
+        roof["traffic"] = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            if tr.get("config") == args.config and dom in tr.get("bytes_per_launch", {}):
+                roof["traffic"] = tr["bytes_per_launch"][dom]
+        except Exception:
+            pass
+        roof["share_of_step"] = tot_ms / max(ms, 1e-9)
+
+    # ------------------------------------------------------------- e2e (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda t: t.detach().cpu().pin_memory()
+        hg = {k: pin(getattr(g, k)) for k in ("mean", "scale", "rot", "opacity", "sh")}
+        hm = [pin(m) for m in masks]
+        hup = {k: pin(v) for k, v in up.items()}
+        hgrad = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for k, t in
+                 (("dmean", r.dmean), ("dscale", r.dscale), ("drot", r.drot), ("dopacity", r.dopacity),
+                  ("dsh", r.dsh))}
+        dg = GaussianTensors(*(torch.empty_like(getattr(g, k)) for k in ("mean", "scale", "rot", "opacity", "sh")),
+                             g.sh_degree)
+        dmask = torch.empty_like(masks[0])
+        dup = {k: torch.empty_like(v) for k, v in up.items()}
+        h2d = sum(t.numel() * t.element_size() for t in hg.values()) + hm[0].numel() + \
+            sum(t.numel() * t.element_size() for t in hup.values())
+        d2h = sum(t.numel() * t.element_size() for t in hgrad.values())
+        ke = min(args.steps, 5)
+
+        def e2e_step(v):
+            for k in hg:
+                getattr(dg, k).copy_(hg[k], non_blocking=True)
+            dmask.copy_(hm[v], non_blocking=True)
+            for k in hup:
+                dup[k].copy_(hup[k], non_blocking=True)
+            r.forward(dg, ccam[v], dmask)
+            gr = r.backward(**dup)
+            for k in hgrad:
+                hgrad[k].copy_(gr[k], non_blocking=True)
+        e2e_step(0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in range(ke):
+            e2e_step(views[s])
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        epix = float(sum(npix[views[s]] for s in range(ke)))
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+            tp = torch.tensor([epix], device=dev, dtype=torch.float64)
+            dist.all_reduce(tp)
+            epix = float(tp.item())
+        e2e = {"value": epix / 1e6 / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": ke,
+               "note": "pinned host Gaussians+mask+upstream -> device, fwd+bwd, gradients -> host"}
+
+    # ------------------------------------------------------------- CPU oracle baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v0 = views[0]
+        n_s = 1024 if args.config in ("c4", "c3", "c5") else 4096
+        p, t = oracle_sample(g_np, cams[v0], masks[v0].cpu().numpy(), n_s)
+        cpu = {"value": p / 1e6 / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{p} sampled masked pixels of view {v0}, fwd+bwd, single thread, incl. full-scene "
+                         f"projection ({t:.1f} s)"}
+
+    if rank == 0:
+        st0 = per_view[views[0]]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wname, "views_per_step": 1, "timed_views": views,
+                       "l2": "inputs larger than L2 (Gaussians 1.5M x 236 B = 354 MB per rank, new view each step)",
+                       "sh_degree": g.sh_degree, "n_gaussians": g.n, "image": [W, H]},
+            "blends_per_s": blends_all / (ms_max / 1e3),
+            "masked_pixels_per_step": pix_all / args.steps,
+            "tile_imbalance_max_over_mean": imbalance,
+            "M_per_view": st0["M"], "evaluated_per_view": st0["evaluated"], "blended_per_view": st0["blended"],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "kernels_ms_per_step": {k: round(v[0], 4) for k, v in sorted(ksteps.items())},
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+        if args.profile:
+            tot = sum(v[0] for v in ksteps.values())
+            for k, v in sorted(ksteps.items(), key=lambda kv: -kv[1][0]):
+                sys.stderr.write(f"{k:24s} {v[0]:9.3f} ms/step  {100 * v[0] / max(tot, 1e-9):5.1f}%  x{v[1]}\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * pgsag.h — C ABI of libpgsag.so, the B200 (sm_100a) masked tile rasterizer of
+ * PG-SAG (arXiv 2501.01677), forward and backward.
+ *
+ * Citations: P:n = PAPER.md line n (/root/reference, §3.1 "3DGS and Unbiased
+ * Depth Rendering", Eq. 1-4, lines 76-96; §4.3 masked, pixel-parallel rendering,
+ * line 163; masked pixels only, line 243).  Rk = reading k of DESIGN.md §3.
+ *
+ * General rules (all calls):
+ *   - Every pointer is a DEVICE pointer unless marked (host).  The caller owns and
+ *     allocates every buffer; the library never allocates device memory.  Scratch
+ *     comes from the caller's workspace `ws` (>= pgsag_workspace_size bytes,
+ *     256-byte aligned).
+ *   - All work is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream) in call order.  The only host synchronisation is the
+ *     read-back of M (the number of (tile, Gaussian) entries) in pgsag_bin_sort.
+ *   - Return value: PGSAG_OK (0) or a negative PGSAG_E* code; the message is in
+ *     pgsag_last_error() (thread-local).  No exception crosses the ABI.  On error
+ *     nothing is guaranteed about the output buffers.
+ *   - Calls with distinct workspaces and outputs may run concurrently on
+ *     different streams.
+ *   - Image planes are planar row-major [H][W] (channel planes [c][H][W]); pixel
+ *     (i, j) = column i, row j, centre (i + 0.5, j + 0.5) (R5).  Tiles are 16x16,
+ *     TX = ceil(W/16), TY = ceil(H/16), tile id = ty*TX + tx.
+ */
+#ifndef PGSAG_H
+#define PGSAG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGSAG_TILE 16
+
+enum {
+  PGSAG_OK = 0,
+  PGSAG_EINVAL = -1,    /* null pointer, n < 0, sh_degree > 3, width/height <= 0, misaligned buffer */
+  PGSAG_ECAPACITY = -2, /* bins->capacity < M; bins->n_dup holds M, nothing else written */
+  PGSAG_ECUDA = -3,     /* a CUDA launch/copy failed; message in pgsag_last_error() */
+  PGSAG_EWORKSPACE = -4 /* ws_bytes < pgsag_workspace_size(...) */
+};
+
+/* Per-Gaussian flag bits written by pgsag_preprocess (A1). */
+enum {
+  PGSAG_F_VISIBLE = 1u << 0,    /* camera z > znear (R9)                               */
+  PGSAG_F_DET_OK = 1u << 1,     /* det(cov2d + 0.3 I) > 0 (R10)                        */
+  PGSAG_F_OPAC_OK = 1u << 2,    /* opacity >= 1/255 (R6)                               */
+  PGSAG_F_RECT = 1u << 3,       /* conservative tile rect non-empty (R8)               */
+  PGSAG_F_CLAMP_X = 1u << 4,    /* x/z clamped to 1.3 half-FoV inside J (R9)           */
+  PGSAG_F_CLAMP_Y = 1u << 5,
+  PGSAG_F_RGB_CLAMP0 = 1u << 6, /* colour channel c clamped at 0: bit 6 + c (R12)      */
+  PGSAG_F_AXIS_SHIFT = 9,       /* bits 9-10: index of the minimum-scale axis (R4)     */
+  PGSAG_F_NFLIP = 1u << 11,     /* normal flipped to face the camera (R4)              */
+  PGSAG_F_LIVE = 15u            /* VISIBLE|DET_OK|OPAC_OK|RECT: Gaussian can emit keys */
+};
+
+/* Camera (host struct, by pointer).  x_cam = R (x_world - C) (P:88 R_c, P:92 T_C);
+ * pinhole u = fx x/z + cx, v = fy y/z + cy (P:96 K).  znear default 0.01 (R9). */
+typedef struct {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float R[9]; /* world -> camera rotation, row-major */
+  float C[3]; /* camera centre in world coordinates  */
+  float znear;
+} pgsag_camera;
+
+/* Gaussians (host struct holding device pointers), structure-of-arrays, float32.
+ * position, anisotropic scale, rotation, opacity, SH colour.  Values are
+ * ACTIVATED (R13): scale > 0 linear, opacity in (0,1).  rot = (w,x,y,z), any
+ * non-zero norm (normalised inside).  sh row (l*3 + c), l < (sh_degree+1)^2. */
+typedef struct {
+  int32_t n, sh_degree;      /* n >= 0, 0 <= sh_degree <= 3              */
+  const float *mean;         /* [3][n]                                    */
+  const float *scale;        /* [3][n]                                    */
+  const float *rot;          /* [4][n]                                    */
+  const float *opacity;      /* [n]                                       */
+  const float *sh;           /* [(sh_degree+1)^2 * 3][n]                  */
+} pgsag_gaussians;
+
+/* A1 output: projected Gaussians (caller-allocated, n entries each, 16-B aligned). */
+typedef struct {
+  float *mean2d;          /* [n][2]  (u, v) pixel coordinates                          */
+  float *conic_o;         /* [n][4]  (ca, cb, cc, o): power = -0.5(ca dx^2 + cc dy^2) - cb dx dy */
+  float *depth;           /* [n]     camera z (sort key, R11)                          */
+  int16_t *rect;          /* [n][4]  tile rect tx0, ty0, tx1, ty1 inclusive; empty = (0,0,-1,-1) */
+  uint32_t *tiles_touched;/* [n]     active tiles inside rect (0 unless LIVE)          */
+  float *rgb_d;           /* [n][4]  (r, g, b, d_i): SH colour (R12) and plane distance d_i (Eq. 3, R2) */
+  float *ncam;            /* [n][4]  (R_c n_i, 0): camera-frame normal (Eq. 2, R4)     */
+  uint32_t *flags;        /* [n]     PGSAG_F_* bits                                    */
+} pgsag_projected;
+
+/* A0 output: building-mask tile occupancy (R14). */
+typedef struct {
+  uint32_t *tile_cnt; /* [TY*TX]        number of mask pixels per tile                  */
+  int32_t *sat;       /* [(TY+1)*(TX+1)] summed-area table of active (cnt > 0) tiles     */
+  uint32_t *active;   /* [TY*TX]        active tile ids ascending; first *n_active valid  */
+  uint32_t *n_active; /* [1]            device scalar                                     */
+  uint32_t *active_bits; /* [TY*ceil(TX/32)] bitmap of active tiles, row-major, bit tx%32 */
+} pgsag_tilemask;
+
+/* A2-A5 output: per-tile sorted lists ("projected onto different image tiles ...
+ * sorted"; R11).  Entry k: (tile_keys[k], vals[k] = Gaussian id), ordered by
+ * (tile, depth bits, id).  ranges[2t], ranges[2t+1] = [start, end) of tile t
+ * (empty tiles [0, 0)). */
+typedef struct {
+  uint32_t *tile_keys; /* [capacity] */
+  uint32_t *vals;      /* [capacity] */
+  uint32_t *ranges;    /* [2*TY*TX]  */
+  int64_t capacity;    /* in: entries allocated            */
+  int64_t n_dup;       /* out (host field): M              */
+} pgsag_bins;
+
+/* A6 output (planar float32 [H][W] unless noted).  Only pixels with mask != 0 are
+ * written; others are left untouched (R14).  Eq. 1 colour C (+ T bg, R15), Eq. 2
+ * normal N, Eq. 3 distance D, alpha A = 1 - T, Eq. 4 unbiased depth Dep (0 = invalid,
+ * R3), final transmittance T, blended count g (P:169 g_i), last = index k into
+ * bins->vals of the last blended entry (-1 if none; used by the backward). */
+typedef struct {
+  float *C;     /* [3][H][W] */
+  float *N;     /* [3][H][W] */
+  float *D, *A, *Dep, *T;
+  int32_t *g, *last;
+  unsigned long long *counters; /* optional [4]: +E evaluated, +B blended (fwd), +E visited (bwd), 0 */
+} pgsag_image;
+
+/* Upstream gradients dL/d(C, N, D, A, Dep) in the pgsag_image layout; any may be NULL (= 0). */
+typedef struct {
+  const float *dC, *dN, *dD, *dA, *dDep;
+} pgsag_image_grad;
+
+/* A8 output, same layouts as pgsag_gaussians; OVERWRITTEN (not accumulated).  Rows of dsh
+ * beyond (sh_degree+1)^2*3 are not touched.  absgrad2d optional [n]: sum over pixels of
+ * |dL/du_p| + |dL/dv_p| (densification statistic).  Non-LIVE Gaussians get 0. */
+typedef struct {
+  float *dmean, *dscale, *drot, *dopacity, *dsh, *absgrad2d;
+} pgsag_gaussian_grad;
+
+/* Bytes of scratch needed by every call for n Gaussians, a width x height image and
+ * dup_capacity (tile, Gaussian) entries. */
+size_t pgsag_workspace_size(int32_t n, int32_t width, int32_t height, int64_t dup_capacity);
+
+/* A0 + A1.  A0: tile occupancy of the building mask `mask` (u8 [H][W], nonzero =
+ * building pixel, the paper's RBM).  A1: per Gaussian, EWA projection
+ * (P:78), culling, opacity-aware conservative tile rect (R8), active tiles touched,
+ * flattened normal n_i (R4), d_i (Eq. 3, R2), SH colour (R12).  Key-path
+ * arithmetic is IEEE float32 with no contraction (bit-exact with the oracle). */
+int pgsag_preprocess(const pgsag_gaussians *g, const pgsag_camera *cam, const uint8_t *mask,
+                     pgsag_tilemask *tm, pgsag_projected *out, void *ws, size_t ws_bytes, void *stream);
+
+/* A2-A5: stable sort of Gaussians by depth, exclusive scan of tiles_touched,
+ * duplication of (tile, id) entries for active tiles in each rect, stable radix sort
+ * by tile, tile ranges.  Host-synchronises once to read M into bins->n_dup; returns
+ * PGSAG_ECAPACITY if M > bins->capacity. */
+int pgsag_bin_sort(const pgsag_projected *p, const pgsag_tilemask *tm, const pgsag_camera *cam, int32_t n,
+                   pgsag_bins *bins, void *ws, size_t ws_bytes, void *stream);
+
+/* A6: per active tile, per masked pixel, front-to-back compositing over the tile's
+ * sorted list (Eq. 1-3; alpha = min(0.99, o exp(power)), skip alpha < 1/255,
+ * stop when T would drop below 1e-4 — the crossing entry is not blended, R6), then
+ * Eq. 4.  bg (host, 3 floats) enters C only via T bg (R15). */
+int pgsag_render_fwd(const pgsag_projected *p, const pgsag_bins *bins, const pgsag_tilemask *tm,
+                     const pgsag_camera *cam, const uint8_t *mask, const float bg[3], pgsag_image *out,
+                     void *ws, size_t ws_bytes, void *stream);
+
+/* A7 + A8: exact reverse-mode gradient of the A6 outputs w.r.t. the Gaussian
+ * parameters, decisions (sort, skip, termination, culls, clamps) frozen (R16, R17).
+ * fwd must be the pgsag_image A6 wrote for the same inputs. */
+int pgsag_render_bwd(const pgsag_gaussians *g, const pgsag_camera *cam, const pgsag_projected *p,
+                     const pgsag_bins *bins, const pgsag_tilemask *tm, const uint8_t *mask, const float bg[3],
+                     const pgsag_image *fwd, const pgsag_image_grad *dL, pgsag_gaussian_grad *out, void *ws,
+                     size_t ws_bytes, void *stream);
+
+/* Message for the last non-zero status on this thread ("" if none). */
+const char *pgsag_last_error(void);
+
+/* Library version string, e.g. "pgsag-b200 0.1 sm_100a". */
+const char *pgsag_version(void);
+
+/* Optional per-kernel timing (profiling aid; off by default, process-global).
+ * pgsag_timing_enable(1) makes every kernel launch of the library record a CUDA
+ * event pair on its own launch stream.  pgsag_timing_collect() synchronises on the
+ * recorded events, aggregates them per kernel name, clears the record list and
+ * returns the number K of distinct kernels; pgsag_timing_get(k, ...) (0 <= k < K)
+ * returns the kernel name (static storage), the summed milliseconds and the number
+ * of launches.  Returns PGSAG_EINVAL for k out of range. */
+void pgsag_timing_enable(int on);
+int pgsag_timing_collect(void);
+int pgsag_timing_get(int k, const char **name, double *ms, long long *launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PGSAG_H */

@@ -1,0 +1,164 @@
+"""ctypes binding of libpgsag.so (include/pgsag.h).  Argument marshalling only:
+every step of the rasterizer runs in the library's sm_100a kernels.  There is no
+CPU fallback: importing a function whose library is missing raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpgsag.so")
+
+PGSAG_OK, PGSAG_EINVAL, PGSAG_ECAPACITY, PGSAG_ECUDA, PGSAG_EWORKSPACE = 0, -1, -2, -3, -4
+F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT, F_LIVE = 1, 2, 4, 8, 15
+
+SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd",
+           "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable",
+           "pgsag_timing_collect", "pgsag_timing_get")
+
+_vp = C.c_void_p
+
+
+class Camera(C.Structure):
+    _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("width", C.c_int32), ("height", C.c_int32), ("R", C.c_float * 9), ("C", C.c_float * 3),
+                ("znear", C.c_float)]
+
+
+class Gaussians(C.Structure):
+    _fields_ = [("n", C.c_int32), ("sh_degree", C.c_int32), ("mean", _vp), ("scale", _vp), ("rot", _vp),
+                ("opacity", _vp), ("sh", _vp)]
+
+
+class Projected(C.Structure):
+    _fields_ = [("mean2d", _vp), ("conic_o", _vp), ("depth", _vp), ("rect", _vp), ("tiles_touched", _vp),
+                ("rgb_d", _vp), ("ncam", _vp), ("flags", _vp)]
+
+
+class TileMask(C.Structure):
+    _fields_ = [("tile_cnt", _vp), ("sat", _vp), ("active", _vp), ("n_active", _vp), ("active_bits", _vp)]
+
+
+class Bins(C.Structure):
+    _fields_ = [("tile_keys", _vp), ("vals", _vp), ("ranges", _vp), ("capacity", C.c_int64),
+                ("n_dup", C.c_int64)]
+
+
+class Image(C.Structure):
+    _fields_ = [("C", _vp), ("N", _vp), ("D", _vp), ("A", _vp), ("Dep", _vp), ("T", _vp), ("g", _vp),
+                ("last", _vp), ("counters", _vp)]
+
+
+class ImageGrad(C.Structure):
+    _fields_ = [("dC", _vp), ("dN", _vp), ("dD", _vp), ("dA", _vp), ("dDep", _vp)]
+
+
+class GaussianGrad(C.Structure):
+    _fields_ = [("dmean", _vp), ("dscale", _vp), ("drot", _vp), ("dopacity", _vp), ("dsh", _vp),
+                ("absgrad2d", _vp)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+class PgsagError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"pgsag error {code}: {msg}")
+        self.code = code
+
+
+def lib():
+    """Load libpgsag.so (fails loudly if it was not built: no fallback path exists)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = C.CDLL(LIB_PATH)
+            P = C.POINTER
+            L.pgsag_workspace_size.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int64]
+            L.pgsag_workspace_size.restype = C.c_size_t
+            L.pgsag_preprocess.argtypes = [P(Gaussians), P(Camera), _vp, P(TileMask), P(Projected), _vp,
+                                           C.c_size_t, _vp]
+            L.pgsag_bin_sort.argtypes = [P(Projected), P(TileMask), P(Camera), C.c_int32, P(Bins), _vp,
+                                         C.c_size_t, _vp]
+            L.pgsag_render_fwd.argtypes = [P(Projected), P(Bins), P(TileMask), P(Camera), _vp,
+                                           P(C.c_float * 3), P(Image), _vp, C.c_size_t, _vp]
+            L.pgsag_render_bwd.argtypes = [P(Gaussians), P(Camera), P(Projected), P(Bins), P(TileMask), _vp,
+                                           P(C.c_float * 3), P(Image), P(ImageGrad), P(GaussianGrad), _vp,
+                                           C.c_size_t, _vp]
+            for nm in ("pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd", "pgsag_render_bwd"):
+                getattr(L, nm).restype = C.c_int
+            L.pgsag_last_error.restype = C.c_char_p
+            L.pgsag_version.restype = C.c_char_p
+            L.pgsag_timing_enable.argtypes = [C.c_int]
+            L.pgsag_timing_enable.restype = None
+            L.pgsag_timing_collect.argtypes = []
+            L.pgsag_timing_collect.restype = C.c_int
+            L.pgsag_timing_get.argtypes = [C.c_int, P(C.c_char_p), P(C.c_double), P(C.c_longlong)]
+            L.pgsag_timing_get.restype = C.c_int
+            _lib = L
+    return _lib
+
+
+def timing_enable(on=True):
+    lib().pgsag_timing_enable(1 if on else 0)
+
+
+def timing_collect():
+    """{kernel name: (total ms, launches)} since the last collect (synchronises on the events)."""
+    L = lib()
+    k = L.pgsag_timing_collect()
+    out = {}
+    for i in range(k):
+        nm, ms, cnt = C.c_char_p(), C.c_double(), C.c_longlong()
+        check(L.pgsag_timing_get(i, C.byref(nm), C.byref(ms), C.byref(cnt)))
+        out[nm.value.decode()] = (ms.value, cnt.value)
+    return out
+
+
+def check(rc):
+    if rc != PGSAG_OK:
+        raise PgsagError(rc, lib().pgsag_last_error().decode())
+    return rc
+
+
+def ptr(t):
+    """Device (or host) address of a tensor / None."""
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def workspace_size(n, W, H, cap):
+    return int(lib().pgsag_workspace_size(int(n), int(W), int(H), int(cap)))
+
+
+def preprocess(g, cam, mask, tm, proj, ws, ws_bytes, stream):
+    return check(lib().pgsag_preprocess(C.byref(g), C.byref(cam), mask, C.byref(tm), C.byref(proj), ws,
+                                        ws_bytes, stream))
+
+
+def bin_sort(proj, tm, cam, n, bins, ws, ws_bytes, stream):
+    """Returns the status code (PGSAG_ECAPACITY is returned, not raised; bins.n_dup then holds M)."""
+    rc = lib().pgsag_bin_sort(C.byref(proj), C.byref(tm), C.byref(cam), int(n), C.byref(bins), ws, ws_bytes,
+                              stream)
+    if rc not in (PGSAG_OK, PGSAG_ECAPACITY):
+        check(rc)
+    return rc
+
+
+def render_fwd(proj, bins, tm, cam, mask, bg, img, ws, ws_bytes, stream):
+    return check(lib().pgsag_render_fwd(C.byref(proj), C.byref(bins), C.byref(tm), C.byref(cam), mask,
+                                        C.byref(bg), C.byref(img), ws, ws_bytes, stream))
+
+
+def render_bwd(g, cam, proj, bins, tm, mask, bg, img, dimg, grad, ws, ws_bytes, stream):
+    return check(lib().pgsag_render_bwd(C.byref(g), C.byref(cam), C.byref(proj), C.byref(bins), C.byref(tm),
+                                        mask, C.byref(bg), C.byref(img), C.byref(dimg), C.byref(grad), ws,
+                                        ws_bytes, stream))
+
+
+def version():
+    return lib().pgsag_version().decode()

@@ -1,0 +1,264 @@
+// C ABI of libpgsag.so (include/pgsag.h): argument validation, workspace
+// carving, stream-ordered launches, error reporting.  No exception or torch type
+// crosses this boundary; the library never allocates device memory.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "internal.cuh"
+
+#include <map>
+#include <mutex>
+#include <vector>
+
+using namespace pgsag;
+
+namespace {
+
+// ------------------------------------------------------------ kernel timing
+struct TimingRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<TimingRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+std::vector<std::pair<const char*, std::pair<double, long long>>> g_agg;
+
+cudaEvent_t take_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+}  // namespace
+
+namespace pgsag {
+KTimer::KTimer(const char* name, cudaStream_t s) : slot(-1), st(s) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (!g_timing) return;
+  TimingRec r{name, take_event(), take_event()};
+  cudaEventRecord(r.a, st);
+  g_recs.push_back(r);
+  slot = (int)g_recs.size() - 1;
+}
+KTimer::~KTimer() {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (slot < (int)g_recs.size()) cudaEventRecord(g_recs[slot].b, st);
+}
+}  // namespace pgsag
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(e));
+  g_err = buf;
+  return PGSAG_ECUDA;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int check_cam(const pgsag_camera* c) {
+  if (!c) return fail(PGSAG_EINVAL, "camera is NULL");
+  if (c->width <= 0 || c->height <= 0) return fail(PGSAG_EINVAL, "width/height must be > 0");
+  if (!(c->fx > 0.f) || !(c->fy > 0.f)) return fail(PGSAG_EINVAL, "fx/fy must be > 0");
+  if (c->width > (1 << 19) || c->height > (1 << 19)) return fail(PGSAG_EINVAL, "image too large");
+  return PGSAG_OK;
+}
+
+int check_proj(const pgsag_projected* p) {
+  if (!p || !p->mean2d || !p->conic_o || !p->depth || !p->rect || !p->tiles_touched || !p->rgb_d || !p->ncam ||
+      !p->flags)
+    return fail(PGSAG_EINVAL, "projected buffer is NULL");
+  if (!aligned(p->conic_o, 16) || !aligned(p->rgb_d, 16) || !aligned(p->ncam, 16) || !aligned(p->mean2d, 8) ||
+      !aligned(p->rect, 8))
+    return fail(PGSAG_EINVAL, "projected buffers must be 16-byte aligned (mean2d, rect: 8)");
+  return PGSAG_OK;
+}
+
+int check_tm(const pgsag_tilemask* tm) {
+  if (!tm || !tm->tile_cnt || !tm->sat || !tm->active || !tm->n_active || !tm->active_bits)
+    return fail(PGSAG_EINVAL, "tilemask buffer is NULL");
+  return PGSAG_OK;
+}
+
+int check_g(const pgsag_gaussians* g) {
+  if (!g) return fail(PGSAG_EINVAL, "gaussians is NULL");
+  if (g->n < 0) return fail(PGSAG_EINVAL, "n < 0");
+  if (g->sh_degree < 0 || g->sh_degree > 3) return fail(PGSAG_EINVAL, "sh_degree must be 0..3");
+  if (g->n > 0 && (!g->mean || !g->scale || !g->rot || !g->opacity || !g->sh))
+    return fail(PGSAG_EINVAL, "gaussian parameter is NULL");
+  return PGSAG_OK;
+}
+
+int check_ws(void* ws, size_t ws_bytes, size_t need) {
+  if (need && !ws) return fail(PGSAG_EINVAL, "workspace is NULL");
+  if (ws && !aligned(ws, 256)) return fail(PGSAG_EINVAL, "workspace must be 256-byte aligned");
+  if (ws_bytes < need) return fail(PGSAG_EWORKSPACE, "workspace too small (see pgsag_workspace_size)");
+  return PGSAG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pgsag_last_error(void) { return g_err.c_str(); }
+
+const char* pgsag_version(void) { return "pgsag-b200 0.1 sm_100a"; }
+
+void pgsag_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing = on != 0;
+}
+
+int pgsag_timing_collect(void) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  std::map<std::string, std::pair<double, long long>> agg;
+  std::map<std::string, const char*> names;
+  for (const TimingRec& r : g_recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& a = agg[r.name];
+    a.first += ms;
+    a.second += 1;
+    names[r.name] = r.name;
+    g_pool.push_back(r.a);
+    g_pool.push_back(r.b);
+  }
+  g_recs.clear();
+  g_agg.clear();
+  for (auto& kv : agg) g_agg.push_back({names[kv.first], kv.second});
+  return (int)g_agg.size();
+}
+
+int pgsag_timing_get(int k, const char** name, double* ms, long long* launches) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (k < 0 || k >= (int)g_agg.size()) return PGSAG_EINVAL;
+  if (name) *name = g_agg[k].first;
+  if (ms) *ms = g_agg[k].second.first;
+  if (launches) *launches = g_agg[k].second.second;
+  return PGSAG_OK;
+}
+
+size_t pgsag_workspace_size(int32_t n, int32_t width, int32_t height, int64_t dup_capacity) {
+  return ws_layout(n, width, height, dup_capacity).total;
+}
+
+int pgsag_preprocess(const pgsag_gaussians* g, const pgsag_camera* cam, const uint8_t* mask, pgsag_tilemask* tm,
+                     pgsag_projected* out, void* ws, size_t ws_bytes, void* stream) {
+  (void)ws; (void)ws_bytes;
+  int rc;
+  if ((rc = check_g(g)) || (rc = check_cam(cam)) || (rc = check_tm(tm))) return rc;
+  if (!mask) return fail(PGSAG_EINVAL, "mask is NULL");
+  if (g->n > 0 && (rc = check_proj(out))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Dims d = make_dims(cam->width, cam->height);
+  cudaError_t e = launch_tilemask(mask, d, tm, st);
+  if (e != cudaSuccess) return cuda_fail(e, "tilemask");
+  e = launch_preprocess(g, cam, d, tm, out, st);
+  if (e != cudaSuccess) return cuda_fail(e, "preprocess");
+  return PGSAG_OK;
+}
+
+int pgsag_bin_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const pgsag_camera* cam, int32_t n,
+                   pgsag_bins* bins, void* ws, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_cam(cam)) || (rc = check_tm(tm))) return rc;
+  if (n < 0) return fail(PGSAG_EINVAL, "n < 0");
+  if (n > 0 && (rc = check_proj(p))) return rc;
+  if (!bins || !bins->ranges || (bins->capacity > 0 && (!bins->tile_keys || !bins->vals)))
+    return fail(PGSAG_EINVAL, "bins buffer is NULL");
+  if (bins->capacity < 0 || bins->capacity >= (int64_t)kLbMask)
+    return fail(PGSAG_EINVAL, "bins capacity must be in [0, 2^30)");
+  const WsLayout L = ws_layout(n, cam->width, cam->height, bins->capacity);
+  if ((rc = check_ws(ws, ws_bytes, L.total))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Dims d = make_dims(cam->width, cam->height);
+  char* w = static_cast<char*>(ws);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(w + L.counters);
+  cudaError_t e;
+  // zero the look-back / histogram / counter state of stage 1 and A2
+  e = cudaMemsetAsync(w + L.status1, 0, 4 * (size_t)kMaxSortPasses * L.tiles1 * kRadix, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w + L.scan_status, 0, L.g2d - L.scan_status, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  unsigned long long M = 0;
+  const uint32_t* ids_sorted = nullptr;
+  if (n > 0) {
+    e = launch_bin_sort_stage1(p, n, L, w, st, &ids_sorted);
+    if (e != cudaSuccess) return cuda_fail(e, "depth sort / scan");
+    e = cudaMemcpyAsync(&M, counters + CNT_M, sizeof(M), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "read M");
+  }
+  bins->n_dup = (int64_t)M;
+  if ((int64_t)M > bins->capacity) return fail(PGSAG_ECAPACITY, "bins capacity < M (bins->n_dup holds M)");
+  e = launch_duplicate_and_sort(p, tm, d, n, (uint32_t)M, ids_sorted, L, w, bins, st);
+  if (e != cudaSuccess) return cuda_fail(e, "duplicate / tile sort / ranges");
+  return PGSAG_OK;
+}
+
+int pgsag_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, const pgsag_tilemask* tm,
+                     const pgsag_camera* cam, const uint8_t* mask, const float bg[3], pgsag_image* out, void* ws,
+                     size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_cam(cam)) || (rc = check_tm(tm)) || (rc = check_proj(p))) return rc;
+  if (!bins || !bins->vals || !bins->ranges) return fail(PGSAG_EINVAL, "bins buffer is NULL");
+  if (!mask || !bg) return fail(PGSAG_EINVAL, "mask/bg is NULL");
+  if (!out || !out->C || !out->N || !out->D || !out->A || !out->Dep || !out->T || !out->g || !out->last)
+    return fail(PGSAG_EINVAL, "image buffer is NULL");
+  const WsLayout L = ws_layout(0, cam->width, cam->height, 0);
+  if ((rc = check_ws(ws, ws_bytes, L.total))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Dims d = make_dims(cam->width, cam->height);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + L.counters);
+  cudaError_t e = cudaMemsetAsync(counters + CNT_FWD, 0, sizeof(uint32_t), st);
+  if (e == cudaSuccess) e = launch_render_fwd(p, bins, tm, d, cam, mask, bg, out, counters + CNT_FWD, st);
+  if (e != cudaSuccess) return cuda_fail(e, "render_fwd");
+  return PGSAG_OK;
+}
+
+int pgsag_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
+                     const pgsag_bins* bins, const pgsag_tilemask* tm, const uint8_t* mask, const float bg[3],
+                     const pgsag_image* fwd, const pgsag_image_grad* dL, pgsag_gaussian_grad* out, void* ws,
+                     size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_g(g)) || (rc = check_cam(cam)) || (rc = check_tm(tm))) return rc;
+  if (g->n > 0 && (rc = check_proj(p))) return rc;
+  if (!bins || !bins->vals || !bins->ranges) return fail(PGSAG_EINVAL, "bins buffer is NULL");
+  if (!mask || !bg || !fwd || !dL || !out) return fail(PGSAG_EINVAL, "argument is NULL");
+  if (!fwd->N || !fwd->D || !fwd->T || !fwd->g || !fwd->last) return fail(PGSAG_EINVAL, "fwd image is NULL");
+  if (g->n > 0 && (!out->dmean || !out->dscale || !out->drot || !out->dopacity || !out->dsh))
+    return fail(PGSAG_EINVAL, "gradient output is NULL");
+  const WsLayout L = ws_layout(g->n, cam->width, cam->height, 0);
+  if ((rc = check_ws(ws, ws_bytes, L.total))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Dims d = make_dims(cam->width, cam->height);
+  char* w = static_cast<char*>(ws);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(w + L.counters);
+  cudaError_t e = cudaMemsetAsync(counters + CNT_BWD, 0, sizeof(uint32_t), st);
+  if (e == cudaSuccess)
+    e = launch_render_bwd(g, cam, p, bins, tm, d, mask, bg, fwd, dL, out, reinterpret_cast<float*>(w + L.g2d),
+                          counters + CNT_BWD, st);
+  if (e != cudaSuccess) return cuda_fail(e, "render_bwd");
+  return PGSAG_OK;
+}
+
+}  // extern "C"

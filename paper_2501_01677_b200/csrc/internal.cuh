@@ -1,0 +1,95 @@
+// Internal declarations shared by the libpgsag.so translation units.
+// Product code only: nothing here is shared with oracle/ (DESIGN.md §1).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pgsag.h"
+
+namespace pgsag {
+
+constexpr int kTile = PGSAG_TILE;        // 16x16 pixel tiles
+constexpr int kTilePix = kTile * kTile;  // 256 pixels -> 256 threads per compositing CTA
+
+// ---- sort configuration (A4) ----
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per CTA
+constexpr uint32_t kLbAgg = 1u << 30;                 // look-back flags (top 2 bits)
+constexpr uint32_t kLbPrefix = 2u << 30;
+constexpr uint32_t kLbMask = (1u << 30) - 1;
+constexpr int kScanTile = 4096;                       // A2 scan items per CTA
+constexpr int kMaxSortPasses = 4;
+
+struct Dims {
+  int W, H, TX, TY, WPR;  // WPR = 32-bit words per bitmap row
+};
+
+inline Dims make_dims(int W, int H) {
+  Dims d;
+  d.W = W; d.H = H;
+  d.TX = (W + kTile - 1) / kTile;
+  d.TY = (H + kTile - 1) / kTile;
+  d.WPR = (d.TX + 31) / 32;
+  return d;
+}
+
+// Workspace carve-up, identical for every call with the same sizes.
+struct WsLayout {
+  size_t depth_keys[2], ids[2];  // stage-1 sort ping-pong [n]
+  size_t offsets;                // [n] exclusive scan of tiles_touched in depth order
+  size_t dup_keys, dup_vals;     // stage-2 sort scratch [capacity]
+  size_t status1;                // stage-1 look-back [passes][tiles1][256] u32
+  size_t status2;                // stage-2 look-back [passes][tiles2][256] u32
+  size_t scan_status;            // A2 look-back [tilesN] u64
+  size_t hist;                   // [2][kMaxSortPasses][256] u32
+  size_t counters;               // [64] u32 (tile counters, M, misc)
+  size_t g2d;                    // [14][n] f32 per-Gaussian 2D gradients (A7 -> A8)
+  size_t total;
+  int tiles1, tiles2, tilesN;
+};
+
+WsLayout ws_layout(int32_t n, int32_t W, int32_t H, int64_t cap);
+
+// counters[] slots
+enum : int {
+  CNT_SORT1 = 0,   // 4 slots: stage-1 pass tile counters
+  CNT_SORT2 = 4,   // 4 slots: stage-2 pass tile counters
+  CNT_SCAN = 8,    // A2 tile counter
+  CNT_FWD = 9,     // A6 work counter
+  CNT_BWD = 10,    // A7 work counter
+  CNT_M = 12,      // 2 slots: M as u64 (A2 total)
+  CNT_N = 16
+};
+
+// ------------------------------------------------------------- kernel timing
+// RAII scope recording a CUDA event pair around one kernel launch when
+// pgsag_timing_enable(1) is on (api.cu).
+struct KTimer {
+  int slot;
+  cudaStream_t st;
+  KTimer(const char* name, cudaStream_t s);
+  ~KTimer();
+};
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_tilemask(const uint8_t* mask, const Dims& d, pgsag_tilemask* tm, cudaStream_t st);
+cudaError_t launch_preprocess(const pgsag_gaussians* g, const pgsag_camera* cam, const Dims& d,
+                              const pgsag_tilemask* tm, pgsag_projected* out, cudaStream_t st);
+cudaError_t launch_bin_sort_stage1(const pgsag_projected* p, int n, const WsLayout& L, char* ws,
+                                   cudaStream_t st, const uint32_t** ids_sorted);
+cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const Dims& d, int n,
+                                      uint32_t M, const uint32_t* ids_sorted, const WsLayout& L, char* ws,
+                                      pgsag_bins* bins, cudaStream_t st);
+cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, const pgsag_tilemask* tm,
+                              const Dims& d, const pgsag_camera* cam, const uint8_t* mask, const float bg[3],
+                              pgsag_image* out, uint32_t* work_counter, cudaStream_t st);
+cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
+                              const pgsag_bins* bins, const pgsag_tilemask* tm, const Dims& d,
+                              const uint8_t* mask, const float bg[3], const pgsag_image* fwd,
+                              const pgsag_image_grad* dL, pgsag_gaussian_grad* out, float* g2d,
+                              uint32_t* work_counter, cudaStream_t st);
+
+}  // namespace pgsag

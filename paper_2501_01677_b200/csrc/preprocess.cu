@@ -1,0 +1,353 @@
+// A0 (building-mask tile occupancy) and A1 (per-Gaussian projection) for sm_100a.
+//
+// This translation unit is compiled with --fmad=false: A1's key path (camera z,
+// the 2D covariance and the tile rect) is IEEE float32 with every product and sum
+// rounded separately, in the order DESIGN.md §4 fixes, so the (tile, depth) keys
+// are bit-exact with any other correct float32 evaluation of the same readings.
+//
+// P:78 "each 3D Gaussian sphere is transformed into a 2D Gaussian based on the
+// viewing direction of each camera and then projected onto different image
+// tiles"; Eq. 2-3 (n_i, R_c n_i, d_i); P:243 masked pixels only.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace pgsag {
+namespace {
+
+// ------------------------------------------------------------------ A0 count
+// One thread per tile; a warp covers 32 horizontally adjacent tiles, so each of
+// its 16 row loads is 512 contiguous bytes (uint4 per lane) -> fully coalesced.
+// The warp's ballot over "tile has a mask pixel" is exactly one bitmap word.
+__global__ void __launch_bounds__(128) tilemask_count_kernel(const uint8_t* __restrict__ mask, Dims d,
+                                                               uint32_t* __restrict__ tile_cnt,
+                                                               uint32_t* __restrict__ bitmap, int vec16) {
+  const int tx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ty = blockIdx.y;
+  uint32_t cnt = 0;
+  if (tx < d.TX) {
+    const int i0 = tx * kTile;
+    const int i1 = min(i0 + kTile, d.W);
+    const int j0 = ty * kTile;
+    const int j1 = min(j0 + kTile, d.H);
+    if (vec16 && i1 - i0 == kTile) {
+#pragma unroll 4
+      for (int j = j0; j < j1; ++j) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(mask + (size_t)j * d.W + i0));
+        // bytes != 0 -> 0xFF per byte; popc / 8 = number of nonzero bytes
+        cnt += (__popc(__vcmpne4(w.x, 0u)) + __popc(__vcmpne4(w.y, 0u)) + __popc(__vcmpne4(w.z, 0u)) +
+                __popc(__vcmpne4(w.w, 0u))) >> 3;
+      }
+    } else {
+      for (int j = j0; j < j1; ++j)
+        for (int i = i0; i < i1; ++i) cnt += mask[(size_t)j * d.W + i] != 0;
+    }
+    tile_cnt[ty * d.TX + tx] = cnt;
+  }
+  const unsigned word = __ballot_sync(0xffffffffu, tx < d.TX && cnt > 0);
+  const int lane = threadIdx.x & 31;
+  const int wtx = tx - lane;  // first tile of this warp (multiple of 32 since blockDim % 32 == 0)
+  if (lane == 0 && wtx < d.TX) bitmap[ty * d.WPR + wtx / 32] = word;
+}
+
+__device__ __forceinline__ uint32_t row_prefix(const uint32_t* __restrict__ row, int x, int WPR) {
+  // number of set bits of the row bitmap at positions < x
+  uint32_t c = 0;
+  const int wq = x >> 5;
+  for (int w = 0; w < wq; ++w) c += __popc(row[w]);
+  const int r = x & 31;
+  if (r && wq < WPR) c += __popc(row[wq] & ((1u << r) - 1u));
+  return c;
+}
+
+// ------------------------------------------------------- A0 SAT + active list
+// Single CTA: the active-tile bitmap (TY x WPR words, 10 KB at 5472x3648) lives in
+// shared memory; one thread per SAT column accumulates down the rows.
+__global__ void __launch_bounds__(1024) tilemask_sat_kernel(Dims d, const uint32_t* __restrict__ bitmap_g,
+                                                              int32_t* __restrict__ sat,
+                                                              uint32_t* __restrict__ active,
+                                                              uint32_t* __restrict__ n_active) {
+  extern __shared__ uint32_t smem[];
+  uint32_t* bm = smem;                       // [TY][WPR]
+  uint32_t* rowpre = smem + d.TY * d.WPR;    // [TY+1] exclusive prefix of row totals
+  const int nt = blockDim.x, tid = threadIdx.x;
+  for (int k = tid; k < d.TY * d.WPR; k += nt) bm[k] = bitmap_g[k];
+  __syncthreads();
+  for (int y = tid; y < d.TY; y += nt) {
+    uint32_t c = 0;
+    for (int w = 0; w < d.WPR; ++w) c += __popc(bm[y * d.WPR + w]);
+    rowpre[y + 1] = c;
+  }
+  __syncthreads();
+  if (tid < 32) {  // warp-0 inclusive scan of rowpre[1..TY]
+    uint32_t carry = 0;
+    for (int base = 0; base < d.TY; base += 32) {
+      const int y = base + tid;
+      uint32_t v = y < d.TY ? rowpre[y + 1] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (tid >= o) v += u;
+      }
+      if (y < d.TY) rowpre[y + 1] = v + carry;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (tid == 0) rowpre[0] = 0;
+  }
+  __syncthreads();
+  const int S = d.TX + 1;
+  for (int x = tid; x <= d.TX; x += nt) {
+    sat[x] = 0;  // row 0
+    uint32_t acc = 0;
+    for (int y = 0; y < d.TY; ++y) {
+      if (x > 0) acc += row_prefix(bm + y * d.WPR, x, d.WPR);
+      sat[(size_t)(y + 1) * S + x] = (int32_t)acc;
+    }
+  }
+  for (int t = tid; t < d.TX * d.TY; t += nt) {
+    const int ty = t / d.TX, tx = t - ty * d.TX;
+    if ((bm[ty * d.WPR + (tx >> 5)] >> (tx & 31)) & 1u)
+      active[rowpre[ty] + row_prefix(bm + ty * d.WPR, tx, d.WPR)] = (uint32_t)t;
+  }
+  if (tid == 0) *n_active = rowpre[d.TY];
+}
+
+// --------------------------------------------------------------- A1 project
+struct CamK {
+  float fx, fy, cx, cy;
+  float R[9];
+  float C[3];
+  float znear;
+  float lx, ly;  // 1.3 x half-FoV tangent (R9)
+};
+
+// real SH constants, degree <= 3 (R12)
+__constant__ float kShC2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                               -1.0925484305920792f, 0.5462742152960396f};
+__constant__ float kShC3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                               0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
+                               -0.5900435899266435f};
+
+__device__ __forceinline__ int fdiv16(int a) { return a >> 4; }  // floor division (arithmetic shift)
+
+// ln upper bound from y = m 2^ex, m in [0.5,1):  e ln2 + f(6+f)/(6+4f) + 2^-18 (R8)
+__device__ __forceinline__ float lnup(float y) {
+  const uint32_t b = __float_as_uint(y);
+  const int ex = (int)((b >> 23) & 0xFFu) - 126;
+  const float m = __uint_as_float((b & 0x807FFFFFu) | 0x3F000000u);
+  const float e = (float)(ex - 1);
+  const float f = 2.0f * m - 1.0f;
+  return (e * 0.6931471805599453f + (f * (6.0f + f)) / (6.0f + 4.0f * f)) + 3.814697265625e-06f;
+}
+
+__global__ void __launch_bounds__(256) preprocess_kernel(
+    int n, int deg, const float* __restrict__ mean, const float* __restrict__ scale,
+    const float* __restrict__ rot, const float* __restrict__ opac, const float* __restrict__ sh, CamK cam,
+    Dims d, const int32_t* __restrict__ sat, float2* __restrict__ mean2d, float4* __restrict__ conic_o,
+    float* __restrict__ depth, short4* __restrict__ rect, uint32_t* __restrict__ tiles_touched,
+    float4* __restrict__ rgb_d, float4* __restrict__ ncam, uint32_t* __restrict__ flags) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float t0 = __ldg(mean + i) - cam.C[0];
+  const float t1 = __ldg(mean + n + i) - cam.C[1];
+  const float t2 = __ldg(mean + 2 * n + i) - cam.C[2];
+  const float* Rc = cam.R;
+  const float x = (Rc[0] * t0 + Rc[1] * t1) + Rc[2] * t2;
+  const float y = (Rc[3] * t0 + Rc[4] * t1) + Rc[5] * t2;
+  const float z = (Rc[6] * t0 + Rc[7] * t1) + Rc[8] * t2;
+
+  uint32_t fl = 0;
+  float2 uv = make_float2(0.f, 0.f);
+  float4 co = make_float4(0.f, 0.f, 0.f, 0.f);
+  short4 rc = make_short4(0, 0, -1, -1);
+  uint32_t touched = 0;
+  float4 cd = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 nc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float zout = 0.f;
+
+  if (z > cam.znear) {
+    fl |= PGSAG_F_VISIBLE;
+    zout = z;
+    const float xz = x / z, yz = y / z;
+    uv.x = cam.fx * xz + cam.cx;
+    uv.y = cam.fy * yz + cam.cy;
+
+    // quaternion -> rotation (w,x,y,z), normalised
+    const float qw0 = __ldg(rot + i), qx0 = __ldg(rot + n + i), qy0 = __ldg(rot + 2 * n + i),
+                qz0 = __ldg(rot + 3 * n + i);
+    const float qn = sqrtf(((qw0 * qw0 + qx0 * qx0) + qy0 * qy0) + qz0 * qz0);
+    const float qw = qw0 / qn, qx = qx0 / qn, qy = qy0 / qn, qz = qz0 / qn;
+    float Rg[3][3];
+    Rg[0][0] = 1.0f - 2.0f * (qy * qy + qz * qz);
+    Rg[0][1] = 2.0f * (qx * qy - qw * qz);
+    Rg[0][2] = 2.0f * (qx * qz + qw * qy);
+    Rg[1][0] = 2.0f * (qx * qy + qw * qz);
+    Rg[1][1] = 1.0f - 2.0f * (qx * qx + qz * qz);
+    Rg[1][2] = 2.0f * (qy * qz - qw * qx);
+    Rg[2][0] = 2.0f * (qx * qz - qw * qy);
+    Rg[2][1] = 2.0f * (qy * qz + qw * qx);
+    Rg[2][2] = 1.0f - 2.0f * (qx * qx + qy * qy);
+    const float s[3] = {__ldg(scale + i), __ldg(scale + n + i), __ldg(scale + 2 * n + i)};
+    float Mg[3][3], Sig[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Mg[a][b] = Rg[a][b] * s[b];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Sig[a][b] = (Mg[a][0] * Mg[b][0] + Mg[a][1] * Mg[b][1]) + Mg[a][2] * Mg[b][2];
+
+    float cxz = xz, cyz = yz;
+    if (xz < -cam.lx) { cxz = -cam.lx; fl |= PGSAG_F_CLAMP_X; }
+    if (xz > cam.lx) { cxz = cam.lx; fl |= PGSAG_F_CLAMP_X; }
+    if (yz < -cam.ly) { cyz = -cam.ly; fl |= PGSAG_F_CLAMP_Y; }
+    if (yz > cam.ly) { cyz = cam.ly; fl |= PGSAG_F_CLAMP_Y; }
+    const float J00 = cam.fx / z, J02 = -((cam.fx * cxz) / z);
+    const float J11 = cam.fy / z, J12 = -((cam.fy * cyz) / z);
+    // Tm = J R_c (J01 = J10 = 0: the omitted products are exact zeros)
+    float Tm[2][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      Tm[0][b] = J00 * Rc[b] + J02 * Rc[6 + b];
+      Tm[1][b] = J11 * Rc[3 + b] + J12 * Rc[6 + b];
+    }
+    float Mt[2][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Mt[a][b] = (Tm[a][0] * Sig[0][b] + Tm[a][1] * Sig[1][b]) + Tm[a][2] * Sig[2][b];
+    const float c00 = (Mt[0][0] * Tm[0][0] + Mt[0][1] * Tm[0][1]) + Mt[0][2] * Tm[0][2];
+    const float c01 = (Mt[0][0] * Tm[1][0] + Mt[0][1] * Tm[1][1]) + Mt[0][2] * Tm[1][2];
+    const float c11 = (Mt[1][0] * Tm[1][0] + Mt[1][1] * Tm[1][1]) + Mt[1][2] * Tm[1][2];
+    const float A = c00 + 0.3f, B = c01, Cc = c11 + 0.3f;  // low-pass (R10)
+    const float det = A * Cc - B * B;
+    if (det > 0.0f) {
+      fl |= PGSAG_F_DET_OK;
+      const float o = __ldg(opac + i);
+      co = make_float4(Cc / det, -B / det, A / det, o);
+      if (!(o < 1.0f / 255.0f)) {
+        fl |= PGSAG_F_OPAC_OK;
+        // opacity-aware conservative ellipse AABB (R8)
+        float k2 = (2.0f * lnup(255.0f * o)) * (1.0f + 0.0009765625f);
+        if (k2 < 0.0f) k2 = 0.0f;
+        const float rx = sqrtf(k2 * A) + 0.015625f, ry = sqrtf(k2 * Cc) + 0.015625f;
+        const float lim = 1048576.0f;
+        const int ix0 = (int)fminf(fmaxf(ceilf((uv.x - rx) - 0.5f), -lim), lim);
+        const int ix1 = (int)fminf(fmaxf(floorf((uv.x + rx) - 0.5f), -lim), lim);
+        const int iy0 = (int)fminf(fmaxf(ceilf((uv.y - ry) - 0.5f), -lim), lim);
+        const int iy1 = (int)fminf(fmaxf(floorf((uv.y + ry) - 0.5f), -lim), lim);
+        const int tx0 = max(0, fdiv16(ix0)), tx1 = min(d.TX - 1, fdiv16(ix1));
+        const int ty0 = max(0, fdiv16(iy0)), ty1 = min(d.TY - 1, fdiv16(iy1));
+        if (tx0 <= tx1 && ty0 <= ty1) {
+          fl |= PGSAG_F_RECT;
+          rc = make_short4((short)tx0, (short)ty0, (short)tx1, (short)ty1);
+          const int S = d.TX + 1;
+          touched = (uint32_t)(__ldg(sat + (ty1 + 1) * S + tx1 + 1) - __ldg(sat + ty0 * S + tx1 + 1) -
+                               __ldg(sat + (ty1 + 1) * S + tx0) + __ldg(sat + ty0 * S + tx0));
+        }
+        // flattened-Gaussian normal (R4) and plane distance (Eq. 3, R2)
+        int k = 0;
+        if (s[1] < s[k]) k = 1;
+        if (s[2] < s[k]) k = 2;
+        fl |= (uint32_t)k << PGSAG_F_AXIS_SHIFT;
+        float n0 = Rg[0][k], n1 = Rg[1][k], n2 = Rg[2][k];
+        const float dotv = (n0 * t0 + n1 * t1) + n2 * t2;
+        if (dotv > 0.0f) { n0 = -n0; n1 = -n1; n2 = -n2; fl |= PGSAG_F_NFLIP; }
+        nc.x = (Rc[0] * n0 + Rc[1] * n1) + Rc[2] * n2;
+        nc.y = (Rc[3] * n0 + Rc[4] * n1) + Rc[5] * n2;
+        nc.z = (Rc[6] * n0 + Rc[7] * n1) + Rc[8] * n2;
+        cd.w = (n0 * t0 + n1 * t1) + n2 * t2;
+        // SH colour (R12)
+        const float len = sqrtf((t0 * t0 + t1 * t1) + t2 * t2);
+        const float dx = t0 / len, dy = t1 / len, dz = t2 / len;
+        float Y[16];
+        const float xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yzp = dy * dz, xzp = dx * dz;
+        Y[0] = 0.28209479177387814f;
+        Y[1] = -0.4886025119029199f * dy;
+        Y[2] = 0.4886025119029199f * dz;
+        Y[3] = -0.4886025119029199f * dx;
+        Y[4] = kShC2[0] * xy;
+        Y[5] = kShC2[1] * yzp;
+        Y[6] = kShC2[2] * ((2.0f * zz - xx) - yy);
+        Y[7] = kShC2[3] * xzp;
+        Y[8] = kShC2[4] * (xx - yy);
+        Y[9] = (kShC3[0] * dy) * (3.0f * xx - yy);
+        Y[10] = (kShC3[1] * xy) * dz;
+        Y[11] = (kShC3[2] * dy) * ((4.0f * zz - xx) - yy);
+        Y[12] = (kShC3[3] * dz) * ((2.0f * zz - 3.0f * xx) - 3.0f * yy);
+        Y[13] = (kShC3[4] * dx) * ((4.0f * zz - xx) - yy);
+        Y[14] = (kShC3[5] * dz) * (xx - yy);
+        Y[15] = (kShC3[6] * dx) * (xx - 3.0f * yy);
+        const int K = (deg + 1) * (deg + 1);
+        float col[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          float acc = Y[0] * __ldg(sh + (size_t)c * n + i);
+          for (int l = 1; l < K; ++l) acc = acc + Y[l] * __ldg(sh + (size_t)(l * 3 + c) * n + i);
+          acc = acc + 0.5f;
+          if (acc < 0.0f) { acc = 0.0f; fl |= PGSAG_F_RGB_CLAMP0 << c; }
+          col[c] = acc;
+        }
+        cd.x = col[0]; cd.y = col[1]; cd.z = col[2];
+      }
+    }
+  }
+  mean2d[i] = uv;
+  conic_o[i] = co;
+  depth[i] = zout;
+  rect[i] = rc;
+  tiles_touched[i] = touched;
+  rgb_d[i] = cd;
+  ncam[i] = nc;
+  flags[i] = fl;
+}
+
+}  // namespace
+
+cudaError_t launch_tilemask(const uint8_t* mask, const Dims& d, pgsag_tilemask* tm, cudaStream_t st) {
+  uint32_t* bitmap = tm->active_bits;
+  const int vec16 = (d.W % 16 == 0) && ((reinterpret_cast<uintptr_t>(mask) & 15u) == 0);
+  dim3 grid((d.TX + 127) / 128, d.TY);
+  {
+    KTimer kt_("A0_tilemask_count", st);
+    tilemask_count_kernel<<<grid, 128, 0, st>>>(mask, d, tm->tile_cnt, bitmap, vec16);
+  }
+  const size_t smem = sizeof(uint32_t) * ((size_t)d.TY * d.WPR + d.TY + 1);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(tilemask_sat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    KTimer kt_("A0_tilemask_sat", st);
+    tilemask_sat_kernel<<<1, 1024, smem, st>>>(d, bitmap, tm->sat, tm->active, tm->n_active);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess(const pgsag_gaussians* g, const pgsag_camera* c, const Dims& d,
+                              const pgsag_tilemask* tm, pgsag_projected* out, cudaStream_t st) {
+  if (g->n == 0) return cudaSuccess;
+  CamK k;
+  k.fx = c->fx; k.fy = c->fy; k.cx = c->cx; k.cy = c->cy;
+  for (int a = 0; a < 9; ++a) k.R[a] = c->R[a];
+  for (int a = 0; a < 3; ++a) k.C[a] = c->C[a];
+  k.znear = c->znear;
+  // evaluated on the host with the same IEEE ops: 1.3 * ((0.5 * W) / fx)
+  volatile float hw = 0.5f * (float)c->width, hh = 0.5f * (float)c->height;
+  volatile float qx = hw / c->fx, qy = hh / c->fy;
+  k.lx = 1.3f * qx;
+  k.ly = 1.3f * qy;
+  const int threads = 256;
+  {
+    KTimer kt_("A1_preprocess", st);
+    preprocess_kernel<<<(g->n + threads - 1) / threads, threads, 0, st>>>(
+        g->n, g->sh_degree, g->mean, g->scale, g->rot, g->opacity, g->sh, k, d, tm->sat,
+        reinterpret_cast<float2*>(out->mean2d), reinterpret_cast<float4*>(out->conic_o), out->depth,
+        reinterpret_cast<short4*>(out->rect), out->tiles_touched, reinterpret_cast<float4*>(out->rgb_d),
+        reinterpret_cast<float4*>(out->ncam), out->flags);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace pgsag

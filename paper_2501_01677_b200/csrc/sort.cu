@@ -1,0 +1,446 @@
+// A2-A5 on sm_100a: depth sort, scan, key duplication, tile radix sort, ranges.
+//
+// P:78 "projected onto different image tiles. The 2D Gaussians are subsequently
+// sorted" — realised as the TWO-STAGE equivalent of the 3DGS (tile|depth) 64-bit
+// key sort: (1) stable LSD sort of the N Gaussians by depth bits
+// (32 bits), (2) duplication in depth order into (tile, id) entries, (3) stable
+// LSD sort of the M entries by tile id only (ceil(log2 #tiles) bits).  The result
+// is exactly the (tile, depth bits, id) order with ~4x fewer bytes moved per entry
+// than a 64-bit key sort.
+//
+// The radix sort is a hand-written onesweep (single read + single write per pass):
+// each CTA ranks a 4096-key tile with warp match_any, publishes per-digit counts,
+// and resolves its global digit offsets by decoupled look-back over predecessor
+// CTAs (tile ids are taken from an atomic counter, so a CTA only ever waits on
+// CTAs that started before it).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace pgsag {
+namespace {
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) { return *(const volatile uint32_t*)p; }
+__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) { *(volatile uint32_t*)p = v; }
+__device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long* p) {
+  return *(const volatile unsigned long long*)p;
+}
+__device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned long long v) {
+  *(volatile unsigned long long*)p = v;
+}
+
+// exclusive scan of one value per thread across a 256-thread CTA; returns the CTA total
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& excl) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += u;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  uint32_t wbase = 0, total = 0;
+#pragma unroll
+  for (int k = 0; k < NT / 32; ++k) {
+    const uint32_t t = s_warp[k];
+    if (k < w) wbase += t;
+    total += t;
+  }
+  excl = wbase + x - v;
+  __syncthreads();
+  return total;
+}
+
+// ----------------------------------------------------------------- keys
+// Stage-1 keys: depth bits for Gaussians that emit entries, else all-ones (last).
+__global__ void depth_keys_kernel(int n, const float* __restrict__ depth, const uint32_t* __restrict__ touched,
+                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = touched[i] > 0 ? __float_as_uint(depth[i]) : 0xFFFFFFFFu;  // z > znear > 0: bit order = value order
+  ids[i] = (uint32_t)i;
+}
+
+// ------------------------------------------------------------ histogram
+// Digit histograms of all passes at once (onesweep's upfront pass).
+__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys,
+                                                          const uint32_t* __restrict__ n_ptr, uint32_t n_fixed,
+                                                          int npass, int end_bit, uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t sh[kMaxSortPasses][kRadix];
+  const uint32_t n = n_ptr ? *n_ptr : n_fixed;
+  for (int k = threadIdx.x; k < kMaxSortPasses * kRadix; k += blockDim.x) (&sh[0][0])[k] = 0;
+  __syncthreads();
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    const uint32_t key = keys[idx];
+    for (int p = 0; p < npass; ++p) {
+      const int shift = p * kRadixBits;
+      const int nb = min(kRadixBits, end_bit - shift);
+      atomicAdd(&sh[p][(key >> shift) & ((1u << nb) - 1u)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < npass * kRadix; k += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[k];
+    if (v) atomicAdd(ghist + k, v);
+  }
+}
+
+// ------------------------------------------------------------ onesweep pass
+__global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ n_ptr, uint32_t n_fixed, int shift, int nbits,
+    const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
+  constexpr int NW = kSortThreads / 32;
+  __shared__ uint32_t s_keys[kSortTile];
+  __shared__ uint32_t s_vals[kSortTile];
+  __shared__ uint32_t s_whist[NW][kRadix];
+  __shared__ uint32_t s_cta_start[kRadix];
+  __shared__ uint32_t s_gbase[kRadix];
+  __shared__ uint32_t s_warp[NW];
+  __shared__ uint32_t s_tile;
+
+  const uint32_t n = n_ptr ? *n_ptr : n_fixed;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int k = tid; k < NW * kRadix; k += kSortThreads) (&s_whist[0][0])[k] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * (uint32_t)kSortTile;
+  if (base >= n) return;  // whole CTA: uniform
+  const uint32_t mask = (1u << nbits) - 1u;
+
+  uint32_t key[kSortItems], val[kSortItems], rank[kSortItems];
+  const uint32_t wbase = base + (uint32_t)w * 32u * kSortItems;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const uint32_t idx = wbase + (uint32_t)k * 32u + lane;
+    if (idx < n) {
+      key[k] = keys_in[idx];
+      val[k] = vals_in[idx];
+    } else {
+      key[k] = 0xFFFFFFFFu;
+      val[k] = 0u;
+    }
+  }
+  const uint32_t lt = lanemask_lt();
+  // stable warp-local ranking: item-major, lane-minor == input order
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const uint32_t idx = wbase + (uint32_t)k * 32u + lane;
+    const uint32_t dg = idx < n ? ((key[k] >> shift) & mask) : (uint32_t)kRadix;
+    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t r = __popc(peers & lt);
+    const uint32_t prev = dg < (uint32_t)kRadix ? s_whist[w][dg] : 0u;
+    __syncwarp();
+    if (r == 0 && dg < (uint32_t)kRadix) s_whist[w][dg] = prev + __popc(peers);
+    __syncwarp();
+    rank[k] = prev + r;
+  }
+  __syncthreads();
+  // per digit: exclusive offsets across warps, CTA total, look-back
+  const int dgt = tid;  // kSortThreads == kRadix
+  uint32_t total = 0;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    const uint32_t t = s_whist[k][dgt];
+    s_whist[k][dgt] = total;
+    total += t;
+  }
+  uint32_t* my = status + (size_t)tile * kRadix + dgt;
+  uint32_t excl = 0;
+  if (tile == 0) {
+    st_volatile(my, kLbPrefix | total);
+  } else {
+    st_volatile(my, kLbAgg | total);
+    int j = (int)tile - 1;
+    while (j >= 0) {
+      uint32_t s;
+      do { s = ld_volatile(status + (size_t)j * kRadix + dgt); } while ((s & ~kLbMask) == 0u);
+      excl += s & kLbMask;
+      if (s & kLbPrefix) break;
+      --j;
+    }
+    st_volatile(my, kLbPrefix | (excl + total));
+  }
+  // global start of digit dgt = (exclusive scan of ghist) + excl
+  uint32_t gex;
+  block_excl_scan<kSortThreads>(ghist[dgt], s_warp, gex);
+  s_gbase[dgt] = gex + excl;
+  uint32_t cex;
+  block_excl_scan<kSortThreads>(total, s_warp, cex);
+  s_cta_start[dgt] = cex;
+  __syncthreads();
+  // scatter into shared memory in CTA-local sorted order
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const uint32_t idx = wbase + (uint32_t)k * 32u + lane;
+    if (idx < n) {
+      const uint32_t dg = (key[k] >> shift) & mask;
+      const uint32_t pos = s_cta_start[dg] + s_whist[w][dg] + rank[k];
+      s_keys[pos] = key[k];
+      s_vals[pos] = val[k];
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = min((uint32_t)kSortTile, n - base);
+  for (uint32_t p = tid; p < cnt; p += kSortThreads) {
+    const uint32_t k = s_keys[p];
+    const uint32_t dg = (k >> shift) & mask;
+    const uint32_t dst = s_gbase[dg] + (p - s_cta_start[dg]);
+    keys_out[dst] = k;
+    vals_out[dst] = s_vals[p];
+  }
+}
+
+// ---------------------------------------------------------------- A2 scan
+// Single-pass decoupled-look-back exclusive scan of touched[ids[k]] (depth
+// order).  Writes offsets[k] and the total M (u64) to *total.
+__global__ void __launch_bounds__(256) scan_kernel(int n, const uint32_t* __restrict__ touched,
+                                                    const uint32_t* __restrict__ ids,
+                                                    uint32_t* __restrict__ offsets,
+                                                    unsigned long long* __restrict__ status,
+                                                    uint32_t* __restrict__ tile_counter,
+                                                    unsigned long long* __restrict__ total) {
+  constexpr int IT = kScanTile / 256;
+  __shared__ uint32_t s_warp[8];
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_excl;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * kScanTile;
+  if (base >= (uint32_t)n) return;
+  uint32_t v[IT];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < IT; ++k) {  // blocked: thread owns IT consecutive items
+    const uint32_t idx = base + tid * IT + k;
+    v[k] = idx < (uint32_t)n ? touched[ids[idx]] : 0u;
+    sum += v[k];
+  }
+  uint32_t texcl;
+  const uint32_t agg = block_excl_scan<256>(sum, s_warp, texcl);
+  constexpr unsigned long long AGG = 1ull << 62, PRE = 2ull << 62, MASK = (1ull << 62) - 1;
+  if (tid == 0) {
+    unsigned long long ex = 0;
+    if (tile == 0) {
+      st_volatile64(status, PRE | agg);
+    } else {
+      st_volatile64(status + tile, AGG | agg);
+      int j = (int)tile - 1;
+      while (j >= 0) {
+        unsigned long long s;
+        do { s = ld_volatile64(status + j); } while ((s & ~MASK) == 0ull);
+        ex += s & MASK;
+        if (s & PRE) break;
+        --j;
+      }
+      st_volatile64(status + tile, PRE | (ex + agg));
+    }
+    s_excl = ex;
+    if (base + kScanTile >= (uint32_t)n) *total = ex + agg;
+  }
+  __syncthreads();
+  uint32_t run = (uint32_t)s_excl + texcl;
+#pragma unroll
+  for (int k = 0; k < IT; ++k) {
+    const uint32_t idx = base + tid * IT + k;
+    if (idx < (uint32_t)n) offsets[idx] = run;
+    run += v[k];
+  }
+}
+
+// ----------------------------------------------------------- A3 duplicate
+// Thread per Gaussian in depth order; emits (tile, id) for every active tile of
+// its rect in row-major order starting at offsets[k].
+__global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* __restrict__ ids,
+                                                         const uint32_t* __restrict__ offsets,
+                                                         const uint32_t* __restrict__ touched,
+                                                         const short4* __restrict__ rect,
+                                                         const uint32_t* __restrict__ bitmap, Dims d,
+                                                         uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t id = ids[k];
+  if (touched[id] == 0) return;
+  const short4 r = rect[id];
+  uint32_t o = offsets[k];
+  for (int ty = r.y; ty <= r.w; ++ty) {
+    const uint32_t* row = bitmap + ty * d.WPR;
+    for (int tx = r.x; tx <= r.z; ++tx) {
+      if ((__ldg(row + (tx >> 5)) >> (tx & 31)) & 1u) {
+        tkeys[o] = (uint32_t)(ty * d.TX + tx);
+        tvals[o] = id;
+        ++o;
+      }
+    }
+  }
+}
+
+// -------------------------------------------------------------- A5 ranges
+__global__ void ranges_kernel(const uint32_t* __restrict__ tkeys, const uint32_t* __restrict__ M_ptr,
+                              uint32_t* __restrict__ ranges) {
+  const uint32_t M = *M_ptr;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < M; k += gridDim.x * blockDim.x) {
+    const uint32_t t = tkeys[k];
+    if (k == 0 || tkeys[k - 1] != t) ranges[2 * t] = k;
+    if (k == M - 1 || tkeys[k + 1] != t) ranges[2 * t + 1] = k + 1;
+  }
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// LSD radix sort of (keys, vals) on bits [0, end_bit).  Ping-pongs between (a)
+// and (b); returns in *res_a whether the result ended in a.  n is a device
+// pointer (n_dev) or a fixed count with a capacity bound for the grid size.
+cudaError_t radix_sort(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, const uint32_t* n_dev,
+                       uint32_t n_fixed, uint32_t grid_bound, int end_bit, uint32_t* status, size_t status_stride,
+                       uint32_t* ghist, uint32_t* counters, cudaStream_t st, bool* res_in_a) {
+  const int npass = (end_bit + kRadixBits - 1) / kRadixBits;
+  *res_in_a = true;
+  if (npass == 0 || grid_bound == 0) return cudaSuccess;
+  const int hist_grid = min((int)((grid_bound + 255) / 256), num_sms() * 4);
+  {
+    KTimer kt_("A4_radix_hist", st);
+    radix_hist_kernel<<<hist_grid, 256, 0, st>>>(ka, n_dev, n_fixed, npass, end_bit, ghist);
+  }
+  const uint32_t tiles = (grid_bound + kSortTile - 1) / kSortTile;
+  uint32_t *ki = ka, *vi = va, *ko = kb, *vo = vb;
+  for (int p = 0; p < npass; ++p) {
+    const int shift = p * kRadixBits;
+    const int nb = min(kRadixBits, end_bit - shift);
+    {
+      KTimer kt_("A4_radix_onesweep", st);
+      radix_pass_kernel<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_fixed, shift, nb,
+                                                        ghist + p * kRadix, status + p * status_stride,
+                                                        counters + p);
+    }
+    uint32_t* t;
+    t = ki; ki = ko; ko = t;
+    t = vi; vi = vo; vo = t;
+  }
+  *res_in_a = (npass % 2) == 0;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+WsLayout ws_layout(int32_t n, int32_t W, int32_t H, int64_t cap) {
+  WsLayout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t nn = (size_t)(n > 0 ? n : 0), cc = (size_t)(cap > 0 ? cap : 0);
+  L.tiles1 = (int)((nn + kSortTile - 1) / kSortTile);
+  L.tiles2 = (int)((cc + kSortTile - 1) / kSortTile);
+  L.tilesN = (int)((nn + kScanTile - 1) / kScanTile);
+  (void)W; (void)H;
+  for (int k = 0; k < 2; ++k) { L.depth_keys[k] = take(4 * nn); L.ids[k] = take(4 * nn); }
+  L.offsets = take(4 * nn);
+  L.dup_keys = take(4 * cc);
+  L.dup_vals = take(4 * cc);
+  L.status1 = take(4 * (size_t)kMaxSortPasses * L.tiles1 * kRadix);
+  L.status2 = take(4 * (size_t)kMaxSortPasses * L.tiles2 * kRadix);
+  L.scan_status = take(8 * (size_t)(L.tilesN > 0 ? L.tilesN : 1));
+  L.hist = take(4 * 2 * kMaxSortPasses * kRadix);
+  L.counters = take(4 * 64);
+  L.g2d = take(4 * 14 * nn);
+  L.total = off;
+  return L;
+}
+
+// Stage 1 (depth sort of Gaussians) + A2 scan.  The zeroed region
+// [status1 .. counters] must have been cleared by the caller.
+cudaError_t launch_bin_sort_stage1(const pgsag_projected* p, int n, const WsLayout& L, char* ws,
+                                   cudaStream_t st, const uint32_t** ids_sorted) {
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(ws + L.depth_keys[0]);
+  uint32_t* k1 = reinterpret_cast<uint32_t*>(ws + L.depth_keys[1]);
+  uint32_t* i0 = reinterpret_cast<uint32_t*>(ws + L.ids[0]);
+  uint32_t* i1 = reinterpret_cast<uint32_t*>(ws + L.ids[1]);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(ws + L.counters);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
+  {
+    KTimer kt_("A4_depth_keys", st);
+    depth_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, p->depth, p->tiles_touched, k0, i0);
+  }
+  bool in_a = true;
+  cudaError_t e = radix_sort(k0, i0, k1, i1, nullptr, (uint32_t)n, (uint32_t)n, 32,
+                             reinterpret_cast<uint32_t*>(ws + L.status1), (size_t)L.tiles1 * kRadix, hist,
+                             counters + CNT_SORT1, st, &in_a);
+  if (e != cudaSuccess) return e;
+  const uint32_t* ids = in_a ? i0 : i1;
+  *ids_sorted = ids;
+  {
+    KTimer kt_("A2_scan", st);
+    scan_kernel<<<L.tilesN, 256, 0, st>>>(n, p->tiles_touched, ids, reinterpret_cast<uint32_t*>(ws + L.offsets),
+                                          reinterpret_cast<unsigned long long*>(ws + L.scan_status),
+                                          counters + CNT_SCAN, reinterpret_cast<unsigned long long*>(counters + CNT_M));
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const Dims& d, int n,
+                                      uint32_t M, const uint32_t* ids_sorted, const WsLayout& L, char* ws,
+                                      pgsag_bins* bins, cudaStream_t st) {
+  uint32_t* counters = reinterpret_cast<uint32_t*>(ws + L.counters);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist) + kMaxSortPasses * kRadix;
+  const int ntiles = d.TX * d.TY;
+  int tile_bits = 0;
+  while ((1 << tile_bits) < ntiles) ++tile_bits;
+  const int npass = (tile_bits + kRadixBits - 1) / kRadixBits;
+  // emit into the buffer that makes the last pass land in bins
+  uint32_t *ek, *ev, *ok, *ov;
+  if (npass % 2 == 0) {
+    ek = bins->tile_keys; ev = bins->vals;
+    ok = reinterpret_cast<uint32_t*>(ws + L.dup_keys); ov = reinterpret_cast<uint32_t*>(ws + L.dup_vals);
+  } else {
+    ek = reinterpret_cast<uint32_t*>(ws + L.dup_keys); ev = reinterpret_cast<uint32_t*>(ws + L.dup_vals);
+    ok = bins->tile_keys; ov = bins->vals;
+  }
+  cudaMemsetAsync(bins->ranges, 0, sizeof(uint32_t) * 2 * (size_t)ntiles, st);
+  if (M == 0) return cudaGetLastError();
+  {
+    KTimer kt_("A3_duplicate", st);
+    duplicate_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, ids_sorted, reinterpret_cast<uint32_t*>(ws + L.offsets),
+                                                      p->tiles_touched, reinterpret_cast<const short4*>(p->rect),
+                                                      tm->active_bits, d, ek, ev);
+  }
+  bool in_a = true;
+  // look-back state for exactly the tiles this M needs
+  const size_t stride = (size_t)((M + kSortTile - 1) / kSortTile) * kRadix;
+  cudaMemsetAsync(ws + L.status2, 0, 4 * stride * (size_t)npass, st);
+  cudaError_t e = radix_sort(ek, ev, ok, ov, nullptr, M, M, tile_bits,
+                             reinterpret_cast<uint32_t*>(ws + L.status2), stride, hist,
+                             counters + CNT_SORT2, st, &in_a);
+  if (e != cudaSuccess) return e;
+  const int grid = min((int)((M + 255) / 256), num_sms() * 8);
+  {
+    KTimer kt_("A5_ranges", st);
+    ranges_kernel<<<grid, 256, 0, st>>>(bins->tile_keys, counters + CNT_M, bins->ranges);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace pgsag

@@ -1,0 +1,197 @@
+"""Thin Python driver over the C ABI: owns the device buffers (PyTorch is used
+for device memory and streams only) and calls pgsag_preprocess -> pgsag_bin_sort
+-> pgsag_render_fwd -> pgsag_render_bwd on the current torch stream.
+
+All arithmetic of the path runs in libpgsag.so; this module only allocates,
+marshals pointers and re-allocates the entry buffers when M outgrows them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+TILE = 16
+
+
+def make_camera(fx, fy, cx, cy, width, height, R, Cw, znear=0.01) -> L.Camera:
+    cam = L.Camera()
+    cam.fx, cam.fy, cam.cx, cam.cy = float(fx), float(fy), float(cx), float(cy)
+    cam.width, cam.height = int(width), int(height)
+    Rf = [float(v) for v in (R.reshape(-1).tolist() if hasattr(R, "reshape") else R)]
+    Cf = [float(v) for v in (Cw.reshape(-1).tolist() if hasattr(Cw, "reshape") else Cw)]
+    for k in range(9):
+        cam.R[k] = Rf[k]
+    for k in range(3):
+        cam.C[k] = Cf[k]
+    cam.znear = float(znear)
+    return cam
+
+
+def camera_from(obj) -> L.Camera:
+    """From any object with fx, fy, cx, cy, width, height, R, C, znear (e.g. synth.scenes.Camera)."""
+    return make_camera(obj.fx, obj.fy, obj.cx, obj.cy, obj.width, obj.height, obj.R, obj.C,
+                       getattr(obj, "znear", 0.01))
+
+
+@dataclass
+class GaussianTensors:
+    mean: torch.Tensor     # (3, n) f32
+    scale: torch.Tensor    # (3, n)
+    rot: torch.Tensor      # (4, n)
+    opacity: torch.Tensor  # (n,)
+    sh: torch.Tensor       # ((deg+1)^2*3, n)
+    sh_degree: int
+
+    @property
+    def n(self):
+        return int(self.opacity.shape[0])
+
+    @staticmethod
+    def from_numpy(g, device="cuda"):
+        t = lambda a: torch.as_tensor(a, dtype=torch.float32).contiguous().to(device)
+        return GaussianTensors(t(g.mean), t(g.scale), t(g.rot), t(g.opacity), t(g.sh), int(g.sh_degree))
+
+    def struct(self) -> L.Gaussians:
+        s = L.Gaussians()
+        s.n, s.sh_degree = self.n, self.sh_degree
+        s.mean, s.scale, s.rot = self.mean.data_ptr(), self.scale.data_ptr(), self.rot.data_ptr()
+        s.opacity, s.sh = self.opacity.data_ptr(), self.sh.data_ptr()
+        return s
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Rasterizer:
+    """Buffers for one (n, width, height, sh_degree) problem; reusable across views."""
+
+    def __init__(self, n, width, height, sh_degree=3, capacity=None, device="cuda", counters=True):
+        self.n, self.W, self.H, self.deg = int(n), int(width), int(height), int(sh_degree)
+        self.device = torch.device(device)
+        dev = self.device
+        n = max(self.n, 1)
+        self.TX, self.TY = (self.W + TILE - 1) // TILE, (self.H + TILE - 1) // TILE
+        T = self.TX * self.TY
+        f32, i32, u8 = torch.float32, torch.int32, torch.uint8
+        e = lambda *shape, dtype=f32: torch.empty(*shape, dtype=dtype, device=dev)
+        # A0 / A1 outputs
+        self.tile_cnt = e(T, dtype=i32)
+        self.sat = e((self.TY + 1) * (self.TX + 1), dtype=i32)
+        self.active = e(T, dtype=i32)
+        self.n_active = e(1, dtype=i32)
+        self.active_bits = e(self.TY * ((self.TX + 31) // 32), dtype=i32)
+        self.mean2d = e(n, 2)
+        self.conic_o = e(n, 4)
+        self.depth = e(n)
+        self.rect = e(n, 4, dtype=torch.int16)
+        self.tiles_touched = e(n, dtype=i32)
+        self.rgb_d = e(n, 4)
+        self.ncam = e(n, 4)
+        self.flags = e(n, dtype=i32)
+        # A6 outputs
+        HW = self.H * self.W
+        self.img_C = torch.zeros(3, self.H, self.W, dtype=f32, device=dev)
+        self.img_N = torch.zeros(3, self.H, self.W, dtype=f32, device=dev)
+        self.img_D = torch.zeros(self.H, self.W, dtype=f32, device=dev)
+        self.img_A = torch.zeros(self.H, self.W, dtype=f32, device=dev)
+        self.img_Dep = torch.zeros(self.H, self.W, dtype=f32, device=dev)
+        self.img_T = torch.ones(self.H, self.W, dtype=f32, device=dev)
+        self.img_g = torch.zeros(self.H, self.W, dtype=i32, device=dev)
+        self.img_last = torch.full((self.H, self.W), -1, dtype=i32, device=dev)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev) if counters else None
+        # A8 outputs
+        K3 = (self.deg + 1) ** 2 * 3
+        self.dmean = e(3, n)
+        self.dscale = e(3, n)
+        self.drot = e(4, n)
+        self.dopacity = e(n)
+        self.dsh = torch.zeros(K3, n, dtype=f32, device=dev)
+        self.absgrad = e(n)
+        self.ranges = e(2 * T, dtype=i32)
+        self._alloc_bins(capacity if capacity is not None else max(1024, 8 * self.n))
+        self.M = 0
+        self._build_structs()
+        del HW, u8
+
+    # ------------------------------------------------------------ buffers
+    def _alloc_bins(self, cap):
+        self.capacity = int(cap)
+        self.tile_keys = torch.empty(max(self.capacity, 1), dtype=torch.int32, device=self.device)
+        self.vals = torch.empty(max(self.capacity, 1), dtype=torch.int32, device=self.device)
+        self.ws_bytes = L.workspace_size(self.n, self.W, self.H, self.capacity)
+        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device)
+
+    def _build_structs(self):
+        p = L.Projected()
+        p.mean2d, p.conic_o, p.depth = self.mean2d.data_ptr(), self.conic_o.data_ptr(), self.depth.data_ptr()
+        p.rect, p.tiles_touched = self.rect.data_ptr(), self.tiles_touched.data_ptr()
+        p.rgb_d, p.ncam, p.flags = self.rgb_d.data_ptr(), self.ncam.data_ptr(), self.flags.data_ptr()
+        self._proj = p
+        tm = L.TileMask()
+        tm.tile_cnt, tm.sat, tm.active = self.tile_cnt.data_ptr(), self.sat.data_ptr(), self.active.data_ptr()
+        tm.n_active, tm.active_bits = self.n_active.data_ptr(), self.active_bits.data_ptr()
+        self._tm = tm
+        b = L.Bins()
+        b.tile_keys, b.vals, b.ranges = self.tile_keys.data_ptr(), self.vals.data_ptr(), self.ranges.data_ptr()
+        b.capacity, b.n_dup = self.capacity, 0
+        self._bins = b
+        im = L.Image()
+        im.C, im.N, im.D, im.A = self.img_C.data_ptr(), self.img_N.data_ptr(), self.img_D.data_ptr(), \
+            self.img_A.data_ptr()
+        im.Dep, im.T, im.g, im.last = self.img_Dep.data_ptr(), self.img_T.data_ptr(), self.img_g.data_ptr(), \
+            self.img_last.data_ptr()
+        im.counters = self.counters.data_ptr() if self.counters is not None else None
+        self._img = im
+        gg = L.GaussianGrad()
+        gg.dmean, gg.dscale, gg.drot = self.dmean.data_ptr(), self.dscale.data_ptr(), self.drot.data_ptr()
+        gg.dopacity, gg.dsh, gg.absgrad2d = self.dopacity.data_ptr(), self.dsh.data_ptr(), self.absgrad.data_ptr()
+        self._grad = gg
+
+    # ---------------------------------------------------------- the path
+    def forward(self, g: GaussianTensors, cam: L.Camera, mask: torch.Tensor, bg=(0.0, 0.0, 0.0)):
+        assert g.n == self.n and g.sh_degree == self.deg
+        assert mask.dtype == torch.uint8 and tuple(mask.shape) == (self.H, self.W) and mask.is_contiguous()
+        st = _stream()
+        self._g = g.struct()
+        self._gt = g
+        self._cam = cam
+        self._mask = mask
+        self._bg = (C.c_float * 3)(*[float(v) for v in bg])
+        if self.counters is not None:
+            self.counters.zero_()
+        ws = C.c_void_p(self.ws.data_ptr())
+        L.preprocess(self._g, cam, C.c_void_p(mask.data_ptr()), self._tm, self._proj, ws, self.ws_bytes, st)
+        rc = L.bin_sort(self._proj, self._tm, cam, self.n, self._bins, ws, self.ws_bytes, st)
+        if rc == L.PGSAG_ECAPACITY:
+            self._alloc_bins(int(self._bins.n_dup * 1.25) + 1024)
+            self._build_structs()
+            ws = C.c_void_p(self.ws.data_ptr())
+            rc = L.bin_sort(self._proj, self._tm, cam, self.n, self._bins, ws, self.ws_bytes, st)
+            L.check(rc)
+        self.M = int(self._bins.n_dup)
+        L.render_fwd(self._proj, self._bins, self._tm, cam, C.c_void_p(mask.data_ptr()), self._bg, self._img, ws,
+                     self.ws_bytes, st)
+        return dict(C=self.img_C, N=self.img_N, D=self.img_D, A=self.img_A, Dep=self.img_Dep, T=self.img_T,
+                    g=self.img_g, last=self.img_last)
+
+    def backward(self, dC=None, dN=None, dD=None, dA=None, dDep=None):
+        ig = L.ImageGrad()
+        for k, t in (("dC", dC), ("dN", dN), ("dD", dD), ("dA", dA), ("dDep", dDep)):
+            if t is not None:
+                assert t.dtype == torch.float32 and t.is_contiguous() and t.device == self.device
+            setattr(ig, k, None if t is None else t.data_ptr())
+        self._keep = (dC, dN, dD, dA, dDep)
+        L.render_bwd(self._g, self._cam, self._proj, self._bins, self._tm, C.c_void_p(self._mask.data_ptr()),
+                     self._bg, self._img, ig, self._grad, C.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream())
+        K3 = (self.deg + 1) ** 2 * 3
+        return dict(dmean=self.dmean, dscale=self.dscale, drot=self.drot, dopacity=self.dopacity,
+                    dsh=self.dsh[:K3], absgrad2d=self.absgrad)
+
+    def stats(self):
+        c = self.counters.tolist() if self.counters is not None else [0, 0, 0, 0]
+        return dict(M=self.M, evaluated=c[0], blended=c[1], bwd_visited=c[2])

@@ -1,0 +1,110 @@
+"""Helpers for the -m gpu parity tests: run the CUDA path (through the C ABI)
+and the oracle on the same seeded scene, and compare with the DESIGN.md §6
+tolerances."""
+import numpy as np
+import torch
+
+import oracle
+from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+
+# Tolerances (BASELINE.json north_star; DESIGN.md §6 / reading R19)
+ABS_IMG = 1e-4        # C, N, D, A, T per masked pixel
+REL_DEP = 1e-4        # unbiased depth (a ratio)
+NEAR_ABS = 5e-3       # pixels the oracle flags as near a decision threshold (R18)
+GRAD_REL = 1e-3       # per element, relative to max(|ref|, 1e-2 * maxabs(class))
+GRAD_NORM = 1e-3      # per class ||d||/||ref||
+
+
+def run_gpu(scene, bg=(0.0, 0.0, 0.0), capacity=None, upstream=None, counters=True):
+    g = GaussianTensors.from_numpy(scene.gaussians)
+    cam = camera_from(scene.camera)
+    mask = torch.from_numpy(np.ascontiguousarray(scene.mask)).cuda()
+    r = Rasterizer(g.n, scene.camera.width, scene.camera.height, g.sh_degree, capacity=capacity,
+                   counters=counters)
+    # sentinel fill so unwritten (masked-out) pixels are detectable
+    for t in (r.img_C, r.img_N, r.img_D, r.img_A, r.img_Dep, r.img_T):
+        t.fill_(-7.0)
+    r.img_g.fill_(-7)
+    r.forward(g, cam, mask, bg)
+    res = {"r": r}
+    if upstream is not None:
+        up = {k: torch.from_numpy(v).cuda() for k, v in upstream.items()}
+        res["grads"] = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in r.backward(**up).items()}
+    torch.cuda.synchronize()
+    res["img"] = {k: v.detach().cpu().numpy() for k, v in dict(
+        C=r.img_C, N=r.img_N, D=r.img_D, A=r.img_A, Dep=r.img_Dep, T=r.img_T, g=r.img_g, last=r.img_last).items()}
+    res["vals"] = r.vals[:r.M].cpu().numpy().view(np.uint32)
+    res["tile_keys"] = r.tile_keys[:r.M].cpu().numpy().view(np.uint32)
+    res["ranges"] = r.ranges.cpu().numpy().view(np.uint32).reshape(-1, 2)
+    res["stats"] = r.stats()
+    return res
+
+
+def upstream_at(pix, H, W, seed, exclude=None):
+    """Random N(0,1) upstream gradients at the listed flat pixels, 0 elsewhere; returns (planar dict,
+    per-listed-pixel (npix, 9) array for the oracle)."""
+    rng = np.random.default_rng(seed)
+    per = rng.normal(size=(len(pix), 9))
+    if exclude is not None:
+        per[exclude] = 0.0
+    planes = {"dC": np.zeros((3, H * W), np.float32), "dN": np.zeros((3, H * W), np.float32),
+              "dD": np.zeros(H * W, np.float32), "dA": np.zeros(H * W, np.float32),
+              "dDep": np.zeros(H * W, np.float32)}
+    per32 = per.astype(np.float32)
+    planes["dC"][:, pix] = per32[:, 0:3].T
+    planes["dN"][:, pix] = per32[:, 3:6].T
+    planes["dD"][pix] = per32[:, 6]
+    planes["dA"][pix] = per32[:, 7]
+    planes["dDep"][pix] = per32[:, 8]
+    planes = {k: np.ascontiguousarray(v.reshape((3, H, W) if v.ndim == 2 else (H, W))) for k, v in planes.items()}
+    return planes, per32.astype(np.float64)
+
+
+def compare_pixels(gpu_img, ora, pix, W, vals):
+    """Element-wise forward parity on the listed pixels. Returns dict of max errors; asserts."""
+    near = ora["near"].astype(bool)
+    flat = lambda a: a.reshape(a.shape[0], -1) if a.ndim == 3 else a.reshape(-1)
+    C = flat(gpu_img["C"])[:, pix].T
+    N = flat(gpu_img["N"])[:, pix].T
+    D, A, Dep, T = (flat(gpu_img[k])[pix] for k in ("D", "A", "Dep", "T"))
+    g, last = flat(gpu_img["g"])[pix], flat(gpu_img["last"])[pix]
+    ok = ~near
+    errs = {}
+    for k, a, b in (("C", C, ora["C"]), ("N", N, ora["N"]), ("D", D, ora["D"]), ("A", A, ora["A"]),
+                    ("T", T, ora["T"])):
+        e = np.abs(a.astype(np.float64) - b.astype(np.float64))
+        e = e.max(axis=1) if e.ndim == 2 else e
+        errs[k] = float(e[ok].max()) if ok.any() else 0.0
+        assert errs[k] <= ABS_IMG, (k, errs[k], np.argmax(np.where(ok, e, 0)))
+        if near.any():
+            assert float(e[near].max()) <= NEAR_ABS, (k, "near", float(e[near].max()))
+    dv = (ora["Dep"] != 0) & ok
+    de = np.abs(Dep[dv].astype(np.float64) - ora["Dep"][dv]) / np.maximum(np.abs(ora["Dep"][dv]), 1e-6)
+    errs["Dep"] = float(de.max()) if de.size else 0.0
+    assert errs["Dep"] <= REL_DEP, errs["Dep"]
+    assert np.array_equal((Dep != 0)[ok], (ora["Dep"] != 0)[ok])
+    assert np.array_equal(g[ok], ora["g"][ok]), int((g[ok] != ora["g"][ok]).sum())
+    has = ok & (ora["last"] >= 0)
+    assert np.array_equal(vals[last[has]], ora["last"][has].astype(np.uint32))
+    assert (last[ok & (ora["last"] < 0)] == -1).all()
+    errs["n_near"] = int(near.sum())
+    return errs
+
+
+def compare_grads(gpu, ref, deg):
+    """Per-class gradient parity (reading R19)."""
+    K3 = (deg + 1) ** 2 * 3
+    classes = {"dmean": (gpu["dmean"], ref[0:3]), "dscale": (gpu["dscale"], ref[3:6]),
+               "drot": (gpu["drot"], ref[6:10]), "dopacity": (gpu["dopacity"], ref[10]),
+               "dsh": (gpu["dsh"][:K3], ref[11:11 + K3])}
+    report = {}
+    for k, (a, b) in classes.items():
+        a = np.asarray(a, np.float64)
+        scale = max(np.abs(b).max(), 1e-30)
+        den = np.maximum(np.abs(b), 1e-2 * scale)
+        el = float((np.abs(a - b) / den).max())
+        nrm = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+        report[k] = (el, nrm)
+        assert el <= GRAD_REL, (k, el)
+        assert nrm <= GRAD_NORM, (k, nrm)
+    return report

@@ -1,0 +1,99 @@
+"""Host-side checks of the C ABI (no GPU needed): the library builds for sm_100a,
+loads, exports every symbol include/pgsag.h declares, and its argument
+validation rejects bad calls before touching a device."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pgsag.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2501_01677_b200 import build
+    build.build()
+    from paper_2501_01677_b200 import _lib
+    return _lib
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(pgsag_\w+)\s*\(", src, re.M)))
+
+
+def test_header_declares_the_four_calls():
+    fns = declared_functions()
+    for f in ("pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd", "pgsag_render_bwd",
+              "pgsag_workspace_size", "pgsag_last_error"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(lib):
+    L = lib.lib()
+    for f in declared_functions():
+        assert hasattr(L, f), f
+    assert set(declared_functions()) == set(lib.SYMBOLS)
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True).stdout
+    for f in declared_functions():
+        assert re.search(rf"\bT {f}\b", out), f
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out, out
+
+
+def test_header_compiles_as_c(tmp_path):
+    src = tmp_path / "t.c"
+    src.write_text('#include "pgsag.h"\nint main(void){ pgsag_camera c; (void)c; return PGSAG_OK; }\n')
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.dirname(HEADER), "-c", str(src),
+                           "-o", str(tmp_path / "t.o")])
+
+
+def test_struct_layouts_match_header(lib, tmp_path):
+    """The ctypes mirror has the C sizes/offsets (checked against the compiled header)."""
+    prog = tmp_path / "s.c"
+    prog.write_text(r'''#include <stdio.h>
+#include <stddef.h>
+#include "pgsag.h"
+int main(void){
+ printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(pgsag_camera), sizeof(pgsag_gaussians),
+   sizeof(pgsag_projected), sizeof(pgsag_tilemask), sizeof(pgsag_bins), sizeof(pgsag_image),
+   sizeof(pgsag_image_grad), sizeof(pgsag_gaussian_grad), offsetof(pgsag_camera, znear), offsetof(pgsag_bins, n_dup));
+ return 0; }''')
+    exe = tmp_path / "s"
+    subprocess.check_call(["gcc", "-I", os.path.dirname(HEADER), str(prog), "-o", str(exe)])
+    got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    exp = [C.sizeof(lib.Camera), C.sizeof(lib.Gaussians), C.sizeof(lib.Projected), C.sizeof(lib.TileMask),
+           C.sizeof(lib.Bins), C.sizeof(lib.Image), C.sizeof(lib.ImageGrad), C.sizeof(lib.GaussianGrad),
+           lib.Camera.znear.offset, lib.Bins.n_dup.offset]
+    assert got == exp
+
+
+def test_workspace_size_monotone(lib):
+    a = lib.workspace_size(1000, 64, 64, 10000)
+    b = lib.workspace_size(2000, 64, 64, 10000)
+    c = lib.workspace_size(2000, 64, 64, 20000)
+    assert 0 < a < b < c
+    assert a % 256 == 0
+
+
+def test_invalid_arguments_rejected_on_host(lib):
+    L = lib.lib()
+    cam = lib.Camera()
+    cam.width, cam.height, cam.fx, cam.fy = 64, 64, 64.0, 64.0
+    rc = L.pgsag_preprocess(None, C.byref(cam), None, None, None, None, 0, None)
+    assert rc == lib.PGSAG_EINVAL and b"NULL" in L.pgsag_last_error()
+    g = lib.Gaussians()
+    g.n, g.sh_degree = 10, 4
+    rc = L.pgsag_preprocess(C.byref(g), C.byref(cam), None, None, None, None, 0, None)
+    assert rc == lib.PGSAG_EINVAL and b"sh_degree" in L.pgsag_last_error()
+    g.sh_degree, g.n = 3, 0
+    bad = lib.Camera()
+    rc = L.pgsag_preprocess(C.byref(g), C.byref(bad), None, None, None, None, 0, None)
+    assert rc == lib.PGSAG_EINVAL and b"width" in L.pgsag_last_error()
+    assert lib.version().startswith("pgsag-b200")
