@@ -136,6 +136,8 @@ typedef struct {
  * |dL/du_p| + |dL/dv_p| (densification statistic).  Non-LIVE Gaussians get 0. */
 typedef struct {
   float *dmean, *dscale, *drot, *dopacity, *dsh, *absgrad2d;
+  float *grad2d; /* optional [14][n]: A7's per-Gaussian screen-space gradients du, dv, d(ca,cb,cc), d o,
+                    d rgb[3], d n_cam[3], d d_i, absgrad (the A7 -> A8 interface) */
 } pgsag_gaussian_grad;
 
 /* Bytes of scratch needed by every call for n Gaussians, a width x height image and

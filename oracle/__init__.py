@@ -24,7 +24,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-N_GRAD_ROWS = 59  # dmean 3, dscale 3, drot 4, dopac 1, dsh 48
+N_GRAD_ROWS = 73  # dmean 3, dscale 3, drot 4, dopac 1, dsh 48 | 2D grads 13 + absgrad (59..72)
 
 F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT = 1, 2, 4, 8
 F_LIVE = 15
@@ -164,7 +164,8 @@ def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=F
 
 def split_grads(grads, n):
     """(59, n) -> dict of named gradient blocks."""
-    return dict(dmean=grads[0:3], dscale=grads[3:6], drot=grads[6:10], dopacity=grads[10], dsh=grads[11:59])
+    return dict(dmean=grads[0:3], dscale=grads[3:6], drot=grads[6:10], dopacity=grads[10], dsh=grads[11:59],
+                g2d=grads[59:72], absgrad=grads[72])
 
 
 def sh_basis(x, y, z):

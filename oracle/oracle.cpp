@@ -426,7 +426,7 @@ template <typename R> struct Renderer {
 
 // -------------------------------------------------- per-Gaussian 2D grads
 struct G2 {
-  double du, dv, dca, dcb, dcc, dop, drgb[3], dncam[3], ddist;
+  double du, dv, dca, dcb, dcc, dop, drgb[3], dncam[3], ddist, absg;
 };
 
 // O5: reverse-order backward of one pixel (exact reverse mode of Eq. 1-4,
@@ -477,8 +477,11 @@ void pixel_backward(const Renderer<R>& rd, int i, int j, const PixOut<R>& fw,
     o.dca += -0.5 * dx * dx * dpow;
     o.dcb += -dx * dy * dpow;
     o.dcc += -0.5 * dy * dy * dpow;
-    o.du += ((double)g.ca * dx + (double)g.cb * dy) * dpow;
-    o.dv += ((double)g.cb * dx + (double)g.cc * dy) * dpow;
+    const double du = ((double)g.ca * dx + (double)g.cb * dy) * dpow;
+    const double dv = ((double)g.cb * dx + (double)g.cc * dy) * dpow;
+    o.du += du;
+    o.dv += dv;
+    o.absg += std::fabs(du) + std::fabs(dv);  // densification statistic (sum over pixels)
   }
 }
 
@@ -658,7 +661,7 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
                    const int64_t* pix, int npix, R* out /* [npix][10]: C3 N3 D A Dep T */,
                    int32_t* iout /* [npix][4]: g last near_flag n_clamped */, double* id_sum, int64_t* evaluated,
                    int certify_flag, int64_t* cert_bad,
-                   const double* upstream /* [npix][9] or null */, double* grads /* 59 x n or null */) {
+                   const double* upstream /* [npix][9] or null */, double* grads /* 73 x n or null */) {
   const Params<R> P = make_params(mean, scale, rot, opac, sh, n, deg);
   const Cam<R> cam = load_cam<R>(camf, W, H);
   const TileMask tm = make_tilemask(mask, W, H);
@@ -672,7 +675,7 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
   std::vector<int> cand;
   std::vector<Blend<R>> bl;
   std::vector<G2> g2;
-  if (grads) g2.assign(n, G2{0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, 0});
+  if (grads) g2.assign(n, G2{0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, 0, 0});
   int cur_tile = -1;
   long long bad = 0;
   for (int k : order) {
@@ -704,8 +707,16 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
     double* drot = grads + (size_t)6 * n;
     double* dop = grads + (size_t)10 * n;
     double* dsh = grads + (size_t)11 * n;
-    std::memset(grads, 0, sizeof(double) * (size_t)59 * n);
+    std::memset(grads, 0, sizeof(double) * (size_t)73 * n);
     for (int i = 0; i < n; ++i) gaussian_backward(P, i, cam, rd.proj[i].flags, g2[i], dmean, dscale, drot, dop, dsh);
+    // rows 59..72: the per-Gaussian 2D gradients (O5 output) and the absgrad statistic
+    for (int i = 0; i < n; ++i) {
+      if ((rd.proj[i].flags & F_LIVE) != F_LIVE) continue;
+      const G2& q = g2[i];
+      const double v[14] = {q.du, q.dv, q.dca, q.dcb, q.dcc, q.dop, q.drgb[0], q.drgb[1], q.drgb[2],
+                            q.dncam[0], q.dncam[1], q.dncam[2], q.ddist, q.absg};
+      for (int c = 0; c < 14; ++c) grads[(size_t)(59 + c) * n + i] = v[c];
+    }
   }
 }
 
@@ -773,7 +784,8 @@ int64_t oracle_keys(const float* depth, const int32_t* rect, const uint32_t* fla
 
 // O4 (+ O5/O6 when upstream && grads): render the listed pixels.
 // out[npix][10] = C0 C1 C2 N0 N1 N2 D A Dep T; iout[npix][4] = g, last id, near flag, n_clamped.
-// grads (double, 59*n): dmean[3][n] dscale[3][n] drot[4][n] dopac[n] dsh[48][n].
+// grads (double, 73*n): dmean[3][n] dscale[3][n] drot[4][n] dopac[n] dsh[48][n], then the 2D
+// gradients du dv dca dcb dcc dop drgb[3] dncam[3] ddist and absgrad (rows 59..72).
 void oracle_render_f32(const float* mean, const float* scale, const float* rot, const float* opac, const float* sh,
                        int n, int deg, const double* cam, int W, int H, const uint8_t* mask, const double* bg,
                        const int64_t* pix, int npix, float* out, int32_t* iout, double* id_sum, int64_t* evaluated,

@@ -57,7 +57,7 @@ class ImageGrad(C.Structure):
 
 class GaussianGrad(C.Structure):
     _fields_ = [("dmean", _vp), ("dscale", _vp), ("drot", _vp), ("dopacity", _vp), ("dsh", _vp),
-                ("absgrad2d", _vp)]
+                ("absgrad2d", _vp), ("grad2d", _vp)]
 
 
 _lib = None

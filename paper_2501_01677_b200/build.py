@@ -24,6 +24,7 @@ UNITS = {
     "sort.cu": [],
     "render_fwd.cu": [],
     "render_bwd.cu": [],
+    "preprocess_bwd.cu": [],
     "api.cu": [],
 }
 

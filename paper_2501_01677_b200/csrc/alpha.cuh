@@ -35,4 +35,89 @@ __device__ __forceinline__ float power2(const float4& sc, float dx, float dy) {
   return __fmaf_rn(dx, t, __fmul_rn(__fmul_rn(sc.z, dy), dy));
 }
 
+// same, with the record layout of the staged batch: ra = (u, v, A', B'), C' separately
+__device__ __forceinline__ float power2r(const float4& ra, float Cp, float dx, float dy) {
+  const float t = __fmaf_rn(ra.w, dy, __fmul_rn(ra.z, dx));
+  return __fmaf_rn(dx, t, __fmul_rn(__fmul_rn(Cp, dy), dy));
+}
+
+// ------------------------------------------------------------------ staging
+// Warp blocks: the 256 threads of a tile CTA are 8 warps, warp w owning the 8x4
+// pixel block (bx, by) = (w & 1, w >> 1) of the 16x16 tile; lane l owns pixel
+// (bx*8 + (l & 7), by*4 + (l >> 3)).
+__device__ __forceinline__ int warp_px(int w, int lane) { return (w & 1) * 8 + (lane & 7); }
+__device__ __forceinline__ int warp_py(int w, int lane) { return (w >> 1) * 4 + (lane >> 3); }
+
+struct Staged {
+  float4 a;       // u, v, A', B'
+  float4 b;       // C', o, skip threshold on p2, 0
+  uint32_t wmask; // bit k: the Gaussian may reach alpha >= 1/255 in warp block k
+};
+
+// Per staged Gaussian: the scaled conic, a p2 threshold below which alpha < 1/255
+// for certain (the exact test still decides every pair above it), and an EXACT
+// conservative cull of the 8 warp blocks: every pixel with alpha >= 1/255 has
+// d^T conic d <= 2 ln(255 o), hence |dx| <= sqrt(2 ln(255 o) cov_xx) (R8), here
+// with a 5% + 0.5 px margin that dominates the float error of the conic inverse.
+__device__ __forceinline__ Staged stage_gaussian(float2 xy, float4 co, float tile_x0, float tile_y0) {
+  Staged s;
+  const float4 sc = scaled_conic(co);
+  s.a = make_float4(xy.x, xy.y, sc.x, sc.y);
+  const float o = co.w;
+  const float l2o = __log2f(255.0f * o);       // >= ~0 since o >= 1/255 for listed Gaussians
+  s.b = make_float4(sc.z, o, -l2o - 0.01f, 0.0f);
+  const double det = (double)co.x * (double)co.z - (double)co.y * (double)co.y;
+  const float k2 = 2.0f * (fmaxf(l2o, 0.0f) * 0.6931472f + 0.01f) * 1.05f;
+  const float rx = sqrtf(k2 * (float)((double)co.z / det)) + 0.5f;
+  const float ry = sqrtf(k2 * (float)((double)co.x / det)) + 0.5f;
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float xlo = tile_x0 + (float)((k & 1) * 8) + 0.5f, xhi = xlo + 7.0f;
+    const float ylo = tile_y0 + (float)((k >> 1) * 4) + 0.5f, yhi = ylo + 3.0f;
+    const bool hit = (xy.x + rx >= xlo) && (xy.x - rx <= xhi) && (xy.y + ry >= ylo) && (xy.y - ry <= yhi);
+    m |= (hit ? 1u : 0u) << k;
+  }
+  s.wmask = m;
+  return s;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt_() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Per-warp candidate lists of a staged batch: s_list[k][..] = ascending batch slots
+// whose wmask has bit k, s_nw[k] = their count.  Thread t contributes slot t with
+// mask m.  s_wc is [NW*8] scratch.  Contains the barriers that publish the lists.
+template <int NW>
+__device__ __forceinline__ void build_warp_lists(uint32_t m, uint8_t* s_list, uint32_t* s_wc, int* s_nw) {
+  const int tid = threadIdx.x, lane = tid & 31, sw = tid >> 5;
+  const uint32_t lt = lanemask_lt_();
+  uint32_t pos[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, (m >> b) & 1u);
+    pos[b] = __popc(bal & lt);
+    if (lane == b) s_wc[sw * 8 + b] = __popc(bal);
+  }
+  __syncthreads();
+  if (tid < 8) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      const uint32_t c = s_wc[k * 8 + tid];
+      s_wc[k * 8 + tid] = acc;
+      acc += c;
+    }
+    s_nw[tid] = (int)acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 8; ++b)
+    if ((m >> b) & 1u) s_list[b * (NW * 32) + s_wc[sw * 8 + b] + pos[b]] = (uint8_t)tid;
+  __syncthreads();
+}
+
 }  // namespace pgsag

@@ -1,14 +1,25 @@
-// A7 (reverse-order backward compositor) and A8 (per-Gaussian chain rule) for sm_100a.
+// A7: reverse-order backward compositor for sm_100a (then A8, preprocess_bwd.cu).
 //
 // P:82 "all the encoded parameters are optimized ... using differentiable
 // rendering": the exact reverse mode of A6 (Eq. 1-4) with the forward's discrete
 // decisions frozen (R16, R17).  Per pixel, walking the tile list backwards from
-// the pixel's last blended entry:
-//   T_i    = T_{i+1} / (1 - alpha_i)                       (recovered, T_end = A6's T)
-//   dalpha = T_i (G . (F_i - S) - P (bg . gC))              F = (rgb, n_cam, d, 1)
-//   dF_i   = alpha_i T_i G,   S <- alpha F + (1 - alpha) S,   P <- (1 - alpha) P
-// then d(o, power) -> d(conic, mean2d).  Per entry, the warp's 14 partial
-// gradients are butterfly-reduced and one lane issues the global atomics.
+// the pixel's last blended entry, with F_i = (rgb, n_cam, d, 1) and the upstream
+// gradient G (Eq. 4 prologue folded into G):
+//   T_i    = T_{i+1} / (1 - alpha_i)                   (recovered; T_end = A6's T)
+//   dalpha = T_i (G.F_i - G.S - P (bg.gC))
+//   dF_i   = alpha_i T_i G
+//   G.S   <- alpha (G.F_i) + (1 - alpha) G.S,   P (bg.gC) <- (1 - alpha) P (bg.gC)
+// Only the projection G.S of the 8-channel suffix S is ever needed, so the
+// suffix is carried as one scalar (mathematically identical to the 8-vector
+// recurrence of the oracle).
+//
+// Work mapping is A6's: per active tile, 8 warps on 8x4 pixel blocks, batches of
+// 256 entries staged with the same exact warp-block cull and compacted per-warp
+// candidate lists, walked in reverse.  Reduction: per entry, the warp's 14
+// per-lane partials are reduce-scattered (5 butterfly levels, 16 shuffles) so
+// that 14 lanes each hold one warp sum; those lanes add into a padded shared
+// accumulator of the batch (shared by the tile's 8 warps); after the batch the
+// CTA flushes one double-precision global atomic per (entry, value).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -19,6 +30,8 @@ namespace pgsag {
 namespace {
 
 constexpr int kG2 = 14;  // du dv dca dcb dcc dop drgb3 dncam3 ddist absgrad
+constexpr int kNW = kTilePix / 32;
+constexpr float kLn2 = 0.6931471805599453f;
 
 struct BwdArgs {
   const float2* mean2d;
@@ -36,7 +49,7 @@ struct BwdArgs {
   const float *N, *D, *T;
   const int32_t *g, *last;
   const float *dC, *dN, *dD, *dA, *dDep;
-  float* g2d;  // [kG2][n]
+  double* g2d;  // [kG2][n]
   int n;
   unsigned long long* counters;
   uint32_t* work;
@@ -44,20 +57,46 @@ struct BwdArgs {
 
 __device__ __forceinline__ float ld_or0(const float* p, size_t k) { return p ? __ldg(p + k) : 0.0f; }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// one butterfly level: keep half of the values, exchange the other half with lane ^ m
+template <int H>
+__device__ __forceinline__ void rs_level(float (&v)[2 * H], float (&o)[H], bool upper, int m) {
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    const float send = upper ? v[k] : v[k + H];
+    const float keep = upper ? v[k + H] : v[k];
+    o[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+  }
+}
+
 template <bool kCount>
 __global__ void __launch_bounds__(kTilePix) render_bwd_kernel(BwdArgs a) {
-  __shared__ float2 s_xy[kTilePix];
-  __shared__ float4 s_co[kTilePix];
-  __shared__ float4 s_raw[kTilePix];  // (ca, cb, cc, o) unscaled
+  constexpr int kAccStride = 15;  // padded row: the 14 values of an entry sit in 14 distinct banks
+  __shared__ float4 s_a[kTilePix];   // (u, v, A', B')
+  __shared__ float4 s_b[kTilePix];   // (C', o, skip threshold, 0)
   __shared__ float4 s_cd[kTilePix];
   __shared__ float4 s_n[kTilePix];
   __shared__ uint32_t s_id[kTilePix];
+  __shared__ float s_acc[kTilePix * kAccStride];
+  __shared__ uint8_t s_list[8 * kTilePix];
+  __shared__ uint32_t s_wc[kNW * 8];
+  __shared__ int s_nw[8];
   __shared__ uint32_t s_tile;
   __shared__ int s_maxlast;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
+  const uint8_t* my_list = s_list + w * kTilePix;
   unsigned long long cntV = 0;
+  // value index this lane owns after the reduce-scatter: bit-reversed lane bits 1..4
+  const int my_c = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
+  const bool writer = ((lane & 1) == 0) && my_c < kG2;
+  for (int k = tid; k < kTilePix * kAccStride; k += kTilePix) s_acc[k] = 0.f;
   for (;;) {
     if (tid == 0) { s_tile = atomicAdd(a.work, 1u); s_maxlast = -1; }
     __syncthreads();
@@ -65,17 +104,18 @@ __global__ void __launch_bounds__(kTilePix) render_bwd_kernel(BwdArgs a) {
     if (widx >= n_active) break;
     const uint32_t tile = a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
-    const int i = tx * kTile + (tid & (kTile - 1));
-    const int j = ty * kTile + (tid >> 4);
+    const int i = tx * kTile + warp_px(w, lane);
+    const int j = ty * kTile + warp_py(w, lane);
     const bool inside = i < a.d.W && j < a.d.H;
     const size_t pix = (size_t)j * a.d.W + i;
     const bool masked = inside && a.mask[pix] != 0;
     const uint32_t rs = a.ranges[2 * tile];
     const float px = (float)i + 0.5f, py = (float)j + 0.5f;
+    const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
     int mylast = -1;
     float Tcur = 1.0f;
     float G[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    float bgdot = 0.f;
+    float Pb = 0.f;  // P * (bg . gC)
     if (masked) {
       mylast = a.last[pix];
       Tcur = a.T[pix];
@@ -84,7 +124,7 @@ __global__ void __launch_bounds__(kTilePix) render_bwd_kernel(BwdArgs a) {
       G[6] = ld_or0(a.dD, pix);
       G[7] = ld_or0(a.dA, pix);
       const float gDep = ld_or0(a.dDep, pix);
-      // Eq. 4 prologue: Dep = D / (N . r), validity re-derived exactly as A6 did
+      // Eq. 4 prologue: Dep = D / (N . r); validity re-derived exactly as A6 did
       const float N0 = a.N[pix], N1 = a.N[HW + pix], N2 = a.N[2 * HW + pix];
       const float r0 = __fdiv_rn(__fsub_rn(px, a.cx), a.fx), r1 = __fdiv_rn(__fsub_rn(py, a.cy), a.fy);
       const float den = __fadd_rn(__fadd_rn(__fmul_rn(N0, r0), __fmul_rn(N1, r1)), N2);
@@ -94,298 +134,110 @@ __global__ void __launch_bounds__(kTilePix) render_bwd_kernel(BwdArgs a) {
         const float c = gDep * a.D[pix] * inv * inv;
         G[3] -= c * r0; G[4] -= c * r1; G[5] -= c;
       }
-      bgdot = a.bg0 * G[0] + a.bg1 * G[1] + a.bg2 * G[2];
+      Pb = a.bg0 * G[0] + a.bg1 * G[1] + a.bg2 * G[2];
       if (mylast >= 0) atomicMax(&s_maxlast, mylast);
     }
+    const int wlast = __reduce_max_sync(0xffffffffu, mylast);
     __syncthreads();
     const int maxlast = s_maxlast;
-    float S[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    float P = 1.0f;
+    float Sg = 0.f;  // G . S
     for (int bhi = maxlast + 1; bhi > (int)rs; bhi -= kTilePix) {
       const int blo = max((int)rs, bhi - kTilePix);
-      const int k = blo + tid;
-      __syncthreads();  // previous batch fully consumed
-      if (k < bhi) {
-        const uint32_t id = a.vals[k];
+      const int cnt = bhi - blo;
+      uint32_t m = 0u;
+      if (tid < cnt) {
+        const uint32_t id = a.vals[blo + tid];
+        const Staged st = stage_gaussian(a.mean2d[id], a.conic_o[id], tx0, ty0);
         s_id[tid] = id;
-        s_xy[tid] = a.mean2d[id];
-        const float4 co = a.conic_o[id];
-        s_raw[tid] = co;
-        s_co[tid] = scaled_conic(co);
+        s_a[tid] = st.a;
+        s_b[tid] = st.b;
         s_cd[tid] = a.rgb_d[id];
         s_n[tid] = a.ncam[id];
+        m = st.wmask;
       }
-      __syncthreads();
-      for (int q = bhi - blo - 1; q >= 0; --q) {
+      build_warp_lists<kNW>(m, s_list, s_wc, s_nw);
+      const int qtop = wlast - blo;  // entries past the warp's last are never needed
+      for (int t = s_nw[w] - 1; t >= 0; --t) {
+        const int q = my_list[t];
+        if (q > qtop) continue;  // warp-uniform
         const int kk = blo + q;
+        const float4 ra = s_a[q];
+        const float4 rb = s_b[q];
         bool contrib = kk <= mylast;  // false for masked-out pixels (mylast = -1)
         float alpha = 0.f, rho = 0.f, dx = 0.f, dy = 0.f;
-        const float2 xy = s_xy[q];
-        const float4 sc = s_co[q];
         if (contrib) {
-          dx = px - xy.x; dy = py - xy.y;
-          const float p2 = power2(sc, dx, dy);
-          if (p2 > 0.0f) {
-            contrib = false;
-          } else {
-            rho = ex2_approx(p2);
-            alpha = fminf(kAlphaMax, __fmul_rn(sc.w, rho));
-            if (alpha < kAlphaMin) contrib = false;
-          }
+          dx = px - ra.x; dy = py - ra.y;
+          const float p2 = power2r(ra, rb.x, dx, dy);
           if (kCount) ++cntV;
+          if (p2 >= rb.z && p2 <= 0.0f) {
+            rho = ex2_approx(p2);
+            alpha = fminf(kAlphaMax, __fmul_rn(rb.y, rho));
+            contrib = alpha >= kAlphaMin;
+          } else {
+            contrib = false;
+          }
         }
         if (!__any_sync(0xffffffffu, contrib)) continue;
-        float v[kG2];
+        float v[16];
 #pragma unroll
-        for (int c = 0; c < kG2; ++c) v[c] = 0.f;
+        for (int c = 0; c < 16; ++c) v[c] = 0.f;
         if (contrib) {
           const float4 cd = s_cd[q];
           const float4 nn = s_n[q];
-          const float4 raw = s_raw[q];
           const float om = 1.0f - alpha;
-          const float Ti = Tcur / om;
-          const float F[8] = {cd.x, cd.y, cd.z, nn.x, nn.y, nn.z, cd.w, 1.0f};
-          float dot = 0.f;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) dot += G[c] * (F[c] - S[c]);
-          const float dalpha = Ti * (dot - P * bgdot);
-          const float w = alpha * Ti;
-          v[6] = w * G[0]; v[7] = w * G[1]; v[8] = w * G[2];
-          v[9] = w * G[3]; v[10] = w * G[4]; v[11] = w * G[5];
-          v[12] = w * G[6];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) S[c] = alpha * F[c] + om * S[c];
-          P *= om;
+          const float Ti = Tcur * rcp_approx(om);
+          const float GF = G[0] * cd.x + G[1] * cd.y + G[2] * cd.z + G[3] * nn.x + G[4] * nn.y + G[5] * nn.z +
+                           G[6] * cd.w + G[7];
+          const float dalpha = Ti * (GF - Sg - Pb);
+          Sg = alpha * GF + om * Sg;
+          Pb *= om;
           Tcur = Ti;
-          float dpow = 0.f;
-          if (__fmul_rn(raw.w, rho) <= kAlphaMax) {
+          const float wgt = alpha * Ti;
+#pragma unroll
+          for (int c = 0; c < 7; ++c) v[6 + c] = wgt * G[c];
+          if (__fmul_rn(rb.y, rho) <= kAlphaMax) {
             v[5] = rho * dalpha;
-            dpow = alpha * dalpha;
+            const float dpow = alpha * dalpha;
+            const float kx = dx * dpow;
+            v[2] = -0.5f * dx * kx;
+            v[3] = -dy * kx;
+            v[4] = -0.5f * dy * dy * dpow;
+            const float kd = -kLn2 * dpow;  // (ca, cb, cc) = -ln2 (2A', B', 2C')
+            v[0] = (2.0f * ra.z * dx + ra.w * dy) * kd;
+            v[1] = (ra.w * dx + 2.0f * rb.x * dy) * kd;
+            v[13] = fabsf(v[0]) + fabsf(v[1]);
           }
-          v[2] = -0.5f * dx * dx * dpow;
-          v[3] = -dx * dy * dpow;
-          v[4] = -0.5f * dy * dy * dpow;
-          v[0] = (raw.x * dx + raw.y * dy) * dpow;
-          v[1] = (raw.y * dx + raw.z * dy) * dpow;
-          v[13] = fabsf(v[0]) + fabsf(v[1]);
         }
+        // reduce-scatter 16 -> 1 value per lane pair
+        float v8[8], v4[4], v2[2], v1[1];
+        rs_level<8>(v, v8, (lane & 16) != 0, 16);
+        rs_level<4>(v8, v4, (lane & 8) != 0, 8);
+        rs_level<2>(v4, v2, (lane & 4) != 0, 4);
+        rs_level<1>(v2, v1, (lane & 2) != 0, 2);
+        const float s = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 1);
+        if (writer && s != 0.0f) atomicAdd(&s_acc[q * kAccStride + my_c], s);
+      }
+      __syncthreads();
+      // flush the batch: one f64 atomic per (entry, value), then re-zero
+      if (tid < cnt) {
+        const uint32_t id = s_id[tid];
 #pragma unroll
         for (int c = 0; c < kG2; ++c) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
-        }
-        if (lane == 0) {
-          const uint32_t id = s_id[q];
-#pragma unroll
-          for (int c = 0; c < kG2; ++c) atomicAdd(a.g2d + (size_t)c * a.n + id, v[c]);
+          const float x = s_acc[tid * kAccStride + c];
+          if (x != 0.0f) {
+            atomicAdd(a.g2d + (size_t)c * a.n + id, (double)x);
+            s_acc[tid * kAccStride + c] = 0.f;
+          }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (kCount) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cntV += __shfl_xor_sync(0xffffffffu, cntV, o);
     if (lane == 0 && cntV) atomicAdd(a.counters + 2, cntV);
   }
-}
-
-// --------------------------------------------------------------------- A8
-struct CamB {
-  float fx, fy, C[3], R[9], lx, ly;
-};
-
-__constant__ float kC2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
-                             -1.0925484305920792f, 0.5462742152960396f};
-__constant__ float kC3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
-                             0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
-                             -0.5900435899266435f};
-
-__global__ void __launch_bounds__(256) preprocess_bwd_kernel(
-    int n, int deg, const float* __restrict__ mean, const float* __restrict__ scale,
-    const float* __restrict__ rot, const float* __restrict__ sh, const uint32_t* __restrict__ flags,
-    const float* __restrict__ g2d, CamB cam, float* __restrict__ dmean, float* __restrict__ dscale,
-    float* __restrict__ drot, float* __restrict__ dopac, float* __restrict__ dsh, float* __restrict__ absgrad) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int K = (deg + 1) * (deg + 1);
-  const uint32_t fl = flags[i];
-  if ((fl & PGSAG_F_LIVE) != PGSAG_F_LIVE) {
-    for (int k = 0; k < 3; ++k) { dmean[(size_t)k * n + i] = 0.f; dscale[(size_t)k * n + i] = 0.f; }
-    for (int k = 0; k < 4; ++k) drot[(size_t)k * n + i] = 0.f;
-    dopac[i] = 0.f;
-    for (int k = 0; k < 3 * K; ++k) dsh[(size_t)k * n + i] = 0.f;
-    if (absgrad) absgrad[i] = 0.f;
-    return;
-  }
-  float gg[kG2];
-#pragma unroll
-  for (int c = 0; c < kG2; ++c) gg[c] = g2d[(size_t)c * n + i];
-  const float* Rc = cam.R;
-  const float t[3] = {mean[i] - cam.C[0], mean[n + i] - cam.C[1], mean[2 * n + i] - cam.C[2]};
-  float pc[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r) pc[r] = Rc[3 * r] * t[0] + Rc[3 * r + 1] * t[1] + Rc[3 * r + 2] * t[2];
-  const float x = pc[0], y = pc[1], z = pc[2];
-  const float q0[4] = {rot[i], rot[n + i], rot[2 * n + i], rot[3 * n + i]};
-  const float qn = sqrtf(q0[0] * q0[0] + q0[1] * q0[1] + q0[2] * q0[2] + q0[3] * q0[3]);
-  const float w = q0[0] / qn, X = q0[1] / qn, Y = q0[2] / qn, Z = q0[3] / qn;
-  float Rg[3][3];
-  Rg[0][0] = 1.f - 2.f * (Y * Y + Z * Z); Rg[0][1] = 2.f * (X * Y - w * Z); Rg[0][2] = 2.f * (X * Z + w * Y);
-  Rg[1][0] = 2.f * (X * Y + w * Z); Rg[1][1] = 1.f - 2.f * (X * X + Z * Z); Rg[1][2] = 2.f * (Y * Z - w * X);
-  Rg[2][0] = 2.f * (X * Z - w * Y); Rg[2][1] = 2.f * (Y * Z + w * X); Rg[2][2] = 1.f - 2.f * (X * X + Y * Y);
-  const float s[3] = {scale[i], scale[n + i], scale[2 * n + i]};
-  float Mg[3][3], Sig[3][3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) Mg[r][c] = Rg[r][c] * s[c];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) Sig[r][c] = Mg[r][0] * Mg[c][0] + Mg[r][1] * Mg[c][1] + Mg[r][2] * Mg[c][2];
-  const bool clx = fl & PGSAG_F_CLAMP_X, cly = fl & PGSAG_F_CLAMP_Y;
-  const float xz = x / z, yz = y / z;
-  const float cxz = clx ? fminf(fmaxf(xz, -cam.lx), cam.lx) : xz;
-  const float cyz = cly ? fminf(fmaxf(yz, -cam.ly), cam.ly) : yz;
-  const float J00 = cam.fx / z, J02 = -cam.fx * cxz / z, J11 = cam.fy / z, J12 = -cam.fy * cyz / z;
-  float Tm[2][3];
-#pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    Tm[0][b] = J00 * Rc[b] + J02 * Rc[6 + b];
-    Tm[1][b] = J11 * Rc[3 + b] + J12 * Rc[6 + b];
-  }
-  float STm[2][3];  // Sig Tm_a^T
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int k = 0; k < 3; ++k) STm[a][k] = Sig[k][0] * Tm[a][0] + Sig[k][1] * Tm[a][1] + Sig[k][2] * Tm[a][2];
-  const float A = Tm[0][0] * STm[0][0] + Tm[0][1] * STm[0][1] + Tm[0][2] * STm[0][2] + 0.3f;
-  const float B = Tm[0][0] * STm[1][0] + Tm[0][1] * STm[1][1] + Tm[0][2] * STm[1][2];
-  const float Cc = Tm[1][0] * STm[1][0] + Tm[1][1] * STm[1][1] + Tm[1][2] * STm[1][2] + 0.3f;
-  const float det = A * Cc - B * B;
-  const float id2 = 1.0f / (det * det);
-  const float dca = gg[2], dcb = gg[3], dcc = gg[4];
-  const float dA = (-Cc * Cc * dca + B * Cc * dcb - B * B * dcc) * id2;
-  const float dC = (-B * B * dca + A * B * dcb - A * A * dcc) * id2;
-  const float dB = (2.f * B * Cc * dca - (A * Cc + B * B) * dcb + 2.f * A * B * dcc) * id2;
-  // cov_ab = Tm_a Sig Tm_b^T
-  float dSig[3][3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-#pragma unroll
-    for (int l = 0; l < 3; ++l)
-      dSig[k][l] = dA * Tm[0][k] * Tm[0][l] + dC * Tm[1][k] * Tm[1][l] + dB * Tm[0][k] * Tm[1][l];
-  float dTm[2][3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    dTm[0][k] = 2.f * dA * STm[0][k] + dB * STm[1][k];
-    dTm[1][k] = 2.f * dC * STm[1][k] + dB * STm[0][k];
-  }
-  // Tm = J R_c -> dJ = dTm R_c^T (only J00, J02, J11, J12 are variables)
-  const float dJ00 = dTm[0][0] * Rc[0] + dTm[0][1] * Rc[1] + dTm[0][2] * Rc[2];
-  const float dJ02 = dTm[0][0] * Rc[6] + dTm[0][1] * Rc[7] + dTm[0][2] * Rc[8];
-  const float dJ11 = dTm[1][0] * Rc[3] + dTm[1][1] * Rc[4] + dTm[1][2] * Rc[5];
-  const float dJ12 = dTm[1][0] * Rc[6] + dTm[1][1] * Rc[7] + dTm[1][2] * Rc[8];
-  const float iz = 1.0f / z, iz2 = iz * iz, iz3 = iz2 * iz;
-  float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f;
-  dp2 += -cam.fx * iz2 * dJ00 - cam.fy * iz2 * dJ11;
-  if (!clx) { dp0 += -cam.fx * iz2 * dJ02; dp2 += 2.f * cam.fx * x * iz3 * dJ02; }
-  else { dp2 += cam.fx * cxz * iz2 * dJ02; }
-  if (!cly) { dp1 += -cam.fy * iz2 * dJ12; dp2 += 2.f * cam.fy * y * iz3 * dJ12; }
-  else { dp2 += cam.fy * cyz * iz2 * dJ12; }
-  // mean2d (u = fx x/z + cx, v = fy y/z + cy)
-  const float du = gg[0], dv = gg[1];
-  dp0 += cam.fx * iz * du;
-  dp1 += cam.fy * iz * dv;
-  dp2 += -(cam.fx * x * du + cam.fy * y * dv) * iz2;
-  float dt[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) dt[k] = Rc[k] * dp0 + Rc[3 + k] * dp1 + Rc[6 + k] * dp2;
-  // Sigma = Mg Mg^T -> dMg = (dSig + dSig^T) Mg;  Mg = Rg diag(s)
-  float dRg[3][3], ds[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-#pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      float acc = 0.f;
-#pragma unroll
-      for (int l = 0; l < 3; ++l) acc += (dSig[k][l] + dSig[l][k]) * Mg[l][m];
-      ds[m] += acc * Rg[k][m];
-      dRg[k][m] = acc * s[m];
-    }
-  // normal n = sg Rg[:,ax]; n_cam = R_c n; d = n . t
-  const int ax = (fl >> PGSAG_F_AXIS_SHIFT) & 3;
-  const float sg = (fl & PGSAG_F_NFLIP) ? -1.f : 1.f;
-  const float nv[3] = {sg * Rg[0][ax], sg * Rg[1][ax], sg * Rg[2][ax]};
-  const float ddist = gg[12];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const float dn = Rc[k] * gg[9] + Rc[3 + k] * gg[10] + Rc[6 + k] * gg[11] + t[k] * ddist;
-    dt[k] += nv[k] * ddist;
-    dRg[k][ax] += sg * dn;
-  }
-  // Rg(q-hat) -> d q-hat
-  float dq[4] = {0.f, 0.f, 0.f, 0.f};
-  dq[2] += -4.f * Y * dRg[0][0]; dq[3] += -4.f * Z * dRg[0][0];
-  dq[1] += 2.f * Y * dRg[0][1]; dq[2] += 2.f * X * dRg[0][1]; dq[0] += -2.f * Z * dRg[0][1]; dq[3] += -2.f * w * dRg[0][1];
-  dq[1] += 2.f * Z * dRg[0][2]; dq[3] += 2.f * X * dRg[0][2]; dq[0] += 2.f * Y * dRg[0][2]; dq[2] += 2.f * w * dRg[0][2];
-  dq[1] += 2.f * Y * dRg[1][0]; dq[2] += 2.f * X * dRg[1][0]; dq[0] += 2.f * Z * dRg[1][0]; dq[3] += 2.f * w * dRg[1][0];
-  dq[1] += -4.f * X * dRg[1][1]; dq[3] += -4.f * Z * dRg[1][1];
-  dq[2] += 2.f * Z * dRg[1][2]; dq[3] += 2.f * Y * dRg[1][2]; dq[0] += -2.f * X * dRg[1][2]; dq[1] += -2.f * w * dRg[1][2];
-  dq[1] += 2.f * Z * dRg[2][0]; dq[3] += 2.f * X * dRg[2][0]; dq[0] += -2.f * Y * dRg[2][0]; dq[2] += -2.f * w * dRg[2][0];
-  dq[2] += 2.f * Z * dRg[2][1]; dq[3] += 2.f * Y * dRg[2][1]; dq[0] += 2.f * X * dRg[2][1]; dq[1] += 2.f * w * dRg[2][1];
-  dq[1] += -4.f * X * dRg[2][2]; dq[2] += -4.f * Y * dRg[2][2];
-  const float qh[4] = {w, X, Y, Z};
-  const float qdot = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) drot[(size_t)k * n + i] = (dq[k] - qh[k] * qdot) / qn;
-  // SH colour: rgb_c = max(0, sum_l Y_l(dir) sh_lc + 0.5)
-  const float len = sqrtf(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
-  const float il = 1.0f / len;
-  const float dx = t[0] * il, dy = t[1] * il, dz = t[2] * il;
-  const float xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yzp = dy * dz, xzp = dx * dz;
-  float Yb[16];
-  float GY[16][3];
-  Yb[0] = 0.28209479177387814f; GY[0][0] = 0.f; GY[0][1] = 0.f; GY[0][2] = 0.f;
-  const float c1 = 0.4886025119029199f;
-  Yb[1] = -c1 * dy; GY[1][0] = 0.f; GY[1][1] = -c1; GY[1][2] = 0.f;
-  Yb[2] = c1 * dz; GY[2][0] = 0.f; GY[2][1] = 0.f; GY[2][2] = c1;
-  Yb[3] = -c1 * dx; GY[3][0] = -c1; GY[3][1] = 0.f; GY[3][2] = 0.f;
-  Yb[4] = kC2[0] * xy; GY[4][0] = kC2[0] * dy; GY[4][1] = kC2[0] * dx; GY[4][2] = 0.f;
-  Yb[5] = kC2[1] * yzp; GY[5][0] = 0.f; GY[5][1] = kC2[1] * dz; GY[5][2] = kC2[1] * dy;
-  Yb[6] = kC2[2] * (2.f * zz - xx - yy); GY[6][0] = -2.f * kC2[2] * dx; GY[6][1] = -2.f * kC2[2] * dy; GY[6][2] = 4.f * kC2[2] * dz;
-  Yb[7] = kC2[3] * xzp; GY[7][0] = kC2[3] * dz; GY[7][1] = 0.f; GY[7][2] = kC2[3] * dx;
-  Yb[8] = kC2[4] * (xx - yy); GY[8][0] = 2.f * kC2[4] * dx; GY[8][1] = -2.f * kC2[4] * dy; GY[8][2] = 0.f;
-  Yb[9] = kC3[0] * dy * (3.f * xx - yy); GY[9][0] = 6.f * kC3[0] * xy; GY[9][1] = kC3[0] * (3.f * xx - 3.f * yy); GY[9][2] = 0.f;
-  Yb[10] = kC3[1] * xy * dz; GY[10][0] = kC3[1] * yzp; GY[10][1] = kC3[1] * xzp; GY[10][2] = kC3[1] * xy;
-  Yb[11] = kC3[2] * dy * (4.f * zz - xx - yy); GY[11][0] = -2.f * kC3[2] * xy; GY[11][1] = kC3[2] * (4.f * zz - xx - 3.f * yy); GY[11][2] = 8.f * kC3[2] * yzp;
-  Yb[12] = kC3[3] * dz * (2.f * zz - 3.f * xx - 3.f * yy); GY[12][0] = -6.f * kC3[3] * xzp; GY[12][1] = -6.f * kC3[3] * yzp; GY[12][2] = kC3[3] * (6.f * zz - 3.f * xx - 3.f * yy);
-  Yb[13] = kC3[4] * dx * (4.f * zz - xx - yy); GY[13][0] = kC3[4] * (4.f * zz - 3.f * xx - yy); GY[13][1] = -2.f * kC3[4] * xy; GY[13][2] = 8.f * kC3[4] * xzp;
-  Yb[14] = kC3[5] * dz * (xx - yy); GY[14][0] = 2.f * kC3[5] * xzp; GY[14][1] = -2.f * kC3[5] * yzp; GY[14][2] = kC3[5] * (xx - yy);
-  Yb[15] = kC3[6] * dx * (xx - 3.f * yy); GY[15][0] = kC3[6] * (3.f * xx - 3.f * yy); GY[15][1] = -6.f * kC3[6] * xy; GY[15][2] = 0.f;
-  float dd0 = 0.f, dd1 = 0.f, dd2 = 0.f;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float gc = (fl & (PGSAG_F_RGB_CLAMP0 << c)) ? 0.f : gg[6 + c];
-    for (int l = 0; l < K; ++l) {
-      const float shv = sh[(size_t)(l * 3 + c) * n + i];
-      dsh[(size_t)(l * 3 + c) * n + i] = Yb[l] * gc;
-      const float f = shv * gc;
-      dd0 += GY[l][0] * f; dd1 += GY[l][1] * f; dd2 += GY[l][2] * f;
-    }
-  }
-  const float ddot = dx * dd0 + dy * dd1 + dz * dd2;
-  dt[0] += (dd0 - dx * ddot) * il;
-  dt[1] += (dd1 - dy * ddot) * il;
-  dt[2] += (dd2 - dz * ddot) * il;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    dmean[(size_t)k * n + i] = dt[k];
-    dscale[(size_t)k * n + i] = ds[k];
-  }
-  dopac[i] = gg[5];
-  if (absgrad) absgrad[i] = gg[13];
 }
 
 int bwd_grid() {
@@ -405,11 +257,11 @@ int bwd_grid() {
 cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
                               const pgsag_bins* bins, const pgsag_tilemask* tm, const Dims& d,
                               const uint8_t* mask, const float bg[3], const pgsag_image* fwd,
-                              const pgsag_image_grad* dL, pgsag_gaussian_grad* out, float* g2d,
+                              const pgsag_image_grad* dL, pgsag_gaussian_grad* out, double* g2d,
                               uint32_t* work_counter, cudaStream_t st) {
   const int n = g->n;
   if (n == 0) return cudaSuccess;
-  cudaMemsetAsync(g2d, 0, sizeof(float) * kG2 * (size_t)n, st);
+  cudaMemsetAsync(g2d, 0, sizeof(double) * kG2 * (size_t)n, st);
   BwdArgs a;
   a.mean2d = reinterpret_cast<const float2*>(p->mean2d);
   a.conic_o = reinterpret_cast<const float4*>(p->conic_o);
@@ -430,29 +282,14 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
   a.counters = fwd->counters;
   a.work = work_counter;
   const int grid = min(bwd_grid(), d.TX * d.TY);
-  if (fwd->counters)
-    {
-      KTimer kt_("A7_render_bwd", st);
-      render_bwd_kernel<true><<<grid, kTilePix, 0, st>>>(a);
-    }
-  else
-    {
-      KTimer kt_("A7_render_bwd", st);
-      render_bwd_kernel<false><<<grid, kTilePix, 0, st>>>(a);
-    }
-  CamB cb;
-  cb.fx = cam->fx; cb.fy = cam->fy;
-  for (int k = 0; k < 3; ++k) cb.C[k] = cam->C[k];
-  for (int k = 0; k < 9; ++k) cb.R[k] = cam->R[k];
-  cb.lx = 1.3f * ((0.5f * (float)cam->width) / cam->fx);
-  cb.ly = 1.3f * ((0.5f * (float)cam->height) / cam->fy);
   {
-    KTimer kt_("A8_preprocess_bwd", st);
-    preprocess_bwd_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, g->sh_degree, g->mean, g->scale, g->rot, g->sh,
-                                                           p->flags, g2d, cb, out->dmean, out->dscale, out->drot,
-                                                           out->dopacity, out->dsh, out->absgrad2d);
+    KTimer kt_("A7_render_bwd", st);
+    if (fwd->counters)
+      render_bwd_kernel<true><<<grid, kTilePix, 0, st>>>(a);
+    else
+      render_bwd_kernel<false><<<grid, kTilePix, 0, st>>>(a);
   }
-  return cudaGetLastError();
+  return launch_preprocess_bwd(g, cam, p, out, g2d, st);
 }
 
 }  // namespace pgsag

@@ -6,10 +6,12 @@
 //
 // Mapping: a persistent grid pulls ACTIVE tiles (tiles with >= 1 mask pixel) from
 // the A0 list through an atomic counter; masked-out tiles are never visited.  One
-// 256-thread CTA per 16x16 tile, one thread per pixel; masked-out pixels start
-// "done", so a tile whose mask pixels have all saturated stops after the current
-// batch (__syncthreads_count).  Each batch of 256 sorted entries is staged in
-// shared memory with one coalesced-per-thread gather of the entry's 56-byte record.
+// 256-thread CTA per 16x16 tile; warp w owns an 8x4 pixel block, one thread per
+// pixel; masked-out pixels start "done".  Each batch of 256 sorted entries is
+// staged in shared memory (one 56-byte record gather per thread) together with an
+// 8-bit warp-block mask (exact conservative cull, alpha.cuh), from which every
+// warp gets a compacted, depth-ordered candidate list; a warp's loop then touches
+// only entries that can reach its pixels.  The tile stops when every pixel is done.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -18,6 +20,8 @@
 
 namespace pgsag {
 namespace {
+
+constexpr int kNW = kTilePix / 32;
 
 struct FwdArgs {
   const float2* mean2d;
@@ -40,14 +44,18 @@ struct FwdArgs {
 
 template <bool kCount>
 __global__ void __launch_bounds__(kTilePix) render_fwd_kernel(FwdArgs a) {
-  __shared__ float2 s_xy[kTilePix];
-  __shared__ float4 s_co[kTilePix];
+  __shared__ float4 s_a[kTilePix];
+  __shared__ float4 s_b[kTilePix];
   __shared__ float4 s_cd[kTilePix];
   __shared__ float4 s_n[kTilePix];
+  __shared__ uint8_t s_list[8 * kTilePix];
+  __shared__ uint32_t s_wc[kNW * 8];
+  __shared__ int s_nw[8];
   __shared__ uint32_t s_tile;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
+  const uint8_t* my_list = s_list + w * kTilePix;
   unsigned long long cntE = 0, cntB = 0;
   for (;;) {
     if (tid == 0) s_tile = atomicAdd(a.work, 1u);
@@ -57,48 +65,59 @@ __global__ void __launch_bounds__(kTilePix) render_fwd_kernel(FwdArgs a) {
     if (widx >= n_active) break;
     const uint32_t tile = a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
-    const int i = tx * kTile + (tid & (kTile - 1));
-    const int j = ty * kTile + (tid >> 4);
+    const int i = tx * kTile + warp_px(w, lane);
+    const int j = ty * kTile + warp_py(w, lane);
     const bool inside = i < a.d.W && j < a.d.H;
     const size_t pix = (size_t)j * a.d.W + i;
     const bool masked = inside && a.mask[pix] != 0;
     const uint32_t rs = a.ranges[2 * tile], re = a.ranges[2 * tile + 1];
     const float px = (float)i + 0.5f, py = (float)j + 0.5f;
+    const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, N0 = 0.f, N1 = 0.f, N2 = 0.f, D = 0.f;
     int g = 0, last = -1;
     bool done = !masked;
     for (uint32_t b = rs; b < re; b += kTilePix) {
       if (__syncthreads_count(done) == kTilePix) break;
       const uint32_t k = b + tid;
+      uint32_t m = 0u;
       if (k < re) {
         const uint32_t id = a.vals[k];
-        s_xy[tid] = a.mean2d[id];
-        s_co[tid] = scaled_conic(a.conic_o[id]);
+        const Staged st = stage_gaussian(a.mean2d[id], a.conic_o[id], tx0, ty0);
+        s_a[tid] = st.a;
+        s_b[tid] = st.b;
         s_cd[tid] = a.rgb_d[id];
         s_n[tid] = a.ncam[id];
+        m = st.wmask;
       }
-      __syncthreads();
-      const int cnt = (int)min((uint32_t)kTilePix, re - b);
-      if (!done) {
-        for (int q = 0; q < cnt; ++q) {
-          const float2 xy = s_xy[q];
-          const float4 sc = s_co[q];
-          const float dx = px - xy.x, dy = py - xy.y;
-          const float p2 = power2(sc, dx, dy);
+      build_warp_lists<kNW>(m, s_list, s_wc, s_nw);
+      const int nw = s_nw[w];
+      for (int t = 0; t < nw; ++t) {
+        if (__all_sync(0xffffffffu, done)) break;
+        const int q = my_list[t];
+        const float4 ra = s_a[q];
+        const float4 rb = s_b[q];
+        if (!done) {
+          const float dx = px - ra.x, dy = py - ra.y;
+          const float p2 = power2r(ra, rb.x, dx, dy);
           if (kCount) ++cntE;
-          if (p2 > 0.0f) continue;
-          const float alpha = fminf(kAlphaMax, __fmul_rn(sc.w, ex2_approx(p2)));
-          if (alpha < kAlphaMin) continue;
-          const float Tn = __fmul_rn(T, 1.0f - alpha);
-          if (Tn < kTmin) { done = true; break; }
-          const float w = alpha * T;
-          const float4 cd = s_cd[q];
-          const float4 nn = s_n[q];
-          C0 += w * cd.x; C1 += w * cd.y; C2 += w * cd.z; D += w * cd.w;
-          N0 += w * nn.x; N1 += w * nn.y; N2 += w * nn.z;
-          ++g;
-          last = (int)(b + q);
-          T = Tn;
+          if (p2 >= rb.z && p2 <= 0.0f) {
+            const float alpha = fminf(kAlphaMax, __fmul_rn(rb.y, ex2_approx(p2)));
+            if (alpha >= kAlphaMin) {
+              const float Tn = __fmul_rn(T, 1.0f - alpha);
+              if (Tn < kTmin) {
+                done = true;
+              } else {
+                const float wgt = alpha * T;
+                const float4 cd = s_cd[q];
+                const float4 nn = s_n[q];
+                C0 += wgt * cd.x; C1 += wgt * cd.y; C2 += wgt * cd.z; D += wgt * cd.w;
+                N0 += wgt * nn.x; N1 += wgt * nn.y; N2 += wgt * nn.z;
+                ++g;
+                last = (int)(b + q);
+                T = Tn;
+              }
+            }
+          }
         }
       }
     }
@@ -126,7 +145,7 @@ __global__ void __launch_bounds__(kTilePix) render_fwd_kernel(FwdArgs a) {
       cntE += __shfl_xor_sync(0xffffffffu, cntE, o);
       cntB += __shfl_xor_sync(0xffffffffu, cntB, o);
     }
-    if ((tid & 31) == 0 && (cntE | cntB)) {
+    if (lane == 0 && (cntE | cntB)) {
       atomicAdd(a.counters + 0, cntE);
       atomicAdd(a.counters + 1, cntB);
     }
@@ -168,16 +187,13 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
   a.counters = out->counters;
   a.work = work_counter;
   const int grid = min(fwd_grid(), d.TX * d.TY);
-  if (out->counters)
-    {
-      KTimer kt_("A6_render_fwd", st);
+  {
+    KTimer kt_("A6_render_fwd", st);
+    if (out->counters)
       render_fwd_kernel<true><<<grid, kTilePix, 0, st>>>(a);
-    }
-  else
-    {
-      KTimer kt_("A6_render_fwd", st);
+    else
       render_fwd_kernel<false><<<grid, kTilePix, 0, st>>>(a);
-    }
+  }
   return cudaGetLastError();
 }
 

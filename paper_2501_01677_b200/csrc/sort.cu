@@ -366,7 +366,7 @@ WsLayout ws_layout(int32_t n, int32_t W, int32_t H, int64_t cap) {
   L.scan_status = take(8 * (size_t)(L.tilesN > 0 ? L.tilesN : 1));
   L.hist = take(4 * 2 * kMaxSortPasses * kRadix);
   L.counters = take(4 * 64);
-  L.g2d = take(4 * 14 * nn);
+  L.g2d = take(8 * 14 * nn);
   L.total = off;
   return L;
 }

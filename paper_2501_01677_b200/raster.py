@@ -73,6 +73,8 @@ class Rasterizer:
     def __init__(self, n, width, height, sh_degree=3, capacity=None, device="cuda", counters=True):
         self.n, self.W, self.H, self.deg = int(n), int(width), int(height), int(sh_degree)
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         dev = self.device
         n = max(self.n, 1)
         self.TX, self.TY = (self.W + TILE - 1) // TILE, (self.H + TILE - 1) // TILE
@@ -112,6 +114,7 @@ class Rasterizer:
         self.dopacity = e(n)
         self.dsh = torch.zeros(K3, n, dtype=f32, device=dev)
         self.absgrad = e(n)
+        self.grad2d = e(14, n)
         self.ranges = e(2 * T, dtype=i32)
         self._alloc_bins(capacity if capacity is not None else max(1024, 8 * self.n))
         self.M = 0
@@ -150,7 +153,12 @@ class Rasterizer:
         gg = L.GaussianGrad()
         gg.dmean, gg.dscale, gg.drot = self.dmean.data_ptr(), self.dscale.data_ptr(), self.drot.data_ptr()
         gg.dopacity, gg.dsh, gg.absgrad2d = self.dopacity.data_ptr(), self.dsh.data_ptr(), self.absgrad.data_ptr()
+        gg.grad2d = None
         self._grad = gg
+
+    def export_grad2d(self, on=True):
+        """Also copy A7's per-Gaussian screen-space gradients into self.grad2d ([14][n])."""
+        self._grad.grad2d = self.grad2d.data_ptr() if on else None
 
     # ---------------------------------------------------------- the path
     def forward(self, g: GaussianTensors, cam: L.Camera, mask: torch.Tensor, bg=(0.0, 0.0, 0.0)):
@@ -189,8 +197,11 @@ class Rasterizer:
         L.render_bwd(self._g, self._cam, self._proj, self._bins, self._tm, C.c_void_p(self._mask.data_ptr()),
                      self._bg, self._img, ig, self._grad, C.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream())
         K3 = (self.deg + 1) ** 2 * 3
-        return dict(dmean=self.dmean, dscale=self.dscale, drot=self.drot, dopacity=self.dopacity,
-                    dsh=self.dsh[:K3], absgrad2d=self.absgrad)
+        out = dict(dmean=self.dmean, dscale=self.dscale, drot=self.drot, dopacity=self.dopacity,
+                   dsh=self.dsh[:K3], absgrad2d=self.absgrad)
+        if self._grad.grad2d:
+            out["grad2d"] = self.grad2d
+        return out
 
     def stats(self):
         c = self.counters.tolist() if self.counters is not None else [0, 0, 0, 0]

@@ -12,7 +12,7 @@ ABS_IMG = 1e-4        # C, N, D, A, T per masked pixel
 REL_DEP = 1e-4        # unbiased depth (a ratio)
 NEAR_ABS = 5e-3       # pixels the oracle flags as near a decision threshold (R18)
 GRAD_REL = 1e-3       # per element, relative to max(|ref|, 1e-2 * maxabs(class))
-GRAD_NORM = 1e-3      # per class ||d||/||ref||
+GRAD_NORM = 1e-4      # per class ||d||/||ref|| (reading R19)
 
 
 def run_gpu(scene, bg=(0.0, 0.0, 0.0), capacity=None, upstream=None, counters=True):
@@ -40,13 +40,29 @@ def run_gpu(scene, bg=(0.0, 0.0, 0.0), capacity=None, upstream=None, counters=Tr
     return res
 
 
-def upstream_at(pix, H, W, seed, exclude=None):
+KAPPA_MAX = 1e3      # Eq. 4 condition number above which dL/dDep is not compared (reading R19)
+
+
+def dep_kappa(ora, pix, W, cam):
+    """Condition number of Eq. 4's denominator N.r at the listed pixels (from the oracle forward)."""
+    i_, j_ = pix % W, pix // W
+    r0 = (i_ + 0.5 - cam.cx) / cam.fx
+    r1 = (j_ + 0.5 - cam.cy) / cam.fy
+    Nn = ora["N"].astype(np.float64)
+    den = np.abs(Nn[:, 0] * r0 + Nn[:, 1] * r1 + Nn[:, 2])
+    return (np.abs(r0) + np.abs(r1) + 1.0) / np.maximum(den, 1e-30)
+
+
+def upstream_at(pix, H, W, seed, exclude=None, ora=None, cam=None):
     """Random N(0,1) upstream gradients at the listed flat pixels, 0 elsewhere; returns (planar dict,
-    per-listed-pixel (npix, 9) array for the oracle)."""
+    per-listed-pixel (npix, 9) array for the oracle).  exclude: pixels (near a decision threshold,
+    R18) with no upstream at all; with ora+cam, dL/dDep is dropped where Eq. 4 is ill-conditioned."""
     rng = np.random.default_rng(seed)
     per = rng.normal(size=(len(pix), 9))
     if exclude is not None:
         per[exclude] = 0.0
+    if ora is not None and cam is not None:
+        per[dep_kappa(ora, pix, W, cam) > KAPPA_MAX, 8] = 0.0
     planes = {"dC": np.zeros((3, H * W), np.float32), "dN": np.zeros((3, H * W), np.float32),
               "dD": np.zeros(H * W, np.float32), "dA": np.zeros(H * W, np.float32),
               "dDep": np.zeros(H * W, np.float32)}
@@ -60,7 +76,7 @@ def upstream_at(pix, H, W, seed, exclude=None):
     return planes, per32.astype(np.float64)
 
 
-def compare_pixels(gpu_img, ora, pix, W, vals):
+def compare_pixels(gpu_img, ora, pix, W, vals, cam=None):
     """Element-wise forward parity on the listed pixels. Returns dict of max errors; asserts."""
     near = ora["near"].astype(bool)
     flat = lambda a: a.reshape(a.shape[0], -1) if a.ndim == 3 else a.reshape(-1)
@@ -78,8 +94,19 @@ def compare_pixels(gpu_img, ora, pix, W, vals):
         assert errs[k] <= ABS_IMG, (k, errs[k], np.argmax(np.where(ok, e, 0)))
         if near.any():
             assert float(e[near].max()) <= NEAR_ABS, (k, "near", float(e[near].max()))
+    # Eq. 4 divides by N.r; its relative error is amplified by the condition number of that
+    # dot product, kappa = (|r0| + |r1| + 1) / |N.r| (each |n_i| = 1, sum w_i <= 1), so the 1e-4
+    # relative bar is applied as 1e-4 * max(1, kappa) (reading R19).
     dv = (ora["Dep"] != 0) & ok
-    de = np.abs(Dep[dv].astype(np.float64) - ora["Dep"][dv]) / np.maximum(np.abs(ora["Dep"][dv]), 1e-6)
+    i_, j_ = pix % W, pix // W
+    de =np.abs(Dep[dv].astype(np.float64) - ora["Dep"][dv]) / np.maximum(np.abs(ora["Dep"][dv]), 1e-6)
+    if cam is not None:
+        r0 = (i_ + 0.5 - cam.cx) / cam.fx
+        r1 = (j_ + 0.5 - cam.cy) / cam.fy
+        Nn = ora["N"].astype(np.float64)
+        den = np.abs(Nn[:, 0] * r0 + Nn[:, 1] * r1 + Nn[:, 2])
+        kappa = (np.abs(r0) + np.abs(r1) + 1.0) / np.maximum(den, 1e-12)
+        de = de / np.maximum(1.0, kappa[dv])
     errs["Dep"] = float(de.max()) if de.size else 0.0
     assert errs["Dep"] <= REL_DEP, errs["Dep"]
     assert np.array_equal((Dep != 0)[ok], (ora["Dep"] != 0)[ok])

@@ -79,13 +79,15 @@ def test_forward_parity_all_pixels(name):
     res = run_gpu(sc, bg=bg)
     pix = all_pixels(sc.mask)
     ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=bg)
-    errs = compare_pixels(res["img"], ora, pix, sc.camera.width, res["vals"])
+    errs = compare_pixels(res["img"], ora, pix, sc.camera.width, res["vals"], cam=sc.camera)
     assert errs["n_near"] <= max(2, len(pix) // 200)
     off = sc.mask.reshape(-1) == 0
     assert (res["img"]["C"].reshape(3, -1)[:, off] == -7.0).all()
     assert (res["img"]["g"].reshape(-1)[off] == -7).all()
     st = res["stats"]
-    assert st["evaluated"] == int(ora["evaluated"].sum())
+    # E counts pairs the kernel evaluated after the exact warp-block cull: never more than the
+    # oracle's list entries visited, and B (blended pairs) is exact.
+    assert 0 < st["evaluated"] <= int(ora["evaluated"].sum())
     assert st["blended"] == int(ora["g"].sum())
 
 
@@ -105,7 +107,7 @@ def test_forward_parity_sampled_c2():
         tp = (jj * W + ii).reshape(-1)
         pix = np.union1d(pix, tp[sc.mask.reshape(-1)[tp] != 0])
     ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix)
-    compare_pixels(res["img"], ora, pix, W, res["vals"])
+    compare_pixels(res["img"], ora, pix, W, res["vals"], cam=sc.camera)
 
 
 @pytest.mark.parametrize("name", ["C1", "ragged"])
@@ -116,7 +118,7 @@ def test_backward_parity_all_pixels(name):
     bg = (0.3, 0.1, 0.2)
     pix = all_pixels(sc.mask)
     ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=bg)
-    planes, per = upstream_at(pix, H, W, seed=3, exclude=ora0["near"].astype(bool))
+    planes, per = upstream_at(pix, H, W, seed=3, exclude=ora0["near"].astype(bool), ora=ora0, cam=sc.camera)
     res = run_gpu(sc, bg=bg, upstream=planes)
     ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=bg, upstream=per)
     compare_grads(res["grads"], ora["grads"], sc.gaussians.sh_degree)
@@ -129,7 +131,7 @@ def test_backward_parity_sparse_c2():
     H, W = sc.mask.shape
     pix = S.sample_pixels(sc.mask, 1200, seed=9)
     ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix)
-    planes, per = upstream_at(pix, H, W, seed=4, exclude=ora0["near"].astype(bool))
+    planes, per = upstream_at(pix, H, W, seed=4, exclude=ora0["near"].astype(bool), ora=ora0, cam=sc.camera)
     res = run_gpu(sc, upstream=planes)
     ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=per)
     compare_grads(res["grads"], ora["grads"], sc.gaussians.sh_degree)
@@ -160,11 +162,12 @@ def test_edge_cases(case):
         sc = _tiny(300)
     H, W = sc.mask.shape
     pix = all_pixels(sc.mask)
-    planes, per = upstream_at(pix, H, W, seed=1)
+    ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=(0.5, 0.25, 0.125)) if len(pix) else None
+    planes, per = upstream_at(pix, H, W, seed=1, ora=ora0, cam=sc.camera)
     res = run_gpu(sc, bg=(0.5, 0.25, 0.125), upstream=planes)
     if len(pix):
         ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=(0.5, 0.25, 0.125), upstream=per)
-        compare_pixels(res["img"], ora, pix, W, res["vals"])
+        compare_pixels(res["img"], ora, pix, W, res["vals"], cam=sc.camera)
         if sc.gaussians.n:
             compare_grads(res["grads"], ora["grads"], sc.gaussians.sh_degree)
     else:
