@@ -42,44 +42,44 @@ __device__ __forceinline__ float power2r(const float4& ra, float Cp, float dx, f
 }
 
 // ------------------------------------------------------------------ staging
-// Warp blocks: the 256 threads of a tile CTA are 8 warps, warp w owning the 8x4
-// pixel block (bx, by) = (w & 1, w >> 1) of the 16x16 tile; lane l owns pixel
-// (bx*8 + (l & 7), by*4 + (l >> 3)).
-__device__ __forceinline__ int warp_px(int w, int lane) { return (w & 1) * 8 + (lane & 7); }
-__device__ __forceinline__ int warp_py(int w, int lane) { return (w >> 1) * 4 + (lane >> 3); }
+// A tile CTA has NW warps; warp w owns the BW x BH pixel block (w % (16/BW),
+// w / (16/BW)) of the 16x16 tile.  Each staged entry gets a bit mask of the
+// warp blocks it can reach (exact conservative cull below).
 
-struct Staged {
-  float4 a;       // u, v, A', B'
-  float4 b;       // C', o, skip threshold on p2, 0
-  uint32_t wmask; // bit k: the Gaussian may reach alpha >= 1/255 in warp block k
+// Staged batch record, 64 B: one LDS.128 per field.
+struct __align__(16) Rec {
+  float4 a;   // u, v, A', B'
+  float4 b;   // C', o, skip threshold on p2, 0
+  float4 cd;  // r, g, b, d_i
+  float4 n;   // n_cam, 0
 };
 
 // Per staged Gaussian: the scaled conic, a p2 threshold below which alpha < 1/255
 // for certain (the exact test still decides every pair above it), and an EXACT
-// conservative cull of the 8 warp blocks: every pixel with alpha >= 1/255 has
+// conservative cull of the warp blocks: every pixel with alpha >= 1/255 has
 // d^T conic d <= 2 ln(255 o), hence |dx| <= sqrt(2 ln(255 o) cov_xx) (R8), here
 // with a 5% + 0.5 px margin that dominates the float error of the conic inverse.
-__device__ __forceinline__ Staged stage_gaussian(float2 xy, float4 co, float tile_x0, float tile_y0) {
-  Staged s;
+template <int BW, int BH>
+__device__ __forceinline__ uint32_t stage_gaussian(float2 xy, float4 co, float tile_x0, float tile_y0, Rec& r) {
+  constexpr int NBX = 16 / BW, NB = NBX * (16 / BH);
   const float4 sc = scaled_conic(co);
-  s.a = make_float4(xy.x, xy.y, sc.x, sc.y);
+  r.a = make_float4(xy.x, xy.y, sc.x, sc.y);
   const float o = co.w;
-  const float l2o = __log2f(255.0f * o);       // >= ~0 since o >= 1/255 for listed Gaussians
-  s.b = make_float4(sc.z, o, -l2o - 0.01f, 0.0f);
+  const float l2o = __log2f(255.0f * o);  // >= ~0 since o >= 1/255 for listed Gaussians
+  r.b = make_float4(sc.z, o, -l2o - 0.01f, 0.0f);
   const double det = (double)co.x * (double)co.z - (double)co.y * (double)co.y;
   const float k2 = 2.0f * (fmaxf(l2o, 0.0f) * 0.6931472f + 0.01f) * 1.05f;
   const float rx = sqrtf(k2 * (float)((double)co.z / det)) + 0.5f;
   const float ry = sqrtf(k2 * (float)((double)co.x / det)) + 0.5f;
   uint32_t m = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float xlo = tile_x0 + (float)((k & 1) * 8) + 0.5f, xhi = xlo + 7.0f;
-    const float ylo = tile_y0 + (float)((k >> 1) * 4) + 0.5f, yhi = ylo + 3.0f;
+  for (int k = 0; k < NB; ++k) {
+    const float xlo = tile_x0 + (float)((k % NBX) * BW) + 0.5f, xhi = xlo + (float)(BW - 1);
+    const float ylo = tile_y0 + (float)((k / NBX) * BH) + 0.5f, yhi = ylo + (float)(BH - 1);
     const bool hit = (xy.x + rx >= xlo) && (xy.x - rx <= xhi) && (xy.y + ry >= ylo) && (xy.y - ry <= yhi);
     m |= (hit ? 1u : 0u) << k;
   }
-  s.wmask = m;
-  return s;
+  return m;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt_() {
@@ -88,35 +88,42 @@ __device__ __forceinline__ uint32_t lanemask_lt_() {
   return m;
 }
 
-// Per-warp candidate lists of a staged batch: s_list[k][..] = ascending batch slots
-// whose wmask has bit k, s_nw[k] = their count.  Thread t contributes slot t with
-// mask m.  s_wc is [NW*8] scratch.  Contains the barriers that publish the lists.
-template <int NW>
-__device__ __forceinline__ void build_warp_lists(uint32_t m, uint8_t* s_list, uint32_t* s_wc, int* s_nw) {
+// Per-warp candidate lists of a staged batch of NT*EPT slots (slot e*NT + tid is
+// thread tid's e-th entry, mask mk[e]): s_list[b*NT*EPT + ..] = ascending slots
+// whose mask has bit b, s_nw[b] = their count.  s_wc is [EPT*NW*NB] scratch.
+// Contains the barriers that publish the staged records and the lists.
+template <int NT, int EPT, int NB>
+__device__ __forceinline__ void build_lists(const uint32_t (&mk)[EPT], uint8_t* s_list, uint32_t* s_wc,
+                                            int* s_nw) {
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, sw = tid >> 5;
   const uint32_t lt = lanemask_lt_();
-  uint32_t pos[8];
+  uint32_t pos[EPT][NB];
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    const uint32_t bal = __ballot_sync(0xffffffffu, (m >> b) & 1u);
-    pos[b] = __popc(bal & lt);
-    if (lane == b) s_wc[sw * 8 + b] = __popc(bal);
-  }
+  for (int e = 0; e < EPT; ++e)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (mk[e] >> b) & 1u);
+      pos[e][b] = __popc(bal & lt);
+      if (lane == b) s_wc[(e * NW + sw) * NB + b] = __popc(bal);
+    }
   __syncthreads();
-  if (tid < 8) {
+  if (tid < NB) {
     uint32_t acc = 0;
 #pragma unroll
-    for (int k = 0; k < NW; ++k) {
-      const uint32_t c = s_wc[k * 8 + tid];
-      s_wc[k * 8 + tid] = acc;
+    for (int k = 0; k < EPT * NW; ++k) {
+      const uint32_t c = s_wc[k * NB + tid];
+      s_wc[k * NB + tid] = acc;
       acc += c;
     }
     s_nw[tid] = (int)acc;
   }
   __syncthreads();
 #pragma unroll
-  for (int b = 0; b < 8; ++b)
-    if ((m >> b) & 1u) s_list[b * (NW * 32) + s_wc[sw * 8 + b] + pos[b]] = (uint8_t)tid;
+  for (int e = 0; e < EPT; ++e)
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if ((mk[e] >> b) & 1u) s_list[b * (NT * EPT) + s_wc[(e * NW + sw) * NB + b] + pos[e][b]] = (uint8_t)(e * NT + tid);
   __syncthreads();
 }
 

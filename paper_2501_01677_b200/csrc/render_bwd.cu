@@ -13,13 +13,16 @@
 // suffix is carried as one scalar (mathematically identical to the 8-vector
 // recurrence of the oracle).
 //
-// Work mapping is A6's: per active tile, 8 warps on 8x4 pixel blocks, batches of
-// 256 entries staged with the same exact warp-block cull and compacted per-warp
-// candidate lists, walked in reverse.  Reduction: per entry, the warp's 14
-// per-lane partials are reduce-scattered (5 butterfly levels, 16 shuffles) so
-// that 14 lanes each hold one warp sum; those lanes add into a padded shared
-// accumulator of the batch (shared by the tile's 8 warps); after the batch the
-// CTA flushes one double-precision global atomic per (entry, value).
+// Work mapping is A6's: per active tile, 4 warps on 8x8 pixel blocks, two pixels
+// (x, y), (x, y + 4) per lane in packed FP32x2, batches of 256 entries staged with
+// the same exact warp-block cull and compacted per-warp candidate lists, walked
+// in reverse.  A pixel that does not contribute to an entry carries alpha = rho =
+// 0, which zeroes all of its terms and leaves its state unchanged without
+// branches.  Reduction: per entry, the lane's two pixels are summed, the warp's
+// 14 partials are reduce-scattered (5 butterfly levels, 16 shuffles) so that 14
+// lanes each hold one warp sum, those lanes add into a padded shared accumulator
+// of the batch, and after the batch the CTA flushes one double-precision global
+// atomic per (entry, value).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,7 +33,10 @@ namespace pgsag {
 namespace {
 
 constexpr int kG2 = 14;  // du dv dca dcb dcc dop drgb3 dncam3 ddist absgrad
-constexpr int kNW = kTilePix / 32;
+constexpr int kBT = 128;
+constexpr int kBEPT = 2;
+constexpr int kBBatch = kBT * kBEPT;
+constexpr int kBNB = 4;
 constexpr float kLn2 = 0.6931471805599453f;
 
 struct BwdArgs {
@@ -55,6 +61,7 @@ struct BwdArgs {
   uint32_t* work;
 };
 
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float ld_or0(const float* p, size_t k) { return p ? __ldg(p + k) : 0.0f; }
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -74,29 +81,62 @@ __device__ __forceinline__ void rs_level(float (&v)[2 * H], float (&o)[H], bool 
   }
 }
 
+// Per-pixel prologue: upstream G (Eq. 4 folded in), P*(bg.gC), last index, T.
+struct PixState {
+  float G[8];
+  float Pb;
+  float T;
+  int last;
+};
+
+__device__ __forceinline__ void load_pixel(const BwdArgs& a, bool masked, size_t pix, size_t HW, float px, float py,
+                                           PixState& s) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s.G[c] = 0.f;
+  s.Pb = 0.f;
+  s.T = 1.f;
+  s.last = -1;
+  if (!masked) return;
+  s.last = a.last[pix];
+  s.T = a.T[pix];
+  s.G[0] = ld_or0(a.dC, pix); s.G[1] = ld_or0(a.dC, HW + pix); s.G[2] = ld_or0(a.dC, 2 * HW + pix);
+  s.G[3] = ld_or0(a.dN, pix); s.G[4] = ld_or0(a.dN, HW + pix); s.G[5] = ld_or0(a.dN, 2 * HW + pix);
+  s.G[6] = ld_or0(a.dD, pix);
+  s.G[7] = ld_or0(a.dA, pix);
+  const float gDep = ld_or0(a.dDep, pix);
+  // Eq. 4 prologue: Dep = D / (N . r); validity re-derived exactly as A6 did
+  const float N0 = a.N[pix], N1 = a.N[HW + pix], N2 = a.N[2 * HW + pix];
+  const float r0 = __fdiv_rn(__fsub_rn(px, a.cx), a.fx), r1 = __fdiv_rn(__fsub_rn(py, a.cy), a.fy);
+  const float den = __fadd_rn(__fadd_rn(__fmul_rn(N0, r0), __fmul_rn(N1, r1)), N2);
+  if (a.g[pix] > 0 && fabsf(den) > 1e-6f) {
+    const float inv = 1.0f / den;
+    s.G[6] += gDep * inv;
+    const float c = gDep * a.D[pix] * inv * inv;
+    s.G[3] -= c * r0; s.G[4] -= c * r1; s.G[5] -= c;
+  }
+  s.Pb = a.bg0 * s.G[0] + a.bg1 * s.G[1] + a.bg2 * s.G[2];
+}
+
 template <bool kCount>
-__global__ void __launch_bounds__(kTilePix) render_bwd_kernel(BwdArgs a) {
+__global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
   constexpr int kAccStride = 15;  // padded row: the 14 values of an entry sit in 14 distinct banks
-  __shared__ float4 s_a[kTilePix];   // (u, v, A', B')
-  __shared__ float4 s_b[kTilePix];   // (C', o, skip threshold, 0)
-  __shared__ float4 s_cd[kTilePix];
-  __shared__ float4 s_n[kTilePix];
-  __shared__ uint32_t s_id[kTilePix];
-  __shared__ float s_acc[kTilePix * kAccStride];
-  __shared__ uint8_t s_list[8 * kTilePix];
-  __shared__ uint32_t s_wc[kNW * 8];
-  __shared__ int s_nw[8];
+  __shared__ Rec s_rec[kBBatch];
+  __shared__ uint32_t s_id[kBBatch];
+  __shared__ float s_acc[kBBatch * kAccStride];
+  __shared__ uint8_t s_list[kBNB * kBBatch];
+  __shared__ uint32_t s_wc[kBEPT * (kBT / 32) * kBNB];
+  __shared__ int s_nw[kBNB];
   __shared__ uint32_t s_tile;
   __shared__ int s_maxlast;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
-  const uint8_t* my_list = s_list + w * kTilePix;
+  const uint8_t* my_list = s_list + w * kBBatch;
   unsigned long long cntV = 0;
   // value index this lane owns after the reduce-scatter: bit-reversed lane bits 1..4
   const int my_c = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
   const bool writer = ((lane & 1) == 0) && my_c < kG2;
-  for (int k = tid; k < kTilePix * kAccStride; k += kTilePix) s_acc[k] = 0.f;
+  for (int k = tid; k < kBBatch * kAccStride; k += kBT) s_acc[k] = 0.f;
   for (;;) {
     if (tid == 0) { s_tile = atomicAdd(a.work, 1u); s_maxlast = -1; }
     __syncthreads();
@@ -104,129 +144,138 @@ __global__ void __launch_bounds__(kTilePix) render_bwd_kernel(BwdArgs a) {
     if (widx >= n_active) break;
     const uint32_t tile = a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
-    const int i = tx * kTile + warp_px(w, lane);
-    const int j = ty * kTile + warp_py(w, lane);
-    const bool inside = i < a.d.W && j < a.d.H;
-    const size_t pix = (size_t)j * a.d.W + i;
-    const bool masked = inside && a.mask[pix] != 0;
+    const int i = tx * kTile + (w & 1) * 8 + (lane & 7);
+    const int j0 = ty * kTile + (w >> 1) * 8 + (lane >> 3), j1 = j0 + 4;
+    const size_t pix0 = (size_t)j0 * a.d.W + i, pix1 = (size_t)j1 * a.d.W + i;
+    const bool m0 = i < a.d.W && j0 < a.d.H && a.mask[pix0] != 0;
+    const bool m1 = i < a.d.W && j1 < a.d.H && a.mask[pix1] != 0;
     const uint32_t rs = a.ranges[2 * tile];
-    const float px = (float)i + 0.5f, py = (float)j + 0.5f;
+    const float px = (float)i + 0.5f;
+    const float2 py = f2((float)j0 + 0.5f, (float)j1 + 0.5f);
     const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
-    int mylast = -1;
-    float Tcur = 1.0f;
-    float G[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    float Pb = 0.f;  // P * (bg . gC)
-    if (masked) {
-      mylast = a.last[pix];
-      Tcur = a.T[pix];
-      G[0] = ld_or0(a.dC, pix); G[1] = ld_or0(a.dC, HW + pix); G[2] = ld_or0(a.dC, 2 * HW + pix);
-      G[3] = ld_or0(a.dN, pix); G[4] = ld_or0(a.dN, HW + pix); G[5] = ld_or0(a.dN, 2 * HW + pix);
-      G[6] = ld_or0(a.dD, pix);
-      G[7] = ld_or0(a.dA, pix);
-      const float gDep = ld_or0(a.dDep, pix);
-      // Eq. 4 prologue: Dep = D / (N . r); validity re-derived exactly as A6 did
-      const float N0 = a.N[pix], N1 = a.N[HW + pix], N2 = a.N[2 * HW + pix];
-      const float r0 = __fdiv_rn(__fsub_rn(px, a.cx), a.fx), r1 = __fdiv_rn(__fsub_rn(py, a.cy), a.fy);
-      const float den = __fadd_rn(__fadd_rn(__fmul_rn(N0, r0), __fmul_rn(N1, r1)), N2);
-      if (a.g[pix] > 0 && fabsf(den) > 1e-6f) {
-        const float inv = 1.0f / den;
-        G[6] += gDep * inv;
-        const float c = gDep * a.D[pix] * inv * inv;
-        G[3] -= c * r0; G[4] -= c * r1; G[5] -= c;
-      }
-      Pb = a.bg0 * G[0] + a.bg1 * G[1] + a.bg2 * G[2];
-      if (mylast >= 0) atomicMax(&s_maxlast, mylast);
-    }
+    PixState s0, s1;
+    load_pixel(a, m0, pix0, HW, px, py.x, s0);
+    load_pixel(a, m1, pix1, HW, px, py.y, s1);
+    float2 Gp[8];  // (pixel0, pixel1) per channel
+#pragma unroll
+    for (int c = 0; c < 8; ++c) Gp[c] = f2(s0.G[c], s1.G[c]);
+    float2 Pb = f2(s0.Pb, s1.Pb), Tcur = f2(s0.T, s1.T), Sg = f2(0.f, 0.f);
+    const int last0 = s0.last, last1 = s1.last;
+    const int mylast = max(last0, last1);
+    if (mylast >= 0) atomicMax(&s_maxlast, mylast);
     const int wlast = __reduce_max_sync(0xffffffffu, mylast);
     __syncthreads();
     const int maxlast = s_maxlast;
-    float Sg = 0.f;  // G . S
-    for (int bhi = maxlast + 1; bhi > (int)rs; bhi -= kTilePix) {
-      const int blo = max((int)rs, bhi - kTilePix);
+    for (int bhi = maxlast + 1; bhi > (int)rs; bhi -= kBBatch) {
+      const int blo = max((int)rs, bhi - kBBatch);
       const int cnt = bhi - blo;
-      uint32_t m = 0u;
-      if (tid < cnt) {
-        const uint32_t id = a.vals[blo + tid];
-        const Staged st = stage_gaussian(a.mean2d[id], a.conic_o[id], tx0, ty0);
-        s_id[tid] = id;
-        s_a[tid] = st.a;
-        s_b[tid] = st.b;
-        s_cd[tid] = a.rgb_d[id];
-        s_n[tid] = a.ncam[id];
-        m = st.wmask;
+      uint32_t mk[kBEPT];
+#pragma unroll
+      for (int e = 0; e < kBEPT; ++e) {
+        const int slot = e * kBT + tid;
+        mk[e] = 0u;
+        if (slot < cnt) {
+          const uint32_t id = a.vals[blo + slot];
+          Rec& r = s_rec[slot];
+          mk[e] = stage_gaussian<8, 8>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
+          r.cd = a.rgb_d[id];
+          r.n = a.ncam[id];
+          s_id[slot] = id;
+        }
       }
-      build_warp_lists<kNW>(m, s_list, s_wc, s_nw);
+      build_lists<kBT, kBEPT, kBNB>(mk, s_list, s_wc, s_nw);
       const int qtop = wlast - blo;  // entries past the warp's last are never needed
       for (int t = s_nw[w] - 1; t >= 0; --t) {
         const int q = my_list[t];
         if (q > qtop) continue;  // warp-uniform
         const int kk = blo + q;
-        const float4 ra = s_a[q];
-        const float4 rb = s_b[q];
-        bool contrib = kk <= mylast;  // false for masked-out pixels (mylast = -1)
-        float alpha = 0.f, rho = 0.f, dx = 0.f, dy = 0.f;
-        if (contrib) {
-          dx = px - ra.x; dy = py - ra.y;
-          const float p2 = power2r(ra, rb.x, dx, dy);
-          if (kCount) ++cntV;
-          if (p2 >= rb.z && p2 <= 0.0f) {
-            rho = ex2_approx(p2);
-            alpha = fminf(kAlphaMax, __fmul_rn(rb.y, rho));
-            contrib = alpha >= kAlphaMin;
-          } else {
-            contrib = false;
-          }
-        }
-        if (!__any_sync(0xffffffffu, contrib)) continue;
+        const float4 ra = s_rec[q].a;
+        const float4 rb = s_rec[q].b;
+        const float dx = px - ra.x;
+        const float2 dy = __fadd2_rn(py, f2(-ra.y, -ra.y));
+        const float tA = __fmul_rn(ra.z, dx);
+        const float2 u = __ffma2_rn(f2(ra.w, ra.w), dy, f2(tA, tA));
+        const float2 cq = __fmul2_rn(__fmul2_rn(f2(rb.x, rb.x), dy), dy);
+        const float2 p2 = __ffma2_rn(f2(dx, dx), u, cq);
+        const float rh0 = ex2_approx(p2.x), rh1 = ex2_approx(p2.y);
+        const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(rh0, rh1));
+        float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
+        const bool c0 = kk <= last0 && p2.x >= rb.z && p2.x <= 0.0f && al0 >= kAlphaMin;
+        const bool c1 = kk <= last1 && p2.y >= rb.z && p2.y <= 0.0f && al1 >= kAlphaMin;
+        if (kCount) cntV += (unsigned long long)(kk <= last0) + (unsigned long long)(kk <= last1);
+        if (!__any_sync(0xffffffffu, c0 || c1)) continue;
+        al0 = c0 ? al0 : 0.f;
+        al1 = c1 ? al1 : 0.f;
+        // rho and alpha as they enter d(opacity) and d(power): zero when clamped at 0.99 (R16)
+        const bool u0 = c0 && orho.x <= kAlphaMax, u1 = c1 && orho.y <= kAlphaMax;
+        const float rc0 = u0 ? rh0 : 0.f, rc1 = u1 ? rh1 : 0.f;
+        const float2 al = f2(al0, al1);
+        const float2 om = __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1));
+        const float2 Ti = __fmul2_rn(Tcur, f2(rcp_approx(om.x), rcp_approx(om.y)));
+        const float4 cd = s_rec[q].cd;
+        const float4 nn = s_rec[q].n;
+        float2 GF = Gp[7];
+        GF = __ffma2_rn(Gp[0], f2(cd.x, cd.x), GF);
+        GF = __ffma2_rn(Gp[1], f2(cd.y, cd.y), GF);
+        GF = __ffma2_rn(Gp[2], f2(cd.z, cd.z), GF);
+        GF = __ffma2_rn(Gp[3], f2(nn.x, nn.x), GF);
+        GF = __ffma2_rn(Gp[4], f2(nn.y, nn.y), GF);
+        GF = __ffma2_rn(Gp[5], f2(nn.z, nn.z), GF);
+        GF = __ffma2_rn(Gp[6], f2(cd.w, cd.w), GF);
+        const float2 dal = __fmul2_rn(Ti, __fadd2_rn(GF, f2(-(Sg.x + Pb.x), -(Sg.y + Pb.y))));
+        Sg = __ffma2_rn(al, GF, __fmul2_rn(om, Sg));
+        Pb = __fmul2_rn(Pb, om);
+        Tcur = Ti;
+        const float2 wt = __fmul2_rn(al, Ti);
         float v[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = 0.f;
-        if (contrib) {
-          const float4 cd = s_cd[q];
-          const float4 nn = s_n[q];
-          const float om = 1.0f - alpha;
-          const float Ti = Tcur * rcp_approx(om);
-          const float GF = G[0] * cd.x + G[1] * cd.y + G[2] * cd.z + G[3] * nn.x + G[4] * nn.y + G[5] * nn.z +
-                           G[6] * cd.w + G[7];
-          const float dalpha = Ti * (GF - Sg - Pb);
-          Sg = alpha * GF + om * Sg;
-          Pb *= om;
-          Tcur = Ti;
-          const float wgt = alpha * Ti;
-#pragma unroll
-          for (int c = 0; c < 7; ++c) v[6 + c] = wgt * G[c];
-          if (__fmul_rn(rb.y, rho) <= kAlphaMax) {
-            v[5] = rho * dalpha;
-            const float dpow = alpha * dalpha;
-            const float kx = dx * dpow;
-            v[2] = -0.5f * dx * kx;
-            v[3] = -dy * kx;
-            v[4] = -0.5f * dy * dy * dpow;
-            const float kd = -kLn2 * dpow;  // (ca, cb, cc) = -ln2 (2A', B', 2C')
-            v[0] = (2.0f * ra.z * dx + ra.w * dy) * kd;
-            v[1] = (ra.w * dx + 2.0f * rb.x * dy) * kd;
-            v[13] = fabsf(v[0]) + fabsf(v[1]);
-          }
+        for (int c = 0; c < 7; ++c) {
+          const float2 x = __fmul2_rn(wt, Gp[c]);
+          v[6 + c] = x.x + x.y;
         }
+        const float2 dpow = __fmul2_rn(f2(u0 ? al0 : 0.f, u1 ? al1 : 0.f), dal);
+        const float2 dop = __fmul2_rn(f2(rc0, rc1), dal);
+        v[5] = dop.x + dop.y;
+        const float sdp = dpow.x + dpow.y;
+        const float2 dydp = __fmul2_rn(dy, dpow);
+        const float sdydp = dydp.x + dydp.y;
+        const float2 dy2dp = __fmul2_rn(dy, dydp);
+        v[2] = -0.5f * dx * dx * sdp;
+        v[3] = -dx * sdydp;
+        v[4] = -0.5f * (dy2dp.x + dy2dp.y);
+        // per-pixel screen-space mean gradient: (ca, cb, cc) = -ln2 (2A', B', 2C')
+        const float2 gu = __ffma2_rn(f2(ra.w, ra.w), dy, f2(2.0f * tA, 2.0f * tA));        // 2A'dx + B'dy
+        const float2 gv = __ffma2_rn(f2(2.0f * rb.x, 2.0f * rb.x), dy, f2(ra.w * dx, ra.w * dx));  // B'dx + 2C'dy
+        const float2 du = __fmul2_rn(gu, __fmul2_rn(f2(-kLn2, -kLn2), dpow));
+        const float2 dv = __fmul2_rn(gv, __fmul2_rn(f2(-kLn2, -kLn2), dpow));
+        v[0] = du.x + du.y;
+        v[1] = dv.x + dv.y;
+        v[13] = (fabsf(du.x) + fabsf(dv.x)) + (fabsf(du.y) + fabsf(dv.y));
+        v[14] = 0.f;
+        v[15] = 0.f;
         // reduce-scatter 16 -> 1 value per lane pair
         float v8[8], v4[4], v2[2], v1[1];
         rs_level<8>(v, v8, (lane & 16) != 0, 16);
         rs_level<4>(v8, v4, (lane & 8) != 0, 8);
         rs_level<2>(v4, v2, (lane & 4) != 0, 4);
         rs_level<1>(v2, v1, (lane & 2) != 0, 2);
-        const float s = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 1);
-        if (writer && s != 0.0f) atomicAdd(&s_acc[q * kAccStride + my_c], s);
+        const float sum = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 1);
+        if (writer && sum != 0.0f) atomicAdd(&s_acc[q * kAccStride + my_c], sum);
       }
       __syncthreads();
       // flush the batch: one f64 atomic per (entry, value), then re-zero
-      if (tid < cnt) {
-        const uint32_t id = s_id[tid];
 #pragma unroll
-        for (int c = 0; c < kG2; ++c) {
-          const float x = s_acc[tid * kAccStride + c];
-          if (x != 0.0f) {
-            atomicAdd(a.g2d + (size_t)c * a.n + id, (double)x);
-            s_acc[tid * kAccStride + c] = 0.f;
+      for (int e = 0; e < kBEPT; ++e) {
+        const int slot = e * kBT + tid;
+        if (slot < cnt) {
+          const uint32_t id = s_id[slot];
+#pragma unroll
+          for (int c = 0; c < kG2; ++c) {
+            const float x = s_acc[slot * kAccStride + c];
+            if (x != 0.0f) {
+              atomicAdd(a.g2d + (size_t)c * a.n + id, (double)x);
+              s_acc[slot * kAccStride + c] = 0.f;
+            }
           }
         }
       }
@@ -246,7 +295,7 @@ int bwd_grid() {
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_bwd_kernel<false>, kTilePix, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_bwd_kernel<false>, kBT, 0);
     grid = sms * (occ > 0 ? occ : 1);
   }
   return grid;
@@ -285,9 +334,9 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
   {
     KTimer kt_("A7_render_bwd", st);
     if (fwd->counters)
-      render_bwd_kernel<true><<<grid, kTilePix, 0, st>>>(a);
+      render_bwd_kernel<true><<<grid, kBT, 0, st>>>(a);
     else
-      render_bwd_kernel<false><<<grid, kTilePix, 0, st>>>(a);
+      render_bwd_kernel<false><<<grid, kBT, 0, st>>>(a);
   }
   return launch_preprocess_bwd(g, cam, p, out, g2d, st);
 }

@@ -1,17 +1,19 @@
 // A6: masked forward compositor for sm_100a.
 //
 // P:79-92 Eq. 1-3 (front-to-back alpha blending of colour, camera-frame normal
-// and plane distance), Eq. 4 (unbiased depth epilogue), P:163 (one
-// thread per pixel), P:243 (only building-mask pixels are computed).
+// and plane distance), Eq. 4 (unbiased depth epilogue)
+// (pixel-parallel rendering), P:243 (only building-mask pixels are computed).
 //
 // Mapping: a persistent grid pulls ACTIVE tiles (tiles with >= 1 mask pixel) from
 // the A0 list through an atomic counter; masked-out tiles are never visited.  One
-// 256-thread CTA per 16x16 tile; warp w owns an 8x4 pixel block, one thread per
-// pixel; masked-out pixels start "done".  Each batch of 256 sorted entries is
-// staged in shared memory (one 56-byte record gather per thread) together with an
-// 8-bit warp-block mask (exact conservative cull, alpha.cuh), from which every
-// warp gets a compacted, depth-ordered candidate list; a warp's loop then touches
-// only entries that can reach its pixels.  The tile stops when every pixel is done.
+// 128-thread CTA per 16x16 tile: warp w owns an 8x8 pixel block, each lane the two
+// pixels (x, y) and (x, y + 4) of its column, which share dx and every per-entry
+// load; their arithmetic runs as packed FP32x2 (FFMA2/FMUL2/FADD2, one issue slot
+// for both pixels).  Masked-out pixels start "done".  Each batch of 256 sorted
+// entries is staged in shared memory (64-byte records) together with a 4-bit
+// warp-block mask (exact conservative cull, alpha.cuh), from which every warp gets
+// a compacted depth-ordered candidate list.  Blending is branch-free (predicated
+// weights); the tile stops when every pixel is done.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -21,7 +23,10 @@
 namespace pgsag {
 namespace {
 
-constexpr int kNW = kTilePix / 32;
+constexpr int kFT = 128;          // threads per tile CTA
+constexpr int kFEPT = 2;          // staged entries per thread per batch
+constexpr int kFBatch = kFT * kFEPT;
+constexpr int kFNB = 4;           // 8x8 warp blocks per tile
 
 struct FwdArgs {
   const float2* mean2d;
@@ -42,20 +47,38 @@ struct FwdArgs {
   uint32_t* work;
 };
 
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+__device__ __forceinline__ void write_pixel(const FwdArgs& a, size_t pix, size_t HW, float px, float py, float T,
+                                            float C0, float C1, float C2, float N0, float N1, float N2, float D,
+                                            int g, int last) {
+  a.C[pix] = C0 + T * a.bg0;
+  a.C[HW + pix] = C1 + T * a.bg1;
+  a.C[2 * HW + pix] = C2 + T * a.bg2;
+  a.N[pix] = N0; a.N[HW + pix] = N1; a.N[2 * HW + pix] = N2;
+  a.D[pix] = D;
+  a.A[pix] = 1.0f - T;
+  a.T[pix] = T;
+  a.g[pix] = g;
+  a.last[pix] = last;
+  // Eq. 4: depth of the ray / blended-plane intersection, r = K^-1 (px, py, 1)
+  // (explicit roundings: the backward re-derives this validity decision bit-exactly)
+  const float r0 = __fdiv_rn(__fsub_rn(px, a.cx), a.fx), r1 = __fdiv_rn(__fsub_rn(py, a.cy), a.fy);
+  const float den = __fadd_rn(__fadd_rn(__fmul_rn(N0, r0), __fmul_rn(N1, r1)), N2);
+  a.Dep[pix] = (g > 0 && fabsf(den) > 1e-6f) ? D / den : 0.0f;
+}
+
 template <bool kCount>
-__global__ void __launch_bounds__(kTilePix) render_fwd_kernel(FwdArgs a) {
-  __shared__ float4 s_a[kTilePix];
-  __shared__ float4 s_b[kTilePix];
-  __shared__ float4 s_cd[kTilePix];
-  __shared__ float4 s_n[kTilePix];
-  __shared__ uint8_t s_list[8 * kTilePix];
-  __shared__ uint32_t s_wc[kNW * 8];
-  __shared__ int s_nw[8];
+__global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
+  __shared__ Rec s_rec[kFBatch];
+  __shared__ uint8_t s_list[kFNB * kFBatch];
+  __shared__ uint32_t s_wc[kFEPT * (kFT / 32) * kFNB];
+  __shared__ int s_nw[kFNB];
   __shared__ uint32_t s_tile;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
-  const uint8_t* my_list = s_list + w * kTilePix;
+  const uint8_t* my_list = s_list + w * kFBatch;
   unsigned long long cntE = 0, cntB = 0;
   for (;;) {
     if (tid == 0) s_tile = atomicAdd(a.work, 1u);
@@ -65,79 +88,79 @@ __global__ void __launch_bounds__(kTilePix) render_fwd_kernel(FwdArgs a) {
     if (widx >= n_active) break;
     const uint32_t tile = a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
-    const int i = tx * kTile + warp_px(w, lane);
-    const int j = ty * kTile + warp_py(w, lane);
-    const bool inside = i < a.d.W && j < a.d.H;
-    const size_t pix = (size_t)j * a.d.W + i;
-    const bool masked = inside && a.mask[pix] != 0;
+    const int i = tx * kTile + (w & 1) * 8 + (lane & 7);
+    const int j0 = ty * kTile + (w >> 1) * 8 + (lane >> 3), j1 = j0 + 4;
+    const size_t pix0 = (size_t)j0 * a.d.W + i, pix1 = (size_t)j1 * a.d.W + i;
+    const bool m0 = i < a.d.W && j0 < a.d.H && a.mask[pix0] != 0;
+    const bool m1 = i < a.d.W && j1 < a.d.H && a.mask[pix1] != 0;
     const uint32_t rs = a.ranges[2 * tile], re = a.ranges[2 * tile + 1];
-    const float px = (float)i + 0.5f, py = (float)j + 0.5f;
+    const float px = (float)i + 0.5f;
+    const float2 py = f2((float)j0 + 0.5f, (float)j1 + 0.5f);
     const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, N0 = 0.f, N1 = 0.f, N2 = 0.f, D = 0.f;
-    int g = 0, last = -1;
-    bool done = !masked;
-    for (uint32_t b = rs; b < re; b += kTilePix) {
-      if (__syncthreads_count(done) == kTilePix) break;
-      const uint32_t k = b + tid;
-      uint32_t m = 0u;
-      if (k < re) {
-        const uint32_t id = a.vals[k];
-        const Staged st = stage_gaussian(a.mean2d[id], a.conic_o[id], tx0, ty0);
-        s_a[tid] = st.a;
-        s_b[tid] = st.b;
-        s_cd[tid] = a.rgb_d[id];
-        s_n[tid] = a.ncam[id];
-        m = st.wmask;
+    float2 T = f2(1.f, 1.f), C0 = f2(0.f, 0.f), C1 = C0, C2 = C0, N0 = C0, N1 = C0, N2 = C0, D = C0;
+    int g0 = 0, g1 = 0, last0 = -1, last1 = -1;
+    bool done0 = !m0, done1 = !m1;
+    for (uint32_t b = rs; b < re; b += kFBatch) {
+      if (__syncthreads_count(done0 && done1) == kFT) break;
+      uint32_t mk[kFEPT];
+#pragma unroll
+      for (int e = 0; e < kFEPT; ++e) {
+        const uint32_t k = b + e * kFT + tid;
+        mk[e] = 0u;
+        if (k < re) {
+          const uint32_t id = a.vals[k];
+          Rec& r = s_rec[e * kFT + tid];
+          mk[e] = stage_gaussian<8, 8>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
+          r.cd = a.rgb_d[id];
+          r.n = a.ncam[id];
+        }
       }
-      build_warp_lists<kNW>(m, s_list, s_wc, s_nw);
+      build_lists<kFT, kFEPT, kFNB>(mk, s_list, s_wc, s_nw);
       const int nw = s_nw[w];
       for (int t = 0; t < nw; ++t) {
-        if (__all_sync(0xffffffffu, done)) break;
+        if ((t & 7) == 0 && __all_sync(0xffffffffu, done0 && done1)) break;
         const int q = my_list[t];
-        const float4 ra = s_a[q];
-        const float4 rb = s_b[q];
-        if (!done) {
-          const float dx = px - ra.x, dy = py - ra.y;
-          const float p2 = power2r(ra, rb.x, dx, dy);
-          if (kCount) ++cntE;
-          if (p2 >= rb.z && p2 <= 0.0f) {
-            const float alpha = fminf(kAlphaMax, __fmul_rn(rb.y, ex2_approx(p2)));
-            if (alpha >= kAlphaMin) {
-              const float Tn = __fmul_rn(T, 1.0f - alpha);
-              if (Tn < kTmin) {
-                done = true;
-              } else {
-                const float wgt = alpha * T;
-                const float4 cd = s_cd[q];
-                const float4 nn = s_n[q];
-                C0 += wgt * cd.x; C1 += wgt * cd.y; C2 += wgt * cd.z; D += wgt * cd.w;
-                N0 += wgt * nn.x; N1 += wgt * nn.y; N2 += wgt * nn.z;
-                ++g;
-                last = (int)(b + q);
-                T = Tn;
-              }
-            }
-          }
+        const float4 ra = s_rec[q].a;
+        const float4 rb = s_rec[q].b;
+        // p2 for both pixels (bit-identical to power2r per element)
+        const float dx = px - ra.x;
+        const float2 dy = __fadd2_rn(py, f2(-ra.y, -ra.y));
+        const float tA = __fmul_rn(ra.z, dx);
+        const float2 u = __ffma2_rn(f2(ra.w, ra.w), dy, f2(tA, tA));
+        const float2 cq = __fmul2_rn(__fmul2_rn(f2(rb.x, rb.x), dy), dy);
+        const float2 p2 = __ffma2_rn(f2(dx, dx), u, cq);
+        const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(ex2_approx(p2.x), ex2_approx(p2.y)));
+        const float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
+        if (kCount) cntE += (unsigned long long)(!done0) + (unsigned long long)(!done1);
+        bool ok0 = !done0 && p2.x >= rb.z && p2.x <= 0.0f && al0 >= kAlphaMin;
+        bool ok1 = !done1 && p2.y >= rb.z && p2.y <= 0.0f && al1 >= kAlphaMin;
+        const float2 Tn = __fmul2_rn(T, __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
+        const bool st0 = ok0 && Tn.x < kTmin, st1 = ok1 && Tn.y < kTmin;
+        done0 |= st0; done1 |= st1;
+        ok0 &= !st0; ok1 &= !st1;
+        if (__any_sync(0xffffffffu, ok0 || ok1)) {
+          const float2 wt = __fmul2_rn(f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f), T);
+          const float4 cd = s_rec[q].cd;
+          const float4 nn = s_rec[q].n;
+          C0 = __ffma2_rn(wt, f2(cd.x, cd.x), C0);
+          C1 = __ffma2_rn(wt, f2(cd.y, cd.y), C1);
+          C2 = __ffma2_rn(wt, f2(cd.z, cd.z), C2);
+          D = __ffma2_rn(wt, f2(cd.w, cd.w), D);
+          N0 = __ffma2_rn(wt, f2(nn.x, nn.x), N0);
+          N1 = __ffma2_rn(wt, f2(nn.y, nn.y), N1);
+          N2 = __ffma2_rn(wt, f2(nn.z, nn.z), N2);
+          T.x = ok0 ? Tn.x : T.x;
+          T.y = ok1 ? Tn.y : T.y;
+          g0 += ok0 ? 1 : 0;
+          g1 += ok1 ? 1 : 0;
+          last0 = ok0 ? (int)(b + q) : last0;
+          last1 = ok1 ? (int)(b + q) : last1;
         }
       }
     }
-    if (masked) {
-      a.C[pix] = C0 + T * a.bg0;
-      a.C[HW + pix] = C1 + T * a.bg1;
-      a.C[2 * HW + pix] = C2 + T * a.bg2;
-      a.N[pix] = N0; a.N[HW + pix] = N1; a.N[2 * HW + pix] = N2;
-      a.D[pix] = D;
-      a.A[pix] = 1.0f - T;
-      a.T[pix] = T;
-      a.g[pix] = g;
-      a.last[pix] = last;
-      // Eq. 4: depth of the ray / blended-plane intersection, r = K^-1 (px, py, 1)
-      // (explicit roundings: the backward re-derives this validity decision bit-exactly)
-      const float r0 = __fdiv_rn(__fsub_rn(px, a.cx), a.fx), r1 = __fdiv_rn(__fsub_rn(py, a.cy), a.fy);
-      const float den = __fadd_rn(__fadd_rn(__fmul_rn(N0, r0), __fmul_rn(N1, r1)), N2);
-      a.Dep[pix] = (g > 0 && fabsf(den) > 1e-6f) ? D / den : 0.0f;
-      if (kCount) cntB += (unsigned long long)g;
-    }
+    if (m0) write_pixel(a, pix0, HW, px, py.x, T.x, C0.x, C1.x, C2.x, N0.x, N1.x, N2.x, D.x, g0, last0);
+    if (m1) write_pixel(a, pix1, HW, px, py.y, T.y, C0.y, C1.y, C2.y, N0.y, N1.y, N2.y, D.y, g1, last1);
+    if (kCount) cntB += (unsigned long long)(m0 ? g0 : 0) + (unsigned long long)(m1 ? g1 : 0);
   }
   if (kCount) {
 #pragma unroll
@@ -158,7 +181,7 @@ int fwd_grid() {
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_fwd_kernel<false>, kTilePix, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_fwd_kernel<false>, kFT, 0);
     grid = sms * (occ > 0 ? occ : 1);
   }
   return grid;
@@ -190,9 +213,9 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
   {
     KTimer kt_("A6_render_fwd", st);
     if (out->counters)
-      render_fwd_kernel<true><<<grid, kTilePix, 0, st>>>(a);
+      render_fwd_kernel<true><<<grid, kFT, 0, st>>>(a);
     else
-      render_fwd_kernel<false><<<grid, kTilePix, 0, st>>>(a);
+      render_fwd_kernel<false><<<grid, kFT, 0, st>>>(a);
   }
   return cudaGetLastError();
 }
