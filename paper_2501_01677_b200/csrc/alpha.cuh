@@ -82,6 +82,20 @@ __device__ __forceinline__ uint32_t stage_gaussian(float2 xy, float4 co, float t
   return m;
 }
 
+// 32-bit shared-window loads (the base address is computed once per kernel, so the
+// hot loops do not re-derive the generic->shared mapping every iteration).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+  return (uint32_t)v;
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt_() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
-  const uint8_t* my_list = s_list + w * kBBatch;
+  const uint32_t rec_base = smem_u32(s_rec), list_base = smem_u32(s_list);
   unsigned long long cntV = 0;
   // value index this lane owns after the reduce-scatter: bit-reversed lane bits 1..4
   const int my_c = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
@@ -185,12 +185,14 @@ __global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
       }
       build_lists<kBT, kBEPT, kBNB>(mk, s_list, s_wc, s_nw);
       const int qtop = wlast - blo;  // entries past the warp's last are never needed
+      const uint32_t lbase = list_base + (uint32_t)(w * kBBatch);
       for (int t = s_nw[w] - 1; t >= 0; --t) {
-        const int q = my_list[t];
+        const int q = (int)lds_u8(lbase + (uint32_t)t);
         if (q > qtop) continue;  // warp-uniform
         const int kk = blo + q;
-        const float4 ra = s_rec[q].a;
-        const float4 rb = s_rec[q].b;
+        const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
+        const float4 ra = lds128(ra_addr);
+        const float4 rb = lds128(ra_addr + 16);
         const float dx = px - ra.x;
         const float2 dy = __fadd2_rn(py, f2(-ra.y, -ra.y));
         const float tA = __fmul_rn(ra.z, dx);
@@ -200,8 +202,9 @@ __global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
         const float rh0 = ex2_approx(p2.x), rh1 = ex2_approx(p2.y);
         const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(rh0, rh1));
         float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
-        const bool c0 = kk <= last0 && p2.x >= rb.z && p2.x <= 0.0f && al0 >= kAlphaMin;
-        const bool c1 = kk <= last1 && p2.y >= rb.z && p2.y <= 0.0f && al1 >= kAlphaMin;
+        // exactly A6's blend decision (R6); entries past the pixel's last were not blended
+        const bool c0 = kk <= last0 && p2.x <= 0.0f && al0 >= kAlphaMin;
+        const bool c1 = kk <= last1 && p2.y <= 0.0f && al1 >= kAlphaMin;
         if (kCount) cntV += (unsigned long long)(kk <= last0) + (unsigned long long)(kk <= last1);
         if (!__any_sync(0xffffffffu, c0 || c1)) continue;
         al0 = c0 ? al0 : 0.f;
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
         const float2 al = f2(al0, al1);
         const float2 om = __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1));
         const float2 Ti = __fmul2_rn(Tcur, f2(rcp_approx(om.x), rcp_approx(om.y)));
-        const float4 cd = s_rec[q].cd;
-        const float4 nn = s_rec[q].n;
+        const float4 cd = lds128(ra_addr + 32);
+        const float4 nn = lds128(ra_addr + 48);
         float2 GF = Gp[7];
         GF = __ffma2_rn(Gp[0], f2(cd.x, cd.x), GF);
         GF = __ffma2_rn(Gp[1], f2(cd.y, cd.y), GF);

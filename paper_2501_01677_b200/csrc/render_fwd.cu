@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
-  const uint8_t* my_list = s_list + w * kFBatch;
+  const uint32_t rec_base = smem_u32(s_rec), list_base = smem_u32(s_list);
   unsigned long long cntE = 0, cntB = 0;
   for (;;) {
     if (tid == 0) s_tile = atomicAdd(a.work, 1u);
@@ -97,11 +97,13 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
     const float px = (float)i + 0.5f;
     const float2 py = f2((float)j0 + 0.5f, (float)j1 + 0.5f);
     const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
-    float2 T = f2(1.f, 1.f), C0 = f2(0.f, 0.f), C1 = C0, C2 = C0, N0 = C0, N1 = C0, N2 = C0, D = C0;
+    // T carries the pixel's "done" state in its sign: T > 0 while the pixel is still
+    // compositing, T = -(final T) once it stopped (or -1 if it is not a mask pixel).
+    float2 T = f2(m0 ? 1.f : -1.f, m1 ? 1.f : -1.f);
+    float2 C0 = f2(0.f, 0.f), C1 = C0, C2 = C0, N0 = C0, N1 = C0, N2 = C0, D = C0;
     int g0 = 0, g1 = 0, last0 = -1, last1 = -1;
-    bool done0 = !m0, done1 = !m1;
     for (uint32_t b = rs; b < re; b += kFBatch) {
-      if (__syncthreads_count(done0 && done1) == kFT) break;
+      if (__syncthreads_count(T.x < 0.f && T.y < 0.f) == kFT) break;
       uint32_t mk[kFEPT];
 #pragma unroll
       for (int e = 0; e < kFEPT; ++e) {
@@ -117,11 +119,13 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
       }
       build_lists<kFT, kFEPT, kFNB>(mk, s_list, s_wc, s_nw);
       const int nw = s_nw[w];
+      const uint32_t lbase = list_base + (uint32_t)(w * kFBatch);
       for (int t = 0; t < nw; ++t) {
-        if ((t & 7) == 0 && __all_sync(0xffffffffu, done0 && done1)) break;
-        const int q = my_list[t];
-        const float4 ra = s_rec[q].a;
-        const float4 rb = s_rec[q].b;
+        if ((t & 7) == 0 && __all_sync(0xffffffffu, T.x < 0.f && T.y < 0.f)) break;
+        const uint32_t q = lds_u8(lbase + (uint32_t)t);
+        const uint32_t ra_addr = rec_base + q * (uint32_t)sizeof(Rec);
+        const float4 ra = lds128(ra_addr);
+        const float4 rb = lds128(ra_addr + 16);
         // p2 for both pixels (bit-identical to power2r per element)
         const float dx = px - ra.x;
         const float2 dy = __fadd2_rn(py, f2(-ra.y, -ra.y));
@@ -131,17 +135,17 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
         const float2 p2 = __ffma2_rn(f2(dx, dx), u, cq);
         const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(ex2_approx(p2.x), ex2_approx(p2.y)));
         const float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
-        if (kCount) cntE += (unsigned long long)(!done0) + (unsigned long long)(!done1);
-        bool ok0 = !done0 && p2.x >= rb.z && p2.x <= 0.0f && al0 >= kAlphaMin;
-        bool ok1 = !done1 && p2.y >= rb.z && p2.y <= 0.0f && al1 >= kAlphaMin;
+        if (kCount) cntE += (unsigned long long)(T.x > 0.f) + (unsigned long long)(T.y > 0.f);
+        // blend iff still compositing, power <= 0 and alpha >= 1/255 (R6)
+        bool ok0 = T.x > 0.f && p2.x <= 0.0f && al0 >= kAlphaMin;
+        bool ok1 = T.y > 0.f && p2.y <= 0.0f && al1 >= kAlphaMin;
         const float2 Tn = __fmul2_rn(T, __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
         const bool st0 = ok0 && Tn.x < kTmin, st1 = ok1 && Tn.y < kTmin;
-        done0 |= st0; done1 |= st1;
         ok0 &= !st0; ok1 &= !st1;
-        if (__any_sync(0xffffffffu, ok0 || ok1)) {
+        if (__any_sync(0xffffffffu, ok0 || ok1 || st0 || st1)) {
           const float2 wt = __fmul2_rn(f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f), T);
-          const float4 cd = s_rec[q].cd;
-          const float4 nn = s_rec[q].n;
+          const float4 cd = lds128(ra_addr + 32);
+          const float4 nn = lds128(ra_addr + 48);
           C0 = __ffma2_rn(wt, f2(cd.x, cd.x), C0);
           C1 = __ffma2_rn(wt, f2(cd.y, cd.y), C1);
           C2 = __ffma2_rn(wt, f2(cd.z, cd.z), C2);
@@ -149,15 +153,17 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
           N0 = __ffma2_rn(wt, f2(nn.x, nn.x), N0);
           N1 = __ffma2_rn(wt, f2(nn.y, nn.y), N1);
           N2 = __ffma2_rn(wt, f2(nn.z, nn.z), N2);
-          T.x = ok0 ? Tn.x : T.x;
-          T.y = ok1 ? Tn.y : T.y;
-          g0 += ok0 ? 1 : 0;
-          g1 += ok1 ? 1 : 0;
+          T.x = ok0 ? Tn.x : (st0 ? -T.x : T.x);
+          T.y = ok1 ? Tn.y : (st1 ? -T.y : T.y);
+          if (ok0) ++g0;
+          if (ok1) ++g1;
           last0 = ok0 ? (int)(b + q) : last0;
           last1 = ok1 ? (int)(b + q) : last1;
         }
       }
     }
+    T.x = fabsf(T.x);
+    T.y = fabsf(T.y);
     if (m0) write_pixel(a, pix0, HW, px, py.x, T.x, C0.x, C1.x, C2.x, N0.x, N1.x, N2.x, D.x, g0, last0);
     if (m1) write_pixel(a, pix1, HW, px, py.y, T.y, C0.y, C1.y, C2.y, N0.y, N1.y, N2.y, D.y, g1, last1);
     if (kCount) cntB += (unsigned long long)(m0 ? g0 : 0) + (unsigned long long)(m1 ? g1 : 0);
