@@ -30,10 +30,10 @@ import numpy as np  # noqa: E402
 METRIC = "masked Mpix/s fwd+bwd and Gaussian-pixel blends/s at 1/2/4/8 B200; % FP32/HBM roofline"
 UNIT = "Mpix/s"
 
-# algorithmic work per unit (DESIGN.md §5 / SURVEY §8(d))
-FLOP_EVAL = 12      # per evaluated (pixel, Gaussian) pair: dx, dy, quadratic form, o*rho
-FLOP_BLEND_FWD = 17  # per blended pair in A6: 1-a, T(1-a), aT, 7 channel FMAs (x2)
-FLOP_BLEND_BWD = 79  # per blended pair in A7
+# algorithmic FP32 work per unit, FMA = 2 flops (exp/rcp on MUFU not counted)
+FLOP_EVAL = 9        # per evaluated (pixel, Gaussian) pair: dx, dy, quadratic form, o*rho
+FLOP_BLEND_FWD = 17  # per blended pair in A6: 1-a, T(1-a), aT, 7 channel FMAs
+FLOP_BLEND_BWD = 48  # per blended pair in A7: T recovery, G.F, dalpha, suffix, dF, d(o,conic,mean2d), absgrad
 BYTES_A1 = {0: 56 + 76, 1: 56 + 36 + 76, 2: 56 + 96 + 76, 3: 56 + 180 + 76}  # params read + 76 B written
 SM_COUNT = 148
 FP32_LANES = 128
@@ -59,11 +59,13 @@ def load_workload(cfg, rank, n_views, device):
     import torch
     from synth import scenes as S
     if cfg == "c4":
-        sub = S.subregion(rank % 8, n_views=n_views)
+        from paper_2501_01677_b200 import shard
+        reg = shard.weak_region(rank)
+        sub = S.subregion(reg, n_views=n_views)
         cams = sub["cameras"]
         masks = [torch.from_numpy(S.ray_cast_mask(c, sub["boxes"], device=device)).to(device) for c in cams]
-        return sub["gaussians"], cams, masks, (f"C4 sub-region {rank % 8}: 1.5M Gaussians, {len(cams)} oblique "
-                                               "5472x3648 views, building mask")
+        return sub["gaussians"], cams, masks, (f"C4: one visibility-grouped sub-region per GPU (rank 0: region {reg}), "
+                                               f"1.5M Gaussians, {len(cams)} oblique 5472x3648 views, building mask")
     sc = {"c2": S.config2, "c3": S.config3, "c5": S.config5}[cfg](device=device)
     mask = torch.from_numpy(sc.mask).to(device)
     return sc.gaussians, [sc.camera], [mask], f"{cfg.upper()}: {sc.gaussians.n} Gaussians, " \
@@ -258,9 +260,10 @@ def main():
         dist.all_reduce(agg)
         pix_all, blends_all = float(agg[0]), float(agg[1])
         # per-rank statistics record all-gathered over NVLink (off the timed region)
-        rec = torch.tensor([rank, ms, pix, blends, imbalance] + [0.0] * 11, device=dev, dtype=torch.float32)
-        recs = [torch.zeros_like(rec) for _ in range(world)]
-        dist.all_gather(recs, rec)
+        from paper_2501_01677_b200 import shard
+        rec = shard.stats_record(rank=rank, ms=ms, masked_pixels=pix, blends=blends, tile_imbalance=imbalance,
+                                 views=len(views)).to(dev)
+        rank_table = shard.gather_stats(rec).cpu()
     else:
         ms_max, pix_all, blends_all = ms, pix, blends
     value = pix_all / 1e6 / (ms_max / 1e3)
@@ -379,9 +382,12 @@ def main():
             "masked_pixels_per_step": pix_all / args.steps,
             "tile_imbalance_max_over_mean": imbalance,
             "M_per_view": st0["M"], "evaluated_per_view": st0["evaluated"], "blended_per_view": st0["blended"],
+            "bwd_visited_per_view": st0["bwd_visited"],
+            "flop_per_unit": {"evaluated": FLOP_EVAL, "blended_fwd": FLOP_BLEND_FWD, "blended_bwd": FLOP_BLEND_BWD},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "kernels_ms_per_step": {k: round(v[0], 4) for k, v in sorted(ksteps.items())},
             "clocks": clk.summary(),
+            "per_rank_ms": (rank_table[:, 1].tolist() if world > 1 else [ms]),
         }
         print(json.dumps(line), flush=True)
         if args.profile:

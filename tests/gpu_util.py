@@ -89,6 +89,8 @@ def compare_pixels(gpu_img, ora, pix, W, vals, cam=None):
     for k, a, b in (("C", C, ora["C"]), ("N", N, ora["N"]), ("D", D, ora["D"]), ("A", A, ora["A"]),
                     ("T", T, ora["T"])):
         e = np.abs(a.astype(np.float64) - b.astype(np.float64))
+        if k == "D":  # plane distance is in scene units (metres): 1e-4 of max(1, |D|) (reading R19)
+            e = e / np.maximum(1.0, np.abs(b.astype(np.float64)))
         e = e.max(axis=1) if e.ndim == 2 else e
         errs[k] = float(e[ok].max()) if ok.any() else 0.0
         assert errs[k] <= ABS_IMG, (k, errs[k], np.argmax(np.where(ok, e, 0)))

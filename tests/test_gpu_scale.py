@@ -1,0 +1,92 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(same kernels, persistent grids, capacities): C3 (2M Gaussians, 5472x3648), C5 (3M
+clustered Gaussians at 4K) and one C4 sub-region view (1.5M, 5472x3648).
+
+- A1 outputs and the whole (tile, depth, id) order and ranges: bit-exact vs the
+  oracle over ALL Gaussians / entries (oracle O2 + O3, std::sort of M entries).
+- Forward: the oracle's brute force (every Gaussian, per pixel) on a fixed-seed
+  sample of masked pixels plus every pixel of the heaviest tile.
+- Backward: sparse upstream on sampled pixels; every Gaussian's
+  gradient must match the oracle's backward over exactly those pixels.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import scenes as S
+from tests.gpu_util import compare_grads, compare_pixels, run_gpu, upstream_at
+
+pytestmark = pytest.mark.gpu
+
+
+def c4_view():
+    sub = S.subregion(0, n_views=1)
+    cam = sub["cameras"][0]
+    mask = S.ray_cast_mask(cam, sub["boxes"], device="cuda")
+    return S.Scene("C4v0", sub["gaussians"], cam, mask)
+
+
+MAKERS = {"C3": lambda: S.config3(device="cuda"), "C5": lambda: S.config5(device="cuda"), "C4v0": c4_view}
+_cache = {}
+
+
+def scene(name):
+    if name not in _cache:
+        _cache.clear()
+        torch.cuda.empty_cache()
+        _cache[name] = MAKERS[name]()
+    return _cache[name]
+
+
+def sample_with_heavy_tile(sc, ranges, n, seed):
+    H, W = sc.mask.shape
+    pix = S.sample_pixels(sc.mask, n, seed=seed)
+    TX = (W + 15) // 16
+    heavy = int(np.argmax(ranges[:, 1] - ranges[:, 0]))
+    ty, tx = divmod(heavy, TX)
+    ii, jj = np.meshgrid(np.arange(tx * 16, min(tx * 16 + 16, W)), np.arange(ty * 16, min(ty * 16 + 16, H)))
+    tp = (jj * W + ii).reshape(-1)
+    return np.union1d(pix, tp[sc.mask.reshape(-1)[tp] != 0])
+
+
+@pytest.mark.parametrize("name", ["C3", "C5", "C4v0"])
+def test_scale_keys_bitexact(name):
+    sc = scene(name)
+    res = run_gpu(sc)
+    r = res["r"]
+    n = sc.gaussians.n
+    p = oracle.project(sc.gaussians, sc.camera, sc.mask)
+    np.testing.assert_array_equal(r.flags.cpu().numpy().view(np.uint32)[:n], p["flags"])
+    live = (p["flags"] & 15) == 15
+    np.testing.assert_array_equal(r.depth.cpu().numpy()[:n][live], p["depth"][live])
+    np.testing.assert_array_equal(r.conic_o.cpu().numpy()[:n][live], p["conic_o"][live])
+    np.testing.assert_array_equal(r.tiles_touched.cpu().numpy().view(np.uint32)[:n], p["tiles"])
+    tl, vl, rg = oracle.keys(p, sc.mask)
+    assert r.M == len(tl)
+    np.testing.assert_array_equal(res["vals"], vl)
+    np.testing.assert_array_equal(res["tile_keys"], tl)
+    np.testing.assert_array_equal(res["ranges"], rg)
+
+
+@pytest.mark.parametrize("name", ["C3", "C5", "C4v0"])
+def test_scale_forward_sampled(name):
+    sc = scene(name)
+    res = run_gpu(sc, bg=(0.1, 0.2, 0.3))
+    pix = sample_with_heavy_tile(sc, res["ranges"], 320, seed=7)
+    ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=(0.1, 0.2, 0.3))
+    errs = compare_pixels(res["img"], ora, pix, sc.camera.width, res["vals"], cam=sc.camera)
+    # near-threshold pixels (R18) are still held to 5e-3 inside compare_pixels; their share stays small
+    assert errs["n_near"] <= max(3, len(pix) // 20)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4v0"])
+def test_scale_backward_sparse(name):
+    sc = scene(name)
+    H, W = sc.mask.shape
+    pix = S.sample_pixels(sc.mask, 200, seed=11)
+    ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix)
+    planes, per = upstream_at(pix, H, W, seed=12, exclude=ora0["near"].astype(bool), ora=ora0, cam=sc.camera)
+    res = run_gpu(sc, upstream=planes)
+    ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=per)
+    compare_grads(res["grads"], ora["grads"], sc.gaussians.sh_degree)
