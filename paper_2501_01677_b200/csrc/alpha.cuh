@@ -67,10 +67,14 @@ __device__ __forceinline__ uint32_t stage_gaussian(float2 xy, float4 co, float t
   const float o = co.w;
   const float l2o = __log2f(255.0f * o);  // >= ~0 since o >= 1/255 for listed Gaussians
   r.b = make_float4(sc.z, o, -l2o - 0.01f, 0.0f);
-  const double det = (double)co.x * (double)co.z - (double)co.y * (double)co.y;
+  // det(conic) = ca cc - cb^2 with Kahan's FMA compensation (accurate to a few ulp even
+  // for strongly anisotropic conics), then cov_xx = cc / det, cov_yy = ca / det.
+  const float bb = co.y * co.y;
+  const float det = __fmaf_rn(co.x, co.z, -bb) - __fmaf_rn(co.y, co.y, -bb);
   const float k2 = 2.0f * (fmaxf(l2o, 0.0f) * 0.6931472f + 0.01f) * 1.05f;
-  const float rx = sqrtf(k2 * (float)((double)co.z / det)) + 0.5f;
-  const float ry = sqrtf(k2 * (float)((double)co.x / det)) + 0.5f;
+  const float kd = __fdividef(k2, det);
+  const float rx = sqrtf(kd * co.z) + 0.5f;
+  const float ry = sqrtf(kd * co.x) + 0.5f;
   uint32_t m = 0;
 #pragma unroll
   for (int k = 0; k < NB; ++k) {

@@ -13,16 +13,17 @@
 // suffix is carried as one scalar (mathematically identical to the 8-vector
 // recurrence of the oracle).
 //
-// Work mapping is A6's: per active tile, 4 warps on 8x8 pixel blocks, two pixels
-// (x, y), (x, y + 4) per lane in packed FP32x2, batches of 256 entries staged with
-// the same exact warp-block cull and compacted per-warp candidate lists, walked
-// in reverse.  A pixel that does not contribute to an entry carries alpha = rho =
-// 0, which zeroes all of its terms and leaves its state unchanged without
-// branches.  Reduction: per entry, the lane's two pixels are summed, the warp's
-// 14 partials are reduce-scattered (5 butterfly levels, 16 shuffles) so that 14
-// lanes each hold one warp sum, those lanes add into a padded shared accumulator
-// of the batch, and after the batch the CTA flushes one double-precision global
-// atomic per (entry, value).
+// Mapping: per active tile one 64-thread CTA (2 warps); warp w owns the 8x16 pixel
+// block of columns 8w..8w+7; a lane owns the FOUR pixels (x, y + 4k), k = 0..3, of
+// its column, which share dx and every per-entry load and run as two packed FP32x2
+// pairs.  Batches of 128 entries are staged with the exact warp-block cull of A6
+// and walked in reverse through compacted per-warp candidate lists.  A pixel that
+// does not contribute to an entry carries alpha = rho = 0, which zeroes all of its
+// terms and leaves its state unchanged without branches.  Reduction: per entry the
+// lane sums its four pixels, the warp reduce-scatters the 14 partials (5 butterfly
+// levels, 16 shuffles) so that 14 lanes each hold one warp sum, those lanes add
+// into a padded shared accumulator of the batch, and after the batch the CTA
+// flushes one double-precision global atomic per (entry, value).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,10 +34,10 @@ namespace pgsag {
 namespace {
 
 constexpr int kG2 = 14;  // du dv dca dcb dcc dop drgb3 dncam3 ddist absgrad
-constexpr int kBT = 128;
+constexpr int kBT = 64;
 constexpr int kBEPT = 2;
 constexpr int kBBatch = kBT * kBEPT;
-constexpr int kBNB = 4;
+constexpr int kBNB = 2;
 constexpr float kLn2 = 0.6931471805599453f;
 
 struct BwdArgs {
@@ -62,6 +63,8 @@ struct BwdArgs {
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float hsum(float2 a) { return a.x + a.y; }
 __device__ __forceinline__ float ld_or0(const float* p, size_t k) { return p ? __ldg(p + k) : 0.0f; }
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -117,8 +120,52 @@ __device__ __forceinline__ void load_pixel(const BwdArgs& a, bool masked, size_t
   s.Pb = a.bg0 * s.G[0] + a.bg1 * s.G[1] + a.bg2 * s.G[2];
 }
 
+// State of one packed pixel pair.
+struct Pair {
+  float2 G[8];
+  float2 Pb, T, Sg;
+  int last0, last1;
+};
+
+__device__ __forceinline__ void make_pair(const PixState& a, const PixState& b, Pair& p) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) p.G[c] = f2(a.G[c], b.G[c]);
+  p.Pb = f2(a.Pb, b.Pb);
+  p.T = f2(a.T, b.T);
+  p.Sg = f2(0.f, 0.f);
+  p.last0 = a.last;
+  p.last1 = b.last;
+}
+
+// Per-entry per-pair screen-space partials (summed over the pair's two pixels into v).
+struct PairOut {
+  float2 wt, dpow, dop, du, dv, dydp;
+};
+
+__device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 rc, const float4& cd,
+                                          const float4& nn, PairOut& o) {
+  const float2 om = __fadd2_rn(bc(1.f), f2(-al.x, -al.y));
+  const float2 Ti = __fmul2_rn(p.T, f2(rcp_approx(om.x), rcp_approx(om.y)));
+  float2 GF = p.G[7];
+  GF = __ffma2_rn(p.G[0], bc(cd.x), GF);
+  GF = __ffma2_rn(p.G[1], bc(cd.y), GF);
+  GF = __ffma2_rn(p.G[2], bc(cd.z), GF);
+  GF = __ffma2_rn(p.G[3], bc(nn.x), GF);
+  GF = __ffma2_rn(p.G[4], bc(nn.y), GF);
+  GF = __ffma2_rn(p.G[5], bc(nn.z), GF);
+  GF = __ffma2_rn(p.G[6], bc(cd.w), GF);
+  const float2 sp = __fadd2_rn(p.Sg, p.Pb);
+  const float2 dal = __fmul2_rn(Ti, __fadd2_rn(GF, f2(-sp.x, -sp.y)));
+  p.Sg = __ffma2_rn(al, GF, __fmul2_rn(om, p.Sg));
+  p.Pb = __fmul2_rn(p.Pb, om);
+  p.T = Ti;
+  o.wt = __fmul2_rn(al, Ti);
+  o.dpow = __fmul2_rn(ac, dal);
+  o.dop = __fmul2_rn(rc, dal);
+}
+
 template <bool kCount>
-__global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
+__global__ void __launch_bounds__(kBT, 10) render_bwd_kernel(BwdArgs a) {
   constexpr int kAccStride = 15;  // padded row: the 14 values of an entry sit in 14 distinct banks
   __shared__ Rec s_rec[kBBatch];
   __shared__ uint32_t s_id[kBBatch];
@@ -144,24 +191,27 @@ __global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
     if (widx >= n_active) break;
     const uint32_t tile = a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
-    const int i = tx * kTile + (w & 1) * 8 + (lane & 7);
-    const int j0 = ty * kTile + (w >> 1) * 8 + (lane >> 3), j1 = j0 + 4;
-    const size_t pix0 = (size_t)j0 * a.d.W + i, pix1 = (size_t)j1 * a.d.W + i;
-    const bool m0 = i < a.d.W && j0 < a.d.H && a.mask[pix0] != 0;
-    const bool m1 = i < a.d.W && j1 < a.d.H && a.mask[pix1] != 0;
+    const int i = tx * kTile + w * 8 + (lane & 7);
+    const int jb = ty * kTile + (lane >> 3);
     const uint32_t rs = a.ranges[2 * tile];
     const float px = (float)i + 0.5f;
-    const float2 py = f2((float)j0 + 0.5f, (float)j1 + 0.5f);
+    const float2 py01 = f2((float)jb + 0.5f, (float)(jb + 4) + 0.5f);
+    const float2 py23 = f2((float)(jb + 8) + 0.5f, (float)(jb + 12) + 0.5f);
     const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
-    PixState s0, s1;
-    load_pixel(a, m0, pix0, HW, px, py.x, s0);
-    load_pixel(a, m1, pix1, HW, px, py.y, s1);
-    float2 Gp[8];  // (pixel0, pixel1) per channel
+    Pair P01, P23;
+    {
+      PixState s[4];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) Gp[c] = f2(s0.G[c], s1.G[c]);
-    float2 Pb = f2(s0.Pb, s1.Pb), Tcur = f2(s0.T, s1.T), Sg = f2(0.f, 0.f);
-    const int last0 = s0.last, last1 = s1.last;
-    const int mylast = max(last0, last1);
+      for (int k = 0; k < 4; ++k) {
+        const int j = jb + 4 * k;
+        const size_t pix = (size_t)j * a.d.W + i;
+        const bool m = i < a.d.W && j < a.d.H && a.mask[pix] != 0;
+        load_pixel(a, m, pix, HW, px, (float)j + 0.5f, s[k]);
+      }
+      make_pair(s[0], s[1], P01);
+      make_pair(s[2], s[3], P23);
+    }
+    const int mylast = max(max(P01.last0, P01.last1), max(P23.last0, P23.last1));
     if (mylast >= 0) atomicMax(&s_maxlast, mylast);
     const int wlast = __reduce_max_sync(0xffffffffu, mylast);
     __syncthreads();
@@ -177,7 +227,7 @@ __global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
         if (slot < cnt) {
           const uint32_t id = a.vals[blo + slot];
           Rec& r = s_rec[slot];
-          mk[e] = stage_gaussian<8, 8>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
+          mk[e] = stage_gaussian<8, 16>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
           r.cd = a.rgb_d[id];
           r.n = a.ncam[id];
           s_id[slot] = id;
@@ -193,67 +243,63 @@ __global__ void __launch_bounds__(kBT) render_bwd_kernel(BwdArgs a) {
         const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
         const float4 ra = lds128(ra_addr);
         const float4 rb = lds128(ra_addr + 16);
+        // p2 for the four pixels (bit-identical to A6's evaluation per element)
         const float dx = px - ra.x;
-        const float2 dy = __fadd2_rn(py, f2(-ra.y, -ra.y));
         const float tA = __fmul_rn(ra.z, dx);
-        const float2 u = __ffma2_rn(f2(ra.w, ra.w), dy, f2(tA, tA));
-        const float2 cq = __fmul2_rn(__fmul2_rn(f2(rb.x, rb.x), dy), dy);
-        const float2 p2 = __ffma2_rn(f2(dx, dx), u, cq);
-        const float rh0 = ex2_approx(p2.x), rh1 = ex2_approx(p2.y);
-        const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(rh0, rh1));
-        float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
+        const float2 dy01 = __fadd2_rn(py01, bc(-ra.y));
+        const float2 dy23 = __fadd2_rn(py23, bc(-ra.y));
+        const float2 p01 = __ffma2_rn(bc(dx), __ffma2_rn(bc(ra.w), dy01, bc(tA)),
+                                      __fmul2_rn(__fmul2_rn(bc(rb.x), dy01), dy01));
+        const float2 p23 = __ffma2_rn(bc(dx), __ffma2_rn(bc(ra.w), dy23, bc(tA)),
+                                      __fmul2_rn(__fmul2_rn(bc(rb.x), dy23), dy23));
+        const float2 rh01 = f2(ex2_approx(p01.x), ex2_approx(p01.y));
+        const float2 rh23 = f2(ex2_approx(p23.x), ex2_approx(p23.y));
+        const float2 or01 = __fmul2_rn(bc(rb.y), rh01);
+        const float2 or23 = __fmul2_rn(bc(rb.y), rh23);
+        float al0 = fminf(kAlphaMax, or01.x), al1 = fminf(kAlphaMax, or01.y);
+        float al2 = fminf(kAlphaMax, or23.x), al3 = fminf(kAlphaMax, or23.y);
         // exactly A6's blend decision (R6); entries past the pixel's last were not blended
-        const bool c0 = kk <= last0 && p2.x <= 0.0f && al0 >= kAlphaMin;
-        const bool c1 = kk <= last1 && p2.y <= 0.0f && al1 >= kAlphaMin;
-        if (kCount) cntV += (unsigned long long)(kk <= last0) + (unsigned long long)(kk <= last1);
-        if (!__any_sync(0xffffffffu, c0 || c1)) continue;
-        al0 = c0 ? al0 : 0.f;
-        al1 = c1 ? al1 : 0.f;
+        const bool c0 = kk <= P01.last0 && p01.x <= 0.0f && al0 >= kAlphaMin;
+        const bool c1 = kk <= P01.last1 && p01.y <= 0.0f && al1 >= kAlphaMin;
+        const bool c2 = kk <= P23.last0 && p23.x <= 0.0f && al2 >= kAlphaMin;
+        const bool c3 = kk <= P23.last1 && p23.y <= 0.0f && al3 >= kAlphaMin;
+        if (kCount)
+          cntV += (unsigned long long)(kk <= P01.last0) + (kk <= P01.last1) + (kk <= P23.last0) + (kk <= P23.last1);
+        if (!__any_sync(0xffffffffu, c0 || c1 || c2 || c3)) continue;
+        al0 = c0 ? al0 : 0.f; al1 = c1 ? al1 : 0.f; al2 = c2 ? al2 : 0.f; al3 = c3 ? al3 : 0.f;
         // rho and alpha as they enter d(opacity) and d(power): zero when clamped at 0.99 (R16)
-        const bool u0 = c0 && orho.x <= kAlphaMax, u1 = c1 && orho.y <= kAlphaMax;
-        const float rc0 = u0 ? rh0 : 0.f, rc1 = u1 ? rh1 : 0.f;
-        const float2 al = f2(al0, al1);
-        const float2 om = __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1));
-        const float2 Ti = __fmul2_rn(Tcur, f2(rcp_approx(om.x), rcp_approx(om.y)));
+        const bool u0 = c0 && or01.x <= kAlphaMax, u1 = c1 && or01.y <= kAlphaMax;
+        const bool u2 = c2 && or23.x <= kAlphaMax, u3 = c3 && or23.y <= kAlphaMax;
         const float4 cd = lds128(ra_addr + 32);
         const float4 nn = lds128(ra_addr + 48);
-        float2 GF = Gp[7];
-        GF = __ffma2_rn(Gp[0], f2(cd.x, cd.x), GF);
-        GF = __ffma2_rn(Gp[1], f2(cd.y, cd.y), GF);
-        GF = __ffma2_rn(Gp[2], f2(cd.z, cd.z), GF);
-        GF = __ffma2_rn(Gp[3], f2(nn.x, nn.x), GF);
-        GF = __ffma2_rn(Gp[4], f2(nn.y, nn.y), GF);
-        GF = __ffma2_rn(Gp[5], f2(nn.z, nn.z), GF);
-        GF = __ffma2_rn(Gp[6], f2(cd.w, cd.w), GF);
-        const float2 dal = __fmul2_rn(Ti, __fadd2_rn(GF, f2(-(Sg.x + Pb.x), -(Sg.y + Pb.y))));
-        Sg = __ffma2_rn(al, GF, __fmul2_rn(om, Sg));
-        Pb = __fmul2_rn(Pb, om);
-        Tcur = Ti;
-        const float2 wt = __fmul2_rn(al, Ti);
+        PairOut o01, o23;
+        pair_grad(P01, f2(al0, al1), f2(u0 ? al0 : 0.f, u1 ? al1 : 0.f), f2(u0 ? rh01.x : 0.f, u1 ? rh01.y : 0.f),
+                  cd, nn, o01);
+        pair_grad(P23, f2(al2, al3), f2(u2 ? al2 : 0.f, u3 ? al3 : 0.f), f2(u2 ? rh23.x : 0.f, u3 ? rh23.y : 0.f),
+                  cd, nn, o23);
         float v[16];
 #pragma unroll
-        for (int c = 0; c < 7; ++c) {
-          const float2 x = __fmul2_rn(wt, Gp[c]);
-          v[6 + c] = x.x + x.y;
-        }
-        const float2 dpow = __fmul2_rn(f2(u0 ? al0 : 0.f, u1 ? al1 : 0.f), dal);
-        const float2 dop = __fmul2_rn(f2(rc0, rc1), dal);
-        v[5] = dop.x + dop.y;
-        const float sdp = dpow.x + dpow.y;
-        const float2 dydp = __fmul2_rn(dy, dpow);
-        const float sdydp = dydp.x + dydp.y;
-        const float2 dy2dp = __fmul2_rn(dy, dydp);
-        v[2] = -0.5f * dx * dx * sdp;
+        for (int c = 0; c < 7; ++c)
+          v[6 + c] = hsum(__ffma2_rn(o23.wt, P23.G[c], __fmul2_rn(o01.wt, P01.G[c])));
+        v[5] = hsum(__fadd2_rn(o01.dop, o23.dop));
+        const float sdp = hsum(__fadd2_rn(o01.dpow, o23.dpow));
+        const float2 dydp01 = __fmul2_rn(dy01, o01.dpow), dydp23 = __fmul2_rn(dy23, o23.dpow);
+        const float sdydp = hsum(__fadd2_rn(dydp01, dydp23));
+        const float sdy2dp = hsum(__ffma2_rn(dy23, dydp23, __fmul2_rn(dy01, dydp01)));
+        v[2] = (-0.5f * dx) * dx * sdp;
         v[3] = -dx * sdydp;
-        v[4] = -0.5f * (dy2dp.x + dy2dp.y);
+        v[4] = -0.5f * sdy2dp;
         // per-pixel screen-space mean gradient: (ca, cb, cc) = -ln2 (2A', B', 2C')
-        const float2 gu = __ffma2_rn(f2(ra.w, ra.w), dy, f2(2.0f * tA, 2.0f * tA));        // 2A'dx + B'dy
-        const float2 gv = __ffma2_rn(f2(2.0f * rb.x, 2.0f * rb.x), dy, f2(ra.w * dx, ra.w * dx));  // B'dx + 2C'dy
-        const float2 du = __fmul2_rn(gu, __fmul2_rn(f2(-kLn2, -kLn2), dpow));
-        const float2 dv = __fmul2_rn(gv, __fmul2_rn(f2(-kLn2, -kLn2), dpow));
-        v[0] = du.x + du.y;
-        v[1] = dv.x + dv.y;
-        v[13] = (fabsf(du.x) + fabsf(dv.x)) + (fabsf(du.y) + fabsf(dv.y));
+        const float2 kd01 = __fmul2_rn(bc(-kLn2), o01.dpow), kd23 = __fmul2_rn(bc(-kLn2), o23.dpow);
+        const float twoA = 2.0f * tA, bdx = ra.w * dx, twoC = 2.0f * rb.x;
+        const float2 du01 = __fmul2_rn(__ffma2_rn(bc(ra.w), dy01, bc(twoA)), kd01);
+        const float2 du23 = __fmul2_rn(__ffma2_rn(bc(ra.w), dy23, bc(twoA)), kd23);
+        const float2 dv01 = __fmul2_rn(__ffma2_rn(bc(twoC), dy01, bc(bdx)), kd01);
+        const float2 dv23 = __fmul2_rn(__ffma2_rn(bc(twoC), dy23, bc(bdx)), kd23);
+        v[0] = hsum(__fadd2_rn(du01, du23));
+        v[1] = hsum(__fadd2_rn(dv01, dv23));
+        v[13] = ((fabsf(du01.x) + fabsf(dv01.x)) + (fabsf(du01.y) + fabsf(dv01.y))) +
+                ((fabsf(du23.x) + fabsf(dv23.x)) + (fabsf(du23.y) + fabsf(dv23.y)));
         v[14] = 0.f;
         v[15] = 0.f;
         // reduce-scatter 16 -> 1 value per lane pair
