@@ -198,7 +198,7 @@ def main():
     g = GaussianTensors.from_numpy(g_np, dev)
     H, W = masks[0].shape
     ccam = [camera_from(c) for c in cams]
-    r = Rasterizer(g.n, W, H, g.sh_degree, capacity=24 * g.n, device=dev, counters=True)
+    r = Rasterizer(g.n, W, H, g.sh_degree, capacity=24 * g.n, device=dev, counters=True, sat=False)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1677 + rank)
     up = {"dC": torch.randn(3, H, W, device=dev, generator=gen), "dN": torch.randn(3, H, W, device=dev, generator=gen),

@@ -95,7 +95,8 @@ typedef struct {
 /* A0 output: building-mask tile occupancy (R14). */
 typedef struct {
   uint32_t *tile_cnt; /* [TY*TX]        number of mask pixels per tile                  */
-  int32_t *sat;       /* [(TY+1)*(TX+1)] summed-area table of active (cnt > 0) tiles     */
+  int32_t *sat;       /* [(TY+1)*(TX+1)] summed-area table of active (cnt > 0) tiles;
+                         OPTIONAL (NULL = not computed; the path itself uses active_bits) */
   uint32_t *active;   /* [TY*TX]        active tile ids ascending; first *n_active valid  */
   uint32_t *n_active; /* [1]            device scalar                                     */
   uint32_t *active_bits; /* [TY*ceil(TX/32)] bitmap of active tiles, row-major, bit tx%32 */

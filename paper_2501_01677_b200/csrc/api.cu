@@ -94,7 +94,7 @@ int check_proj(const pgsag_projected* p) {
 }
 
 int check_tm(const pgsag_tilemask* tm) {
-  if (!tm || !tm->tile_cnt || !tm->sat || !tm->active || !tm->n_active || !tm->active_bits)
+  if (!tm || !tm->tile_cnt || !tm->active || !tm->n_active || !tm->active_bits)
     return fail(PGSAG_EINVAL, "tilemask buffer is NULL");
   return PGSAG_OK;
 }
@@ -196,7 +196,7 @@ int pgsag_bin_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const pgs
   uint32_t* counters = reinterpret_cast<uint32_t*>(w + L.counters);
   cudaError_t e;
   // zero the look-back / histogram / counter state of stage 1 and A2
-  e = cudaMemsetAsync(w + L.status1, 0, 4 * (size_t)kMaxSortPasses * L.tiles1 * kRadix, st);
+  e = cudaMemsetAsync(w + L.status1, 0, 4 * (size_t)kMaxSortPasses * L.tiles1 * kMaxRadix, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(w + L.scan_status, 0, L.g2d - L.scan_status, st);
   if (e != cudaSuccess) return cuda_fail(e, "memset");
   unsigned long long M = 0;

@@ -14,6 +14,7 @@ constexpr int kTilePix = kTile * kTile;  // 256 pixels -> 256 threads per compos
 // ---- sort configuration (A4) ----
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
+constexpr int kMaxRadix = 512;  // 9-bit digits where they save a pass
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per CTA

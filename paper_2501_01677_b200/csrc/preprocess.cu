@@ -51,16 +51,6 @@ __global__ void __launch_bounds__(128) tilemask_count_kernel(const uint8_t* __re
   if (lane == 0 && wtx < d.TX) bitmap[ty * d.WPR + wtx / 32] = word;
 }
 
-__device__ __forceinline__ uint32_t row_prefix(const uint32_t* __restrict__ row, int x, int WPR) {
-  // number of set bits of the row bitmap at positions < x
-  uint32_t c = 0;
-  const int wq = x >> 5;
-  for (int w = 0; w < wq; ++w) c += __popc(row[w]);
-  const int r = x & 31;
-  if (r && wq < WPR) c += __popc(row[wq] & ((1u << r) - 1u));
-  return c;
-}
-
 // ------------------------------------------------------- A0 SAT + active list
 // Single CTA: the active-tile bitmap (TY x WPR words, 10 KB at 5472x3648) lives in
 // shared memory; one thread per SAT column accumulates down the rows.
@@ -96,21 +86,49 @@ __global__ void __launch_bounds__(1024) tilemask_sat_kernel(Dims d, const uint32
     if (tid == 0) rowpre[0] = 0;
   }
   __syncthreads();
-  const int S = d.TX + 1;
-  for (int x = tid; x <= d.TX; x += nt) {
-    sat[x] = 0;  // row 0
-    uint32_t acc = 0;
-    for (int y = 0; y < d.TY; ++y) {
-      if (x > 0) acc += row_prefix(bm + y * d.WPR, x, d.WPR);
-      sat[(size_t)(y + 1) * S + x] = (int32_t)acc;
+  (void)sat;
+  // word-parallel active list: thread per bitmap word, set bits in ascending order
+  for (int k = tid; k < d.TY * d.WPR; k += nt) {
+    const int y = k / d.WPR, wq = k - y * d.WPR;
+    uint32_t bits = bm[k];
+    if (!bits) continue;
+    uint32_t pos = rowpre[y];
+    for (int w = 0; w < wq; ++w) pos += __popc(bm[y * d.WPR + w]);
+    const uint32_t t0 = (uint32_t)(y * d.TX + wq * 32);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      active[pos++] = t0 + (uint32_t)b;
     }
   }
-  for (int t = tid; t < d.TX * d.TY; t += nt) {
-    const int ty = t / d.TX, tx = t - ty * d.TX;
-    if ((bm[ty * d.WPR + (tx >> 5)] >> (tx & 31)) & 1u)
-      active[rowpre[ty] + row_prefix(bm + ty * d.WPR, tx, d.WPR)] = (uint32_t)t;
-  }
   if (tid == 0) *n_active = rowpre[d.TY];
+}
+
+// SAT of the active flags, SAT[y][x] = #active tiles with ty < y, tx < x: one warp per
+// 32 columns; per-row word prefixes in shared memory, one running sum per lane.
+__global__ void __launch_bounds__(32) tilemask_satcol_kernel(Dims d, const uint32_t* __restrict__ bitmap,
+                                                              int32_t* __restrict__ sat) {
+  extern __shared__ uint32_t pre[];  // [TY]: set bits in words < b of each row
+  const int lane = threadIdx.x;
+  const int b = blockIdx.x;  // word / 32-column block
+  const int x = b * 32 + lane;
+  const int S = d.TX + 1;
+  for (int y = lane; y < d.TY; y += 32) {
+    uint32_t c = 0;
+    for (int w = 0; w < b && w < d.WPR; ++w) c += __popc(__ldg(bitmap + y * d.WPR + w));
+    pre[y] = c;
+  }
+  __syncwarp();
+  if (x > d.TX) return;
+  sat[x] = 0;
+  const uint32_t lowmask = lane ? ((1u << lane) - 1u) : 0u;
+  uint32_t acc = 0;
+#pragma unroll 4
+  for (int y = 0; y < d.TY; ++y) {
+    const uint32_t word = b < d.WPR ? __ldg(bitmap + y * d.WPR + b) : 0u;
+    acc += pre[y] + __popc(word & lowmask);
+    sat[(size_t)(y + 1) * S + x] = (int32_t)acc;
+  }
 }
 
 // --------------------------------------------------------------- A1 project
@@ -144,7 +162,7 @@ __device__ __forceinline__ float lnup(float y) {
 __global__ void __launch_bounds__(256) preprocess_kernel(
     int n, int deg, const float* __restrict__ mean, const float* __restrict__ scale,
     const float* __restrict__ rot, const float* __restrict__ opac, const float* __restrict__ sh, CamK cam,
-    Dims d, const int32_t* __restrict__ sat, float2* __restrict__ mean2d, float4* __restrict__ conic_o,
+    Dims d, const uint32_t* __restrict__ bits, float2* __restrict__ mean2d, float4* __restrict__ conic_o,
     float* __restrict__ depth, short4* __restrict__ rect, uint32_t* __restrict__ tiles_touched,
     float4* __restrict__ rgb_d, float4* __restrict__ ncam, uint32_t* __restrict__ flags) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -243,9 +261,18 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         if (tx0 <= tx1 && ty0 <= ty1) {
           fl |= PGSAG_F_RECT;
           rc = make_short4((short)tx0, (short)ty0, (short)tx1, (short)ty1);
-          const int S = d.TX + 1;
-          touched = (uint32_t)(__ldg(sat + (ty1 + 1) * S + tx1 + 1) - __ldg(sat + ty0 * S + tx1 + 1) -
-                               __ldg(sat + (ty1 + 1) * S + tx0) + __ldg(sat + ty0 * S + tx0));
+          // active tiles in the rect, straight from the A0 bitmap (rows of 32-tile words)
+          const int w0 = tx0 >> 5, w1 = tx1 >> 5;
+          const uint32_t m0 = ~0u << (tx0 & 31), m1 = ~0u >> (31 - (tx1 & 31));
+          for (int y = ty0; y <= ty1; ++y) {
+            const uint32_t* row = bits + y * d.WPR;
+            if (w0 == w1) {
+              touched += __popc(__ldg(row + w0) & m0 & m1);
+            } else {
+              touched += __popc(__ldg(row + w0) & m0) + __popc(__ldg(row + w1) & m1);
+              for (int w = w0 + 1; w < w1; ++w) touched += __popc(__ldg(row + w));
+            }
+          }
         }
         // flattened-Gaussian normal (R4) and plane distance (Eq. 3, R2)
         int k = 0;
@@ -319,8 +346,12 @@ cudaError_t launch_tilemask(const uint8_t* mask, const Dims& d, pgsag_tilemask* 
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(tilemask_sat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   {
-    KTimer kt_("A0_tilemask_sat", st);
+    KTimer kt_("A0_tilemask_list", st);
     tilemask_sat_kernel<<<1, 1024, smem, st>>>(d, bitmap, tm->sat, tm->active, tm->n_active);
+  }
+  if (tm->sat) {  // optional output (not needed by the path: A1 counts from the bitmap)
+    KTimer kt_("A0_tilemask_sat", st);
+    tilemask_satcol_kernel<<<(d.TX + 1 + 31) / 32, 32, sizeof(uint32_t) * d.TY, st>>>(d, bitmap, tm->sat);
   }
   return cudaGetLastError();
 }
@@ -342,7 +373,7 @@ cudaError_t launch_preprocess(const pgsag_gaussians* g, const pgsag_camera* c, c
   {
     KTimer kt_("A1_preprocess", st);
     preprocess_kernel<<<(g->n + threads - 1) / threads, threads, 0, st>>>(
-        g->n, g->sh_degree, g->mean, g->scale, g->rot, g->opacity, g->sh, k, d, tm->sat,
+        g->n, g->sh_degree, g->mean, g->scale, g->rot, g->opacity, g->sh, k, d, tm->active_bits,
         reinterpret_cast<float2*>(out->mean2d), reinterpret_cast<float4*>(out->conic_o), out->depth,
         reinterpret_cast<short4*>(out->rect), out->tiles_touched, reinterpret_cast<float4*>(out->rgb_d),
         reinterpret_cast<float4*>(out->ncam), out->flags);

@@ -19,7 +19,7 @@ struct CamB {
 };
 
 template <int DEG>
-__global__ void __launch_bounds__(256) preprocess_bwd_kernel(
+__global__ void __launch_bounds__(128, 4) preprocess_bwd_kernel(
     int n, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
     const float* __restrict__ sh, const uint32_t* __restrict__ flags, const double* __restrict__ g2d, CamB cam,
     float* __restrict__ dmean, float* __restrict__ dscale, float* __restrict__ drot, float* __restrict__ dopac,
@@ -167,39 +167,50 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
   const double len = sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
   const double il = 1.0 / len;
   const double dx = t[0] * il, dy = t[1] * il, dz = t[2] * il;
-  const double xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yzp = dy * dz, xzp = dx * dz;
-  const double c1 = 0.4886025119029199;
-  const double c2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
-                        0.5462742152960396};
-  const double c3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
-                        -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
-  double Yb[16], GY[16][3];
-  Yb[0] = 0.28209479177387814; GY[0][0] = 0.; GY[0][1] = 0.; GY[0][2] = 0.;
-  Yb[1] = -c1 * dy; GY[1][0] = 0.; GY[1][1] = -c1; GY[1][2] = 0.;
-  Yb[2] = c1 * dz; GY[2][0] = 0.; GY[2][1] = 0.; GY[2][2] = c1;
-  Yb[3] = -c1 * dx; GY[3][0] = -c1; GY[3][1] = 0.; GY[3][2] = 0.;
-  Yb[4] = c2[0] * xy; GY[4][0] = c2[0] * dy; GY[4][1] = c2[0] * dx; GY[4][2] = 0.;
-  Yb[5] = c2[1] * yzp; GY[5][0] = 0.; GY[5][1] = c2[1] * dz; GY[5][2] = c2[1] * dy;
-  Yb[6] = c2[2] * (2. * zz - xx - yy); GY[6][0] = -2. * c2[2] * dx; GY[6][1] = -2. * c2[2] * dy; GY[6][2] = 4. * c2[2] * dz;
-  Yb[7] = c2[3] * xzp; GY[7][0] = c2[3] * dz; GY[7][1] = 0.; GY[7][2] = c2[3] * dx;
-  Yb[8] = c2[4] * (xx - yy); GY[8][0] = 2. * c2[4] * dx; GY[8][1] = -2. * c2[4] * dy; GY[8][2] = 0.;
-  Yb[9] = c3[0] * dy * (3. * xx - yy); GY[9][0] = 6. * c3[0] * xy; GY[9][1] = c3[0] * (3. * xx - 3. * yy); GY[9][2] = 0.;
-  Yb[10] = c3[1] * xy * dz; GY[10][0] = c3[1] * yzp; GY[10][1] = c3[1] * xzp; GY[10][2] = c3[1] * xy;
-  Yb[11] = c3[2] * dy * (4. * zz - xx - yy); GY[11][0] = -2. * c3[2] * xy; GY[11][1] = c3[2] * (4. * zz - xx - 3. * yy); GY[11][2] = 8. * c3[2] * yzp;
-  Yb[12] = c3[3] * dz * (2. * zz - 3. * xx - 3. * yy); GY[12][0] = -6. * c3[3] * xzp; GY[12][1] = -6. * c3[3] * yzp; GY[12][2] = c3[3] * (6. * zz - 3. * xx - 3. * yy);
-  Yb[13] = c3[4] * dx * (4. * zz - xx - yy); GY[13][0] = c3[4] * (4. * zz - 3. * xx - yy); GY[13][1] = -2. * c3[4] * xy; GY[13][2] = 8. * c3[4] * xzp;
-  Yb[14] = c3[5] * dz * (xx - yy); GY[14][0] = 2. * c3[5] * xzp; GY[14][1] = -2. * c3[5] * yzp; GY[14][2] = c3[5] * (xx - yy);
-  Yb[15] = c3[6] * dx * (xx - 3. * yy); GY[15][0] = c3[6] * (3. * xx - 3. * yy); GY[15][1] = -6. * c3[6] * xy; GY[15][2] = 0.;
-  double dd0 = 0., dd1 = 0., dd2 = 0.;
+  // SH part in float, one basis function at a time (value and gradient inline, streamed to dsh):
+  // no per-thread arrays, so A8 stays in registers at a useful occupancy.
+  float dd0 = 0.f, dd1 = 0.f, dd2 = 0.f;
+  {
+    const float x = (float)dx, y = (float)dy, z = (float)dz;
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    const float gcs[3] = {(fl & PGSAG_F_RGB_CLAMP0) ? 0.f : (float)gg[6],
+                          (fl & (PGSAG_F_RGB_CLAMP0 << 1)) ? 0.f : (float)gg[7],
+                          (fl & (PGSAG_F_RGB_CLAMP0 << 2)) ? 0.f : (float)gg[8]};
+    auto term = [&](int l, float Yl, float gx, float gy, float gz) {
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const double gc = (fl & (PGSAG_F_RGB_CLAMP0 << c)) ? 0. : gg[6 + c];
-#pragma unroll
-    for (int l = 0; l < K; ++l) {
-      const double shv = sh[(size_t)(l * 3 + c) * n + i];
-      dsh[(size_t)(l * 3 + c) * n + i] = (float)(Yb[l] * gc);
-      const double f = shv * gc;
-      dd0 += GY[l][0] * f; dd1 += GY[l][1] * f; dd2 += GY[l][2] * f;
+      for (int c = 0; c < 3; ++c) {
+        const size_t k = (size_t)(l * 3 + c) * n + i;
+        dsh[k] = Yl * gcs[c];
+        const float f = __ldg(sh + k) * gcs[c];
+        dd0 += gx * f; dd1 += gy * f; dd2 += gz * f;
+      }
+    };
+    term(0, 0.28209479177387814f, 0.f, 0.f, 0.f);
+    if (DEG >= 1) {
+      const float c1 = 0.4886025119029199f;
+      term(1, -c1 * y, 0.f, -c1, 0.f);
+      term(2, c1 * z, 0.f, 0.f, c1);
+      term(3, -c1 * x, -c1, 0.f, 0.f);
+    }
+    if (DEG >= 2) {
+      const float a = 1.0925484305920792f, b = 0.31539156525252005f, e = 0.5462742152960396f;
+      term(4, a * xy, a * y, a * x, 0.f);
+      term(5, -a * yz, 0.f, -a * z, -a * y);
+      term(6, b * (2.f * zz - xx - yy), -2.f * b * x, -2.f * b * y, 4.f * b * z);
+      term(7, -a * xz, -a * z, 0.f, -a * x);
+      term(8, e * (xx - yy), 2.f * e * x, -2.f * e * y, 0.f);
+    }
+    if (DEG >= 3) {
+      const float c0 = -0.5900435899266435f, cA = 2.890611442640554f, cB = -0.4570457994644658f,
+                  cC = 0.3731763325901154f, cD = 1.445305721320277f;
+      term(9, c0 * y * (3.f * xx - yy), 6.f * c0 * xy, c0 * (3.f * xx - 3.f * yy), 0.f);
+      term(10, cA * xy * z, cA * yz, cA * xz, cA * xy);
+      term(11, cB * y * (4.f * zz - xx - yy), -2.f * cB * xy, cB * (4.f * zz - xx - 3.f * yy), 8.f * cB * yz);
+      term(12, cC * z * (2.f * zz - 3.f * xx - 3.f * yy), -6.f * cC * xz, -6.f * cC * yz,
+           cC * (6.f * zz - 3.f * xx - 3.f * yy));
+      term(13, cB * x * (4.f * zz - xx - yy), cB * (4.f * zz - 3.f * xx - yy), -2.f * cB * xy, 8.f * cB * xz);
+      term(14, cD * z * (xx - yy), 2.f * cD * xz, -2.f * cD * yz, cD * (xx - yy));
+      term(15, c0 * x * (xx - 3.f * yy), c0 * (3.f * xx - 3.f * yy), -6.f * c0 * xy, 0.f);
     }
   }
   const double ddot = dx * dd0 + dy * dd1 + dz * dd2;
@@ -228,9 +239,9 @@ cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* 
   cb.ly = (double)(1.3f * ((0.5f * (float)cam->height) / cam->fy));
   {
     KTimer kt_("A8_preprocess_bwd", st);
-    const int blocks = (n + 255) / 256;
+    const int blocks = (n + 127) / 128;
 #define PGSAG_A8(DEG)                                                                                         \
-  preprocess_bwd_kernel<DEG><<<blocks, 256, 0, st>>>(n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d, cb, \
+  preprocess_bwd_kernel<DEG><<<blocks, 128, 0, st>>>(n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d, cb, \
                                                       out->dmean, out->dscale, out->drot, out->dopacity,      \
                                                       out->dsh, out->absgrad2d, out->grad2d)
     switch (g->sh_degree) {

@@ -70,48 +70,80 @@ __global__ void depth_keys_kernel(int n, const float* __restrict__ depth, const 
   ids[i] = (uint32_t)i;
 }
 
+// ------------------------------------------------------------ pass plan
+// Digit widths of an LSD sort over `bits` key bits: 8-bit digits, or 9-bit ones
+// where that saves a pass (17-18 bits: 2 passes instead of 3; 25-27: 3 instead of 4).
+struct PassPlan {
+  int n;
+  int shift[kMaxSortPasses];
+  int width[kMaxSortPasses];
+};
+
+PassPlan make_plan(int bits) {
+  PassPlan p;
+  p.n = 0;
+  int w[kMaxSortPasses];
+  if (bits <= 0) return p;
+  if (bits <= 9) { w[0] = bits; p.n = 1; }
+  else if (bits <= 16) { w[0] = 8; w[1] = bits - 8; p.n = 2; }
+  else if (bits <= 18) { w[0] = 9; w[1] = bits - 9; p.n = 2; }
+  else if (bits <= 24) { w[0] = 8; w[1] = 8; w[2] = bits - 16; p.n = 3; }
+  else if (bits <= 27) { w[0] = 9; w[1] = 9; w[2] = bits - 18; p.n = 3; }
+  else { w[0] = 8; w[1] = 8; w[2] = 8; w[3] = bits - 24; p.n = 4; }
+  int s = 0;
+  for (int k = 0; k < p.n; ++k) { p.shift[k] = s; p.width[k] = w[k]; s += w[k]; }
+  return p;
+}
+
 // ------------------------------------------------------------ histogram
-// Digit histograms of all passes at once (onesweep's upfront pass).
+// Digit histograms of all passes at once (onesweep's upfront pass); ghist is
+// [pass][kMaxRadix].
 __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys,
                                                           const uint32_t* __restrict__ n_ptr, uint32_t n_fixed,
-                                                          int npass, int end_bit, uint32_t* __restrict__ ghist) {
-  __shared__ uint32_t sh[kMaxSortPasses][kRadix];
+                                                          PassPlan plan, uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t sh[kMaxSortPasses][kMaxRadix];
   const uint32_t n = n_ptr ? *n_ptr : n_fixed;
-  for (int k = threadIdx.x; k < kMaxSortPasses * kRadix; k += blockDim.x) (&sh[0][0])[k] = 0;
+  for (int k = threadIdx.x; k < kMaxSortPasses * kMaxRadix; k += blockDim.x) (&sh[0][0])[k] = 0;
   __syncthreads();
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
     const uint32_t key = keys[idx];
-    for (int p = 0; p < npass; ++p) {
-      const int shift = p * kRadixBits;
-      const int nb = min(kRadixBits, end_bit - shift);
-      atomicAdd(&sh[p][(key >> shift) & ((1u << nb) - 1u)], 1u);
-    }
+    for (int p = 0; p < plan.n; ++p)
+      atomicAdd(&sh[p][(key >> plan.shift[p]) & ((1u << plan.width[p]) - 1u)], 1u);
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < npass * kRadix; k += blockDim.x) {
+  for (int k = threadIdx.x; k < plan.n * kMaxRadix; k += blockDim.x) {
     const uint32_t v = (&sh[0][0])[k];
     if (v) atomicAdd(ghist + k, v);
   }
 }
 
 // ------------------------------------------------------------ onesweep pass
+template <int RB>
+constexpr size_t pass_smem() {
+  return sizeof(uint32_t) * (2 * kSortTile + (kSortThreads / 32 + 2) * (1 << RB));
+}
+
+template <int RB>
 __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ n_ptr, uint32_t n_fixed, int shift, int nbits,
     const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
   constexpr int NW = kSortThreads / 32;
-  __shared__ uint32_t s_keys[kSortTile];
-  __shared__ uint32_t s_vals[kSortTile];
-  __shared__ uint32_t s_whist[NW][kRadix];
-  __shared__ uint32_t s_cta_start[kRadix];
-  __shared__ uint32_t s_gbase[kRadix];
+  constexpr int R = 1 << RB;
+  constexpr int DPT = R / kSortThreads;  // digits per thread (1 or 2)
+  extern __shared__ uint32_t sm[];
+  uint32_t* s_keys = sm;
+  uint32_t* s_vals = s_keys + kSortTile;
+  uint32_t* s_whist = s_vals + kSortTile;  // [NW][R]
+  uint32_t* s_cta_start = s_whist + NW * R;
+  uint32_t* s_gbase = s_cta_start + R;
   __shared__ uint32_t s_warp[NW];
   __shared__ uint32_t s_tile;
 
   const uint32_t n = n_ptr ? *n_ptr : n_fixed;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int k = tid; k < NW * kRadix; k += kSortThreads) (&s_whist[0][0])[k] = 0;
+  for (int k = tid; k < NW * R; k += kSortThreads) s_whist[k] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint32_t base = tile * (uint32_t)kSortTile;
@@ -136,48 +168,65 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
 #pragma unroll
   for (int k = 0; k < kSortItems; ++k) {
     const uint32_t idx = wbase + (uint32_t)k * 32u + lane;
-    const uint32_t dg = idx < n ? ((key[k] >> shift) & mask) : (uint32_t)kRadix;
+    const uint32_t dg = idx < n ? ((key[k] >> shift) & mask) : (uint32_t)R;
     const uint32_t peers = __match_any_sync(0xffffffffu, dg);
     const uint32_t r = __popc(peers & lt);
-    const uint32_t prev = dg < (uint32_t)kRadix ? s_whist[w][dg] : 0u;
+    const uint32_t prev = dg < (uint32_t)R ? s_whist[w * R + dg] : 0u;
     __syncwarp();
-    if (r == 0 && dg < (uint32_t)kRadix) s_whist[w][dg] = prev + __popc(peers);
+    if (r == 0 && dg < (uint32_t)R) s_whist[w * R + dg] = prev + __popc(peers);
     __syncwarp();
     rank[k] = prev + r;
   }
   __syncthreads();
-  // per digit: exclusive offsets across warps, CTA total, look-back
-  const int dgt = tid;  // kSortThreads == kRadix
-  uint32_t total = 0;
+  // per digit (DPT consecutive digits per thread): exclusive offsets across warps,
+  // CTA total, decoupled look-back over predecessor CTAs
+  uint32_t tot[DPT], excl[DPT], gh[DPT];
+  uint32_t tsum = 0, gsum = 0;
 #pragma unroll
-  for (int k = 0; k < NW; ++k) {
-    const uint32_t t = s_whist[k][dgt];
-    s_whist[k][dgt] = total;
-    total += t;
-  }
-  uint32_t* my = status + (size_t)tile * kRadix + dgt;
-  uint32_t excl = 0;
-  if (tile == 0) {
-    st_volatile(my, kLbPrefix | total);
-  } else {
-    st_volatile(my, kLbAgg | total);
-    int j = (int)tile - 1;
-    while (j >= 0) {
-      uint32_t s;
-      do { s = ld_volatile(status + (size_t)j * kRadix + dgt); } while ((s & ~kLbMask) == 0u);
-      excl += s & kLbMask;
-      if (s & kLbPrefix) break;
-      --j;
+  for (int j = 0; j < DPT; ++j) {
+    const int dgt = tid * DPT + j;
+    uint32_t total = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      const uint32_t t = s_whist[k * R + dgt];
+      s_whist[k * R + dgt] = total;
+      total += t;
     }
-    st_volatile(my, kLbPrefix | (excl + total));
+    tot[j] = total;
+    tsum += total;
+    gh[j] = ghist[dgt];
+    gsum += gh[j];
+    st_volatile(status + (size_t)tile * R + dgt, (tile == 0 ? kLbPrefix : kLbAgg) | total);
   }
-  // global start of digit dgt = (exclusive scan of ghist) + excl
-  uint32_t gex;
-  block_excl_scan<kSortThreads>(ghist[dgt], s_warp, gex);
-  s_gbase[dgt] = gex + excl;
-  uint32_t cex;
-  block_excl_scan<kSortThreads>(total, s_warp, cex);
-  s_cta_start[dgt] = cex;
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int dgt = tid * DPT + j;
+    uint32_t ex = 0;
+    if (tile != 0) {
+      int q = (int)tile - 1;
+      while (q >= 0) {
+        uint32_t s;
+        do { s = ld_volatile(status + (size_t)q * R + dgt); } while ((s & ~kLbMask) == 0u);
+        ex += s & kLbMask;
+        if (s & kLbPrefix) break;
+        --q;
+      }
+      st_volatile(status + (size_t)tile * R + dgt, kLbPrefix | (ex + tot[j]));
+    }
+    excl[j] = ex;
+  }
+  // global start of each digit = (exclusive scan of ghist) + excl; CTA-local starts
+  uint32_t gex, cex;
+  block_excl_scan<kSortThreads>(gsum, s_warp, gex);
+  block_excl_scan<kSortThreads>(tsum, s_warp, cex);
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int dgt = tid * DPT + j;
+    s_gbase[dgt] = gex + excl[j];
+    s_cta_start[dgt] = cex;
+    gex += gh[j];
+    cex += tot[j];
+  }
   __syncthreads();
   // scatter into shared memory in CTA-local sorted order
 #pragma unroll
@@ -185,7 +234,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
     const uint32_t idx = wbase + (uint32_t)k * 32u + lane;
     if (idx < n) {
       const uint32_t dg = (key[k] >> shift) & mask;
-      const uint32_t pos = s_cta_start[dg] + s_whist[w][dg] + rank[k];
+      const uint32_t pos = s_cta_start[dg] + s_whist[w * R + dg] + rank[k];
       s_keys[pos] = key[k];
       s_vals[pos] = val[k];
     }
@@ -315,24 +364,34 @@ int num_sms() {
 cudaError_t radix_sort(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, const uint32_t* n_dev,
                        uint32_t n_fixed, uint32_t grid_bound, int end_bit, uint32_t* status, size_t status_stride,
                        uint32_t* ghist, uint32_t* counters, cudaStream_t st, bool* res_in_a) {
-  const int npass = (end_bit + kRadixBits - 1) / kRadixBits;
+  const PassPlan plan = make_plan(end_bit);
+  const int npass = plan.n;
   *res_in_a = true;
   if (npass == 0 || grid_bound == 0) return cudaSuccess;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(radix_pass_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem<8>());
+    cudaFuncSetAttribute(radix_pass_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem<9>());
+    attr_set = true;
+  }
   const int hist_grid = min((int)((grid_bound + 255) / 256), num_sms() * 4);
   {
     KTimer kt_("A4_radix_hist", st);
-    radix_hist_kernel<<<hist_grid, 256, 0, st>>>(ka, n_dev, n_fixed, npass, end_bit, ghist);
+    radix_hist_kernel<<<hist_grid, 256, 0, st>>>(ka, n_dev, n_fixed, plan, ghist);
   }
   const uint32_t tiles = (grid_bound + kSortTile - 1) / kSortTile;
   uint32_t *ki = ka, *vi = va, *ko = kb, *vo = vb;
   for (int p = 0; p < npass; ++p) {
-    const int shift = p * kRadixBits;
-    const int nb = min(kRadixBits, end_bit - shift);
     {
       KTimer kt_("A4_radix_onesweep", st);
-      radix_pass_kernel<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_fixed, shift, nb,
-                                                        ghist + p * kRadix, status + p * status_stride,
-                                                        counters + p);
+      if (plan.width[p] <= 8)
+        radix_pass_kernel<8><<<tiles, kSortThreads, pass_smem<8>(), st>>>(
+            ki, vi, ko, vo, n_dev, n_fixed, plan.shift[p], plan.width[p], ghist + p * kMaxRadix,
+            status + p * status_stride, counters + p);
+      else
+        radix_pass_kernel<9><<<tiles, kSortThreads, pass_smem<9>(), st>>>(
+            ki, vi, ko, vo, n_dev, n_fixed, plan.shift[p], plan.width[p], ghist + p * kMaxRadix,
+            status + p * status_stride, counters + p);
     }
     uint32_t* t;
     t = ki; ki = ko; ko = t;
@@ -361,10 +420,10 @@ WsLayout ws_layout(int32_t n, int32_t W, int32_t H, int64_t cap) {
   L.offsets = take(4 * nn);
   L.dup_keys = take(4 * cc);
   L.dup_vals = take(4 * cc);
-  L.status1 = take(4 * (size_t)kMaxSortPasses * L.tiles1 * kRadix);
-  L.status2 = take(4 * (size_t)kMaxSortPasses * L.tiles2 * kRadix);
+  L.status1 = take(4 * (size_t)kMaxSortPasses * L.tiles1 * kMaxRadix);
+  L.status2 = take(4 * (size_t)kMaxSortPasses * L.tiles2 * kMaxRadix);
   L.scan_status = take(8 * (size_t)(L.tilesN > 0 ? L.tilesN : 1));
-  L.hist = take(4 * 2 * kMaxSortPasses * kRadix);
+  L.hist = take(4 * 2 * kMaxSortPasses * kMaxRadix);
   L.counters = take(4 * 64);
   L.g2d = take(8 * 14 * nn);
   L.total = off;
@@ -387,7 +446,7 @@ cudaError_t launch_bin_sort_stage1(const pgsag_projected* p, int n, const WsLayo
   }
   bool in_a = true;
   cudaError_t e = radix_sort(k0, i0, k1, i1, nullptr, (uint32_t)n, (uint32_t)n, 32,
-                             reinterpret_cast<uint32_t*>(ws + L.status1), (size_t)L.tiles1 * kRadix, hist,
+                             reinterpret_cast<uint32_t*>(ws + L.status1), (size_t)L.tiles1 * kMaxRadix, hist,
                              counters + CNT_SORT1, st, &in_a);
   if (e != cudaSuccess) return e;
   const uint32_t* ids = in_a ? i0 : i1;
@@ -405,11 +464,11 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
                                       uint32_t M, const uint32_t* ids_sorted, const WsLayout& L, char* ws,
                                       pgsag_bins* bins, cudaStream_t st) {
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + L.counters);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist) + kMaxSortPasses * kRadix;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist) + kMaxSortPasses * kMaxRadix;
   const int ntiles = d.TX * d.TY;
   int tile_bits = 0;
   while ((1 << tile_bits) < ntiles) ++tile_bits;
-  const int npass = (tile_bits + kRadixBits - 1) / kRadixBits;
+  const int npass = make_plan(tile_bits).n;
   // emit into the buffer that makes the last pass land in bins
   uint32_t *ek, *ev, *ok, *ov;
   if (npass % 2 == 0) {
@@ -429,7 +488,7 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
   }
   bool in_a = true;
   // look-back state for exactly the tiles this M needs
-  const size_t stride = (size_t)((M + kSortTile - 1) / kSortTile) * kRadix;
+  const size_t stride = (size_t)((M + kSortTile - 1) / kSortTile) * kMaxRadix;
   cudaMemsetAsync(ws + L.status2, 0, 4 * stride * (size_t)npass, st);
   cudaError_t e = radix_sort(ek, ev, ok, ov, nullptr, M, M, tile_bits,
                              reinterpret_cast<uint32_t*>(ws + L.status2), stride, hist,

@@ -70,7 +70,8 @@ def _stream():
 class Rasterizer:
     """Buffers for one (n, width, height, sh_degree) problem; reusable across views."""
 
-    def __init__(self, n, width, height, sh_degree=3, capacity=None, device="cuda", counters=True):
+    def __init__(self, n, width, height, sh_degree=3, capacity=None, device="cuda", counters=True, sat=True):
+        self.want_sat = bool(sat)
         self.n, self.W, self.H, self.deg = int(n), int(width), int(height), int(sh_degree)
         self.device = torch.device(device)
         if self.device.type == "cuda" and self.device.index is None:
@@ -136,7 +137,8 @@ class Rasterizer:
         p.rgb_d, p.ncam, p.flags = self.rgb_d.data_ptr(), self.ncam.data_ptr(), self.flags.data_ptr()
         self._proj = p
         tm = L.TileMask()
-        tm.tile_cnt, tm.sat, tm.active = self.tile_cnt.data_ptr(), self.sat.data_ptr(), self.active.data_ptr()
+        tm.tile_cnt, tm.active = self.tile_cnt.data_ptr(), self.active.data_ptr()
+        tm.sat = self.sat.data_ptr() if self.want_sat else None
         tm.n_active, tm.active_bits = self.n_active.data_ptr(), self.active_bits.data_ptr()
         self._tm = tm
         b = L.Bins()

@@ -19,7 +19,7 @@ else:
     gnp, cams, masks = sc.gaussians, [sc.camera], [torch.from_numpy(sc.mask).to(dev)]
 g = GaussianTensors.from_numpy(gnp, dev)
 H, W = masks[0].shape
-r = Rasterizer(g.n, W, H, g.sh_degree, capacity=24 * g.n, device=dev, counters=False)
+r = Rasterizer(g.n, W, H, g.sh_degree, capacity=24 * g.n, device=dev, counters=False, sat=False)
 gen = torch.Generator(device=dev); gen.manual_seed(0)
 up = {"dC": torch.randn(3, H, W, device=dev, generator=gen), "dN": torch.randn(3, H, W, device=dev, generator=gen),
       "dD": torch.randn(H, W, device=dev, generator=gen), "dA": torch.randn(H, W, device=dev, generator=gen),
