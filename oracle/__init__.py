@@ -57,8 +57,12 @@ def lib():
             L.oracle_keys.restype = i64
             for nm in ("oracle_render_f32", "oracle_render_f64"):
                 getattr(L, nm).argtypes = [P, P, P, P, P, i32, i32, P, i32, i32, P, P, P, i32, P, P, P, P,
-                                           i32, P, P, P]
+                                           P, i32, P, P, P]
                 getattr(L, nm).restype = None
+            L.oracle_gc_weights.argtypes = [P, P, i32, i32, P]
+            L.oracle_gc_weights.restype = None
+            L.oracle_gc_load.argtypes = [P, P, i32, P, P]
+            L.oracle_gc_load.restype = C.c_double
             L.oracle_sh_basis.argtypes = [C.c_double, C.c_double, C.c_double, P]
             L.oracle_sh_basis.restype = None
             L.oracle_lnup_f32.argtypes = [C.c_float]
@@ -132,9 +136,10 @@ def keys(proj, mask):
 def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=False, upstream=None):
     """O4 (and O5/O6 if upstream is given) for the listed flat pixel indices.
 
-    upstream: (npix, 9) float64 = gC(3), gN(3), gD, gA, gDep per listed pixel.
-    Returns dict: C (npix,3) N (npix,3) D A Dep T (npix,), g, last (Gaussian id), near, n_clamped,
-    id_sum, evaluated, cert_bad, and grads (59, n) float64 if upstream was given.
+    upstream: (npix, 9) or (npix, 10) float64 = gC(3), gN(3), gD, gA, gDep[, gG] per listed pixel,
+    gG = dL/d(soft count) of the L_GC-load surrogate (R24).
+    Returns dict: C (npix,3) N (npix,3) D A Dep T (npix,), g, gsoft, last (Gaussian id), near, n_clamped,
+    id_sum, evaluated, cert_bad, and grads (73, n) float64 if upstream was given.
     """
     n = int(np.asarray(g.opacity).shape[0])
     prm = _params(g, dtype)
@@ -148,15 +153,20 @@ def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=F
     evaluated = np.zeros(npix, np.int64)
     cert = np.zeros(1, np.int64)
     bgd = np.asarray(bg, np.float64)
-    up = None if upstream is None else np.ascontiguousarray(upstream, np.float64).reshape(npix, 9)
+    up = None
+    if upstream is not None:
+        u = np.asarray(upstream, np.float64).reshape(npix, -1)
+        up = np.zeros((npix, 10), np.float64)
+        up[:, :u.shape[1]] = u
     grads = None if upstream is None else np.zeros((N_GRAD_ROWS, n), np.float64)
+    gsoft = np.zeros(npix, np.float64)
     fn = lib().oracle_render_f32 if dtype == np.float32 else lib().oracle_render_f64
     ca = cam_array(cam)
     fn(*[_p(a) for a in prm], n, int(g.sh_degree), _p(ca), W, H, _p(m), _p(bgd), _p(pix), npix, _p(out),
-       _p(iout), _p(id_sum), _p(evaluated), int(bool(certify)), _p(cert), _p(up), _p(grads))
+       _p(iout), _p(id_sum), _p(evaluated), _p(gsoft), int(bool(certify)), _p(cert), _p(up), _p(grads))
     res = dict(C=out[:, 0:3], N=out[:, 3:6], D=out[:, 6], A=out[:, 7], Dep=out[:, 8], T=out[:, 9],
                g=iout[:, 0], last=iout[:, 1], near=iout[:, 2], n_clamped=iout[:, 3], id_sum=id_sum,
-               evaluated=evaluated, cert_bad=int(cert[0]))
+               evaluated=evaluated, cert_bad=int(cert[0]), gsoft=gsoft)
     if grads is not None:
         res["grads"] = grads
     return res
@@ -166,6 +176,26 @@ def split_grads(grads, n):
     """(59, n) -> dict of named gradient blocks."""
     return dict(dmean=grads[0:3], dscale=grads[3:6], drot=grads[6:10], dopacity=grads[10], dsh=grads[11:59],
                 g2d=grads[59:72], absgrad=grads[72])
+
+
+def gc_weights(image, mask):
+    """Eq. 9 weights w (H, W) from a (3, H, W) image (R23)."""
+    H, W = mask.shape
+    img = np.ascontiguousarray(image, np.float64).reshape(3, H, W)
+    m = np.ascontiguousarray(mask, np.uint8)
+    w = np.zeros((H, W), np.float64)
+    lib().oracle_gc_weights(_p(img), _p(m), W, H, _p(w))
+    return w
+
+
+def gc_load(g, w):
+    """L_GC-load over the listed pixels: (loss, mean ratio, dL/dg per pixel)."""
+    g = np.ascontiguousarray(g, np.float64)
+    w = np.ascontiguousarray(w, np.float64)
+    mu = np.zeros(1, np.float64)
+    d = np.zeros(len(g), np.float64)
+    L = lib().oracle_gc_load(_p(g), _p(w), len(g), _p(mu), _p(d))
+    return float(L), float(mu[0]), d
 
 
 def sh_basis(x, y, z):

@@ -319,7 +319,13 @@ template <typename R> struct PixOut {
   long long evaluated;  // list entries visited (E counter)
   double id_sum;        // checksum of blended ids (FD validity)
   int n_clamped;        // blended pairs with o*rho > 0.99
+  double gsoft;         // soft count sum_blended sigmoid(k (alpha - 1/255)) (R24)
 };
+
+// Soft-count surrogate of g_i (reading R24 after SPEC's DESIGN DECISIONS):
+// each blended pair counts sigmoid(k (alpha - 1/255)), k = 100.
+const double kGcK = 100.0;
+inline double sigmoid(double z) { return 1.0 / (1.0 + std::exp(-z)); }
 
 template <typename R> struct Blend {
   int id;
@@ -388,6 +394,7 @@ template <typename R> struct Renderer {
       o.D = o.D + w * g.dist;
       if (blends) blends->push_back(Blend<R>{id, alpha, T, rho, orho, dx, dy});
       o.g += 1;
+      o.gsoft += sigmoid(kGcK * ((double)alpha - 1.0 / 255.0));
       o.last = id;
       o.id_sum += (double)id;
       if (orho > (R)0.99) o.n_clamped += 1;
@@ -433,11 +440,12 @@ struct G2 {
 // P:82; decisions frozen per R17; clamp gradient per R16).
 template <typename R>
 void pixel_backward(const Renderer<R>& rd, int i, int j, const PixOut<R>& fw,
-                    const std::vector<Blend<R>>& bl, const R bg[3], const double up[9],
+                    const std::vector<Blend<R>>& bl, const R bg[3], const double up[10],
                     std::vector<G2>& g2) {
-  // up = (gC0,gC1,gC2, gN0,gN1,gN2, gD, gA, gDep)
+  // up = (gC0,gC1,gC2, gN0,gN1,gN2, gD, gA, gDep, gG) with gG = dL/d(soft count) (R24)
   double G[8] = {up[0], up[1], up[2], up[3], up[4], up[5], up[6], up[7]};
   const double gDep = up[8];
+  const double gG = up[9];
   const double px = i + 0.5, py = j + 0.5;
   const double r[3] = {(px - (double)rd.cam.cx) / (double)rd.cam.fx,
                        (py - (double)rd.cam.cy) / (double)rd.cam.fy, 1.0};
@@ -460,7 +468,11 @@ void pixel_backward(const Renderer<R>& rd, int i, int j, const PixOut<R>& fw,
     const double a = (double)b.alpha, T = (double)b.T;
     double dot = 0.0;
     for (int c = 0; c < 8; ++c) dot += G[c] * (F[c] - S[c]);
-    const double dalpha = T * (dot - Pp * bgdot);
+    double dalpha = T * (dot - Pp * bgdot);
+    if (gG != 0.0) {  // d(soft count)/d alpha = k s (1 - s), s = sigmoid(k (alpha - 1/255))
+      const double s = sigmoid(kGcK * (a - 1.0 / 255.0));
+      dalpha += gG * kGcK * s * (1.0 - s);
+    }
     const double w = a * T;
     G2& o = g2[b.id];
     for (int c = 0; c < 3; ++c) o.drgb[c] += w * G[c];
@@ -660,8 +672,8 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
                    const double* camf, int W, int H, const uint8_t* mask, const double* bgd,
                    const int64_t* pix, int npix, R* out /* [npix][10]: C3 N3 D A Dep T */,
                    int32_t* iout /* [npix][4]: g last near_flag n_clamped */, double* id_sum, int64_t* evaluated,
-                   int certify_flag, int64_t* cert_bad,
-                   const double* upstream /* [npix][9] or null */, double* grads /* 73 x n or null */) {
+                   double* gsoft /* [npix] soft counts (R24) or null */, int certify_flag, int64_t* cert_bad,
+                   const double* upstream /* [npix][10] or null */, double* grads /* 73 x n or null */) {
   const Params<R> P = make_params(mean, scale, rot, opac, sh, n, deg);
   const Cam<R> cam = load_cam<R>(camf, W, H);
   const TileMask tm = make_tilemask(mask, W, H);
@@ -697,8 +709,9 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
     iout[(size_t)k * 4 + 2] = o.near_flag; iout[(size_t)k * 4 + 3] = o.n_clamped;
     if (id_sum) id_sum[k] = o.id_sum;
     if (evaluated) evaluated[k] = o.evaluated;
+    if (gsoft) gsoft[k] = o.gsoft;
     if (certify_flag) bad += rd.certify(i, j);
-    if (grads) pixel_backward(rd, i, j, o, bl, bg, upstream + (size_t)k * 9, g2);
+    if (grads) pixel_backward(rd, i, j, o, bl, bg, upstream + (size_t)k * 10, g2);
   }
   if (cert_bad) *cert_bad = bad;
   if (grads) {
@@ -786,19 +799,70 @@ int64_t oracle_keys(const float* depth, const int32_t* rect, const uint32_t* fla
 // out[npix][10] = C0 C1 C2 N0 N1 N2 D A Dep T; iout[npix][4] = g, last id, near flag, n_clamped.
 // grads (double, 73*n): dmean[3][n] dscale[3][n] drot[4][n] dopac[n] dsh[48][n], then the 2D
 // gradients du dv dca dcb dcc dop drgb[3] dncam[3] ddist and absgrad (rows 59..72).
+// gsoft[npix]: soft counts (R24); upstream [npix][10] with column 9 = dL/d(soft count).
 void oracle_render_f32(const float* mean, const float* scale, const float* rot, const float* opac, const float* sh,
                        int n, int deg, const double* cam, int W, int H, const uint8_t* mask, const double* bg,
                        const int64_t* pix, int npix, float* out, int32_t* iout, double* id_sum, int64_t* evaluated,
-                       int certify, int64_t* cert_bad, const double* upstream, double* grads) {
+                       double* gsoft, int certify, int64_t* cert_bad, const double* upstream, double* grads) {
   render_pixels<float>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, bg, pix, npix, out, iout, id_sum,
-                       evaluated, certify, cert_bad, upstream, grads);
+                       evaluated, gsoft, certify, cert_bad, upstream, grads);
 }
 void oracle_render_f64(const double* mean, const double* scale, const double* rot, const double* opac,
                        const double* sh, int n, int deg, const double* cam, int W, int H, const uint8_t* mask,
                        const double* bg, const int64_t* pix, int npix, double* out, int32_t* iout, double* id_sum,
-                       int64_t* evaluated, int certify, int64_t* cert_bad, const double* upstream, double* grads) {
+                       int64_t* evaluated, double* gsoft, int certify, int64_t* cert_bad, const double* upstream,
+                       double* grads) {
   render_pixels<double>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, bg, pix, npix, out, iout, id_sum,
-                        evaluated, certify, cert_bad, upstream, grads);
+                        evaluated, gsoft, certify, cert_bad, upstream, grads);
+}
+
+// ---------------------------------------------------- L_GC-load (NEXT-1)
+// Eq. 9 weight w_i from the image gradient ("gradient-dependent weight
+// nabla I"; R23): gray = 0.299 R + 0.587 G + 0.114 B, 3x3 Sobel with replicated
+// borders, |grad| normalised by its mean over the mask pixels, clamped to [0.1, 10]
+// (a mean of 0 gives the floor everywhere).  image [3][H][W]; w [H][W] (1 off-mask).
+void oracle_gc_weights(const double* image, const uint8_t* mask, int W, int H, double* w) {
+  const size_t HW = (size_t)W * H;
+  std::vector<double> gray(HW), mag(HW);
+  for (size_t p = 0; p < HW; ++p) gray[p] = 0.299 * image[p] + 0.587 * image[HW + p] + 0.114 * image[2 * HW + p];
+  auto I = [&](int x, int y) {
+    x = std::min(std::max(x, 0), W - 1);
+    y = std::min(std::max(y, 0), H - 1);
+    return gray[(size_t)y * W + x];
+  };
+  double sum = 0.0;
+  long long cnt = 0;
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      const double gx = (I(x + 1, y - 1) + 2 * I(x + 1, y) + I(x + 1, y + 1)) -
+                        (I(x - 1, y - 1) + 2 * I(x - 1, y) + I(x - 1, y + 1));
+      const double gy = (I(x - 1, y + 1) + 2 * I(x, y + 1) + I(x + 1, y + 1)) -
+                        (I(x - 1, y - 1) + 2 * I(x, y - 1) + I(x + 1, y - 1));
+      const size_t p = (size_t)y * W + x;
+      mag[p] = std::sqrt(gx * gx + gy * gy);
+      if (mask[p]) { sum += mag[p]; ++cnt; }
+    }
+  const double m = cnt ? sum / (double)cnt : 0.0;
+  for (size_t p = 0; p < HW; ++p) {
+    if (!mask[p]) { w[p] = 1.0; continue; }
+    w[p] = m > 0.0 ? std::min(std::max(mag[p] / m, 0.1), 10.0) : 0.1;
+  }
+}
+
+// L_GC-load = population std over the listed (mask) pixels of r_i = g_i / w_i (Eq. 9),
+// and dL/dg_i = (r_i - mean r) / (N L w_i) (0 where L = 0).  Returns L.
+double oracle_gc_load(const double* g, const double* w, int npix, double* mean_out, double* dLdg) {
+  if (npix <= 0) { if (mean_out) *mean_out = 0.0; return 0.0; }
+  double s = 0.0;
+  for (int k = 0; k < npix; ++k) s += g[k] / w[k];
+  const double mu = s / npix;
+  double v = 0.0;
+  for (int k = 0; k < npix; ++k) { const double d = g[k] / w[k] - mu; v += d * d; }
+  const double L = std::sqrt(v / npix);
+  if (mean_out) *mean_out = mu;
+  if (dLdg)
+    for (int k = 0; k < npix; ++k) dLdg[k] = L > 0.0 ? (g[k] / w[k] - mu) / (npix * L * w[k]) : 0.0;
+  return L;
 }
 
 // SH basis in double (for the library pin against scipy).
