@@ -125,11 +125,21 @@ typedef struct {
   float *D, *A, *Dep, *T;
   int32_t *g, *last;
   unsigned long long *counters; /* optional [4]: +E evaluated, +B blended (fwd), +E visited (bwd), 0 */
+  /* Optional fused L_GC-load statistics (NEXT-1, Eq. 9).  If gc_w (input, [H][W], the
+   * weights of pgsag_gc_weights) is non-NULL, A6 accumulates over the mask pixels
+   * gc_stats[0] = N, gc_stats[1] = sum r, gc_stats[2] = sum r^2 with r = g / w (gc_stats is
+   * zeroed by the call); L_GC-load = sqrt(sum r^2 / N - (sum r / N)^2). */
+  const float *gc_w;
+  double *gc_stats;
 } pgsag_image;
 
-/* Upstream gradients dL/d(C, N, D, A, Dep) in the pgsag_image layout; any may be NULL (= 0). */
+/* Upstream gradients dL/d(C, N, D, A, Dep) in the pgsag_image layout; any may be NULL (= 0).
+ * gc_lambda != 0 adds gc_lambda * L_GC-load (Eq. 11's lambda term) through the soft-count
+ * surrogate sum_blended sigmoid(100 (alpha - 1/255)) (R24); it needs the forward's gc_w and
+ * gc_stats. */
 typedef struct {
   const float *dC, *dN, *dD, *dA, *dDep;
+  float gc_lambda;
 } pgsag_image_grad;
 
 /* A8 output, same layouts as pgsag_gaussians; OVERWRITTEN (not accumulated).  Rows of dsh
@@ -175,6 +185,14 @@ int pgsag_render_bwd(const pgsag_gaussians *g, const pgsag_camera *cam, const pg
                      const pgsag_bins *bins, const pgsag_tilemask *tm, const uint8_t *mask, const float bg[3],
                      const pgsag_image *fwd, const pgsag_image_grad *dL, pgsag_gaussian_grad *out, void *ws,
                      size_t ws_bytes, void *stream);
+
+/* NEXT-1: Eq. 9's gradient-dependent weights w_i ("gradient-dependent weight nabla I",
+ * P:165-169; reading R23): gray = 0.299 R + 0.587 G + 0.114 B of image ([3][H][W] float),
+ * 3x3 Sobel magnitude with replicated borders, divided by its mean over the mask pixels,
+ * clamped to [0.1, 10] (floor everywhere if that mean is 0); w = 1 off the mask.
+ * w is [H][W] float, caller-allocated. */
+int pgsag_gc_weights(const float *image, const uint8_t *mask, int32_t width, int32_t height, float *w,
+                     void *ws, size_t ws_bytes, void *stream);
 
 /* Message for the last non-zero status on this thread ("" if none). */
 const char *pgsag_last_error(void);

@@ -16,7 +16,7 @@ F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT, F_LIVE = 1, 2, 4, 8, 15
 
 SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd",
            "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable",
-           "pgsag_timing_collect", "pgsag_timing_get")
+           "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights")
 
 _vp = C.c_void_p
 
@@ -48,11 +48,11 @@ class Bins(C.Structure):
 
 class Image(C.Structure):
     _fields_ = [("C", _vp), ("N", _vp), ("D", _vp), ("A", _vp), ("Dep", _vp), ("T", _vp), ("g", _vp),
-                ("last", _vp), ("counters", _vp)]
+                ("last", _vp), ("counters", _vp), ("gc_w", _vp), ("gc_stats", _vp)]
 
 
 class ImageGrad(C.Structure):
-    _fields_ = [("dC", _vp), ("dN", _vp), ("dD", _vp), ("dA", _vp), ("dDep", _vp)]
+    _fields_ = [("dC", _vp), ("dN", _vp), ("dD", _vp), ("dA", _vp), ("dDep", _vp), ("gc_lambda", C.c_float)]
 
 
 class GaussianGrad(C.Structure):
@@ -100,6 +100,8 @@ def lib():
             L.pgsag_timing_collect.restype = C.c_int
             L.pgsag_timing_get.argtypes = [C.c_int, P(C.c_char_p), P(C.c_double), P(C.c_longlong)]
             L.pgsag_timing_get.restype = C.c_int
+            L.pgsag_gc_weights.argtypes = [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp, C.c_size_t, _vp]
+            L.pgsag_gc_weights.restype = C.c_int
             _lib = L
     return _lib
 
@@ -158,6 +160,10 @@ def render_bwd(g, cam, proj, bins, tm, mask, bg, img, dimg, grad, ws, ws_bytes, 
     return check(lib().pgsag_render_bwd(C.byref(g), C.byref(cam), C.byref(proj), C.byref(bins), C.byref(tm),
                                         mask, C.byref(bg), C.byref(img), C.byref(dimg), C.byref(grad), ws,
                                         ws_bytes, stream))
+
+
+def gc_weights(image, mask, W, H, w, ws, ws_bytes, stream):
+    return check(lib().pgsag_gc_weights(image, mask, int(W), int(H), w, ws, ws_bytes, stream))
 
 
 def version():

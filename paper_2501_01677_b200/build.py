@@ -25,6 +25,7 @@ UNITS = {
     "render_fwd.cu": [],
     "render_bwd.cu": [],
     "preprocess_bwd.cu": [],
+    "gc_load.cu": [],
     "api.cu": [],
 }
 

@@ -261,4 +261,17 @@ int pgsag_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pg
   return PGSAG_OK;
 }
 
+int pgsag_gc_weights(const float* image, const uint8_t* mask, int32_t width, int32_t height, float* w, void* ws,
+                     size_t ws_bytes, void* stream) {
+  if (!image || !mask || !w) return fail(PGSAG_EINVAL, "gc_weights: NULL argument");
+  if (width <= 0 || height <= 0) return fail(PGSAG_EINVAL, "width/height must be > 0");
+  const WsLayout L = ws_layout(0, width, height, 0);
+  int rc;
+  if ((rc = check_ws(ws, ws_bytes, L.total))) return rc;
+  double* acc = reinterpret_cast<double*>(static_cast<char*>(ws) + L.counters + 4 * CNT_GC);
+  cudaError_t e = launch_gc_weights(image, mask, width, height, w, acc, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "gc_weights");
+  return PGSAG_OK;
+}
+
 }  // extern "C"

@@ -94,5 +94,10 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
                               uint32_t* work_counter, cudaStream_t st);
 cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
                                   pgsag_gaussian_grad* out, const double* g2d, cudaStream_t st);
+cudaError_t launch_gc_weights(const float* image, const uint8_t* mask, int W, int H, float* w, double* acc,
+                              cudaStream_t st);
+
+// counters[] slot (as 2 doubles at byte offset 4*CNT_GC) for pgsag_gc_weights
+constexpr int CNT_GC = 32;
 
 }  // namespace pgsag

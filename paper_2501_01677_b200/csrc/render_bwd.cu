@@ -60,7 +60,12 @@ struct BwdArgs {
   int n;
   unsigned long long* counters;
   uint32_t* work;
+  const float* gc_w;        // NEXT-1: L_GC-load weights, statistics and weight lambda
+  const double* gc_stats;
+  float gc_lambda;
 };
+
+constexpr float kGcK = 100.0f;  // soft-count sharpness (R24)
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
@@ -89,6 +94,7 @@ struct PixState {
   float G[8];
   float Pb;
   float T;
+  float gG;  // dL/d(soft count) of lambda * L_GC-load (R24)
   int last;
 };
 
@@ -98,8 +104,15 @@ __device__ __forceinline__ void load_pixel(const BwdArgs& a, bool masked, size_t
   for (int c = 0; c < 8; ++c) s.G[c] = 0.f;
   s.Pb = 0.f;
   s.T = 1.f;
+  s.gG = 0.f;
   s.last = -1;
   if (!masked) return;
+  if (a.gc_w) {  // Eq. 9: L = std(r), r = g / w  ->  dL/dg = (r - mean) / (N L w)
+    const double N = a.gc_stats[0], mu = a.gc_stats[1] / N;
+    const double L = sqrt(fmax(a.gc_stats[2] / N - mu * mu, 0.0));
+    const float w = __ldg(a.gc_w + pix);
+    if (L > 0.0) s.gG = (float)((double)a.gc_lambda * ((double)a.g[pix] / w - mu) / (N * L * w));
+  }
   s.last = a.last[pix];
   s.T = a.T[pix];
   s.G[0] = ld_or0(a.dC, pix); s.G[1] = ld_or0(a.dC, HW + pix); s.G[2] = ld_or0(a.dC, 2 * HW + pix);
@@ -123,7 +136,7 @@ __device__ __forceinline__ void load_pixel(const BwdArgs& a, bool masked, size_t
 // State of one packed pixel pair.
 struct Pair {
   float2 G[8];
-  float2 Pb, T, Sg;
+  float2 Pb, T, Sg, gG;
   int last0, last1;
 };
 
@@ -131,6 +144,7 @@ __device__ __forceinline__ void make_pair(const PixState& a, const PixState& b, 
 #pragma unroll
   for (int c = 0; c < 8; ++c) p.G[c] = f2(a.G[c], b.G[c]);
   p.Pb = f2(a.Pb, b.Pb);
+  p.gG = f2(a.gG, b.gG);
   p.T = f2(a.T, b.T);
   p.Sg = f2(0.f, 0.f);
   p.last0 = a.last;
@@ -142,6 +156,7 @@ struct PairOut {
   float2 wt, dpow, dop, du, dv, dydp;
 };
 
+template <bool kGC>
 __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 rc, const float4& cd,
                                           const float4& nn, PairOut& o) {
   const float2 om = __fadd2_rn(bc(1.f), f2(-al.x, -al.y));
@@ -155,7 +170,13 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 
   GF = __ffma2_rn(p.G[5], bc(nn.z), GF);
   GF = __ffma2_rn(p.G[6], bc(cd.w), GF);
   const float2 sp = __fadd2_rn(p.Sg, p.Pb);
-  const float2 dal = __fmul2_rn(Ti, __fadd2_rn(GF, f2(-sp.x, -sp.y)));
+  float2 dal = __fmul2_rn(Ti, __fadd2_rn(GF, f2(-sp.x, -sp.y)));
+  if (kGC) {  // + gG * d(sigmoid(k (alpha - 1/255)))/d alpha; only reaches the outputs through ac / rc
+    const float2 z = __fmul2_rn(bc(-kGcK * kLog2e), __fadd2_rn(al, bc(-kAlphaMin)));
+    const float2 s = f2(rcp_approx(1.0f + ex2_approx(z.x)), rcp_approx(1.0f + ex2_approx(z.y)));
+    const float2 ds = __fmul2_rn(__fmul2_rn(bc(kGcK), s), __fadd2_rn(bc(1.0f), f2(-s.x, -s.y)));
+    dal = __ffma2_rn(p.gG, ds, dal);
+  }
   p.Sg = __ffma2_rn(al, GF, __fmul2_rn(om, p.Sg));
   p.Pb = __fmul2_rn(p.Pb, om);
   p.T = Ti;
@@ -164,7 +185,7 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 
   o.dop = __fmul2_rn(rc, dal);
 }
 
-template <bool kCount>
+template <bool kCount, bool kGC>
 __global__ void __launch_bounds__(kBT, 10) render_bwd_kernel(BwdArgs a) {
   constexpr int kAccStride = 15;  // padded row: the 14 values of an entry sit in 14 distinct banks
   __shared__ Rec s_rec[kBBatch];
@@ -273,9 +294,9 @@ __global__ void __launch_bounds__(kBT, 10) render_bwd_kernel(BwdArgs a) {
         const float4 cd = lds128(ra_addr + 32);
         const float4 nn = lds128(ra_addr + 48);
         PairOut o01, o23;
-        pair_grad(P01, f2(al0, al1), f2(u0 ? al0 : 0.f, u1 ? al1 : 0.f), f2(u0 ? rh01.x : 0.f, u1 ? rh01.y : 0.f),
+        pair_grad<kGC>(P01, f2(al0, al1), f2(u0 ? al0 : 0.f, u1 ? al1 : 0.f), f2(u0 ? rh01.x : 0.f, u1 ? rh01.y : 0.f),
                   cd, nn, o01);
-        pair_grad(P23, f2(al2, al3), f2(u2 ? al2 : 0.f, u3 ? al3 : 0.f), f2(u2 ? rh23.x : 0.f, u3 ? rh23.y : 0.f),
+        pair_grad<kGC>(P23, f2(al2, al3), f2(u2 ? al2 : 0.f, u3 ? al3 : 0.f), f2(u2 ? rh23.x : 0.f, u3 ? rh23.y : 0.f),
                   cd, nn, o23);
         float v[16];
 #pragma unroll
@@ -344,7 +365,7 @@ int bwd_grid() {
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_bwd_kernel<false>, kBT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_bwd_kernel<false, false>, kBT, 0);
     grid = sms * (occ > 0 ? occ : 1);
   }
   return grid;
@@ -379,13 +400,21 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
   a.n = n;
   a.counters = fwd->counters;
   a.work = work_counter;
+  const bool gc = dL->gc_lambda != 0.0f && fwd->gc_w && fwd->gc_stats;
+  a.gc_w = gc ? fwd->gc_w : nullptr;
+  a.gc_stats = fwd->gc_stats;
+  a.gc_lambda = dL->gc_lambda;
   const int grid = min(bwd_grid(), d.TX * d.TY);
   {
     KTimer kt_("A7_render_bwd", st);
-    if (fwd->counters)
-      render_bwd_kernel<true><<<grid, kBT, 0, st>>>(a);
+    if (fwd->counters && gc)
+      render_bwd_kernel<true, true><<<grid, kBT, 0, st>>>(a);
+    else if (fwd->counters)
+      render_bwd_kernel<true, false><<<grid, kBT, 0, st>>>(a);
+    else if (gc)
+      render_bwd_kernel<false, true><<<grid, kBT, 0, st>>>(a);
     else
-      render_bwd_kernel<false><<<grid, kBT, 0, st>>>(a);
+      render_bwd_kernel<false, false><<<grid, kBT, 0, st>>>(a);
   }
   return launch_preprocess_bwd(g, cam, p, out, g2d, st);
 }

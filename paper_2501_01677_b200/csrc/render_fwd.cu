@@ -45,6 +45,8 @@ struct FwdArgs {
   int32_t *g, *last;
   unsigned long long* counters;
   uint32_t* work;
+  const float* gc_w;   // optional L_GC-load weights (NEXT-1)
+  double* gc_stats;    // N, sum r, sum r^2
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -166,6 +168,22 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
     T.y = fabsf(T.y);
     if (m0) write_pixel(a, pix0, HW, px, py.x, T.x, C0.x, C1.x, C2.x, N0.x, N1.x, N2.x, D.x, g0, last0);
     if (m1) write_pixel(a, pix1, HW, px, py.y, T.y, C0.y, C1.y, C2.y, N0.y, N1.y, N2.y, D.y, g1, last1);
+    if (a.gc_w) {  // fused Eq. 9 statistics over the mask pixels of this tile (NEXT-1)
+      float n = 0.f, s1 = 0.f, s2 = 0.f;
+      if (m0) { const float r = (float)g0 / __ldg(a.gc_w + pix0); n += 1.f; s1 += r; s2 += r * r; }
+      if (m1) { const float r = (float)g1 / __ldg(a.gc_w + pix1); n += 1.f; s1 += r; s2 += r * r; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        n += __shfl_xor_sync(0xffffffffu, n, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (lane == 0 && n > 0.f) {
+        atomicAdd(a.gc_stats, (double)n);
+        atomicAdd(a.gc_stats + 1, (double)s1);
+        atomicAdd(a.gc_stats + 2, (double)s2);
+      }
+    }
     if (kCount) cntB += (unsigned long long)(m0 ? g0 : 0) + (unsigned long long)(m1 ? g1 : 0);
   }
   if (kCount) {
@@ -215,6 +233,9 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
   a.g = out->g; a.last = out->last;
   a.counters = out->counters;
   a.work = work_counter;
+  a.gc_w = out->gc_w;
+  a.gc_stats = out->gc_stats;
+  if (a.gc_w) cudaMemsetAsync(a.gc_stats, 0, 3 * sizeof(double), st);
   const int grid = min(fwd_grid(), d.TX * d.TY);
   {
     KTimer kt_("A6_render_fwd", st);

@@ -107,6 +107,8 @@ class Rasterizer:
         self.img_g = torch.zeros(self.H, self.W, dtype=i32, device=dev)
         self.img_last = torch.full((self.H, self.W), -1, dtype=i32, device=dev)
         self.counters = torch.zeros(4, dtype=torch.int64, device=dev) if counters else None
+        self.gc_stats = torch.zeros(3, dtype=torch.float64, device=dev)  # NEXT-1: N, sum r, sum r^2
+        self.gc_w = None
         # A8 outputs
         K3 = (self.deg + 1) ** 2 * 3
         self.dmean = e(3, n)
@@ -163,10 +165,27 @@ class Rasterizer:
         self._grad.grad2d = self.grad2d.data_ptr() if on else None
 
     # ---------------------------------------------------------- the path
-    def forward(self, g: GaussianTensors, cam: L.Camera, mask: torch.Tensor, bg=(0.0, 0.0, 0.0)):
+    def gc_weights(self, image: torch.Tensor, mask: torch.Tensor) -> torch.Tensor:
+        """Eq. 9 weights w (H, W) of a (3, H, W) float32 image on the mask (pgsag_gc_weights)."""
+        assert image.dtype == torch.float32 and tuple(image.shape) == (3, self.H, self.W) and image.is_contiguous()
+        w = torch.empty(self.H, self.W, dtype=torch.float32, device=self.device)
+        L.gc_weights(C.c_void_p(image.data_ptr()), C.c_void_p(mask.data_ptr()), self.W, self.H,
+                     C.c_void_p(w.data_ptr()), C.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream())
+        return w
+
+    def gc_load(self):
+        """(L_GC-load, mean ratio, N) from the last forward with gc_w (fused A6 statistics)."""
+        n, s1, s2 = self.gc_stats.tolist()
+        mu = s1 / n if n else 0.0
+        return (max(s2 / n - mu * mu, 0.0) ** 0.5 if n else 0.0), mu, n
+
+    def forward(self, g: GaussianTensors, cam: L.Camera, mask: torch.Tensor, bg=(0.0, 0.0, 0.0), gc_w=None):
         assert g.n == self.n and g.sh_degree == self.deg
         assert mask.dtype == torch.uint8 and tuple(mask.shape) == (self.H, self.W) and mask.is_contiguous()
         st = _stream()
+        self.gc_w = gc_w
+        self._img.gc_w = None if gc_w is None else gc_w.data_ptr()
+        self._img.gc_stats = self.gc_stats.data_ptr()
         self._g = g.struct()
         self._gt = g
         self._cam = cam
@@ -189,8 +208,9 @@ class Rasterizer:
         return dict(C=self.img_C, N=self.img_N, D=self.img_D, A=self.img_A, Dep=self.img_Dep, T=self.img_T,
                     g=self.img_g, last=self.img_last)
 
-    def backward(self, dC=None, dN=None, dD=None, dA=None, dDep=None):
+    def backward(self, dC=None, dN=None, dD=None, dA=None, dDep=None, gc_lambda=0.0):
         ig = L.ImageGrad()
+        ig.gc_lambda = float(gc_lambda)
         for k, t in (("dC", dC), ("dN", dN), ("dD", dD), ("dA", dA), ("dDep", dDep)):
             if t is not None:
                 assert t.dtype == torch.float32 and t.is_contiguous() and t.device == self.device

@@ -460,3 +460,19 @@ def sample_pixels(mask, n, seed):
     if idx.size <= n:
         return idx
     return np.sort(rng.choice(idx, size=n, replace=False))
+
+
+def reference_image(H, W, seed):
+    """Synthetic 'photo' (3, H, W) float32 in [0, 1]: smooth shading, a few sharp-edged
+    rectangles (facade-like structure) and mild noise — input for Eq. 9's nabla I weights."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    yy, xx = np.mgrid[0:H, 0:W].astype(np.float64)
+    img = np.empty((3, H, W))
+    for c in range(3):
+        img[c] = 0.4 + 0.2 * np.sin(xx / max(W, 1) * rng.uniform(2, 6) + c) * np.cos(yy / max(H, 1) * rng.uniform(2, 6))
+    for _ in range(max(3, (H * W) // 400)):
+        x0, y0 = rng.integers(0, W), rng.integers(0, H)
+        x1, y1 = min(W, x0 + rng.integers(2, max(3, W // 4))), min(H, y0 + rng.integers(2, max(3, H // 4)))
+        img[:, y0:y1, x0:x1] += rng.uniform(-0.3, 0.3, size=(3, 1, 1))
+    img += rng.normal(0, 0.01, size=img.shape)
+    return np.clip(img, 0, 1).astype(np.float32)
