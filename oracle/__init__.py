@@ -63,6 +63,10 @@ def lib():
             L.oracle_gc_weights.restype = None
             L.oracle_gc_load.argtypes = [P, P, i32, P, P]
             L.oracle_gc_load.restype = C.c_double
+            L.oracle_boundary_band.argtypes = [P, i32, i32, i32, P]
+            L.oracle_boundary_band.restype = None
+            L.oracle_ban_loss.argtypes = [P, i32, i32, P, P, P, P, C.c_double, C.c_double, P, P, P]
+            L.oracle_ban_loss.restype = None
             L.oracle_sh_basis.argtypes = [C.c_double, C.c_double, C.c_double, P]
             L.oracle_sh_basis.restype = None
             L.oracle_lnup_f32.argtypes = [C.c_float]
@@ -196,6 +200,33 @@ def gc_load(g, w):
     d = np.zeros(len(g), np.float64)
     L = lib().oracle_gc_load(_p(g), _p(w), len(g), _p(mu), _p(d))
     return float(L), float(mu[0]), d
+
+
+def boundary_band(mask, r=1):
+    """MB = dilation(RBM, r) XOR erosion(RBM, r), square SE, zero padding (R25)."""
+    H, W = mask.shape
+    m = np.ascontiguousarray(mask, np.uint8)
+    band = np.zeros((H, W), np.uint8)
+    lib().oracle_boundary_band(_p(m), W, H, int(r), _p(band))
+    return band
+
+
+def ban_loss(cam, mask, band, N, Dep, bw=0.1, lam=1.0, grads=False):
+    """Eq. 8 L_ban (R26, R27).  N (3,H,W), Dep (H,W).  Returns (sum, count[, dN, dDep]) with the
+    gradients of lam * sum / count."""
+    H, W = mask.shape
+    m = np.ascontiguousarray(mask, np.uint8)
+    b = np.ascontiguousarray(band, np.uint8)
+    Nd = np.ascontiguousarray(N, np.float64).reshape(3, H, W)
+    Dd = np.ascontiguousarray(Dep, np.float64).reshape(H, W)
+    loss = np.zeros(2, np.float64)
+    dN = np.zeros((3, H, W), np.float64) if grads else None
+    dD = np.zeros((H, W), np.float64) if grads else None
+    lib().oracle_ban_loss(_p(cam_array(cam)), W, H, _p(m), _p(b), _p(Nd), _p(Dd), float(bw), float(lam),
+                          _p(loss), _p(dN), _p(dD))
+    if grads:
+        return float(loss[0]), float(loss[1]), dN, dD
+    return float(loss[0]), float(loss[1])
 
 
 def sh_basis(x, y, z):

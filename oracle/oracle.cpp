@@ -865,6 +865,114 @@ double oracle_gc_load(const double* g, const double* w, int npix, double* mean_o
   return L;
 }
 
+// ------------------------------------------------------ L_ban (NEXT-2)
+// Boundary band MB ("extract ... building masked boundaries"; R25):
+// dilation(RBM, r) XOR erosion(RBM, r) with a (2r+1)^2 square structuring element,
+// zero outside the image (erosion shrinks at the image border).
+void oracle_boundary_band(const uint8_t* mask, int W, int H, int r, uint8_t* band) {
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      bool any = false, all = true;
+      for (int dy = -r; dy <= r; ++dy)
+        for (int dx = -r; dx <= r; ++dx) {
+          const int xx = x + dx, yy = y + dy;
+          const bool v = xx >= 0 && yy >= 0 && xx < W && yy < H && mask[(size_t)yy * W + xx];
+          any = any || v;
+          all = all && v;
+        }
+      band[(size_t)y * W + x] = (uint8_t)(any != all);
+    }
+}
+
+// Eq. 8 with the normal-from-depth of P:153 ("computed from the depth map
+// using four neighboring points"; R26, R27): per mask pixel p with valid unbiased depth
+// at its four axis neighbours (all inside the image and the mask, Dep != 0),
+// P_k = Dep_k r_k (r = K^-1 (x+.5, y+.5, 1)), c = (P_right - P_left) x (P_down - P_up),
+// n_depth = c/|c| flipped to face the camera (n . P_p <= 0 with P_p = Dep_p r_p; P_p only
+// decides the sign), n_r = N/|N|.  Weight w = bw on the band inside the mask, 1 elsewhere
+// in the mask.  L = sum_p w |n_depth - n_r|^2 / #valid.  Outputs loss[0] = sum, loss[1] =
+// #valid; if dN / dDep are given, ADDS lambda * dL/dN and lambda * dL/dDep.
+void oracle_ban_loss(const double* camf, int W, int H, const uint8_t* mask, const uint8_t* band, const double* N,
+                     const double* Dep, double bw, double lambda, double* loss, double* dN, double* dDep) {
+  const double fx = camf[0], fy = camf[1], cx = camf[2], cy = camf[3];
+  const size_t HW = (size_t)W * H;
+  auto ray = [&](int x, int y, double* r) { r[0] = (x + 0.5 - cx) / fx; r[1] = (y + 0.5 - cy) / fy; r[2] = 1.0; };
+  auto ok = [&](int x, int y) {
+    return x >= 0 && y >= 0 && x < W && y < H && mask[(size_t)y * W + x] && Dep[(size_t)y * W + x] != 0.0;
+  };
+  struct Term { int x, y; double e[3], w, c[3], cn, nd[3], nr[3], Nn, s; };
+  std::vector<Term> terms;
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      const size_t p = (size_t)y * W + x;
+      if (!mask[p] || !ok(x, y) || !ok(x - 1, y) || !ok(x + 1, y) || !ok(x, y - 1) || !ok(x, y + 1)) continue;
+      const double Nn = std::sqrt(N[p] * N[p] + N[HW + p] * N[HW + p] + N[2 * HW + p] * N[2 * HW + p]);
+      if (!(Nn > 0.0)) continue;
+      double rl[3], rr[3], ru[3], rd[3], rp[3];
+      ray(x - 1, y, rl); ray(x + 1, y, rr); ray(x, y - 1, ru); ray(x, y + 1, rd); ray(x, y, rp);
+      double a[3], b[3];
+      for (int k = 0; k < 3; ++k) {
+        a[k] = Dep[p + 1] * rr[k] - Dep[p - 1] * rl[k];
+        b[k] = Dep[p + W] * rd[k] - Dep[p - W] * ru[k];
+      }
+      Term t;
+      t.x = x; t.y = y;
+      t.c[0] = a[1] * b[2] - a[2] * b[1];
+      t.c[1] = a[2] * b[0] - a[0] * b[2];
+      t.c[2] = a[0] * b[1] - a[1] * b[0];
+      t.cn = std::sqrt(t.c[0] * t.c[0] + t.c[1] * t.c[1] + t.c[2] * t.c[2]);
+      if (!(t.cn > 0.0)) continue;
+      const double facing = (t.c[0] * rp[0] + t.c[1] * rp[1] + t.c[2] * rp[2]) * Dep[p];
+      t.s = facing > 0.0 ? -1.0 : 1.0;
+      for (int k = 0; k < 3; ++k) {
+        t.nd[k] = t.s * t.c[k] / t.cn;
+        t.nr[k] = N[k * HW + p] / Nn;
+        t.e[k] = t.nd[k] - t.nr[k];
+      }
+      t.Nn = Nn;
+      t.w = band[p] ? bw : 1.0;
+      terms.push_back(t);
+    }
+  double sum = 0.0;
+  for (const Term& t : terms) sum += t.w * (t.e[0] * t.e[0] + t.e[1] * t.e[1] + t.e[2] * t.e[2]);
+  const double cnt = (double)terms.size();
+  loss[0] = sum;
+  loss[1] = cnt;
+  if (!dN && !dDep) return;
+  if (cnt == 0.0) return;
+  const double sc = lambda / cnt;
+  for (const Term& t : terms) {
+    const size_t p = (size_t)t.y * W + t.x;
+    double gnd[3], gnr[3];
+    for (int k = 0; k < 3; ++k) { gnd[k] = 2.0 * sc * t.w * t.e[k]; gnr[k] = -gnd[k]; }
+    if (dN) {  // n_r = N/|N|: dN = (g - n (n.g)) / |N|
+      const double d = gnr[0] * t.nr[0] + gnr[1] * t.nr[1] + gnr[2] * t.nr[2];
+      for (int k = 0; k < 3; ++k) dN[k * HW + p] += (gnr[k] - t.nr[k] * d) / t.Nn;
+    }
+    if (dDep) {  // n_d = s c/|c|; c = a x b
+      double cu[3];
+      for (int k = 0; k < 3; ++k) cu[k] = t.c[k] / t.cn;
+      const double d = gnd[0] * cu[0] + gnd[1] * cu[1] + gnd[2] * cu[2];
+      double gc[3];
+      for (int k = 0; k < 3; ++k) gc[k] = t.s * (gnd[k] - cu[k] * d) / t.cn;
+      double rl[3], rr[3], ru[3], rd[3];
+      ray(t.x - 1, t.y, rl); ray(t.x + 1, t.y, rr); ray(t.x, t.y - 1, ru); ray(t.x, t.y + 1, rd);
+      double a[3], b[3];
+      for (int k = 0; k < 3; ++k) {
+        a[k] = Dep[p + 1] * rr[k] - Dep[p - 1] * rl[k];
+        b[k] = Dep[p + W] * rd[k] - Dep[p - W] * ru[k];
+      }
+      // d/da (c . g) = b x g ; d/db (c . g) = g x a
+      const double ga[3] = {b[1] * gc[2] - b[2] * gc[1], b[2] * gc[0] - b[0] * gc[2], b[0] * gc[1] - b[1] * gc[0]};
+      const double gb[3] = {gc[1] * a[2] - gc[2] * a[1], gc[2] * a[0] - gc[0] * a[2], gc[0] * a[1] - gc[1] * a[0]};
+      dDep[p + 1] += ga[0] * rr[0] + ga[1] * rr[1] + ga[2] * rr[2];
+      dDep[p - 1] -= ga[0] * rl[0] + ga[1] * rl[1] + ga[2] * rl[2];
+      dDep[p + W] += gb[0] * rd[0] + gb[1] * rd[1] + gb[2] * rd[2];
+      dDep[p - W] -= gb[0] * ru[0] + gb[1] * ru[1] + gb[2] * ru[2];
+    }
+  }
+}
+
 // SH basis in double (for the library pin against scipy).
 void oracle_sh_basis(double x, double y, double z, double* Y) { sh_basis<double>(x, y, z, Y); }
 // log upper bound used by the rect (for the pin that it bounds ln from above).
