@@ -194,6 +194,25 @@ int pgsag_render_bwd(const pgsag_gaussians *g, const pgsag_camera *cam, const pg
 int pgsag_gc_weights(const float *image, const uint8_t *mask, int32_t width, int32_t height, float *w,
                      void *ws, size_t ws_bytes, void *stream);
 
+/* NEXT-2: boundary band MB ("extract more accurate building masked boundaries"; R25):
+ * band = dilation(mask, r) XOR erosion(mask, r) with a (2r+1)^2 square structuring element,
+ * zero outside the image.  mask, band: u8 [H][W]; r >= 1. */
+int pgsag_boundary_band(const uint8_t *mask, int32_t width, int32_t height, int32_t r, uint8_t *band,
+                        void *stream);
+
+/* NEXT-2: boundary-aware normal loss L_ban (Eq. 8; R26, R27).  For each mask pixel
+ * whose four axis neighbours are inside the image and the mask with a valid unbiased depth
+ * (Dep != 0): P_k = Dep_k K^-1 (x+.5, y+.5, 1); n_depth = normalize((P_right - P_left) x
+ * (P_down - P_up)) turned to face the camera ("four neighboring points"); n_rendered =
+ * N/|N|; term = w |n_depth - n_rendered|^2 with w = boundary_w on the band ("0.1") and 1
+ * elsewhere in the mask.  loss (device, double[2], zeroed by the call) receives
+ * (sum of terms, number of terms).  If dN ([3][H][W]) / dDep ([H][W]) are non-NULL the call
+ * ADDS lambda * d(S)/dN, lambda * d(S)/dDep, with S = sum (mean = 0) or sum / count (mean = 1),
+ * ready to be passed as upstream to pgsag_render_bwd.  N and Dep are A6 outputs. */
+int pgsag_ban_loss(const pgsag_camera *cam, const uint8_t *mask, const uint8_t *band, const float *N,
+                   const float *Dep, float boundary_w, float lambda, int32_t mean, double *loss, float *dN,
+                   float *dDep, void *stream);
+
 /* Message for the last non-zero status on this thread ("" if none). */
 const char *pgsag_last_error(void);
 

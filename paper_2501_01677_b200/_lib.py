@@ -16,7 +16,8 @@ F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT, F_LIVE = 1, 2, 4, 8, 15
 
 SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd",
            "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable",
-           "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights")
+           "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights", "pgsag_boundary_band",
+           "pgsag_ban_loss")
 
 _vp = C.c_void_p
 
@@ -102,6 +103,11 @@ def lib():
             L.pgsag_timing_get.restype = C.c_int
             L.pgsag_gc_weights.argtypes = [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp, C.c_size_t, _vp]
             L.pgsag_gc_weights.restype = C.c_int
+            L.pgsag_boundary_band.argtypes = [_vp, C.c_int32, C.c_int32, C.c_int32, _vp, _vp]
+            L.pgsag_boundary_band.restype = C.c_int
+            L.pgsag_ban_loss.argtypes = [P(Camera), _vp, _vp, _vp, _vp, C.c_float, C.c_float, C.c_int32, _vp,
+                                         _vp, _vp, _vp]
+            L.pgsag_ban_loss.restype = C.c_int
             _lib = L
     return _lib
 
@@ -164,6 +170,15 @@ def render_bwd(g, cam, proj, bins, tm, mask, bg, img, dimg, grad, ws, ws_bytes, 
 
 def gc_weights(image, mask, W, H, w, ws, ws_bytes, stream):
     return check(lib().pgsag_gc_weights(image, mask, int(W), int(H), w, ws, ws_bytes, stream))
+
+
+def boundary_band(mask, W, H, r, band, stream):
+    return check(lib().pgsag_boundary_band(mask, int(W), int(H), int(r), band, stream))
+
+
+def ban_loss(cam, mask, band, N, Dep, bw, lam, mean, loss, dN, dDep, stream):
+    return check(lib().pgsag_ban_loss(C.byref(cam), mask, band, N, Dep, float(bw), float(lam), int(mean), loss, dN,
+                                      dDep, stream))
 
 
 def version():

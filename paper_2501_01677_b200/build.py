@@ -26,6 +26,7 @@ UNITS = {
     "render_bwd.cu": [],
     "preprocess_bwd.cu": [],
     "gc_load.cu": [],
+    "ban.cu": [],
     "api.cu": [],
 }
 

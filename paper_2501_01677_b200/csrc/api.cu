@@ -274,4 +274,24 @@ int pgsag_gc_weights(const float* image, const uint8_t* mask, int32_t width, int
   return PGSAG_OK;
 }
 
+int pgsag_boundary_band(const uint8_t* mask, int32_t width, int32_t height, int32_t r, uint8_t* band, void* stream) {
+  if (!mask || !band) return fail(PGSAG_EINVAL, "boundary_band: NULL argument");
+  if (width <= 0 || height <= 0 || r < 1) return fail(PGSAG_EINVAL, "boundary_band: bad size or radius");
+  cudaError_t e = launch_boundary_band(mask, width, height, r, band, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "boundary_band");
+  return PGSAG_OK;
+}
+
+int pgsag_ban_loss(const pgsag_camera* cam, const uint8_t* mask, const uint8_t* band, const float* N,
+                   const float* Dep, float boundary_w, float lambda, int32_t mean, double* loss, float* dN,
+                   float* dDep, void* stream) {
+  int rc;
+  if ((rc = check_cam(cam))) return rc;
+  if (!mask || !band || !N || !Dep || !loss) return fail(PGSAG_EINVAL, "ban_loss: NULL argument");
+  cudaError_t e = launch_ban_loss(cam, mask, band, N, Dep, boundary_w, lambda, mean, loss, dN, dDep,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "ban_loss");
+  return PGSAG_OK;
+}
+
 }  // extern "C"

@@ -97,6 +97,11 @@ cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* 
 cudaError_t launch_gc_weights(const float* image, const uint8_t* mask, int W, int H, float* w, double* acc,
                               cudaStream_t st);
 
+cudaError_t launch_boundary_band(const uint8_t* mask, int W, int H, int r, uint8_t* band, cudaStream_t st);
+cudaError_t launch_ban_loss(const pgsag_camera* cam, const uint8_t* mask, const uint8_t* band, const float* N,
+                            const float* Dep, float bw, float lambda, int mean, double* loss, float* dN, float* dDep,
+                            cudaStream_t st);
+
 // counters[] slot (as 2 doubles at byte offset 4*CNT_GC) for pgsag_gc_weights
 constexpr int CNT_GC = 32;
 

@@ -173,6 +173,21 @@ class Rasterizer:
                      C.c_void_p(w.data_ptr()), C.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream())
         return w
 
+    def boundary_band(self, mask: torch.Tensor, r: int = 1) -> torch.Tensor:
+        """NEXT-2 boundary band MB of the building mask (pgsag_boundary_band)."""
+        band = torch.empty_like(mask)
+        L.boundary_band(C.c_void_p(mask.data_ptr()), self.W, self.H, r, C.c_void_p(band.data_ptr()), _stream())
+        return band
+
+    def ban_loss(self, band: torch.Tensor, lam=1.0, bw=0.1, mean=True, dN=None, dDep=None):
+        """NEXT-2 L_ban (Eq. 8) on the last forward's N and Dep; returns the device (sum, count) and ADDS
+        lam * dS/dN, lam * dS/dDep into dN / dDep when given (S = sum/count if mean)."""
+        loss = torch.zeros(2, dtype=torch.float64, device=self.device)
+        p = lambda t: None if t is None else C.c_void_p(t.data_ptr())
+        L.ban_loss(self._cam, C.c_void_p(self._mask.data_ptr()), p(band), p(self.img_N), p(self.img_Dep), bw, lam,
+                   int(mean), p(loss), p(dN), p(dDep), _stream())
+        return loss
+
     def gc_load(self):
         """(L_GC-load, mean ratio, N) from the last forward with gc_w (fused A6 statistics)."""
         n, s1, s2 = self.gc_stats.tolist()

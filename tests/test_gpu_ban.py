@@ -1,0 +1,97 @@
+"""NEXT-2 (boundary band, L_ban with normal-from-depth; Eq. 8; R25-R27)
+through the C ABI vs the oracle, on N and Dep rendered by A6, and chained into A7/A8."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import scenes as S
+from tests.gpu_util import KAPPA_MAX, compare_grads, dep_kappa
+from tests.helpers import all_pixels
+from tests.test_gpu_parity import ragged_scene
+from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+
+pytestmark = pytest.mark.gpu
+
+SCENES = {"ragged": ragged_scene, "C2s": lambda: S.config2(n=30000)}
+
+
+def _render(sc):
+    H, W = sc.mask.shape
+    g = GaussianTensors.from_numpy(sc.gaussians)
+    r = Rasterizer(g.n, W, H, g.sh_degree)
+    mask = torch.from_numpy(sc.mask).cuda()
+    for t in (r.img_N, r.img_Dep):
+        t.zero_()
+    r.forward(g, camera_from(sc.camera), mask)
+    return g, r, mask
+
+
+def _elementwise(a, b, rel=1e-3, floor=1e-2):
+    scale = max(np.abs(b).max(), 1e-30)
+    return float((np.abs(a - b) / np.maximum(np.abs(b), floor * scale)).max())
+
+
+@pytest.mark.parametrize("name", list(SCENES))
+@pytest.mark.parametrize("radius", [1, 2])
+def test_boundary_band_bitexact(name, radius):
+    sc = SCENES[name]()
+    _, r, mask = _render(sc)
+    band = r.boundary_band(mask, radius).cpu().numpy()
+    np.testing.assert_array_equal(band, oracle.boundary_band(sc.mask, radius))
+
+
+@pytest.mark.parametrize("name", list(SCENES))
+def test_ban_loss_and_gradients(name):
+    sc = SCENES[name]()
+    _, r, mask = _render(sc)
+    band = r.boundary_band(mask, 1)
+    H, W = sc.mask.shape
+    dN = torch.zeros(3, H, W, device="cuda")
+    dD = torch.zeros(H, W, device="cuda")
+    lam = 0.01  # Eq. 10's lambda_4
+    loss = r.ban_loss(band, lam=lam, dN=dN, dDep=dD).cpu().numpy()
+    torch.cuda.synchronize()
+    N = r.img_N.cpu().numpy().astype(np.float64)
+    Dep = r.img_Dep.cpu().numpy().astype(np.float64)
+    s, c, rN, rD = oracle.ban_loss(sc.camera, sc.mask, band.cpu().numpy(), N, Dep, lam=lam, grads=True)
+    assert loss[1] == c and c > 100
+    assert abs(loss[0] - s) <= 1e-4 * max(1.0, s)
+    assert _elementwise(dN.cpu().numpy(), rN) <= 1e-3
+    assert _elementwise(dD.cpu().numpy(), rD) <= 1e-3
+    assert np.linalg.norm(dD.cpu().numpy() - rD) <= 1e-4 * np.linalg.norm(rD)
+
+
+@pytest.mark.parametrize("name", list(SCENES))
+def test_ban_chained_into_backward(name):
+    """lambda_4 L_ban as the whole loss: its dN, dDep as A7's upstream; parameter gradients vs the
+    oracle backward fed with the oracle's own L_ban gradients (depth upstream dropped where Eq. 4
+    is ill-conditioned, R19)."""
+    sc = SCENES[name]()
+    g, r, mask = _render(sc)
+    band = r.boundary_band(mask, 1)
+    H, W = sc.mask.shape
+    dN = torch.zeros(3, H, W, device="cuda")
+    dD = torch.zeros(H, W, device="cuda")
+    r.ban_loss(band, lam=0.01, dN=dN, dDep=dD)
+    torch.cuda.synchronize()
+    pix = all_pixels(sc.mask)
+    ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix)
+    N = r.img_N.cpu().numpy().astype(np.float64)
+    Dep = r.img_Dep.cpu().numpy().astype(np.float64)
+    _, _, rN, rD = oracle.ban_loss(sc.camera, sc.mask, band.cpu().numpy(), N, Dep, lam=0.01, grads=True)
+    drop = (dep_kappa(ora0, pix, W, sc.camera) > KAPPA_MAX) | ora0["near"].astype(bool)
+    rDf = rD.reshape(-1)
+    rDf[pix[drop]] = 0.0
+    dDg = dD.reshape(-1)
+    dDg[torch.from_numpy(pix[drop]).cuda()] = 0.0
+    rNf = rN.reshape(3, -1)
+    rNf[:, pix[ora0["near"].astype(bool)]] = 0.0
+    dNg = dN.reshape(3, -1)
+    dNg[:, torch.from_numpy(pix[ora0["near"].astype(bool)]).cuda()] = 0.0
+    grads = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in r.backward(dN=dN, dDep=dD).items()}
+    up = np.zeros((len(pix), 10))
+    up[:, 3:6] = rN.reshape(3, -1)[:, pix].T
+    up[:, 8] = rD.reshape(-1)[pix]
+    ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=up)
+    compare_grads(grads, ora["grads"], sc.gaussians.sh_degree)
