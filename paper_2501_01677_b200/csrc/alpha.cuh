@@ -54,6 +54,34 @@ struct __align__(16) Rec {
   float4 n;   // n_cam, 0
 };
 
+// Exact refinement of the block cull: does the ellipse {d : d^T Q d <= k2} (Q = the
+// conic) meet the rectangle of pixel centres?  If the centre is outside, the minimum
+// of the convex quadratic over the rectangle lies on an edge; on each edge it is a 1D
+// quadratic minimised in closed form and clamped.  The rectangle is declared missed
+// only if that minimum exceeds k2 by more than a bound on its float rounding error.
+__device__ __forceinline__ float edge_min(float ca, float cb, float cc, float dfix, float lo, float hi,
+                                          bool fix_is_x, float& err) {
+  // q(t) = ca dx^2 + 2 cb dx dy + cc dy^2 along an edge: dx (or dy) fixed, the other in [lo, hi]
+  float t = fix_is_x ? -cb * dfix / cc : -cb * dfix / ca;
+  t = fminf(fmaxf(t, lo), hi);
+  const float dx = fix_is_x ? dfix : t, dy = fix_is_x ? t : dfix;
+  const float a = ca * dx * dx, b = 2.0f * cb * dx * dy, c = cc * dy * dy;
+  err = fabsf(a) + fabsf(b) + fabsf(c);
+  return a + b + c;
+}
+
+__device__ __forceinline__ bool ellipse_meets_rect(float2 mu, float4 co, float k2, float xlo, float xhi, float ylo,
+                                                   float yhi) {
+  if (mu.x >= xlo && mu.x <= xhi && mu.y >= ylo && mu.y <= yhi) return true;
+  const float ca = co.x, cb = co.y, cc = co.z;
+  float e0, e1, e2, e3;
+  const float q0 = edge_min(ca, cb, cc, xlo - mu.x, ylo - mu.y, yhi - mu.y, true, e0);
+  const float q1 = edge_min(ca, cb, cc, xhi - mu.x, ylo - mu.y, yhi - mu.y, true, e1);
+  const float q2 = edge_min(ca, cb, cc, ylo - mu.y, xlo - mu.x, xhi - mu.x, false, e2);
+  const float q3 = edge_min(ca, cb, cc, yhi - mu.y, xlo - mu.x, xhi - mu.x, false, e3);
+  return (q0 - 1e-5f * e0 <= k2) || (q1 - 1e-5f * e1 <= k2) || (q2 - 1e-5f * e2 <= k2) || (q3 - 1e-5f * e3 <= k2);
+}
+
 // Per staged Gaussian: the scaled conic, a p2 threshold below which alpha < 1/255
 // for certain (the exact test still decides every pair above it), and an EXACT
 // conservative cull of the warp blocks: every pixel with alpha >= 1/255 has
@@ -75,12 +103,14 @@ __device__ __forceinline__ uint32_t stage_gaussian(float2 xy, float4 co, float t
   const float kd = __fdividef(k2, det);
   const float rx = sqrtf(kd * co.z) + 0.5f;
   const float ry = sqrtf(kd * co.x) + 0.5f;
+  const float k2m = k2 + 0.05f;
   uint32_t m = 0;
 #pragma unroll
   for (int k = 0; k < NB; ++k) {
     const float xlo = tile_x0 + (float)((k % NBX) * BW) + 0.5f, xhi = xlo + (float)(BW - 1);
     const float ylo = tile_y0 + (float)((k / NBX) * BH) + 0.5f, yhi = ylo + (float)(BH - 1);
-    const bool hit = (xy.x + rx >= xlo) && (xy.x - rx <= xhi) && (xy.y + ry >= ylo) && (xy.y - ry <= yhi);
+    bool hit = (xy.x + rx >= xlo) && (xy.x - rx <= xhi) && (xy.y + ry >= ylo) && (xy.y - ry <= yhi);
+    if (hit) hit = ellipse_meets_rect(xy, co, k2m, xlo, xhi, ylo, yhi);
     m |= (hit ? 1u : 0u) << k;
   }
   return m;
