@@ -179,9 +179,18 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import torch
     import torch.distributed as dist
+    # NCCL over NVLink for the (off-path) statistics collectives; PGSAG_DIST_BACKEND=gloo runs the
+    # same multi-rank code with host collectives (used to smoke-test N>1 on a single test GPU).
+    backend = os.environ.get("PGSAG_DIST_BACKEND", "nccl")
+    if backend != "nccl" and torch.cuda.is_available():
+        local = local % torch.cuda.device_count()
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    cdev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     if args.impl == "reference":
         run_reference(args, rank, world)
         if world > 1:
@@ -253,16 +262,16 @@ def main():
     pix = float(sum(npix[v] for v in views))
     blends = float(sum(per_view[v]["blended"] for v in views))
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
-        agg = torch.tensor([pix, blends], device=dev, dtype=torch.float64)
+        agg = torch.tensor([pix, blends], device=cdev, dtype=torch.float64)
         dist.all_reduce(agg)
         pix_all, blends_all = float(agg[0]), float(agg[1])
         # per-rank statistics record all-gathered over NVLink (off the timed region)
         from paper_2501_01677_b200 import shard
         rec = shard.stats_record(rank=rank, ms=ms, masked_pixels=pix, blends=blends, tile_imbalance=imbalance,
-                                 views=len(views)).to(dev)
+                                 views=len(views)).to(cdev)
         rank_table = shard.gather_stats(rec).cpu()
     else:
         ms_max, pix_all, blends_all = ms, pix, blends
@@ -349,10 +358,10 @@ def main():
         ems = e0.elapsed_time(e1)
         epix = float(sum(npix[views[s]] for s in range(ke)))
         if world > 1:
-            t = torch.tensor([ems], device=dev)
+            t = torch.tensor([ems], device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-            tp = torch.tensor([epix], device=dev, dtype=torch.float64)
+            tp = torch.tensor([epix], device=cdev, dtype=torch.float64)
             dist.all_reduce(tp)
             epix = float(tp.item())
         e2e = {"value": epix / 1e6 / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
