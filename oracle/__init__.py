@@ -67,6 +67,8 @@ def lib():
             L.oracle_boundary_band.restype = None
             L.oracle_ban_loss.argtypes = [P, i32, i32, P, P, P, P, C.c_double, C.c_double, P, P, P]
             L.oracle_ban_loss.restype = None
+            L.oracle_rgb_loss.argtypes = [P, P, P, i32, i32, P, P]
+            L.oracle_rgb_loss.restype = None
             L.oracle_sh_basis.argtypes = [C.c_double, C.c_double, C.c_double, P]
             L.oracle_sh_basis.restype = None
             L.oracle_lnup_f32.argtypes = [C.c_float]
@@ -227,6 +229,68 @@ def ban_loss(cam, mask, band, N, Dep, bw=0.1, lam=1.0, grads=False):
     if grads:
         return float(loss[0]), float(loss[1]), dN, dD
     return float(loss[0]), float(loss[1])
+
+
+def rgb_loss(Cimg, Iimg, mask, grads=False):
+    """Masked L_rgb = 0.8 L1 + 0.2 (1 - SSIM) (R28).  Returns (L, L1, S[, dC])."""
+    H, W = mask.shape
+    c = np.ascontiguousarray(Cimg, np.float64).reshape(3, H, W)
+    i = np.ascontiguousarray(Iimg, np.float64).reshape(3, H, W)
+    m = np.ascontiguousarray(mask, np.uint8)
+    out = np.zeros(3, np.float64)
+    dC = np.zeros((3, H, W), np.float64) if grads else None
+    lib().oracle_rgb_loss(_p(c), _p(i), _p(m), W, H, _p(out), _p(dC))
+    return (float(out[0]), float(out[1]), float(out[2])) + ((dC,) if grads else ())
+
+
+def flatten_loss(scale):
+    """L_s (PGSR flattening): mean over Gaussians of the minimum (activated) scale,
+    and its gradient (1/N on the minimum axis, ties -> lowest index as in R4)."""
+    s = np.asarray(scale, np.float64)
+    k = np.argmin(s, axis=0)
+    g = np.zeros_like(s)
+    n = s.shape[1]
+    g[k, np.arange(n)] = 1.0 / n
+    return float(s[k, np.arange(n)].mean()), g
+
+
+def adam_step(raw, grad, m, v, t, lr, b1=0.9, b2=0.999, eps=1e-15):
+    """One Adam step (Kingma & Ba, bias-corrected) on raw parameters, written out plainly."""
+    m = b1 * m + (1 - b1) * grad
+    v = b2 * v + (1 - b2) * grad * grad
+    mh = m / (1 - b1 ** t)
+    vh = v / (1 - b2 ** t)
+    return raw - lr * mh / (np.sqrt(vh) + eps), m, v
+
+
+ADAM_ROWS = ("mean", 3), ("log_scale", 3), ("rot", 4), ("logit_opacity", 1)
+
+
+def raw_grads(scale, opacity, dscale, dopacity, flatten_weight):
+    """Chain rule to the raw parameters (R30): d/dlog s = s (dL/ds + w dL_s/ds), d/dlogit o = o (1 - o) dL/do."""
+    _, gflat = flatten_loss(scale)
+    s = np.asarray(scale, np.float64)
+    o = np.asarray(opacity, np.float64)
+    return (np.asarray(dscale, np.float64) + flatten_weight * gflat) * s, np.asarray(dopacity, np.float64) * o * (1 - o)
+
+
+def train_update(p, g, m, v, t, hp, flatten_weight):
+    """One NEXT-3 optimiser step, plainly: p = dict(mean, scale, rot, opacity, sh, log_scale, logit_opacity)
+    (activated + raw), g = dict(dmean, dscale, drot, dopacity, dsh) (w.r.t. the activated values),
+    m, v = [11 + K3][n] moments; hp = dict(lr_mean, lr_scale, lr_rot, lr_opacity, lr_sh_dc, lr_sh_rest,
+    beta1, beta2, eps).  Returns (new p, m, v, L_s)."""
+    f64 = lambda a: np.asarray(a, np.float64)
+    Ls, _ = flatten_loss(p["scale"])
+    g_logs, g_logit = raw_grads(p["scale"], p["opacity"], g["dscale"], g["dopacity"], flatten_weight)
+    K3 = f64(p["sh"]).shape[0]
+    raw = np.vstack([f64(p["mean"]), f64(p["log_scale"]), f64(p["rot"]), f64(p["logit_opacity"])[None], f64(p["sh"])])
+    grad = np.vstack([f64(g["dmean"]), g_logs, f64(g["drot"]), g_logit[None], f64(g["dsh"])[:K3]])
+    lr = np.array([hp["lr_mean"]] * 3 + [hp["lr_scale"]] * 3 + [hp["lr_rot"]] * 4 + [hp["lr_opacity"]] +
+                  [hp["lr_sh_dc"]] * 3 + [hp["lr_sh_rest"]] * (K3 - 3))[:, None]
+    raw, m, v = adam_step(raw, grad, f64(m), f64(v), t, lr, hp["beta1"], hp["beta2"], hp["eps"])
+    q = dict(mean=raw[0:3], log_scale=raw[3:6], scale=np.exp(raw[3:6]), rot=raw[6:10], logit_opacity=raw[10],
+             opacity=1.0 / (1.0 + np.exp(-raw[10])), sh=raw[11:])
+    return q, m, v, Ls
 
 
 def sh_basis(x, y, z):

@@ -973,6 +973,90 @@ void oracle_ban_loss(const double* camf, int W, int H, const uint8_t* mask, cons
   }
 }
 
+// ------------------------------------------------- L_rgb (NEXT-3)
+// Masked photometric loss ("only the refined building masks RBM are involved";
+// L_rgb's form is 3DGS's, R28): x = C m, y = I m (zero off the mask), per channel the
+// 11x11 Gaussian-window (sigma 1.5, normalised, zero padding) SSIM map of Wang et al.
+// with C1 = 0.01^2, C2 = 0.03^2; L1 = mean over mask pixels and channels of |C - I|,
+// S = mean over mask pixels and channels of the SSIM map,
+// L_rgb = 0.8 L1 + 0.2 (1 - S).  Writes out[0..2] = (L_rgb, L1, S) and, if dC is given,
+// dL_rgb/dC (zero off the mask).  Plain window sums: O(121 HW) per statistic.
+void oracle_rgb_loss(const double* C, const double* I, const uint8_t* mask, int W, int H, double* out,
+                     double* dC) {
+  const int R = 5;
+  double g1[2 * R + 1], gs = 0.0;
+  for (int k = -R; k <= R; ++k) { g1[k + R] = std::exp(-(double)(k * k) / (2.0 * 1.5 * 1.5)); gs += g1[k + R]; }
+  for (int k = 0; k <= 2 * R; ++k) g1[k] /= gs;
+  const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+  const size_t HW = (size_t)W * H;
+  long long npx = 0;
+  for (size_t p = 0; p < HW; ++p) npx += mask[p] ? 1 : 0;
+  double l1 = 0.0, ssum = 0.0;
+  if (dC) std::memset(dC, 0, sizeof(double) * 3 * HW);
+  std::vector<double> x(HW), y(HW), mx(HW), my(HW), sxx(HW), syy(HW), sxy(HW), A(HW), B(HW), Cm(HW);
+  for (int c = 0; c < 3; ++c) {
+    for (size_t p = 0; p < HW; ++p) {
+      x[p] = mask[p] ? C[c * HW + p] : 0.0;
+      y[p] = mask[p] ? I[c * HW + p] : 0.0;
+    }
+    // window statistics at every pixel
+    for (int j = 0; j < H; ++j)
+      for (int i = 0; i < W; ++i) {
+        double a = 0, b = 0, xx = 0, yy = 0, xy = 0;
+        for (int dj = -R; dj <= R; ++dj)
+          for (int di = -R; di <= R; ++di) {
+            const int ii = i + di, jj = j + dj;
+            if (ii < 0 || jj < 0 || ii >= W || jj >= H) continue;
+            const double wgt = g1[di + R] * g1[dj + R];
+            const size_t q = (size_t)jj * W + ii;
+            a += wgt * x[q]; b += wgt * y[q]; xx += wgt * x[q] * x[q]; yy += wgt * y[q] * y[q];
+            xy += wgt * x[q] * y[q];
+          }
+        const size_t p = (size_t)j * W + i;
+        mx[p] = a; my[p] = b; sxx[p] = xx - a * a; syy[p] = yy - b * b; sxy[p] = xy - a * b;
+      }
+    for (size_t p = 0; p < HW; ++p) {
+      A[p] = B[p] = Cm[p] = 0.0;
+      if (!mask[p]) continue;
+      const double n1 = 2 * mx[p] * my[p] + C1, n2 = 2 * sxy[p] + C2;
+      const double d1 = mx[p] * mx[p] + my[p] * my[p] + C1, d2 = sxx[p] + syy[p] + C2;
+      const double s = (n1 * n2) / (d1 * d2);
+      ssum += s;
+      l1 += std::fabs(C[c * HW + p] - I[c * HW + p]);
+      // dS/d(mu_x, sigma_x^2, sigma_xy) holding the others fixed; L = ... - 0.2 S / (3 npx)
+      const double k = -0.2 / (3.0 * (double)npx);
+      const double dmx = s * (2 * my[p] / n1 - 2 * mx[p] / d1);
+      const double dsxx = -s / d2;
+      const double dsxy = s * 2 / n2;
+      A[p] = k * (dmx - 2 * dsxx * mx[p] - dsxy * my[p]);
+      B[p] = k * dsxx;
+      Cm[p] = k * dsxy;
+    }
+    if (!dC) continue;
+    // dL/dx_q = (G*A)_q + 2 x_q (G*B)_q + y_q (G*C)_q, then x = C m
+    for (int j = 0; j < H; ++j)
+      for (int i = 0; i < W; ++i) {
+        const size_t q = (size_t)j * W + i;
+        if (!mask[q]) continue;
+        double ga = 0, gb = 0, gc = 0;
+        for (int dj = -R; dj <= R; ++dj)
+          for (int di = -R; di <= R; ++di) {
+            const int ii = i + di, jj = j + dj;
+            if (ii < 0 || jj < 0 || ii >= W || jj >= H) continue;
+            const double wgt = g1[di + R] * g1[dj + R];
+            const size_t p = (size_t)jj * W + ii;
+            ga += wgt * A[p]; gb += wgt * B[p]; gc += wgt * Cm[p];
+          }
+        const double d = C[c * HW + q] - I[c * HW + q];
+        dC[c * HW + q] = ga + 2 * x[q] * gb + y[q] * gc + 0.8 / (3.0 * (double)npx) * (d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0));
+      }
+  }
+  const double L1 = npx ? l1 / (3.0 * (double)npx) : 0.0, S = npx ? ssum / (3.0 * (double)npx) : 1.0;
+  out[0] = 0.8 * L1 + 0.2 * (1.0 - S);
+  out[1] = L1;
+  out[2] = S;
+}
+
 // SH basis in double (for the library pin against scipy).
 void oracle_sh_basis(double x, double y, double z, double* Y) { sh_basis<double>(x, y, z, Y); }
 // log upper bound used by the rect (for the pin that it bounds ln from above).
