@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--views", type=int, default=40)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the NEXT-3 training-iteration timing")
     ap.add_argument("--profile", action="store_true", help="per-kernel table on stderr")
     return ap.parse_args()
 
@@ -368,6 +369,49 @@ def main():
                "d2h_bytes_per_step": int(d2h), "steps": ke,
                "note": "pinned host Gaussians+mask+upstream -> device, fwd+bwd, gradients -> host"}
 
+    # ------------------------------------------- NEXT-3: full training iteration (Eq. 10-11)
+    train = None
+    if not args.no_train:
+        from paper_2501_01677_b200.train import Trainer
+        gt_ = GaussianTensors(*(getattr(g, k).clone() for k in ("mean", "scale", "rot", "opacity", "sh")),
+                              g.sh_degree)
+        tr = Trainer(r, gt_)
+        kt = min(args.steps, 5)
+        tviews = views[:kt]
+        tgt = torch.rand(3, H, W, device=dev, generator=gen)  # synthetic target photo
+        extras = {v: (r.gc_weights(tgt, masks[v]), r.boundary_band(masks[v], 1)) for v in set(tviews)}
+        for v in tviews[:2]:
+            tr.step(ccam[v], masks[v], tgt, gc_w=extras[v][0], band=extras[v][1])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        L.timing_enable(True)
+        L.timing_collect()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for v in tviews:
+            tr.step(ccam[v], masks[v], tgt, gc_w=extras[v][0], band=extras[v][1])
+        t1.record()
+        torch.cuda.synchronize()
+        L.timing_enable(False)
+        tk = L.timing_collect()
+        tms = t0.elapsed_time(t1)
+        tpix = float(sum(npix[v] for v in tviews))
+        if world > 1:
+            t = torch.tensor([tms], device=cdev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tms = float(t.item())
+            tp = torch.tensor([tpix], device=cdev, dtype=torch.float64)
+            dist.all_reduce(tp)
+            tpix = float(tp.item())
+        lo = tr.losses()
+        train = {"ms_per_iter": tms / kt, "value": tpix / 1e6 / (tms / 1e3), "unit": UNIT, "iters": kt,
+                 "terms": "L_rgb (L1+SSIM) + L_s + L_ban + L_GC-load with P:179 weights; Adam on raw params",
+                 "gpu_launches": int(sum(v[1] for v in tk.values())),
+                 "kernels_ms_per_iter": {k: round(v[0] / kt, 4) for k, v in sorted(tk.items())},
+                 "last_loss": {k: round(float(x), 6) for k, x in lo.items()}}
+        del tr, gt_, extras
+
     # ------------------------------------------------------------- CPU oracle baseline
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -393,7 +437,7 @@ def main():
             "M_per_view": st0["M"], "evaluated_per_view": st0["evaluated"], "blended_per_view": st0["blended"],
             "bwd_visited_per_view": st0["bwd_visited"],
             "flop_per_unit": {"evaluated": FLOP_EVAL, "blended_fwd": FLOP_BLEND_FWD, "blended_bwd": FLOP_BLEND_BWD},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "train_step": train,
             "kernels_ms_per_step": {k: round(v[0], 4) for k, v in sorted(ksteps.items())},
             "clocks": clk.summary(),
             "per_rank_ms": (rank_table[:, 1].tolist() if world > 1 else [ms]),

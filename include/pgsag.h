@@ -213,6 +213,54 @@ int pgsag_ban_loss(const pgsag_camera *cam, const uint8_t *mask, const uint8_t *
                    const float *Dep, float boundary_w, float lambda, int32_t mean, double *loss, float *dN,
                    float *dDep, void *stream);
 
+/* ------------------------------------------------------------------ NEXT-3: training step
+ * Eq. 10-11: L = (1 - lambda) (L_rgb + lambda3 L_s + lambda4 L_ban) + lambda L_GC-load,
+ * lambda = 0.41, lambda3 = 100, lambda4 = 0.01; the multi-view PGSR terms (lambda1, lambda2)
+ * are out of scope.  The driver composes: A0-A6 -> pgsag_rgb_loss (+ pgsag_ban_loss)
+ * -> A7/A8 (gc_lambda = lambda) -> pgsag_adam_step. */
+
+/* Scratch bytes for pgsag_rgb_loss on a width x height image (36 W H). */
+size_t pgsag_rgb_loss_workspace_size(int32_t width, int32_t height);
+
+/* Masked photometric loss L_rgb = 0.8 L1 + 0.2 (1 - SSIM) over the RBM pixels ("only the refined
+ * building masks RBM are involved in these losses"; form R28): x = image m, y = target m (zero off
+ * the mask); per channel the 11x11 Gaussian-window (sigma 1.5, zero padding) SSIM map with
+ * C1 = 0.01^2, C2 = 0.03^2; L1 and S are means over mask pixels and the 3 channels.
+ * image, target: [3][H][W] float; mask u8 [H][W].  loss (device double[6], zeroed by the call):
+ * (L_rgb, L1, S, sum |C - I|, sum S, mask pixel count).  If dC ([3][H][W]) is non-NULL it receives
+ * weight * dL_rgb/dimage at the mask pixels (other pixels untouched). */
+int pgsag_rgb_loss(const float *image, const float *target, const uint8_t *mask, int32_t width, int32_t height,
+                   float weight, double *loss, float *dC, void *ws, size_t ws_bytes, void *stream);
+
+/* Optimiser state of one sub-region's Gaussians (device pointers, caller-owned).  The activated
+ * arrays (pgsag_gaussians layouts) are rewritten from the raw ones after every step (R30):
+ * scale = exp(log_scale), opacity = sigmoid(logit_opacity); mean, rot, sh are their own raw values.
+ * m, v: Adam moments, [11 + K3][n] rows mean 0-2, log_scale 3-5, rot 6-9, logit_opacity 10,
+ * sh 11.. (K3 = (sh_degree+1)^2 * 3); zero-initialise them before step 1. */
+typedef struct {
+  float *mean, *scale, *rot, *opacity, *sh;
+  float *log_scale;     /* [3][n] */
+  float *logit_opacity; /* [n]    */
+  float *m, *v;
+} pgsag_adam_state;
+
+/* Adam hyper-parameters (host struct).  step = t >= 1 for the bias corrections 1 - beta^t.
+ * flatten_weight = the weight of L_s in L ((1 - lambda) lambda3 for Eq. 10-11). */
+typedef struct {
+  float lr_mean, lr_scale, lr_rot, lr_opacity, lr_sh_dc, lr_sh_rest;
+  float beta1, beta2, eps;
+  float flatten_weight;
+  int32_t step;
+} pgsag_adam_hparams;
+
+/* One Adam step (Kingma & Ba) on the raw parameters with the gradients of pgsag_render_bwd (w.r.t.
+ * the activated values, chained through exp / sigmoid here) plus flatten_weight * dL_s/dscale,
+ * L_s = mean over the n Gaussians of min(scale) (PGSR flattening; R29; ties -> lowest
+ * axis).  flatten_loss (device double[1], optional, zeroed by the call) receives L_s evaluated
+ * before the update. */
+int pgsag_adam_step(int32_t n, int32_t sh_degree, const pgsag_gaussian_grad *grad, pgsag_adam_state *state,
+                    const pgsag_adam_hparams *hp, double *flatten_loss, void *stream);
+
 /* Message for the last non-zero status on this thread ("" if none). */
 const char *pgsag_last_error(void);
 

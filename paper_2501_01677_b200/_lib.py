@@ -17,7 +17,7 @@ F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT, F_LIVE = 1, 2, 4, 8, 15
 SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd",
            "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable",
            "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights", "pgsag_boundary_band",
-           "pgsag_ban_loss")
+           "pgsag_ban_loss", "pgsag_rgb_loss_workspace_size", "pgsag_rgb_loss", "pgsag_adam_step")
 
 _vp = C.c_void_p
 
@@ -59,6 +59,17 @@ class ImageGrad(C.Structure):
 class GaussianGrad(C.Structure):
     _fields_ = [("dmean", _vp), ("dscale", _vp), ("drot", _vp), ("dopacity", _vp), ("dsh", _vp),
                 ("absgrad2d", _vp), ("grad2d", _vp)]
+
+
+class AdamState(C.Structure):
+    _fields_ = [("mean", _vp), ("scale", _vp), ("rot", _vp), ("opacity", _vp), ("sh", _vp), ("log_scale", _vp),
+                ("logit_opacity", _vp), ("m", _vp), ("v", _vp)]
+
+
+class AdamHparams(C.Structure):
+    _fields_ = [("lr_mean", C.c_float), ("lr_scale", C.c_float), ("lr_rot", C.c_float), ("lr_opacity", C.c_float),
+                ("lr_sh_dc", C.c_float), ("lr_sh_rest", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("eps", C.c_float), ("flatten_weight", C.c_float), ("step", C.c_int32)]
 
 
 _lib = None
@@ -108,6 +119,14 @@ def lib():
             L.pgsag_ban_loss.argtypes = [P(Camera), _vp, _vp, _vp, _vp, C.c_float, C.c_float, C.c_int32, _vp,
                                          _vp, _vp, _vp]
             L.pgsag_ban_loss.restype = C.c_int
+            L.pgsag_rgb_loss_workspace_size.argtypes = [C.c_int32, C.c_int32]
+            L.pgsag_rgb_loss_workspace_size.restype = C.c_size_t
+            L.pgsag_rgb_loss.argtypes = [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_float, _vp, _vp, _vp, C.c_size_t,
+                                         _vp]
+            L.pgsag_rgb_loss.restype = C.c_int
+            L.pgsag_adam_step.argtypes = [C.c_int32, C.c_int32, P(GaussianGrad), P(AdamState), P(AdamHparams), _vp,
+                                          _vp]
+            L.pgsag_adam_step.restype = C.c_int
             _lib = L
     return _lib
 
@@ -183,3 +202,16 @@ def ban_loss(cam, mask, band, N, Dep, bw, lam, mean, loss, dN, dDep, stream):
 
 def version():
     return lib().pgsag_version().decode()
+
+
+def rgb_loss_workspace_size(W, H):
+    return int(lib().pgsag_rgb_loss_workspace_size(int(W), int(H)))
+
+
+def rgb_loss(image, target, mask, W, H, weight, loss, dC, ws, ws_bytes, stream):
+    return check(lib().pgsag_rgb_loss(image, target, mask, int(W), int(H), float(weight), loss, dC, ws, int(ws_bytes),
+                                      stream))
+
+
+def adam_step(n, deg, grad, state, hp, flat, stream):
+    return check(lib().pgsag_adam_step(int(n), int(deg), C.byref(grad), C.byref(state), C.byref(hp), flat, stream))

@@ -27,6 +27,7 @@ UNITS = {
     "preprocess_bwd.cu": [],
     "gc_load.cu": [],
     "ban.cu": [],
+    "train.cu": [],
     "api.cu": [],
 }
 

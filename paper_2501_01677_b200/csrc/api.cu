@@ -294,4 +294,35 @@ int pgsag_ban_loss(const pgsag_camera* cam, const uint8_t* mask, const uint8_t* 
   return PGSAG_OK;
 }
 
+size_t pgsag_rgb_loss_workspace_size(int32_t width, int32_t height) {
+  if (width <= 0 || height <= 0) return 0;
+  return (size_t)36 * (size_t)width * (size_t)height;
+}
+
+int pgsag_rgb_loss(const float* image, const float* target, const uint8_t* mask, int32_t width, int32_t height,
+                   float weight, double* loss, float* dC, void* ws, size_t ws_bytes, void* stream) {
+  if (!image || !target || !mask || !loss) return fail(PGSAG_EINVAL, "rgb_loss: NULL argument");
+  if (width <= 0 || height <= 0) return fail(PGSAG_EINVAL, "width/height must be > 0");
+  int rc;
+  if ((rc = check_ws(ws, ws_bytes, pgsag_rgb_loss_workspace_size(width, height)))) return rc;
+  cudaError_t e = launch_rgb_loss(image, target, mask, width, height, weight, loss, dC, static_cast<float*>(ws),
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "rgb_loss");
+  return PGSAG_OK;
+}
+
+int pgsag_adam_step(int32_t n, int32_t sh_degree, const pgsag_gaussian_grad* grad, pgsag_adam_state* state,
+                    const pgsag_adam_hparams* hp, double* flatten_loss, void* stream) {
+  if (n < 0 || sh_degree < 0 || sh_degree > 3) return fail(PGSAG_EINVAL, "adam: bad n / sh_degree");
+  if (!grad || !state || !hp) return fail(PGSAG_EINVAL, "adam: NULL argument");
+  if (hp->step < 1) return fail(PGSAG_EINVAL, "adam: step must be >= 1");
+  if (n > 0 && (!grad->dmean || !grad->dscale || !grad->drot || !grad->dopacity || !grad->dsh || !state->mean ||
+                !state->scale || !state->rot || !state->opacity || !state->sh || !state->log_scale ||
+                !state->logit_opacity || !state->m || !state->v))
+    return fail(PGSAG_EINVAL, "adam: NULL buffer");
+  cudaError_t e = launch_adam(n, sh_degree, grad, state, hp, flatten_loss, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "adam");
+  return PGSAG_OK;
+}
+
 }  // extern "C"

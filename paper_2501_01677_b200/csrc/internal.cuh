@@ -102,6 +102,11 @@ cudaError_t launch_ban_loss(const pgsag_camera* cam, const uint8_t* mask, const 
                             const float* Dep, float bw, float lambda, int mean, double* loss, float* dN, float* dDep,
                             cudaStream_t st);
 
+cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8_t* mask, int W, int H, float weight,
+                            double* loss, float* dC, float* abc, cudaStream_t st);
+cudaError_t launch_adam(int n, int sh_degree, const pgsag_gaussian_grad* gr, pgsag_adam_state* s,
+                        const pgsag_adam_hparams* hp, double* flat, cudaStream_t st);
+
 // counters[] slot (as 2 doubles at byte offset 4*CNT_GC) for pgsag_gc_weights
 constexpr int CNT_GC = 32;
 
