@@ -293,6 +293,94 @@ def train_update(p, g, m, v, t, hp, flatten_weight):
     return q, m, v, Ls
 
 
+# ------------------------------------------------------------------ densification (R31)
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(x):
+    """SplitMix64 finaliser of x (python ints, exact 64-bit arithmetic)."""
+    z = (x + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def split_normals(seed, i, child):
+    """The three N(0, 1) samples of split child `child` (0/1) of source Gaussian i (R31): counter
+    c = 4 i + 2 child + k, h_k = splitmix64(seed ^ c) for k = 0, 1; u = (24-bit field + 0.5) / 2^24
+    (high field of h_k, then its low field); Box-Muller (z0, z1) = sqrt(-2 ln u_a) (cos, sin)(2 pi u_b)
+    on (u_a, u_b) = both fields of h_0, then of h_1; the first three of the four values are used."""
+    out = []
+    for k in (0, 1):
+        h = splitmix64((seed ^ (4 * i + 2 * child + k)) & _M64)
+        ua = ((h >> 40) + 0.5) / 16777216.0
+        ub = ((h & 0xFFFFFF) + 0.5) / 16777216.0
+        r = np.sqrt(-2.0 * np.log(ua))
+        out += [r * np.cos(2 * np.pi * ub), r * np.sin(2 * np.pi * ub)]
+    return np.array(out[:3])
+
+
+def densify_actions(scale, opacity, accum, count, grad_threshold, dense_limit, min_opacity):
+    """Per Gaussian: 0 drop (opacity < min_opacity), 3 split (mean view-space gradient >= threshold and
+    max scale > dense_limit), 2 keep + clone (gradient >= threshold, max scale <= dense_limit), else
+    1 keep.  Every decision in float32, as the GPU takes it (mean = accum / count, 0 if count = 0)."""
+    f = np.float32
+    s = np.asarray(scale, f)
+    o = np.asarray(opacity, f)
+    a, c = np.asarray(accum, f), np.asarray(count, f)
+    avg = np.where(c > 0, a / np.where(c > 0, c, f(1)), f(0)).astype(f)
+    big = s.max(axis=0) > f(dense_limit)
+    hot = avg >= f(grad_threshold)
+    act = np.where(hot, np.where(big, 3, 2), 1).astype(np.uint8)
+    act[o < f(min_opacity)] = 0
+    return act
+
+
+def quat_to_rot(q):
+    w, x, y, z = np.asarray(q, np.float64) / np.linalg.norm(q)
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+def densify_apply(p, m, v, act, seed):
+    """3DGS clone / split / prune (R31), written out plainly.  Output order: the kept sources
+    (actions 1, 2) in source order, then the clones (action 2) in source order, then the two split
+    children (action 3) of each split source in source order.  A clone copies the source; a split
+    child has mean mu + R(q) (s * z), scale s / 1.6 (log-scale = log of that), the source's rotation,
+    opacity and SH; clones and children start with zero Adam moments.  p: dict of the activated and
+    raw arrays ([rows][n]); returns (p', m', v')."""
+    act = np.asarray(act)
+    keep = np.flatnonzero((act == 1) | (act == 2))
+    clone = np.flatnonzero(act == 2)
+    split = np.flatnonzero(act == 3)
+    keys = ("mean", "scale", "rot", "opacity", "sh", "log_scale", "logit_opacity")
+    cols = lambda a, idx: np.asarray(a, np.float64)[..., idx]
+    out = {k: [cols(p[k], keep), cols(p[k], clone)] for k in keys}
+    mm = [cols(m, keep), np.zeros((m.shape[0], len(clone)))]
+    vv = [cols(v, keep), np.zeros((v.shape[0], len(clone)))]
+    ch = {k: [] for k in keys}
+    for i in split:
+        s = np.asarray(p["scale"], np.float64)[:, i]
+        R = quat_to_rot(np.asarray(p["rot"], np.float64)[:, i])
+        for c in (0, 1):
+            z = split_normals(seed, int(i), c)
+            sc = (np.asarray(p["scale"], np.float32)[:, i] / np.float32(1.6)).astype(np.float64)  # float32 as stored
+            ch["mean"].append(np.asarray(p["mean"], np.float64)[:, i] + R @ (s * z))
+            ch["scale"].append(sc)
+            ch["log_scale"].append(np.log(sc))
+            for k in ("rot", "opacity", "sh", "logit_opacity"):
+                ch[k].append(np.asarray(p[k], np.float64)[..., i])
+    for k in keys:
+        base = np.asarray(p[k])
+        shape = base.shape[:-1] + (len(split) * 2,)
+        out[k].append(np.stack(ch[k], axis=-1) if ch[k] else np.zeros(shape))
+        out[k] = np.concatenate(out[k], axis=-1)
+    mm.append(np.zeros((m.shape[0], 2 * len(split))))
+    vv.append(np.zeros((v.shape[0], 2 * len(split))))
+    return out, np.concatenate(mm, axis=1), np.concatenate(vv, axis=1)
+
+
 def sh_basis(x, y, z):
     Y = np.zeros(16, np.float64)
     lib().oracle_sh_basis(float(x), float(y), float(z), _p(Y))

@@ -169,3 +169,82 @@ def test_train_update_rows_and_activations():
     assert np.allclose(q["sh"][3:], p["sh"][3:] - 6e-3 * np.sign(g["dsh"][3:]), atol=1e-12)
     assert np.allclose(m, 0.1 * np.vstack([g["dmean"], g["dscale"] * p["scale"], g["drot"],
                                            (g["dopacity"] * p["opacity"] * (1 - p["opacity"]))[None], g["dsh"]]))
+
+
+# ------------------------------------------------------------ densification (R31)
+def test_splitmix64_reference_values():
+    """SplitMix64 (Steele, Lea, Flood 2014): the first outputs of the generator seeded with 0 are the
+    published 0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F."""
+    g = 0x9E3779B97F4A7C15
+    outs = [oracle.splitmix64((k * g) & ((1 << 64) - 1)) for k in range(3)]
+    assert outs == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F]
+
+
+def test_split_normals_moments():
+    z = np.array([oracle.split_normals(1677, i, c) for i in range(4000) for c in (0, 1)])
+    assert abs(z.mean()) < 0.02 and abs(z.std() - 1) < 0.02
+    assert abs(np.corrcoef(z[:, 0], z[:, 1])[0, 1]) < 0.03
+    assert not np.array_equal(oracle.split_normals(1, 5, 0), oracle.split_normals(1, 5, 1))
+
+
+def test_densify_actions_decisions():
+    s = np.array([[0.01, 0.5, 0.01, 0.5, 0.02], [0.01, 0.01, 0.01, 0.01, 0.02], [0.01, 0.01, 0.01, 0.01, 0.02]])
+    o = np.array([0.5, 0.5, 0.5, 0.5, 0.001])
+    acc = np.array([0.0, 0.0, 1.0, 1.0, 1.0])
+    cnt = np.array([0.0, 3.0, 2.0, 2.0, 2.0])
+    a = oracle.densify_actions(s, o, acc, cnt, grad_threshold=0.4, dense_limit=0.1, min_opacity=0.005)
+    assert a.tolist() == [1, 1, 2, 3, 0]
+    # the threshold is inclusive and the dense limit exclusive (float32 decisions)
+    a = oracle.densify_actions(s[:, 2:4], o[2:4], acc[2:4], cnt[2:4], grad_threshold=0.5, dense_limit=0.5,
+                               min_opacity=0.005)
+    assert a.tolist() == [2, 2]
+
+
+def _dens_state(rng, n, K3=12):
+    p = dict(mean=rng.normal(size=(3, n)), rot=rng.normal(size=(4, n)), sh=rng.normal(size=(K3, n)),
+             log_scale=rng.normal(-2, 0.5, (3, n)), logit_opacity=rng.normal(size=n))
+    p["scale"] = np.exp(p["log_scale"]).astype(np.float32).astype(np.float64)
+    p["opacity"] = 1 / (1 + np.exp(-p["logit_opacity"]))
+    return p, rng.normal(size=(11 + K3, n)), rng.uniform(size=(11 + K3, n))
+
+
+def test_densify_apply_layout_and_counts():
+    rng = np.random.default_rng(13)
+    n = 9
+    p, m, v = _dens_state(rng, n)
+    act = np.array([1, 0, 2, 3, 1, 2, 3, 0, 1], np.uint8)
+    q, m2, v2 = oracle.densify_apply(p, m, v, act, seed=7)
+    keep, clone, split = [0, 2, 4, 5, 8], [2, 5], [3, 6]
+    n2 = len(keep) + len(clone) + 2 * len(split)
+    assert q["mean"].shape == (3, n2) and m2.shape == (23, n2)
+    for k in ("mean", "rot", "sh", "scale", "opacity", "log_scale", "logit_opacity"):
+        assert np.array_equal(q[k][..., :5], np.asarray(p[k])[..., keep])            # kept, source order
+        assert np.array_equal(q[k][..., 5:7], np.asarray(p[k])[..., clone])          # clones = copies
+    assert np.array_equal(m2[:, :5], m[:, keep]) and (m2[:, 5:] == 0).all() and (v2[:, 5:] == 0).all()
+    for j, i in enumerate(split):  # children: scale / 1.6, same rot / opacity / sh
+        for c in (0, 1):
+            col = 7 + 2 * j + c
+            assert np.allclose(q["scale"][:, col], p["scale"][:, i] / 1.6, rtol=1e-7)
+            assert np.allclose(q["log_scale"][:, col], np.log(p["scale"][:, i] / 1.6), rtol=1e-6)
+            for k in ("rot", "sh", "opacity", "logit_opacity"):
+                assert np.array_equal(q[k][..., col], np.asarray(p[k])[..., i])
+            R = oracle.quat_to_rot(p["rot"][:, i])
+            z = R.T @ (q["mean"][:, col] - p["mean"][:, i]) / p["scale"][:, i]
+            assert np.allclose(z, oracle.split_normals(7, int(i), c))
+
+
+def test_split_children_covariance():
+    """Children of one Gaussian are samples of N(mu, R S^2 R^T): empirical covariance over many
+    (seeded) splits of the same source matches it within sampling error."""
+    rng = np.random.default_rng(14)
+    p, m, v = _dens_state(rng, 1)
+    p["scale"][:, 0] = [0.5, 0.2, 0.05]
+    R = oracle.quat_to_rot(p["rot"][:, 0])
+    pts = []
+    for seed in range(1500):
+        q, _, _ = oracle.densify_apply(p, m, v, np.array([3], np.uint8), seed=seed * 7919)
+        pts += [q["mean"][:, 0], q["mean"][:, 1]]
+    d = np.array(pts) - p["mean"][:, 0]
+    cov = np.cov(d.T)
+    ref = R @ np.diag(p["scale"][:, 0] ** 2) @ R.T
+    assert np.abs(cov - ref).max() < 0.06 * ref.max()
