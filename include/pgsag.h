@@ -12,8 +12,9 @@
  *     comes from the caller's workspace `ws` (>= pgsag_workspace_size bytes,
  *     256-byte aligned).
  *   - All work is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
- *     legacy default stream) in call order.  The only host synchronisation is the
- *     read-back of M (the number of (tile, Gaussian) entries) in pgsag_bin_sort.
+ *     legacy default stream) in call order.  The only host synchronisations are the
+ *     read-back of M (the number of (tile, Gaussian) entries) in pgsag_bin_sort and of
+ *     the output counts in pgsag_densify_plan.
  *   - Return value: PGSAG_OK (0) or a negative PGSAG_E* code; the message is in
  *     pgsag_last_error() (thread-local).  No exception crosses the ABI.  On error
  *     nothing is guaranteed about the output buffers.
@@ -149,6 +150,10 @@ typedef struct {
   float *dmean, *dscale, *drot, *dopacity, *dsh, *absgrad2d;
   float *grad2d; /* optional [14][n]: A7's per-Gaussian screen-space gradients du, dv, d(ca,cb,cc), d o,
                     d rgb[3], d n_cam[3], d d_i, absgrad (the A7 -> A8 interface) */
+  /* Optional densification statistic (NEXT-3, R31), ACCUMULATED across calls: for every Gaussian with
+   * tiles_touched > 0, densify_accum[i] += |(du W/2, dv H/2)| (3DGS's view-space positional gradient
+   * norm) and densify_count[i] += 1.  Both NULL or both [n]. */
+  float *densify_accum, *densify_count;
 } pgsag_gaussian_grad;
 
 /* Bytes of scratch needed by every call for n Gaussians, a width x height image and
@@ -260,6 +265,41 @@ typedef struct {
  * before the update. */
 int pgsag_adam_step(int32_t n, int32_t sh_degree, const pgsag_gaussian_grad *grad, pgsag_adam_state *state,
                     const pgsag_adam_hparams *hp, double *flatten_loss, void *stream);
+
+/* ------------------------------------------------------------ NEXT-3: densification (R31)
+ * 3DGS adaptive density control on a sub-region's optimiser state (the paper
+ * trains every group with it, and gives no parameters: 3DGS's conventions). */
+typedef struct {
+  float grad_threshold; /* densify if accum / count >= this (3DGS 0.0002, NDC units)          */
+  float dense_limit;    /* percent_dense * scene extent: clone if max scale <= it, else split */
+  float min_opacity;    /* prune if opacity < it (3DGS 0.005)                                 */
+  uint64_t seed;        /* split samples: SplitMix64 + Box-Muller counter generator (R31)     */
+} pgsag_densify_params;
+
+/* Scratch bytes for pgsag_densify_plan / _apply on n Gaussians. */
+size_t pgsag_densify_workspace_size(int32_t n);
+
+/* Plan: action[i] (device u8 [n], out) = 0 drop (opacity < min_opacity), 3 split (accum/count >=
+ * grad_threshold and max scale > dense_limit), 2 keep + clone (same, max scale <= dense_limit),
+ * 1 keep; every decision in float32.  counts (host int64[3], out) = (kept, cloned, split); the
+ * output has n_out = kept + cloned + 2 split Gaussians.  Synchronises the stream once (the caller
+ * needs n_out to allocate).  ws must be passed unchanged to pgsag_densify_apply. */
+int pgsag_densify_plan(int32_t n, const float *scale, const float *opacity, const float *accum, const float *count,
+                       const pgsag_densify_params *dp, uint8_t *action, int64_t counts[3], void *ws, size_t ws_bytes,
+                       void *stream);
+
+/* Apply the plan: dst (n_out Gaussians, caller-allocated, same layouts) receives the kept sources
+ * (source order), then the clones (source order), then the two children of each split source
+ * (source order): mean + R(q)(s * z), scale s / 1.6, log_scale = log of it, rot / opacity / SH
+ * copied.  Kept Gaussians keep their Adam moments; clones and children get zero moments.
+ * src and dst must not overlap. */
+int pgsag_densify_apply(int32_t n, int32_t sh_degree, const pgsag_adam_state *src, const uint8_t *action,
+                        const pgsag_densify_params *dp, const int64_t counts[3], pgsag_adam_state *dst,
+                        const void *ws, size_t ws_bytes, void *stream);
+
+/* 3DGS opacity reset: opacity = min(opacity, cap), logit_opacity updated, the Adam moments of the
+ * opacity row zeroed. */
+int pgsag_opacity_reset(int32_t n, pgsag_adam_state *state, float cap, void *stream);
 
 /* Message for the last non-zero status on this thread ("" if none). */
 const char *pgsag_last_error(void);

@@ -17,7 +17,8 @@ F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT, F_LIVE = 1, 2, 4, 8, 15
 SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd",
            "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable",
            "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights", "pgsag_boundary_band",
-           "pgsag_ban_loss", "pgsag_rgb_loss_workspace_size", "pgsag_rgb_loss", "pgsag_adam_step")
+           "pgsag_ban_loss", "pgsag_rgb_loss_workspace_size", "pgsag_rgb_loss", "pgsag_adam_step",
+           "pgsag_densify_workspace_size", "pgsag_densify_plan", "pgsag_densify_apply", "pgsag_opacity_reset")
 
 _vp = C.c_void_p
 
@@ -58,7 +59,12 @@ class ImageGrad(C.Structure):
 
 class GaussianGrad(C.Structure):
     _fields_ = [("dmean", _vp), ("dscale", _vp), ("drot", _vp), ("dopacity", _vp), ("dsh", _vp),
-                ("absgrad2d", _vp), ("grad2d", _vp)]
+                ("absgrad2d", _vp), ("grad2d", _vp), ("densify_accum", _vp), ("densify_count", _vp)]
+
+
+class DensifyParams(C.Structure):
+    _fields_ = [("grad_threshold", C.c_float), ("dense_limit", C.c_float), ("min_opacity", C.c_float),
+                ("seed", C.c_uint64)]
 
 
 class AdamState(C.Structure):
@@ -127,6 +133,16 @@ def lib():
             L.pgsag_adam_step.argtypes = [C.c_int32, C.c_int32, P(GaussianGrad), P(AdamState), P(AdamHparams), _vp,
                                           _vp]
             L.pgsag_adam_step.restype = C.c_int
+            L.pgsag_densify_workspace_size.argtypes = [C.c_int32]
+            L.pgsag_densify_workspace_size.restype = C.c_size_t
+            L.pgsag_densify_plan.argtypes = [C.c_int32, _vp, _vp, _vp, _vp, P(DensifyParams), _vp, P(C.c_int64 * 3),
+                                             _vp, C.c_size_t, _vp]
+            L.pgsag_densify_plan.restype = C.c_int
+            L.pgsag_densify_apply.argtypes = [C.c_int32, C.c_int32, P(AdamState), _vp, P(DensifyParams),
+                                              P(C.c_int64 * 3), P(AdamState), _vp, C.c_size_t, _vp]
+            L.pgsag_densify_apply.restype = C.c_int
+            L.pgsag_opacity_reset.argtypes = [C.c_int32, P(AdamState), C.c_float, _vp]
+            L.pgsag_opacity_reset.restype = C.c_int
             _lib = L
     return _lib
 
@@ -215,3 +231,24 @@ def rgb_loss(image, target, mask, W, H, weight, loss, dC, ws, ws_bytes, stream):
 
 def adam_step(n, deg, grad, state, hp, flat, stream):
     return check(lib().pgsag_adam_step(int(n), int(deg), C.byref(grad), C.byref(state), C.byref(hp), flat, stream))
+
+
+def densify_workspace_size(n):
+    return int(lib().pgsag_densify_workspace_size(int(n)))
+
+
+def densify_plan(n, scale, opacity, accum, count, dp, action, ws, ws_bytes, stream):
+    counts = (C.c_int64 * 3)()
+    check(lib().pgsag_densify_plan(int(n), scale, opacity, accum, count, C.byref(dp), action, C.byref(counts), ws,
+                                   int(ws_bytes), stream))
+    return [int(c) for c in counts]
+
+
+def densify_apply(n, deg, src, action, dp, counts, dst, ws, ws_bytes, stream):
+    cc = (C.c_int64 * 3)(*counts)
+    return check(lib().pgsag_densify_apply(int(n), int(deg), C.byref(src), action, C.byref(dp), C.byref(cc),
+                                           C.byref(dst), ws, int(ws_bytes), stream))
+
+
+def opacity_reset(n, state, cap, stream):
+    return check(lib().pgsag_opacity_reset(int(n), C.byref(state), float(cap), stream))

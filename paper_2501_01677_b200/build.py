@@ -28,6 +28,7 @@ UNITS = {
     "gc_load.cu": [],
     "ban.cu": [],
     "train.cu": [],
+    "densify.cu": [],
     "api.cu": [],
 }
 

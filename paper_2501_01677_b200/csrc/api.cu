@@ -325,4 +325,54 @@ int pgsag_adam_step(int32_t n, int32_t sh_degree, const pgsag_gaussian_grad* gra
   return PGSAG_OK;
 }
 
+size_t pgsag_densify_workspace_size(int32_t n) { return n < 0 ? 0 : densify_ws_bytes(n); }
+
+static int check_state(const pgsag_adam_state* s) {
+  if (!s || !s->mean || !s->scale || !s->rot || !s->opacity || !s->sh || !s->log_scale || !s->logit_opacity || !s->m ||
+      !s->v)
+    return fail(PGSAG_EINVAL, "adam state: NULL buffer");
+  return PGSAG_OK;
+}
+
+int pgsag_densify_plan(int32_t n, const float* scale, const float* opacity, const float* accum, const float* count,
+                       const pgsag_densify_params* dp, uint8_t* action, int64_t counts[3], void* ws, size_t ws_bytes,
+                       void* stream) {
+  if (n < 0 || !dp || !counts) return fail(PGSAG_EINVAL, "densify_plan: bad argument");
+  if (n > 0 && (!scale || !opacity || !accum || !count || !action)) return fail(PGSAG_EINVAL, "densify_plan: NULL");
+  int rc;
+  if ((rc = check_ws(ws, ws_bytes, densify_ws_bytes(n)))) return rc;
+  unsigned long long tot[3] = {0, 0, 0};
+  cudaError_t e = launch_densify_plan(n, scale, opacity, accum, count, dp, action, ws,
+                                      static_cast<cudaStream_t>(stream), tot);
+  if (e != cudaSuccess) return cuda_fail(e, "densify_plan");
+  for (int k = 0; k < 3; ++k) counts[k] = (int64_t)tot[k];
+  return PGSAG_OK;
+}
+
+int pgsag_densify_apply(int32_t n, int32_t sh_degree, const pgsag_adam_state* src, const uint8_t* action,
+                        const pgsag_densify_params* dp, const int64_t counts[3], pgsag_adam_state* dst,
+                        const void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || sh_degree < 0 || sh_degree > 3 || !dp || !counts || !dst) return fail(PGSAG_EINVAL, "densify_apply");
+  const int64_t n_out = counts[0] + counts[1] + 2 * counts[2];
+  if (counts[0] < 0 || counts[1] < 0 || counts[2] < 0 || counts[0] > n || counts[1] > counts[0] || n_out > INT32_MAX)
+    return fail(PGSAG_EINVAL, "densify_apply: counts inconsistent with n");
+  int rc;
+  if (n > 0 && ((rc = check_state(src)) || !action)) return rc ? rc : fail(PGSAG_EINVAL, "densify_apply: NULL");
+  if (n_out > 0 && (rc = check_state(dst))) return rc;
+  if ((rc = check_ws(const_cast<void*>(ws), ws_bytes, densify_ws_bytes(n)))) return rc;
+  cudaError_t e = launch_densify_apply(n, sh_degree, src, action, dp, dst, (int)n_out, (uint32_t)counts[0],
+                                       (uint32_t)counts[1], ws, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "densify_apply");
+  return PGSAG_OK;
+}
+
+int pgsag_opacity_reset(int32_t n, pgsag_adam_state* state, float cap, void* stream) {
+  if (n < 0 || !(cap > 0.f && cap < 1.f)) return fail(PGSAG_EINVAL, "opacity_reset: bad n / cap");
+  int rc;
+  if (n > 0 && (rc = check_state(state))) return rc;
+  cudaError_t e = launch_opacity_reset(n, state, cap, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "opacity_reset");
+  return PGSAG_OK;
+}
+
 }  // extern "C"

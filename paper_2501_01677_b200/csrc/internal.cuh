@@ -107,6 +107,15 @@ cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8
 cudaError_t launch_adam(int n, int sh_degree, const pgsag_gaussian_grad* gr, pgsag_adam_state* s,
                         const pgsag_adam_hparams* hp, double* flat, cudaStream_t st);
 
+size_t densify_ws_bytes(int n);
+cudaError_t launch_densify_plan(int n, const float* scale, const float* op, const float* accum, const float* count,
+                                const pgsag_densify_params* dp, uint8_t* action, void* ws, cudaStream_t st,
+                                unsigned long long* totals_host);
+cudaError_t launch_densify_apply(int n, int sh_degree, const pgsag_adam_state* src, const uint8_t* action,
+                                 const pgsag_densify_params* dp, pgsag_adam_state* dst, int n_out, uint32_t K,
+                                 uint32_t Cn, const void* ws, cudaStream_t st);
+cudaError_t launch_opacity_reset(int n, pgsag_adam_state* s, float cap, cudaStream_t st);
+
 // counters[] slot (as 2 doubles at byte offset 4*CNT_GC) for pgsag_gc_weights
 constexpr int CNT_GC = 32;
 

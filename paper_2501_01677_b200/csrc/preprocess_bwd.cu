@@ -23,7 +23,9 @@ __global__ void __launch_bounds__(128, 4) preprocess_bwd_kernel(
     int n, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
     const float* __restrict__ sh, const uint32_t* __restrict__ flags, const double* __restrict__ g2d, CamB cam,
     float* __restrict__ dmean, float* __restrict__ dscale, float* __restrict__ drot, float* __restrict__ dopac,
-    float* __restrict__ dsh, float* __restrict__ absgrad, float* __restrict__ grad2d) {
+    float* __restrict__ dsh, float* __restrict__ absgrad, float* __restrict__ grad2d,
+    const uint32_t* __restrict__ tiles_touched, float* __restrict__ daccum, float* __restrict__ dcount, double hw,
+    double hh) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -120,6 +122,10 @@ __global__ void __launch_bounds__(128, 4) preprocess_bwd_kernel(
   if (!cly) { dp1 += -cam.fy * iz2 * dJ12; dp2 += 2. * cam.fy * y * iz3 * dJ12; }
   else { dp2 += cam.fy * cyz * iz2 * dJ12; }
   const double du = gg[0], dv = gg[1];
+  if (daccum && tiles_touched[i] > 0) {  // densification statistic (R31): |(du W/2, dv H/2)|
+    daccum[i] += (float)sqrt((du * hw) * (du * hw) + (dv * hh) * (dv * hh));
+    dcount[i] += 1.0f;
+  }
   dp0 += cam.fx * iz * du;
   dp1 += cam.fy * iz * dv;
   dp2 += -(cam.fx * x * du + cam.fy * y * dv) * iz2;
@@ -243,7 +249,9 @@ cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* 
 #define PGSAG_A8(DEG)                                                                                         \
   preprocess_bwd_kernel<DEG><<<blocks, 128, 0, st>>>(n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d, cb, \
                                                       out->dmean, out->dscale, out->drot, out->dopacity,      \
-                                                      out->dsh, out->absgrad2d, out->grad2d)
+                                                      out->dsh, out->absgrad2d, out->grad2d,                  \
+                                                      p->tiles_touched, out->densify_accum, out->densify_count, \
+                                                      0.5 * cam->width, 0.5 * cam->height)
     switch (g->sh_degree) {
       case 0: PGSAG_A8(0); break;
       case 1: PGSAG_A8(1); break;

@@ -23,6 +23,16 @@ LAMBDA, LAMBDA3, LAMBDA4 = 0.41, 100.0, 0.01
 
 
 @dataclass
+class DensifyConfig:
+    """3DGS adaptive density control (R31): 3DGS's defaults; dense_limit = percent_dense (0.01) x the
+    scene extent."""
+    grad_threshold: float = 2e-4
+    dense_limit: float = 0.01
+    min_opacity: float = 0.005
+    seed: int = 1677
+
+
+@dataclass
 class AdamConfig:
     """3DGS's default learning rates (R30); lr_mean is usually scaled by the scene extent."""
     lr_mean: float = 1.6e-4
@@ -66,6 +76,12 @@ class Trainer:
         self._state = st
         self.t = 0
         self.used_ban = self.used_gc = False
+        self._alloc_stats(n)
+
+    def _alloc_stats(self, n):
+        dev = self.r.device
+        self.accum = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
+        self.count = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
 
     def hparams(self) -> L.AdamHparams:
         c, hp = self.cfg, L.AdamHparams()
@@ -93,8 +109,12 @@ class Trainer:
             L.ban_loss(cam, p(mask), p(band), p(r.img_N), p(r.img_Dep), self.bw, (1.0 - self.lam) * self.lam4, 1,
                        p(self.loss_ban), p(self.dN), p(self.dDep), st)
         self.used_gc = gc_w is not None
-        r.backward(dC=self.dC, dN=self.dN if self.used_ban else None, dDep=self.dDep if self.used_ban else None,
-                   gc_lambda=self.lam if self.used_gc else 0.0)
+        r._grad.densify_accum, r._grad.densify_count = self.accum.data_ptr(), self.count.data_ptr()
+        try:
+            r.backward(dC=self.dC, dN=self.dN if self.used_ban else None, dDep=self.dDep if self.used_ban else None,
+                       gc_lambda=self.lam if self.used_gc else 0.0)
+        finally:
+            r._grad.densify_accum = r._grad.densify_count = None
         L.adam_step(self.g.n, self.g.sh_degree, r._grad, self._state, self.hparams(), p(self.loss_flat), st)
 
     def losses(self) -> dict:
@@ -106,3 +126,53 @@ class Trainer:
         Lgc = self.r.gc_load()[0] if self.used_gc else 0.0
         total = (1 - self.lam) * (rgb[0] + self.lam3 * Ls + self.lam4 * Lban) + self.lam * Lgc
         return dict(total=total, rgb=rgb[0], l1=rgb[1], ssim=rgb[2], flat=Ls, ban=Lban, gc_load=Lgc)
+
+    # ------------------------------------------------------------ densification (R31)
+    def _state_tensors(self, n, K3, dev):
+        f = lambda *sh: torch.empty(*sh, dtype=torch.float32, device=dev)
+        return dict(mean=f(3, n), scale=f(3, n), rot=f(4, n), opacity=f(n), sh=f(K3, n), log_scale=f(3, n),
+                    logit_opacity=f(n), m=f(11 + K3, n), v=f(11 + K3, n))
+
+    @staticmethod
+    def _state_struct(t) -> L.AdamState:
+        st = L.AdamState()
+        for k in ("mean", "scale", "rot", "opacity", "sh", "log_scale", "logit_opacity", "m", "v"):
+            setattr(st, k, t[k].data_ptr())
+        return st
+
+    def densify(self, cfg: DensifyConfig | None = None, capacity_per_gaussian=24):
+        """Clone / split / prune from the statistics accumulated since the last call (pgsag_densify_plan /
+        _apply), then re-allocate the optimiser state and the rasterizer for the new count.  Returns
+        (kept, cloned, split)."""
+        cfg = cfg or DensifyConfig()
+        g, r, dev = self.g, self.r, self.r.device
+        n, K3 = g.n, (g.sh_degree + 1) ** 2 * 3
+        dp = L.DensifyParams(cfg.grad_threshold, cfg.dense_limit, cfg.min_opacity, int(cfg.seed) + self.t)
+        action = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        wsb = L.densify_workspace_size(n)
+        ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
+        st = _stream()
+        p = lambda t: C.c_void_p(t.data_ptr())
+        counts = L.densify_plan(n, p(g.scale), p(g.opacity), p(self.accum), p(self.count), dp, p(action), p(ws), wsb,
+                                st)
+        n_out = counts[0] + counts[1] + 2 * counts[2]
+        new = self._state_tensors(max(n_out, 1), K3, dev)
+        L.densify_apply(n, g.sh_degree, self._state, p(action), dp, counts, self._state_struct(new), p(ws), wsb, st)
+        sl = lambda t: t[..., :n_out].contiguous() if n_out != t.shape[-1] else t
+        self.g = GaussianTensors(sl(new["mean"]), sl(new["scale"]), sl(new["rot"]), sl(new["opacity"]), sl(new["sh"]),
+                                 g.sh_degree)
+        self.log_scale, self.logit_opacity = sl(new["log_scale"]), sl(new["logit_opacity"])
+        self.m, self.v = new["m"], new["v"]
+        if n_out != self.m.shape[-1]:
+            self.m, self.v = self.m[:, :n_out].contiguous(), self.v[:, :n_out].contiguous()
+        self._state = self._state_struct(dict(mean=self.g.mean, scale=self.g.scale, rot=self.g.rot,
+                                              opacity=self.g.opacity, sh=self.g.sh, log_scale=self.log_scale,
+                                              logit_opacity=self.logit_opacity, m=self.m, v=self.v))
+        self.r = Rasterizer(n_out, r.W, r.H, g.sh_degree, capacity=max(1024, capacity_per_gaussian * n_out),
+                            device=dev, counters=r.counters is not None, sat=r.want_sat)
+        self._alloc_stats(n_out)
+        return tuple(counts)
+
+    def reset_opacity(self, cap=0.01):
+        """3DGS opacity reset (pgsag_opacity_reset)."""
+        L.opacity_reset(self.g.n, self._state, cap, _stream())

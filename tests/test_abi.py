@@ -61,10 +61,11 @@ def test_struct_layouts_match_header(lib, tmp_path):
 #include <stddef.h>
 #include "pgsag.h"
 int main(void){
- printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(pgsag_camera), sizeof(pgsag_gaussians),
+ printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(pgsag_camera), sizeof(pgsag_gaussians),
    sizeof(pgsag_projected), sizeof(pgsag_tilemask), sizeof(pgsag_bins), sizeof(pgsag_image),
    sizeof(pgsag_image_grad), sizeof(pgsag_gaussian_grad), offsetof(pgsag_camera, znear), offsetof(pgsag_bins, n_dup),
-   sizeof(pgsag_adam_state), sizeof(pgsag_adam_hparams), offsetof(pgsag_adam_hparams, step));
+   sizeof(pgsag_adam_state), sizeof(pgsag_adam_hparams), offsetof(pgsag_adam_hparams, step),
+   sizeof(pgsag_densify_params), offsetof(pgsag_densify_params, seed));
  return 0; }''')
     exe = tmp_path / "s"
     subprocess.check_call(["gcc", "-I", os.path.dirname(HEADER), str(prog), "-o", str(exe)])
@@ -72,7 +73,7 @@ int main(void){
     exp = [C.sizeof(lib.Camera), C.sizeof(lib.Gaussians), C.sizeof(lib.Projected), C.sizeof(lib.TileMask),
            C.sizeof(lib.Bins), C.sizeof(lib.Image), C.sizeof(lib.ImageGrad), C.sizeof(lib.GaussianGrad),
            lib.Camera.znear.offset, lib.Bins.n_dup.offset, C.sizeof(lib.AdamState), C.sizeof(lib.AdamHparams),
-           lib.AdamHparams.step.offset]
+           lib.AdamHparams.step.offset, C.sizeof(lib.DensifyParams), lib.DensifyParams.seed.offset]
     assert got == exp
 
 

@@ -189,3 +189,133 @@ def test_training_descends():
     assert hist[-1]["rgb"] < 0.95 * hist[0]["rgb"], (hist[0], hist[-1])
     assert hist[-1]["total"] < hist[0]["total"]
     assert hist[-1]["gc_load"] > 0 and hist[-1]["ban"] > 0
+
+
+# ------------------------------------------------------------ densification (R31)
+def test_densify_statistic_in_A8():
+    """A8's accumulated |(du W/2, dv H/2)| (tiles_touched > 0) against the oracle's 2D gradients, two views."""
+    sc = S.config1(seed=70, n=600, W=64, H=48)
+    H, W = sc.mask.shape
+    pix = all_pixels(sc.mask)
+    g = GaussianTensors.from_numpy(sc.gaussians)
+    r = Rasterizer(g.n, W, H, g.sh_degree)
+    acc = torch.zeros(g.n, device="cuda")
+    cnt = torch.zeros(g.n, device="cuda")
+    rng = np.random.default_rng(70)
+    ref_acc, ref_cnt = np.zeros(g.n), np.zeros(g.n)
+    for view in range(2):
+        up = rng.normal(size=(len(pix), 9))
+        ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=up)
+        near = ora["near"].astype(bool)
+        up[near] = 0.0
+        ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=up)
+        tiles = oracle.project(sc.gaussians, sc.camera, sc.mask)["tiles"]
+        du, dv = ora["grads"][59], ora["grads"][60]
+        vis = tiles > 0
+        ref_acc[vis] += np.sqrt((du * W / 2) ** 2 + (dv * H / 2) ** 2)[vis]
+        ref_cnt[vis] += 1
+        planes = {"dC": np.zeros((3, H * W), np.float32), "dN": np.zeros((3, H * W), np.float32),
+                  "dD": np.zeros(H * W, np.float32), "dA": np.zeros(H * W, np.float32),
+                  "dDep": np.zeros(H * W, np.float32)}
+        u32 = up.astype(np.float32)
+        planes["dC"][:, pix], planes["dN"][:, pix] = u32[:, 0:3].T, u32[:, 3:6].T
+        planes["dD"][pix], planes["dA"][pix], planes["dDep"][pix] = u32[:, 6], u32[:, 7], u32[:, 8]
+        r.forward(g, camera_from(sc.camera), torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda())
+        r._grad.densify_accum, r._grad.densify_count = acc.data_ptr(), cnt.data_ptr()
+        r.backward(**{k: torch.from_numpy(np.ascontiguousarray(
+            v.reshape((3, H, W) if v.ndim == 2 else (H, W)))).cuda() for k, v in planes.items()})
+    torch.cuda.synchronize()
+    assert np.array_equal(cnt.cpu().numpy(), ref_cnt)
+    a = acc.cpu().numpy().astype(np.float64)
+    assert (np.abs(a - ref_acc) <= 1e-3 * np.maximum(ref_acc, 1e-2 * ref_acc.max())).all()
+
+
+def _densify_inputs(rng, n, deg):
+    p = _adam_inputs(rng, n, deg)
+    K3 = (deg + 1) ** 2 * 3
+    m = rng.normal(size=(11 + K3, n)).astype(np.float32)
+    v = rng.uniform(size=(11 + K3, n)).astype(np.float32)
+    # statistics spread around the thresholds used below; a few zero counts and low opacities
+    count = rng.integers(0, 5, n).astype(np.float32)
+    accum = (count * rng.lognormal(np.log(2e-4), 0.6, n)).astype(np.float32)
+    p["opacity"][rng.uniform(size=n) < 0.1] = np.float32(0.003)
+    return p, m, v, accum, count
+
+
+@pytest.mark.parametrize("n,deg", [(5000, 3), (1, 0), (2049, 1)])
+def test_densify_parity(n, deg):
+    rng = np.random.default_rng(80 + n)
+    p, m, v, accum, count = _densify_inputs(rng, n, deg)
+    thr, lim, mo, seed = 2e-4, float(np.median(p["scale"].max(axis=0))), 0.005, 99
+    act_ref = oracle.densify_actions(p["scale"], p["opacity"], accum, count, thr, lim, mo)
+    q_ref, m_ref, v_ref = oracle.densify_apply({k: x.astype(np.float64) for k, x in p.items()}, m.astype(np.float64),
+                                               v.astype(np.float64), act_ref, seed)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    T = {k: dev(x) for k, x in p.items()}
+    T["m"], T["v"] = dev(m), dev(v)
+    src = Trainer._state_struct(T)
+    dp = L.DensifyParams(thr, lim, mo, seed)
+    action = torch.empty(n, dtype=torch.uint8, device="cuda")
+    wsb = L.densify_workspace_size(n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    acc_t, cnt_t = dev(accum), dev(count)  # keep references: temporaries would be freed before the launch
+    counts = L.densify_plan(n, T["scale"].data_ptr(), T["opacity"].data_ptr(), acc_t.data_ptr(), cnt_t.data_ptr(), dp,
+                            action.data_ptr(), ws.data_ptr(), wsb, st)
+    assert np.array_equal(action.cpu().numpy(), act_ref)
+    assert counts == [int(((act_ref == 1) | (act_ref == 2)).sum()), int((act_ref == 2).sum()), int((act_ref == 3).sum())]
+    n_out = counts[0] + counts[1] + 2 * counts[2]
+    K3 = (deg + 1) ** 2 * 3
+    D = {k: torch.full(x.shape[:-1] + (max(n_out, 1),), -7.0, device="cuda") for k, x in T.items()}
+    L.densify_apply(n, deg, src, action.data_ptr(), dp, counts, Trainer._state_struct(D), ws.data_ptr(), wsb, st)
+    torch.cuda.synchronize()
+    nk = counts[0] + counts[1]
+    for k in ("mean", "scale", "rot", "opacity", "sh", "log_scale", "logit_opacity"):
+        got = D[k].cpu().numpy()[..., :n_out].astype(np.float64)
+        ref = q_ref[k]
+        assert got.shape == ref.shape, k
+        assert np.array_equal(got[..., :nk], ref[..., :nk]), k  # kept + clones: exact copies
+        tol = 1e-5 * (1 + np.abs(ref[..., nk:]))
+        assert (np.abs(got[..., nk:] - ref[..., nk:]) <= tol).all(), (k, np.abs(got[..., nk:] - ref[..., nk:]).max())
+    assert np.array_equal(D["m"].cpu().numpy()[:, :n_out], m_ref.astype(np.float32))
+    assert np.array_equal(D["v"].cpu().numpy()[:, :n_out], v_ref.astype(np.float32))
+
+
+def test_opacity_reset():
+    rng = np.random.default_rng(90)
+    p = _adam_inputs(rng, 1000, 0)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    T = {k: dev(x) for k, x in p.items()}
+    T["m"], T["v"] = torch.ones(14, 1000, device="cuda"), torch.ones(14, 1000, device="cuda")
+    L.opacity_reset(1000, Trainer._state_struct(T), 0.01, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    o = T["opacity"].cpu().numpy()
+    assert np.allclose(o, np.minimum(p["opacity"], np.float32(0.01)))
+    assert np.allclose(1 / (1 + np.exp(-T["logit_opacity"].cpu().numpy().astype(np.float64))), o, rtol=1e-5)
+    mm = T["m"].cpu().numpy()
+    assert (mm[10] == 0).all() and (mm[:10] == 1).all() and (mm[11:] == 1).all()
+
+
+def test_training_with_densification():
+    """Training with 3DGS-style densify / prune / opacity reset stays finite and changes the count."""
+    sc = S.config1(seed=95, n=800, W=96, H=64)
+    H, W = sc.mask.shape
+    g = GaussianTensors.from_numpy(sc.gaussians)
+    r = Rasterizer(g.n, W, H, g.sh_degree)
+    tr = Trainer(r, g, AdamConfig(lr_mean=1e-3))
+    cam = camera_from(sc.camera)
+    m_t = torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda()
+    tgt = torch.from_numpy(np.ascontiguousarray(S.reference_image(H, W, 95), np.float32)).cuda()
+    from paper_2501_01677_b200.train import DensifyConfig
+    ns = [g.n]
+    for it in range(30):
+        tr.step(cam, m_t, tgt)
+        if it % 10 == 9:
+            tr.densify(DensifyConfig(grad_threshold=1e-5, dense_limit=0.3))
+            ns.append(tr.g.n)
+        if it == 19:
+            tr.reset_opacity(0.01)
+    lo = tr.losses()
+    assert np.isfinite(lo["total"]) and len(set(ns)) > 1, ns
+    for t in (tr.g.mean, tr.g.scale, tr.g.rot, tr.g.opacity, tr.g.sh, tr.m, tr.v):
+        assert torch.isfinite(t).all()
