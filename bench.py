@@ -317,8 +317,23 @@ def main():
             pass
         roof["share_of_step"] = tot_ms / max(ms, 1e-9)
 
-    # ------------------------------------------------------------- e2e (host buffers)
-    e2e = None
+    def dmax(x):  # max over ranks of a device time
+        if world > 1:
+            t = torch.tensor([x], device=cdev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    def dsum(x):
+        if world > 1:
+            t = torch.tensor([x], device=cdev, dtype=torch.float64)
+            dist.all_reduce(t)
+            return float(t.item())
+        return x
+
+    # ------------------------------------------- e2e_raster: rasterizer fwd+bwd from host buffers
+    # (every input of pgsag_* copied in each step: Gaussians, mask, upstream planes; gradients out)
+    e2e_raster = None
     if not args.no_e2e:
         pin = lambda t: t.detach().cpu().pin_memory()
         hg = {k: pin(getattr(g, k)) for k in ("mean", "scale", "rot", "opacity", "sh")}
@@ -352,26 +367,24 @@ def main():
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for s in range(ke):
-            e2e_step(views[s])
+        for s_ in range(ke):
+            e2e_step(views[s_])
         e1.record()
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        epix = float(sum(npix[views[s]] for s in range(ke)))
-        if world > 1:
-            t = torch.tensor([ems], device=cdev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-            tp = torch.tensor([epix], device=cdev, dtype=torch.float64)
-            dist.all_reduce(tp)
-            epix = float(tp.item())
-        e2e = {"value": epix / 1e6 / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "steps": ke,
-               "note": "pinned host Gaussians+mask+upstream -> device, fwd+bwd, gradients -> host"}
+        ems = dmax(e0.elapsed_time(e1))
+        epix = dsum(float(sum(npix[views[s_]] for s_ in range(ke))))
+        e2e_raster = {"value": epix / 1e6 / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                      "d2h_bytes_per_step": int(d2h), "steps": ke,
+                      "note": "pinned host Gaussians+mask+upstream planes -> device, fwd+bwd, gradients -> host"}
+        del dg, dup, hg, hup, hgrad
 
     # ------------------------------------------- NEXT-3: full training iteration (Eq. 10-11)
-    train = None
-    if not args.no_train:
+    # train_step: device-resident inputs; e2e: the same iterations through the public API
+    # (train.Trainer.step) with each step's inputs (target photo + building mask) copied from
+    # pinned host memory on a copy stream (double-buffered, prefetching the next view while the
+    # current one trains) and the loss terms read back to the host every step.
+    train, e2e = None, None
+    if not (args.no_train and args.no_e2e):
         from paper_2501_01677_b200.train import Trainer
         gt_ = GaussianTensors(*(getattr(g, k).clone() for k in ("mean", "scale", "rot", "opacity", "sh")),
                               g.sh_degree)
@@ -379,38 +392,78 @@ def main():
         kt = min(args.steps, 5)
         tviews = views[:kt]
         tgt = torch.rand(3, H, W, device=dev, generator=gen)  # synthetic target photo
-        extras = {v: (r.gc_weights(tgt, masks[v]), r.boundary_band(masks[v], 1)) for v in set(tviews)}
-        for v in tviews[:2]:
-            tr.step(ccam[v], masks[v], tgt, gc_w=extras[v][0], band=extras[v][1])
+        for v in tviews[:2]:  # warm-up
+            tr.step(ccam[v], masks[v], tgt, gc_w=r.gc_weights(tgt, masks[v]), band=r.boundary_band(masks[v], 1))
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        L.timing_enable(True)
-        L.timing_collect()
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record()
-        for v in tviews:
-            tr.step(ccam[v], masks[v], tgt, gc_w=extras[v][0], band=extras[v][1])
-        t1.record()
-        torch.cuda.synchronize()
-        L.timing_enable(False)
-        tk = L.timing_collect()
-        tms = t0.elapsed_time(t1)
-        tpix = float(sum(npix[v] for v in tviews))
-        if world > 1:
-            t = torch.tensor([tms], device=cdev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            tms = float(t.item())
-            tp = torch.tensor([tpix], device=cdev, dtype=torch.float64)
-            dist.all_reduce(tp)
-            tpix = float(tp.item())
-        lo = tr.losses()
-        train = {"ms_per_iter": tms / kt, "value": tpix / 1e6 / (tms / 1e3), "unit": UNIT, "iters": kt,
-                 "terms": "L_rgb (L1+SSIM) + L_s + L_ban + L_GC-load with P:179 weights; Adam on raw params",
-                 "gpu_launches": int(sum(v[1] for v in tk.values())),
-                 "kernels_ms_per_iter": {k: round(v[0] / kt, 4) for k, v in sorted(tk.items())},
-                 "last_loss": {k: round(float(x), 6) for k, x in lo.items()}}
-        del tr, gt_, extras
+        if not args.no_train:
+            extras = {v: (r.gc_weights(tgt, masks[v]), r.boundary_band(masks[v], 1)) for v in set(tviews)}
+            if world > 1:
+                dist.barrier()
+            L.timing_enable(True)
+            L.timing_collect()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for v in tviews:
+                tr.step(ccam[v], masks[v], tgt, gc_w=extras[v][0], band=extras[v][1])
+            t1.record()
+            torch.cuda.synchronize()
+            L.timing_enable(False)
+            tk = L.timing_collect()
+            tms = dmax(t0.elapsed_time(t1))
+            tpix = dsum(float(sum(npix[v] for v in tviews)))
+            lo = tr.losses()
+            train = {"ms_per_iter": tms / kt, "value": tpix / 1e6 / (tms / 1e3), "unit": UNIT, "iters": kt,
+                     "terms": "L_rgb (L1+SSIM) + L_s + L_ban + L_GC-load with P:179 weights; Adam on raw params",
+                     "gpu_launches": int(sum(v[1] for v in tk.values())),
+                     "kernels_ms_per_iter": {k: round(v[0] / kt, 4) for k, v in sorted(tk.items())},
+                     "last_loss": {k: round(float(x), 6) for k, x in lo.items()}}
+            del extras
+        if not args.no_e2e:
+            htgt = tgt.cpu().pin_memory()
+            hmask = [m.cpu().pin_memory() for m in masks]
+            dt = [torch.empty_like(tgt) for _ in range(2)]
+            dm = [torch.empty_like(masks[0]) for _ in range(2)]
+            hloss = torch.empty(kt, 6, dtype=torch.float64, pin_memory=True)
+            cs = torch.cuda.Stream(device=dev)
+            main = torch.cuda.current_stream()
+            ready = [torch.cuda.Event() for _ in range(2)]
+            free = [torch.cuda.Event() for _ in range(2)]
+
+            def fetch(slot, v):
+                with torch.cuda.stream(cs):
+                    cs.wait_event(free[slot])
+                    dt[slot].copy_(htgt, non_blocking=True)
+                    dm[slot].copy_(hmask[v], non_blocking=True)
+                    ready[slot].record(cs)
+
+            for k in range(2):
+                free[k].record(main)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(main)
+            fetch(0, tviews[0])
+            for s_, v in enumerate(tviews):
+                cur = s_ & 1
+                if s_ + 1 < kt:
+                    fetch(cur ^ 1, tviews[s_ + 1])
+                main.wait_event(ready[cur])
+                tr.step(ccam[v], dm[cur], dt[cur], gc_w=r.gc_weights(dt[cur], dm[cur]),
+                        band=r.boundary_band(dm[cur], 1))
+                hloss[s_].copy_(tr.loss_rgb, non_blocking=True)
+                free[cur].record(main)
+            e1.record(main)
+            torch.cuda.synchronize()
+            ems = dmax(e0.elapsed_time(e1))
+            epix = dsum(float(sum(npix[v] for v in tviews)))
+            e2e = {"value": epix / 1e6 / (ems / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(htgt.numel() * 4 + hmask[0].numel()),
+                   "d2h_bytes_per_step": int(hloss[0].numel() * 8), "steps": kt,
+                   "note": "train.Trainer.step per view: pinned host target photo (3xHxW f32) + building mask "
+                           "-> device (copy stream, prefetched), A0-A8 + L_rgb + L_ban + L_GC-load + L_s/Adam, "
+                           "loss terms -> host; Gaussians and optimiser state are resident model state"}
+        del tr, gt_
 
     # ------------------------------------------------------------- CPU oracle baseline
     cpu = None
@@ -437,7 +490,8 @@ def main():
             "M_per_view": st0["M"], "evaluated_per_view": st0["evaluated"], "blended_per_view": st0["blended"],
             "bwd_visited_per_view": st0["bwd_visited"],
             "flop_per_unit": {"evaluated": FLOP_EVAL, "blended_fwd": FLOP_BLEND_FWD, "blended_bwd": FLOP_BLEND_BWD},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "train_step": train,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_raster": e2e_raster, "gpu_launches": launches,
+            "train_step": train,
             "kernels_ms_per_step": {k: round(v[0], 4) for k, v in sorted(ksteps.items())},
             "clocks": clk.summary(),
             "per_rank_ms": (rank_table[:, 1].tolist() if world > 1 else [ms]),

@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr_t):
-            jobs.append([nvcc, *ARCH, *COMMON, *extra, "-c", s, "-o", o])
+            jobs.append([nvcc, *ARCH, *COMMON, *extra, *os.environ.get("PGSAG_NVCC_EXTRA", "").split(), "-c", s,
+                         "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -287,6 +287,16 @@ __global__ void __launch_bounds__(kBT, 10) render_bwd_kernel(BwdArgs a) {
         if (kCount)
           cntV += (unsigned long long)(kk <= P01.last0) + (kk <= P01.last1) + (kk <= P23.last0) + (kk <= P23.last1);
         if (!__any_sync(0xffffffffu, c0 || c1 || c2 || c3)) continue;
+#ifdef PGSAG_HIST
+        if (kCount) {  // experiment: histogram of contributing lanes / pixels per (warp, candidate)
+          const uint32_t bl = __ballot_sync(0xffffffffu, c0 || c1 || c2 || c3);
+          const int npx = __reduce_add_sync(0xffffffffu, (int)c0 + (int)c1 + (int)c2 + (int)c3);
+          if (lane == 0) {
+            atomicAdd(a.counters + 4 + __popc(bl), 1ull);
+            atomicAdd(a.counters + 40 + min(npx / 4, 32), 1ull);
+          }
+        }
+#endif
         al0 = c0 ? al0 : 0.f; al1 = c1 ? al1 : 0.f; al2 = c2 ? al2 : 0.f; al3 = c3 ? al3 : 0.f;
         // rho and alpha as they enter d(opacity) and d(power): zero when clamped at 0.99 (R16)
         const bool u0 = c0 && or01.x <= kAlphaMax, u1 = c1 && or01.y <= kAlphaMax;
