@@ -2,12 +2,14 @@
 and profiles/<tag>_ncu.md (key counters of the full captures) from gpurun_out/ files."""
 import collections, csv, io, subprocess, sys
 
-OURS = ("render_bwd_kernel", "render_fwd_kernel", "preprocess_bwd_kernel", "radix_pass_kernel",
-        "preprocess_kernel", "tilemask_sat_kernel", "duplicate_kernel", "radix_hist_kernel", "scan_kernel",
-        "ranges_kernel", "tilemask_count_kernel", "depth_keys_kernel")
 STAGE = {"tilemask_count_kernel": "A0", "tilemask_sat_kernel": "A0", "preprocess_kernel": "A1", "scan_kernel": "A2",
          "duplicate_kernel": "A3", "depth_keys_kernel": "A4", "radix_hist_kernel": "A4", "radix_pass_kernel": "A4",
-         "ranges_kernel": "A5", "render_fwd_kernel": "A6", "render_bwd_kernel": "A7", "preprocess_bwd_kernel": "A8"}
+         "ranges_kernel": "A5", "render_fwd_kernel": "A6", "render_bwd_kernel": "A7", "preprocess_bwd_kernel": "A8",
+         "sobel_kernel": "N1", "gc_normalize_kernel": "N1", "band_kernel": "N2", "ban_loss_kernel": "N2",
+         "ban_grad_kernel": "N2", "rgb_fwd_kernel": "N3", "rgb_bwd_kernel": "N3", "rgb_finalize_kernel": "N3",
+         "adam_kernel": "N3", "densify_classify_kernel": "N3", "densify_scan_kernel": "N3",
+         "densify_apply_kernel": "N3", "opacity_reset_kernel": "N3"}
+OURS = tuple(STAGE)
 
 
 def launches(path, steps):
@@ -27,10 +29,15 @@ def launches(path, steps):
         us = v / 1e3 if u in ('nsecond', 'ns') else v * 1e3 if u in ('msecond', 'ms') else v
         tot[nm] += us
         cnt[nm] += 1
-    T = sum(tot.values())
-    out = ["| stage | kernel | launches | total us | share of our kernels |", "|---|---|---|---|---|"]
-    for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-        out.append(f"| {STAGE[k]} | `{k}` | {cnt[k]} | {v:.1f} | {100 * v / T:.1f}% |")
+    out = []
+    for title, pick in (("Rasterizer path A0-A8 (the bench step)", lambda k: STAGE[k][0] == "A"),
+                        ("NEXT rows (training iteration kernels)", lambda k: STAGE[k][0] == "N")):
+        sel = {k: v for k, v in tot.items() if pick(k)}
+        T = sum(sel.values()) or 1.0
+        out += [f"\n#### {title}\n", "| stage | kernel | launches | total us | share of the group |",
+                "|---|---|---|---|---|"]
+        for k, v in sorted(sel.items(), key=lambda kv: -kv[1]):
+            out.append(f"| {STAGE[k]} | `{k}` | {cnt[k]} | {v:.1f} | {100 * v / T:.1f}% |")
     return "\n".join(out)
 
 
@@ -70,5 +77,6 @@ if __name__ == "__main__":
         "Per-launch times are cold-cache and serialised (ncu); compare SHARES with the bench's live CUDA-event "
         "split (`kernels_ms_per_step`), not absolutes.\n\n" + launches(launch_csv, 2) + "\n")
     open(f"profiles/{tag}_ncu.md", "w").write(
-        f"# {tag}: ncu --set full captures (C4 view, tools/profile_step.py)\n\n" + ncu(rep) + "\n")
+        f"# {tag}: ncu --set full captures (C4 view)\n\nCommand: `{sys.argv[5] if len(sys.argv) > 5 else ''}`\n\n"
+        + "\n".join(ncu(x) for x in rep.split(",")) + "\n")
     print("ok")
