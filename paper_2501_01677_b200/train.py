@@ -17,6 +17,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib as L
+from . import shard
 from .raster import GaussianTensors, Rasterizer, _stream
 
 LAMBDA, LAMBDA3, LAMBDA4 = 0.41, 100.0, 0.01
@@ -92,8 +93,10 @@ class Trainer:
         return hp
 
     def step(self, cam, mask: torch.Tensor, target: torch.Tensor, gc_w: torch.Tensor | None = None,
-             band: torch.Tensor | None = None, bg=(0.0, 0.0, 0.0)):
-        """One iteration on one view; returns nothing (losses stay on the device, see losses())."""
+             band: torch.Tensor | None = None, bg=(0.0, 0.0, 0.0), dp_group=None):
+        """One iteration on one view; returns nothing (losses stay on the device, see losses()).
+        dp_group: process group of the ranks training the same sub-region view-parallel (NEXT-4);
+        their parameter gradients are averaged before the (identical) Adam step."""
         r = self.r
         self.t += 1
         st = _stream()
@@ -115,6 +118,9 @@ class Trainer:
                        gc_lambda=self.lam if self.used_gc else 0.0)
         finally:
             r._grad.densify_accum = r._grad.densify_count = None
+        if dp_group is not None:
+            K3 = (self.g.sh_degree + 1) ** 2 * 3
+            shard.allreduce_mean([r.dmean, r.dscale, r.drot, r.dopacity, r.dsh[:K3]], dp_group)
         L.adam_step(self.g.n, self.g.sh_degree, r._grad, self._state, self.hparams(), p(self.loss_flat), st)
 
     def losses(self) -> dict:
@@ -140,11 +146,14 @@ class Trainer:
             setattr(st, k, t[k].data_ptr())
         return st
 
-    def densify(self, cfg: DensifyConfig | None = None, capacity_per_gaussian=24):
+    def densify(self, cfg: DensifyConfig | None = None, capacity_per_gaussian=24, dp_group=None):
         """Clone / split / prune from the statistics accumulated since the last call (pgsag_densify_plan /
         _apply), then re-allocate the optimiser state and the rasterizer for the new count.  Returns
-        (kept, cloned, split)."""
+        (kept, cloned, split).  With dp_group the statistics are summed over the group first, so every
+        member takes the same decisions (same seed) and stays in sync."""
         cfg = cfg or DensifyConfig()
+        if dp_group is not None:
+            shard.allreduce_sum([self.accum, self.count], dp_group)
         g, r, dev = self.g, self.r, self.r.device
         n, K3 = g.n, (g.sh_degree + 1) ** 2 * 3
         dp = L.DensifyParams(cfg.grad_threshold, cfg.dense_limit, cfg.min_opacity, int(cfg.seed) + self.t)

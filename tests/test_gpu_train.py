@@ -319,3 +319,14 @@ def test_training_with_densification():
     assert np.isfinite(lo["total"]) and len(set(ns)) > 1, ns
     for t in (tr.g.mean, tr.g.scale, tr.g.rot, tr.g.opacity, tr.g.sh, tr.m, tr.v):
         assert torch.isfinite(t).all()
+
+
+def test_group_driver_single_rank():
+    """The parallel group-training driver (shard.rank_layout + view_schedule + Trainer + densify) on
+    two small regions, one rank: every region trains, losses stay finite."""
+    from paper_2501_01677_b200 import groups
+    rep = groups.main(["--small", "--regions", "2", "--iters", "12", "--densify-every", "5",
+                       "--grad-threshold", "1e-5", "--dense-limit", "0.3", "--reset-every", "10"])
+    assert sorted(r["region"] for r in rep) == [0, 1]
+    for r in rep:
+        assert np.isfinite(r["final_loss"]["total"]) and r["n_gaussians"] > 0 and r["ms"] > 0
