@@ -33,7 +33,7 @@ UNIT = "Mpix/s"
 # algorithmic FP32 work per unit, FMA = 2 flops (exp/rcp on MUFU not counted)
 FLOP_EVAL = 9        # per evaluated (pixel, Gaussian) pair: dx, dy, quadratic form, o*rho
 FLOP_BLEND_FWD = 17  # per blended pair in A6: 1-a, T(1-a), aT, 7 channel FMAs
-FLOP_BLEND_BWD = 48  # per blended pair in A7: T recovery, G.F, dalpha, suffix, dF, d(o,conic,mean2d), absgrad
+FLOP_BLEND_BWD = 46  # per blended pair in A7: 1-a, T recovery, G.F, dalpha, suffix, P, aT, dF, d o, d power, d conic
 BYTES_A1 = {0: 56 + 76, 1: 56 + 36 + 76, 2: 56 + 96 + 76, 3: 56 + 180 + 76}  # params read + 76 B written
 SM_COUNT = 148
 FP32_LANES = 128

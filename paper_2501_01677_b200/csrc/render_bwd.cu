@@ -38,6 +38,9 @@ constexpr int kBT = 64;
 constexpr int kBEPT = 2;
 constexpr int kBBatch = kBT * kBEPT;
 constexpr int kBNB = 2;
+#ifndef PGSAG_BWD_MINB
+#define PGSAG_BWD_MINB 10  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr float kLn2 = 0.6931471805599453f;
 
 struct BwdArgs {
@@ -71,6 +74,17 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 __device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float hsum(float2 a) { return a.x + a.y; }
 __device__ __forceinline__ float ld_or0(const float* p, size_t k) { return p ? __ldg(p + k) : 0.0f; }
+
+// Opaque copies: values the compiler would otherwise rematerialise inside the candidate loop
+// (from S2R / integer-to-float sequences) under register pressure.
+__device__ __forceinline__ float opaque(float x) {
+  asm volatile("mov.b32 %0, %0;" : "+f"(x));
+  return x;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
@@ -185,8 +199,8 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 
   o.dop = __fmul2_rn(rc, dal);
 }
 
-template <bool kCount, bool kGC>
-__global__ void __launch_bounds__(kBT, 10) render_bwd_kernel(BwdArgs a) {
+template <bool kCount, bool kGC, bool kAbs>
+__global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs a) {
   constexpr int kAccStride = 15;  // padded row: the 14 values of an entry sit in 14 distinct banks
   __shared__ Rec s_rec[kBBatch];
   __shared__ uint32_t s_id[kBBatch];
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(kBT, 10) render_bwd_kernel(BwdArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
-  const uint32_t rec_base = smem_u32(s_rec), list_base = smem_u32(s_list);
+  const uint32_t rec_base = opaque(smem_u32(s_rec)), list_base = opaque(smem_u32(s_list));
   unsigned long long cntV = 0;
   // value index this lane owns after the reduce-scatter: bit-reversed lane bits 1..4
   const int my_c = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
@@ -215,9 +229,9 @@ __global__ void __launch_bounds__(kBT, 10) render_bwd_kernel(BwdArgs a) {
     const int i = tx * kTile + w * 8 + (lane & 7);
     const int jb = ty * kTile + (lane >> 3);
     const uint32_t rs = a.ranges[2 * tile];
-    const float px = (float)i + 0.5f;
-    const float2 py01 = f2((float)jb + 0.5f, (float)(jb + 4) + 0.5f);
-    const float2 py23 = f2((float)(jb + 8) + 0.5f, (float)(jb + 12) + 0.5f);
+    const float px = opaque((float)i + 0.5f);
+    const float2 py01 = f2(opaque((float)jb + 0.5f), opaque((float)(jb + 4) + 0.5f));
+    const float2 py23 = f2(opaque((float)(jb + 8) + 0.5f), opaque((float)(jb + 12) + 0.5f));
     const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
     Pair P01, P23;
     {
@@ -321,16 +335,22 @@ __global__ void __launch_bounds__(kBT, 10) render_bwd_kernel(BwdArgs a) {
         v[3] = -dx * sdydp;
         v[4] = -0.5f * sdy2dp;
         // per-pixel screen-space mean gradient: (ca, cb, cc) = -ln2 (2A', B', 2C')
-        const float2 kd01 = __fmul2_rn(bc(-kLn2), o01.dpow), kd23 = __fmul2_rn(bc(-kLn2), o23.dpow);
         const float twoA = 2.0f * tA, bdx = ra.w * dx, twoC = 2.0f * rb.x;
-        const float2 du01 = __fmul2_rn(__ffma2_rn(bc(ra.w), dy01, bc(twoA)), kd01);
-        const float2 du23 = __fmul2_rn(__ffma2_rn(bc(ra.w), dy23, bc(twoA)), kd23);
-        const float2 dv01 = __fmul2_rn(__ffma2_rn(bc(twoC), dy01, bc(bdx)), kd01);
-        const float2 dv23 = __fmul2_rn(__ffma2_rn(bc(twoC), dy23, bc(bdx)), kd23);
-        v[0] = hsum(__fadd2_rn(du01, du23));
-        v[1] = hsum(__fadd2_rn(dv01, dv23));
-        v[13] = ((fabsf(du01.x) + fabsf(dv01.x)) + (fabsf(du01.y) + fabsf(dv01.y))) +
-                ((fabsf(du23.x) + fabsf(dv23.x)) + (fabsf(du23.y) + fabsf(dv23.y)));
+        if (kAbs) {  // per-pixel du, dv: needed for the absgrad statistic sum |du| + |dv|
+          const float2 kd01 = __fmul2_rn(bc(-kLn2), o01.dpow), kd23 = __fmul2_rn(bc(-kLn2), o23.dpow);
+          const float2 du01 = __fmul2_rn(__ffma2_rn(bc(ra.w), dy01, bc(twoA)), kd01);
+          const float2 du23 = __fmul2_rn(__ffma2_rn(bc(ra.w), dy23, bc(twoA)), kd23);
+          const float2 dv01 = __fmul2_rn(__ffma2_rn(bc(twoC), dy01, bc(bdx)), kd01);
+          const float2 dv23 = __fmul2_rn(__ffma2_rn(bc(twoC), dy23, bc(bdx)), kd23);
+          v[0] = hsum(__fadd2_rn(du01, du23));
+          v[1] = hsum(__fadd2_rn(dv01, dv23));
+          v[13] = ((fabsf(du01.x) + fabsf(dv01.x)) + (fabsf(du01.y) + fabsf(dv01.y))) +
+                  ((fabsf(du23.x) + fabsf(dv23.x)) + (fabsf(du23.y) + fabsf(dv23.y)));
+        } else {  // sums only: du = -ln2 (B' dy + 2 A' dx) dpow, dv = -ln2 (2 C' dy + B' dx) dpow per pixel
+          v[0] = -kLn2 * fmaf(ra.w, sdydp, twoA * sdp);
+          v[1] = -kLn2 * fmaf(twoC, sdydp, bdx * sdp);
+          v[13] = 0.f;
+        }
         v[14] = 0.f;
         v[15] = 0.f;
         // reduce-scatter 16 -> 1 value per lane pair
@@ -375,7 +395,7 @@ int bwd_grid() {
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_bwd_kernel<false, false>, kBT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_bwd_kernel<false, false, false>, kBT, 0);
     grid = sms * (occ > 0 ? occ : 1);
   }
   return grid;
@@ -417,14 +437,21 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
   const int grid = min(bwd_grid(), d.TX * d.TY);
   {
     KTimer kt_("A7_render_bwd", st);
-    if (fwd->counters && gc)
-      render_bwd_kernel<true, true><<<grid, kBT, 0, st>>>(a);
-    else if (fwd->counters)
-      render_bwd_kernel<true, false><<<grid, kBT, 0, st>>>(a);
-    else if (gc)
-      render_bwd_kernel<false, true><<<grid, kBT, 0, st>>>(a);
-    else
-      render_bwd_kernel<false, false><<<grid, kBT, 0, st>>>(a);
+    const bool abs_ = out->absgrad2d || out->grad2d;
+    const int variant = (fwd->counters ? 4 : 0) | (gc ? 2 : 0) | (abs_ ? 1 : 0);
+    switch (variant) {
+#define PGSAG_A7(V, C, G, A) \
+  case V: render_bwd_kernel<C, G, A><<<grid, kBT, 0, st>>>(a); break;
+      PGSAG_A7(0, false, false, false)
+      PGSAG_A7(1, false, false, true)
+      PGSAG_A7(2, false, true, false)
+      PGSAG_A7(3, false, true, true)
+      PGSAG_A7(4, true, false, false)
+      PGSAG_A7(5, true, false, true)
+      PGSAG_A7(6, true, true, false)
+      PGSAG_A7(7, true, true, true)
+#undef PGSAG_A7
+    }
   }
   return launch_preprocess_bwd(g, cam, p, out, g2d, st);
 }

@@ -70,8 +70,10 @@ def _stream():
 class Rasterizer:
     """Buffers for one (n, width, height, sh_degree) problem; reusable across views."""
 
-    def __init__(self, n, width, height, sh_degree=3, capacity=None, device="cuda", counters=True, sat=True):
+    def __init__(self, n, width, height, sh_degree=3, capacity=None, device="cuda", counters=True, sat=True,
+                 absgrad=False):
         self.want_sat = bool(sat)
+        self.want_absgrad = bool(absgrad)
         self.n, self.W, self.H, self.deg = int(n), int(width), int(height), int(sh_degree)
         self.device = torch.device(device)
         if self.device.type == "cuda" and self.device.index is None:
@@ -156,7 +158,8 @@ class Rasterizer:
         self._img = im
         gg = L.GaussianGrad()
         gg.dmean, gg.dscale, gg.drot = self.dmean.data_ptr(), self.dscale.data_ptr(), self.drot.data_ptr()
-        gg.dopacity, gg.dsh, gg.absgrad2d = self.dopacity.data_ptr(), self.dsh.data_ptr(), self.absgrad.data_ptr()
+        gg.dopacity, gg.dsh = self.dopacity.data_ptr(), self.dsh.data_ptr()
+        gg.absgrad2d = self.absgrad.data_ptr() if self.want_absgrad else None
         gg.grad2d = None
         self._grad = gg
 
@@ -235,7 +238,9 @@ class Rasterizer:
                      self._bg, self._img, ig, self._grad, C.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream())
         K3 = (self.deg + 1) ** 2 * 3
         out = dict(dmean=self.dmean, dscale=self.dscale, drot=self.drot, dopacity=self.dopacity,
-                   dsh=self.dsh[:K3], absgrad2d=self.absgrad)
+                   dsh=self.dsh[:K3])
+        if self._grad.absgrad2d:
+            out["absgrad2d"] = self.absgrad
         if self._grad.grad2d:
             out["grad2d"] = self.grad2d
         return out

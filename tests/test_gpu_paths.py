@@ -66,3 +66,35 @@ def test_jacobian_clamp_and_large_splats():
     assert ((p["flags"] & (16 | 32)) != 0)[live].sum() >= 5  # clamped Jacobians among emitting splats
     assert p["tiles"].max() >= 9
     _check(sc)
+
+
+@pytest.mark.parametrize("absgrad", [True, False])
+def test_screen_space_gradients_and_absgrad(absgrad):
+    """A7's 14 per-Gaussian screen-space values (exported grad2d: du dv dca dcb dcc dop drgb dncam ddist
+    absgrad) and the absgrad2d output against the oracle's rows 59-72.  With absgrad off, A7 takes its
+    sums-only path for (du, dv) and the export is requested without it (row 13 then still exported)."""
+    import torch
+    from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+    sc = S.config1(seed=77, n=700)
+    H, W = sc.mask.shape
+    pix = all_pixels(sc.mask)
+    ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix)
+    planes, per = upstream_at(pix, H, W, seed=77, exclude=ora0["near"].astype(bool), ora=ora0, cam=sc.camera)
+    ref = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=per)["grads"]
+    g = GaussianTensors.from_numpy(sc.gaussians)
+    r = Rasterizer(g.n, W, H, g.sh_degree, absgrad=absgrad)
+    r.export_grad2d(absgrad)
+    r.forward(g, camera_from(sc.camera), torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda())
+    out = r.backward(**{k: torch.from_numpy(v).cuda() for k, v in planes.items()})
+    torch.cuda.synchronize()
+    got = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in out.items()}
+    compare_grads(got, ref, sc.gaussians.sh_degree)
+    if absgrad:
+        g2 = r.grad2d.cpu().numpy().astype(np.float64)
+        for c in range(14):
+            a, b = g2[c], ref[59 + c]
+            scale = max(np.abs(b).max(), 1e-30)
+            assert (np.abs(a - b) <= 1e-3 * np.maximum(np.abs(b), 1e-2 * scale)).all(), c
+        assert np.allclose(got["absgrad2d"], ref[72], rtol=1e-3, atol=1e-5 * np.abs(ref[72]).max())
+    else:
+        assert "absgrad2d" not in got
