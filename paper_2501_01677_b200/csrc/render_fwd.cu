@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
     // compositing, T = -(final T) once it stopped (or -1 if it is not a mask pixel).
     float2 T = f2(m0 ? 1.f : -1.f, m1 ? 1.f : -1.f);
     float2 C0 = f2(0.f, 0.f), C1 = C0, C2 = C0, N0 = C0, N1 = C0, N2 = C0, D = C0;
-    int g0 = 0, g1 = 0, last0 = -1, last1 = -1;
+    float2 gc = f2(0.f, 0.f);
+    int last0 = -1, last1 = -1;
     for (uint32_t b = rs; b < re; b += kFBatch) {
       if (__syncthreads_count(T.x < 0.f && T.y < 0.f) == kFT) break;
       uint32_t mk[kFEPT];
@@ -144,7 +145,10 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
         const float2 Tn = __fmul2_rn(T, __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
         const bool st0 = ok0 && Tn.x < kTmin, st1 = ok1 && Tn.y < kTmin;
         ok0 &= !st0; ok1 &= !st1;
-        if (__any_sync(0xffffffffu, ok0 || ok1 || st0 || st1)) {
+#ifdef PGSAG_FWD_ANYSKIP
+        if (__any_sync(0xffffffffu, ok0 || ok1 || st0 || st1))
+#endif
+        {  // branch-free blend (predicated weights): no loop-carried phi copies
           const float2 wt = __fmul2_rn(f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f), T);
           const float4 cd = lds128(ra_addr + 32);
           const float4 nn = lds128(ra_addr + 48);
@@ -157,15 +161,16 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
           N2 = __ffma2_rn(wt, f2(nn.z, nn.z), N2);
           T.x = ok0 ? Tn.x : (st0 ? -T.x : T.x);
           T.y = ok1 ? Tn.y : (st1 ? -T.y : T.y);
-          if (ok0) ++g0;
-          if (ok1) ++g1;
-          last0 = ok0 ? (int)(b + q) : last0;
-          last1 = ok1 ? (int)(b + q) : last1;
+          gc = __fadd2_rn(gc, f2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f));  // blend counts (exact below 2^24)
+          const int kq = (int)(b + q);
+          last0 = ok0 ? kq : last0;
+          last1 = ok1 ? kq : last1;
         }
       }
     }
     T.x = fabsf(T.x);
     T.y = fabsf(T.y);
+    const int g0 = (int)gc.x, g1 = (int)gc.y;
     if (m0) write_pixel(a, pix0, HW, px, py.x, T.x, C0.x, C1.x, C2.x, N0.x, N1.x, N2.x, D.x, g0, last0);
     if (m1) write_pixel(a, pix1, HW, px, py.y, T.y, C0.y, C1.y, C2.y, N0.y, N1.y, N2.y, D.y, g1, last1);
     if (a.gc_w) {  // fused Eq. 9 statistics over the mask pixels of this tile (NEXT-1)
