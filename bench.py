@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--views", type=int, default=40)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-parallel", action="store_true", help="skip the whole-host oracle baseline")
     ap.add_argument("--no-train", action="store_true", help="skip the NEXT-3 training-iteration timing")
     ap.add_argument("--profile", action="store_true", help="per-kernel table on stderr")
     return ap.parse_args()
@@ -141,6 +142,35 @@ def oracle_sample(g, cam, mask_np, n_pix, seed=0):
     t0 = time.perf_counter()
     oracle.render(g, cam, mask_np, pix, upstream=up)
     return len(pix), time.perf_counter() - t0
+
+
+_PAR = {}
+
+
+def _oracle_shard(k):
+    """Worker of the whole-host oracle baseline (forked; reads the scene from _PAR)."""
+    import oracle
+    g, cam, mask_np, pix, up = _PAR["g"], _PAR["cam"], _PAR["mask"], _PAR["pix"][k], _PAR["up"][k]
+    t0 = time.perf_counter()
+    oracle.render(g, cam, mask_np, pix, upstream=up)
+    return len(pix), time.perf_counter() - t0
+
+
+def oracle_sample_parallel(g, cam, mask_np, n_per, procs, seed=0):
+    """SURVEY §8(d) whole-host oracle number: `procs` independent oracle processes (the oracle as it
+    stands, one thread each) over disjoint shards of n_per sampled masked pixels each."""
+    import multiprocessing as mproc
+    from synth import scenes as S
+    pix = S.sample_pixels(mask_np, n_per * procs, seed=seed)
+    shards = np.array_split(pix, procs)
+    rng = np.random.default_rng(seed)
+    _PAR.update(g=g, cam=cam, mask=mask_np, pix=shards, up=[rng.normal(size=(len(x), 9)) for x in shards])
+    t0 = time.perf_counter()
+    with mproc.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_oracle_shard, range(procs))
+    wall = time.perf_counter() - t0
+    _PAR.clear()
+    return sum(r[0] for r in res), wall
 
 
 def run_reference(args, rank, world):
@@ -250,9 +280,11 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in views]
         ev0.record()
-        for v in views:
+        for v, e in zip(views, evs):
             step(v)
+            e.record()
         ev1.record()
         torch.cuda.synchronize()
         if world > 1:
@@ -260,6 +292,8 @@ def main():
     L.timing_enable(False)
     ktimes = L.timing_collect()
     ms = ev0.elapsed_time(ev1)
+    per_step = [ev0.elapsed_time(evs[0])] + [evs[k - 1].elapsed_time(evs[k]) for k in range(1, len(evs))]
+    pct = lambda q: float(np.percentile(per_step, q))
     pix = float(sum(npix[v] for v in views))
     blends = float(sum(per_view[v]["blended"] for v in views))
     if world > 1:
@@ -308,6 +342,12 @@ def main():
             roof["frac"] = roof["achieved"] / roof["peak"]
         roof["peak_source"] = ("148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"
                                if roof["bound"] == "alu" else "MEASURED_PEAKS.json hbm_gbs")
+        if roof["bound"] == "alu":  # cross-check of the derived FP32 peak: FFMA2 chains, all SMs
+            scratch = torch.empty(256, device=dev)
+            st_ = torch.cuda.current_stream().cuda_stream
+            roof["peak_measured"] = {"ffma2_tflops": L.microbench_fp32(1, 16384, scratch.data_ptr(), st_),
+                                     "ffma_tflops": L.microbench_fp32(0, 16384, scratch.data_ptr(), st_),
+                                     "source": "pgsag_microbench_fp32: 16 independent FMA chains per thread, 8 CTAs/SM"}
         roof["traffic"] = None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
@@ -470,10 +510,17 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         v0 = views[0]
         n_s = 1024 if args.config in ("c4", "c3", "c5") else 4096
-        p, t = oracle_sample(g_np, cams[v0], masks[v0].cpu().numpy(), n_s)
+        mnp = masks[v0].cpu().numpy()
+        p, t = oracle_sample(g_np, cams[v0], mnp, n_s)
         cpu = {"value": p / 1e6 / t, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{p} sampled masked pixels of view {v0}, fwd+bwd, single thread, incl. full-scene "
                          f"projection ({t:.1f} s)"}
+        if not args.no_cpu_parallel:
+            procs = max(1, min(os.cpu_count() or 1, 64))
+            pp, tw = oracle_sample_parallel(g_np, cams[v0], mnp, n_s // 2, procs, seed=1)
+            cpu["whole_host"] = {"value": pp / 1e6 / tw, "unit": UNIT, "cores": procs, "kind": "oracle",
+                                 "sample": f"{procs} forked oracle processes x {n_s // 2} disjoint sampled pixels "
+                                           f"({pp} total, wall {tw:.1f} s, each incl. its full-scene projection)"}
 
     if rank == 0:
         st0 = per_view[views[0]]
@@ -495,6 +542,7 @@ def main():
             "kernels_ms_per_step": {k: round(v[0], 4) for k, v in sorted(ksteps.items())},
             "clocks": clk.summary(),
             "per_rank_ms": (rank_table[:, 1].tolist() if world > 1 else [ms]),
+            "step_ms_p10_p50_p90": [round(pct(10), 4), round(pct(50), 4), round(pct(90), 4)],
         }
         print(json.dumps(line), flush=True)
         if args.profile:

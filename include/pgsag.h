@@ -301,6 +301,11 @@ int pgsag_densify_apply(int32_t n, int32_t sh_degree, const pgsag_adam_state *sr
  * opacity row zeroed. */
 int pgsag_opacity_reset(int32_t n, pgsag_adam_state *state, float cap, void *stream);
 
+/* Measurement aid: FP32 FMA throughput of the device from independent chains on
+ * all SMs; mode 0 = scalar FFMA, mode 1 = packed FFMA2 (FP32x2).  Synchronises; writes TFLOP/s
+ * (FMA = 2 flop) to *tflops (host).  scratch: device float[256]. */
+int pgsag_microbench_fp32(int32_t mode, int32_t iters, float *scratch, double *tflops, void *stream);
+
 /* Message for the last non-zero status on this thread ("" if none). */
 const char *pgsag_last_error(void);
 

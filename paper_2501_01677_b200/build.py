@@ -29,6 +29,7 @@ UNITS = {
     "ban.cu": [],
     "train.cu": [],
     "densify.cu": [],
+    "microbench.cu": [],
     "api.cu": [],
 }
 

@@ -375,4 +375,14 @@ int pgsag_opacity_reset(int32_t n, pgsag_adam_state* state, float cap, void* str
   return PGSAG_OK;
 }
 
+int pgsag_microbench_fp32(int32_t mode, int32_t iters, float* scratch, double* tflops, void* stream) {
+  if ((mode != 0 && mode != 1) || iters <= 0 || !scratch || !tflops) return fail(PGSAG_EINVAL, "microbench: bad argument");
+  float ms = 0.f;
+  double flops = 0.0;
+  cudaError_t e = launch_fp32_microbench(mode, iters, scratch, &ms, &flops, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "microbench");
+  *tflops = flops / ((double)ms * 1e-3) / 1e12;
+  return PGSAG_OK;
+}
+
 }  // extern "C"

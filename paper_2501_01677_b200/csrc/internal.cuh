@@ -116,6 +116,8 @@ cudaError_t launch_densify_apply(int n, int sh_degree, const pgsag_adam_state* s
                                  uint32_t Cn, const void* ws, cudaStream_t st);
 cudaError_t launch_opacity_reset(int n, pgsag_adam_state* s, float cap, cudaStream_t st);
 
+cudaError_t launch_fp32_microbench(int mode, int iters, float* scratch, float* ms, double* flops, cudaStream_t st);
+
 // counters[] slot (as 2 doubles at byte offset 4*CNT_GC) for pgsag_gc_weights
 constexpr int CNT_GC = 32;
 
