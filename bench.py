@@ -543,7 +543,6 @@ def main():
             "clocks": clk.summary(),
             "per_rank_ms": (rank_table[:, 1].tolist() if world > 1 else [ms]),
             "step_ms_p10_p50_p90": [round(pct(10), 4), round(pct(50), 4), round(pct(90), 4)],
-            "step_ms_p10_p50_p90": [round(pct(10), 4), round(pct(50), 4), round(pct(90), 4)],
         }
         print(json.dumps(line), flush=True)
         if args.profile:
