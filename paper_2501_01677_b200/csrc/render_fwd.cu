@@ -23,10 +23,6 @@
 namespace pgsag {
 namespace {
 
-constexpr int kFT = 128;          // threads per tile CTA
-constexpr int kFEPT = 2;          // staged entries per thread per batch
-constexpr int kFBatch = kFT * kFEPT;
-constexpr int kFNB = 4;           // 8x8 warp blocks per tile
 
 struct FwdArgs {
   const float2* mean2d;
@@ -70,12 +66,26 @@ __device__ __forceinline__ void write_pixel(const FwdArgs& a, size_t pix, size_t
   a.Dep[pix] = (g > 0 && fabsf(den) > 1e-6f) ? D / den : 0.0f;
 }
 
-template <bool kCount>
-__global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
-  __shared__ Rec s_rec[kFBatch];
-  __shared__ uint8_t s_list[kFNB * kFBatch];
-  __shared__ uint32_t s_wc[kFEPT * (kFT / 32) * kFNB];
-  __shared__ int s_nw[kFNB];
+// NP packed pixel pairs per lane: NP = 1 -> 8x8 warp blocks, 4 warps per tile (a lane owns
+// rows y, y+4); NP = 2 -> 8x16 warp blocks, 2 warps per tile (rows y, y+4 | y+8, y+12), which
+// amortises each candidate's list / record / address work over four pixels.
+template <int NP>
+struct FwdCfg {
+  static constexpr int BH = 8 * NP;                // warp block height
+  static constexpr int NT = 32 * 2 * (16 / BH);    // threads per tile CTA
+  static constexpr int NB = NT / 32;               // warp blocks per tile
+  static constexpr int EPT = 256 / NT;             // staged entries per thread (batch of 256)
+  static constexpr int BATCH = NT * EPT;
+};
+
+template <bool kCount, int NP>
+__global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
+  using Cfg = FwdCfg<NP>;
+  constexpr int NT = Cfg::NT, EPT = Cfg::EPT, NB = Cfg::NB, BATCH = Cfg::BATCH;
+  __shared__ Rec s_rec[BATCH];
+  __shared__ uint8_t s_list[NB * BATCH];
+  __shared__ uint32_t s_wc[EPT * (NT / 32) * NB];
+  __shared__ int s_nw[NB];
   __shared__ uint32_t s_tile;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t n_active = *a.n_active;
@@ -91,92 +101,118 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
     const uint32_t tile = a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
     const int i = tx * kTile + (w & 1) * 8 + (lane & 7);
-    const int j0 = ty * kTile + (w >> 1) * 8 + (lane >> 3), j1 = j0 + 4;
-    const size_t pix0 = (size_t)j0 * a.d.W + i, pix1 = (size_t)j1 * a.d.W + i;
-    const bool m0 = i < a.d.W && j0 < a.d.H && a.mask[pix0] != 0;
-    const bool m1 = i < a.d.W && j1 < a.d.H && a.mask[pix1] != 0;
+    const int jb = ty * kTile + (w >> 1) * Cfg::BH + (lane >> 3);
     const uint32_t rs = a.ranges[2 * tile], re = a.ranges[2 * tile + 1];
     const float px = (float)i + 0.5f;
-    const float2 py = f2((float)j0 + 0.5f, (float)j1 + 0.5f);
     const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
-    // T carries the pixel's "done" state in its sign: T > 0 while the pixel is still
-    // compositing, T = -(final T) once it stopped (or -1 if it is not a mask pixel).
-    float2 T = f2(m0 ? 1.f : -1.f, m1 ? 1.f : -1.f);
-    float2 C0 = f2(0.f, 0.f), C1 = C0, C2 = C0, N0 = C0, N1 = C0, N2 = C0, D = C0;
-    float2 gc = f2(0.f, 0.f);
-    int last0 = -1, last1 = -1;
-    for (uint32_t b = rs; b < re; b += kFBatch) {
-      if (__syncthreads_count(T.x < 0.f && T.y < 0.f) == kFT) break;
-      uint32_t mk[kFEPT];
+    // per pair p: rows jb + 8p and jb + 8p + 4.  T carries the pixel's "done" state in its
+    // sign: T > 0 while compositing, T = -(final T) once stopped (-1 if not a mask pixel).
+    bool m[NP][2];
+    size_t pix[NP][2];
+    float2 py[NP], T[NP], C0[NP], C1[NP], C2[NP], N0[NP], N1[NP], N2[NP], D[NP], gc[NP];
+    int last[NP][2];
 #pragma unroll
-      for (int e = 0; e < kFEPT; ++e) {
-        const uint32_t k = b + e * kFT + tid;
+    for (int p = 0; p < NP; ++p) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = jb + 8 * p + 4 * h;
+        pix[p][h] = (size_t)j * a.d.W + i;
+        m[p][h] = i < a.d.W && j < a.d.H && a.mask[pix[p][h]] != 0;
+        last[p][h] = -1;
+      }
+      py[p] = f2((float)(jb + 8 * p) + 0.5f, (float)(jb + 8 * p + 4) + 0.5f);
+      T[p] = f2(m[p][0] ? 1.f : -1.f, m[p][1] ? 1.f : -1.f);
+      C0[p] = C1[p] = C2[p] = N0[p] = N1[p] = N2[p] = D[p] = gc[p] = f2(0.f, 0.f);
+    }
+    auto all_done = [&]() {
+      bool d = true;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) d = d && T[p].x < 0.f && T[p].y < 0.f;
+      return d;
+    };
+    for (uint32_t b = rs; b < re; b += BATCH) {
+      if (__syncthreads_count(all_done()) == NT) break;
+      uint32_t mk[EPT];
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const uint32_t k = b + e * NT + tid;
         mk[e] = 0u;
         if (k < re) {
           const uint32_t id = a.vals[k];
-          Rec& r = s_rec[e * kFT + tid];
-          mk[e] = stage_gaussian<8, 8>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
+          Rec& r = s_rec[e * NT + tid];
+          mk[e] = stage_gaussian<8, Cfg::BH>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
           r.cd = a.rgb_d[id];
           r.n = a.ncam[id];
         }
       }
-      build_lists<kFT, kFEPT, kFNB>(mk, s_list, s_wc, s_nw);
+      build_lists<NT, EPT, NB>(mk, s_list, s_wc, s_nw);
       const int nw = s_nw[w];
-      const uint32_t lbase = list_base + (uint32_t)(w * kFBatch);
+      const uint32_t lbase = list_base + (uint32_t)(w * BATCH);
       for (int t = 0; t < nw; ++t) {
-        if ((t & 7) == 0 && __all_sync(0xffffffffu, T.x < 0.f && T.y < 0.f)) break;
+        if ((t & 7) == 0 && __all_sync(0xffffffffu, all_done())) break;
         const uint32_t q = lds_u8(lbase + (uint32_t)t);
         const uint32_t ra_addr = rec_base + q * (uint32_t)sizeof(Rec);
         const float4 ra = lds128(ra_addr);
         const float4 rb = lds128(ra_addr + 16);
-        // p2 for both pixels (bit-identical to power2r per element)
         const float dx = px - ra.x;
-        const float2 dy = __fadd2_rn(py, f2(-ra.y, -ra.y));
         const float tA = __fmul_rn(ra.z, dx);
-        const float2 u = __ffma2_rn(f2(ra.w, ra.w), dy, f2(tA, tA));
-        const float2 cq = __fmul2_rn(__fmul2_rn(f2(rb.x, rb.x), dy), dy);
-        const float2 p2 = __ffma2_rn(f2(dx, dx), u, cq);
-        const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(ex2_approx(p2.x), ex2_approx(p2.y)));
-        const float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
-        if (kCount) cntE += (unsigned long long)(T.x > 0.f) + (unsigned long long)(T.y > 0.f);
-        // blend iff still compositing, power <= 0 and alpha >= 1/255 (R6)
-        bool ok0 = T.x > 0.f && p2.x <= 0.0f && al0 >= kAlphaMin;
-        bool ok1 = T.y > 0.f && p2.y <= 0.0f && al1 >= kAlphaMin;
-        const float2 Tn = __fmul2_rn(T, __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
-        const bool st0 = ok0 && Tn.x < kTmin, st1 = ok1 && Tn.y < kTmin;
-        ok0 &= !st0; ok1 &= !st1;
-#ifdef PGSAG_FWD_ANYSKIP
-        if (__any_sync(0xffffffffu, ok0 || ok1 || st0 || st1))
-#endif
-        {  // branch-free blend (predicated weights): no loop-carried phi copies
-          const float2 wt = __fmul2_rn(f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f), T);
-          const float4 cd = lds128(ra_addr + 32);
-          const float4 nn = lds128(ra_addr + 48);
-          C0 = __ffma2_rn(wt, f2(cd.x, cd.x), C0);
-          C1 = __ffma2_rn(wt, f2(cd.y, cd.y), C1);
-          C2 = __ffma2_rn(wt, f2(cd.z, cd.z), C2);
-          D = __ffma2_rn(wt, f2(cd.w, cd.w), D);
-          N0 = __ffma2_rn(wt, f2(nn.x, nn.x), N0);
-          N1 = __ffma2_rn(wt, f2(nn.y, nn.y), N1);
-          N2 = __ffma2_rn(wt, f2(nn.z, nn.z), N2);
-          T.x = ok0 ? Tn.x : (st0 ? -T.x : T.x);
-          T.y = ok1 ? Tn.y : (st1 ? -T.y : T.y);
-          gc = __fadd2_rn(gc, f2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f));  // blend counts (exact below 2^24)
-          const int kq = (int)(b + q);
-          last0 = ok0 ? kq : last0;
-          last1 = ok1 ? kq : last1;
+        const float4 cd = lds128(ra_addr + 32);
+        const float4 nn = lds128(ra_addr + 48);
+        const int kq = (int)(b + q);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          // p2 for the pair (bit-identical to power2r per element)
+          const float2 dy = __fadd2_rn(py[p], f2(-ra.y, -ra.y));
+          const float2 u = __ffma2_rn(f2(ra.w, ra.w), dy, f2(tA, tA));
+          const float2 cq = __fmul2_rn(__fmul2_rn(f2(rb.x, rb.x), dy), dy);
+          const float2 p2 = __ffma2_rn(f2(dx, dx), u, cq);
+          const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(ex2_approx(p2.x), ex2_approx(p2.y)));
+          const float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
+          if (kCount) cntE += (unsigned long long)(T[p].x > 0.f) + (unsigned long long)(T[p].y > 0.f);
+          // blend iff still compositing, power <= 0 and alpha >= 1/255 (R6)
+          bool ok0 = T[p].x > 0.f && p2.x <= 0.0f && al0 >= kAlphaMin;
+          bool ok1 = T[p].y > 0.f && p2.y <= 0.0f && al1 >= kAlphaMin;
+          const float2 Tn = __fmul2_rn(T[p], __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
+          const bool st0 = ok0 && Tn.x < kTmin, st1 = ok1 && Tn.y < kTmin;
+          ok0 &= !st0; ok1 &= !st1;
+          // branch-free blend (predicated weights): no loop-carried phi copies
+          const float2 wt = __fmul2_rn(f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f), T[p]);
+          C0[p] = __ffma2_rn(wt, f2(cd.x, cd.x), C0[p]);
+          C1[p] = __ffma2_rn(wt, f2(cd.y, cd.y), C1[p]);
+          C2[p] = __ffma2_rn(wt, f2(cd.z, cd.z), C2[p]);
+          D[p] = __ffma2_rn(wt, f2(cd.w, cd.w), D[p]);
+          N0[p] = __ffma2_rn(wt, f2(nn.x, nn.x), N0[p]);
+          N1[p] = __ffma2_rn(wt, f2(nn.y, nn.y), N1[p]);
+          N2[p] = __ffma2_rn(wt, f2(nn.z, nn.z), N2[p]);
+          T[p].x = ok0 ? Tn.x : (st0 ? -T[p].x : T[p].x);
+          T[p].y = ok1 ? Tn.y : (st1 ? -T[p].y : T[p].y);
+          gc[p] = __fadd2_rn(gc[p], f2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f));  // blend counts (exact below 2^24)
+          last[p][0] = ok0 ? kq : last[p][0];
+          last[p][1] = ok1 ? kq : last[p][1];
         }
       }
     }
-    T.x = fabsf(T.x);
-    T.y = fabsf(T.y);
-    const int g0 = (int)gc.x, g1 = (int)gc.y;
-    if (m0) write_pixel(a, pix0, HW, px, py.x, T.x, C0.x, C1.x, C2.x, N0.x, N1.x, N2.x, D.x, g0, last0);
-    if (m1) write_pixel(a, pix1, HW, px, py.y, T.y, C0.y, C1.y, C2.y, N0.y, N1.y, N2.y, D.y, g1, last1);
-    if (a.gc_w) {  // fused Eq. 9 statistics over the mask pixels of this tile (NEXT-1)
-      float n = 0.f, s1 = 0.f, s2 = 0.f;
-      if (m0) { const float r = (float)g0 / __ldg(a.gc_w + pix0); n += 1.f; s1 += r; s2 += r * r; }
-      if (m1) { const float r = (float)g1 / __ldg(a.gc_w + pix1); n += 1.f; s1 += r; s2 += r * r; }
+    float n = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float Tf = fabsf(h ? T[p].y : T[p].x);
+        const int g = (int)(h ? gc[p].y : gc[p].x);
+        const float py_ = h ? py[p].y : py[p].x;
+        if (m[p][h]) {
+          write_pixel(a, pix[p][h], HW, px, py_, Tf, h ? C0[p].y : C0[p].x, h ? C1[p].y : C1[p].x,
+                      h ? C2[p].y : C2[p].x, h ? N0[p].y : N0[p].x, h ? N1[p].y : N1[p].x, h ? N2[p].y : N2[p].x,
+                      h ? D[p].y : D[p].x, g, last[p][h]);
+          if (a.gc_w) {  // fused Eq. 9 statistics over the mask pixels of this tile (NEXT-1)
+            const float r = (float)g / __ldg(a.gc_w + pix[p][h]);
+            n += 1.f; s1 += r; s2 += r * r;
+          }
+          if (kCount) cntB += (unsigned long long)g;
+        }
+      }
+    }
+    if (a.gc_w) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         n += __shfl_xor_sync(0xffffffffu, n, o);
@@ -189,7 +225,6 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
         atomicAdd(a.gc_stats + 2, (double)s2);
       }
     }
-    if (kCount) cntB += (unsigned long long)(m0 ? g0 : 0) + (unsigned long long)(m1 ? g1 : 0);
   }
   if (kCount) {
 #pragma unroll
@@ -204,13 +239,19 @@ __global__ void __launch_bounds__(kFT) render_fwd_kernel(FwdArgs a) {
   }
 }
 
+#ifndef PGSAG_FWD_NP
+#define PGSAG_FWD_NP 1
+#endif
+constexpr int kNP = PGSAG_FWD_NP;
+constexpr int kFT = FwdCfg<kNP>::NT;
+
 int fwd_grid() {
   static int grid = 0;
   if (!grid) {
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_fwd_kernel<false>, kFT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_fwd_kernel<false, kNP>, kFT, 0);
     grid = sms * (occ > 0 ? occ : 1);
   }
   return grid;
@@ -245,9 +286,9 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
   {
     KTimer kt_("A6_render_fwd", st);
     if (out->counters)
-      render_fwd_kernel<true><<<grid, kFT, 0, st>>>(a);
+      render_fwd_kernel<true, kNP><<<grid, kFT, 0, st>>>(a);
     else
-      render_fwd_kernel<false><<<grid, kFT, 0, st>>>(a);
+      render_fwd_kernel<false, kNP><<<grid, kFT, 0, st>>>(a);
   }
   return cudaGetLastError();
 }
