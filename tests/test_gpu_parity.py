@@ -206,3 +206,20 @@ def test_masked_render_equals_unmasked_restricted():
             np.testing.assert_array_equal(x[:, m], y[:, m])
         else:
             np.testing.assert_array_equal(x[m], y[m])
+
+
+def test_counting_and_timed_variants_agree():
+    """The bench times the non-counting kernel variants (kCount = false); the parity tests mostly run
+    the counting ones.  Forward outputs must be bitwise equal, and the non-counting backward must
+    match the oracle on its own."""
+    sc = S.config1(seed=123, n=900)
+    H, W = sc.mask.shape
+    pix = all_pixels(sc.mask)
+    ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix)
+    planes, per = upstream_at(pix, H, W, seed=124, exclude=ora0["near"].astype(bool), ora=ora0, cam=sc.camera)
+    a = run_gpu(sc, upstream=planes, counters=True)
+    b = run_gpu(sc, upstream=planes, counters=False)
+    for k in ("C", "N", "D", "A", "Dep", "T", "g", "last"):
+        assert np.array_equal(a["img"][k], b["img"][k]), k
+    ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=per)
+    compare_grads(b["grads"], ora["grads"], sc.gaussians.sh_degree)
