@@ -62,3 +62,28 @@ def test_gc_surrogate_gradient(name):
     ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=up)
     compare_grads(grads, ora["grads"], sc.gaussians.sh_degree)
     assert np.abs(grads["dsh"]).max() == 0.0  # the surrogate does not touch colour
+
+
+def test_gc_weights_full_resolution():
+    """Eq. 9 weights at the paper's full image size (5472x3648, the C3/C4 frame) on a blocky mask,
+    in the launch configuration the training iteration uses."""
+    from paper_2501_01677_b200 import _lib as L
+    H, W = 3648, 5472
+    rng = np.random.default_rng(77)
+    img = S.reference_image(H, W, 77)
+    mask = np.zeros((H, W), np.uint8)
+    for _ in range(40):
+        y, x = rng.integers(0, H), rng.integers(0, W)
+        mask[y:y + rng.integers(50, 900), x:x + rng.integers(50, 1200)] = 1
+    w_ref = oracle.gc_weights(img, mask)
+    m = torch.from_numpy(mask).cuda()
+    w = torch.empty(H, W, device="cuda")
+    nb = L.workspace_size(1, W, H, 0)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    img_d = torch.from_numpy(img).cuda()  # keep a reference until the kernel has run
+    L.gc_weights(img_d.data_ptr(), m.data_ptr(), W, H, w.data_ptr(), ws.data_ptr(), nb,
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    # float32 Sobel components are 6-term sums of values <= 1 (absolute error <= ~8 ulp(1) = 5e-7); divided
+    # by the mean magnitude (~0.1 here) that is <= 5e-6 absolute on w, plus 2e-5 relative for the mean
+    np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=2e-5, atol=1e-5)

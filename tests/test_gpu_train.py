@@ -45,7 +45,7 @@ def _rgb_gpu(Cimg, Iimg, mask, weight=1.0):
     return loss.cpu().numpy(), dC.cpu().numpy().astype(np.float64)
 
 
-@pytest.mark.parametrize("H,W,seed", [(20, 24, 0), (67, 100, 1), (389, 517, 2), (16, 32, 3)])
+@pytest.mark.parametrize("H,W,seed", [(20, 24, 0), (67, 100, 1), (389, 517, 2), (16, 32, 3), (1080, 1920, 4)])
 def test_rgb_loss_parity(H, W, seed):
     rng = np.random.default_rng(seed)
     Iimg = S.reference_image(H, W, seed).astype(np.float32)
