@@ -100,3 +100,46 @@ def test_invalid_arguments_rejected_on_host(lib):
     rc = L.pgsag_preprocess(C.byref(g), C.byref(bad), None, None, None, None, 0, None)
     assert rc == lib.PGSAG_EINVAL and b"width" in L.pgsag_last_error()
     assert lib.version().startswith("pgsag-b200")
+
+
+def test_next_row_calls_validate_on_host(lib):
+    """The NEXT-row entry points reject bad calls before any device work."""
+    L = lib.lib()
+    err = lambda: L.pgsag_last_error()
+    # pgsag_rgb_loss: NULL buffers, bad size, small workspace
+    assert L.pgsag_rgb_loss(None, None, None, 8, 8, 1.0, None, None, None, 0, None) == lib.PGSAG_EINVAL
+    assert b"NULL" in err()
+    dummy = C.c_void_p(256)  # never dereferenced: validation fails first
+    assert L.pgsag_rgb_loss(dummy, dummy, dummy, 0, 8, 1.0, dummy, None, dummy, 1 << 20, None) == lib.PGSAG_EINVAL
+    assert L.pgsag_rgb_loss(dummy, dummy, dummy, 8, 8, 1.0, dummy, None, dummy, 16, None) == lib.PGSAG_EWORKSPACE
+    assert lib.rgb_loss_workspace_size(8, 8) == 36 * 64 and lib.rgb_loss_workspace_size(0, 8) == 0
+    # pgsag_adam_step: step must be >= 1, NULL state
+    gr, st, hp = lib.GaussianGrad(), lib.AdamState(), lib.AdamHparams()
+    hp.step = 0
+    assert L.pgsag_adam_step(10, 3, C.byref(gr), C.byref(st), C.byref(hp), None, None) == lib.PGSAG_EINVAL
+    assert b"step" in err()
+    hp.step = 1
+    assert L.pgsag_adam_step(10, 3, C.byref(gr), C.byref(st), C.byref(hp), None, None) == lib.PGSAG_EINVAL
+    assert L.pgsag_adam_step(10, 4, C.byref(gr), C.byref(st), C.byref(hp), None, None) == lib.PGSAG_EINVAL
+    # densification: counts inconsistent with n; missing workspace
+    dp = lib.DensifyParams(2e-4, 0.01, 0.005, 1)
+    counts = (C.c_int64 * 3)(5, 6, 0)  # more clones than kept
+    assert L.pgsag_densify_apply(5, 3, C.byref(st), None, C.byref(dp), C.byref(counts), C.byref(st), None, 0,
+                                 None) == lib.PGSAG_EINVAL
+    assert b"counts" in err()
+    out = (C.c_int64 * 3)()
+    assert L.pgsag_densify_plan(-1, None, None, None, None, C.byref(dp), None, C.byref(out), None, 0,
+                                None) == lib.PGSAG_EINVAL
+    assert lib.densify_workspace_size(0) > 0 and lib.densify_workspace_size(5000) > lib.densify_workspace_size(10)
+    # opacity reset: cap must lie in (0, 1)
+    assert L.pgsag_opacity_reset(10, C.byref(st), 1.5, None) == lib.PGSAG_EINVAL
+    # band / ban / gc weights: NULL or bad radius
+    assert L.pgsag_boundary_band(dummy, 8, 8, 0, dummy, None) == lib.PGSAG_EINVAL
+    assert L.pgsag_gc_weights(None, None, 8, 8, None, None, 0, None) == lib.PGSAG_EINVAL
+    cam = lib.Camera()
+    cam.width, cam.height, cam.fx, cam.fy = 8, 8, 8.0, 8.0
+    assert L.pgsag_ban_loss(C.byref(cam), None, None, None, None, 0.1, 1.0, 1, None, None, None,
+                            None) == lib.PGSAG_EINVAL
+    # measurement aid: bad mode
+    t = C.c_double()
+    assert L.pgsag_microbench_fp32(7, 10, dummy, C.byref(t), None) == lib.PGSAG_EINVAL
