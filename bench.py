@@ -266,14 +266,35 @@ def main():
     act = tb[tb > 0]
     imbalance = float(act.max() / act.mean()) if act.numel() else 0.0
     r._img.counters = None  # timed steps run the non-counting kernels
+    # timed steps use the sync-free sort (no host synchronisation inside a step); the counting pass
+    # above read every view's M: size the entry buffers to the largest (+15 %), which also bounds the
+    # sync-free sort's grids
+    r._alloc_bins(int(1.15 * max(per_view[v]["M"] for v in per_view)) + 4096)
+    r._build_structs()
+    r._img.counters = None
+    r.sync_free = True
 
     views = [(args.warmup + s) % len(cams) for s in range(args.steps)]
     for s in range(args.warmup):
         step(s % len(cams))
     torch.cuda.synchronize()
+    # per-kernel split: one untimed pass over the same views with every kernel bracketed by CUDA
+    # events (pgsag_timing_*); it names the dominant kernel
+    L.timing_filter(None)
+    L.timing_enable(True)
+    L.timing_collect()
+    for v in views:
+        step(v)
+    torch.cuda.synchronize()
+    L.timing_enable(False)
+    ksplit = L.timing_collect()
+    dom = max(ksplit.items(), key=lambda kv: kv[1][0])[0] if ksplit else None
     if world > 1:
         dist.barrier()
-    L.timing_enable(True)
+    # the timed region: only the dominant kernel carries an event pair (its live launch time for the
+    # roofline), so the other launches run without event records
+    L.timing_filter(dom)
+    L.timing_enable(dom is not None)
     L.timing_collect()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
@@ -290,7 +311,8 @@ def main():
         if world > 1:
             dist.barrier()
     L.timing_enable(False)
-    ktimes = L.timing_collect()
+    L.timing_filter(None)
+    kdom = L.timing_collect()
     ms = ev0.elapsed_time(ev1)
     per_step = [ev0.elapsed_time(evs[0])] + [evs[k - 1].elapsed_time(evs[k]) for k in range(1, len(evs))]
     pct = lambda q: float(np.percentile(per_step, q))
@@ -314,12 +336,11 @@ def main():
 
     # ---------------------------------------------------- roofline (dominant kernel)
     peaks = measured_peaks()
-    ksteps = {k: (v[0] / args.steps, v[1] // max(args.steps, 1)) for k, v in ktimes.items()}
-    launches = int(sum(v[1] for v in ktimes.values()))
-    dom = max(ktimes.items(), key=lambda kv: kv[1][0])[0] if ktimes else None
+    ksteps = {k: (v[0] / args.steps, v[1] // max(args.steps, 1)) for k, v in ksplit.items()}
+    launches = int(sum(v[1] for v in ksplit.values()))
     roof = None
-    if dom:
-        tot_ms, nl = ktimes[dom]
+    if dom and dom in kdom:
+        tot_ms, nl = kdom[dom]
         avg_s = tot_ms / 1e3 / max(nl, 1)
         E = sum(per_view[v]["evaluated"] for v in views) / len(views)
         B = sum(per_view[v]["blended"] for v in views) / len(views)
@@ -540,6 +561,8 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_raster": e2e_raster, "gpu_launches": launches,
             "train_step": train,
             "kernels_ms_per_step": {k: round(v[0], 4) for k, v in sorted(ksteps.items())},
+            "kernels_split_source": "untimed pass over the same views with every kernel event-bracketed; inside "
+                                    "the timed region only the dominant kernel is (roofline.achieved)",
             "clocks": clk.summary(),
             "per_rank_ms": (rank_table[:, 1].tolist() if world > 1 else [ms]),
             "step_ms_p10_p50_p90": [round(pct(10), 4), round(pct(50), 4), round(pct(90), 4)],

@@ -13,8 +13,8 @@
  *     256-byte aligned).
  *   - All work is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
  *     legacy default stream) in call order.  The only host synchronisations are the
- *     read-back of M (the number of (tile, Gaussian) entries) in pgsag_bin_sort and of
- *     the output counts in pgsag_densify_plan.
+ *     read-back of M (the number of (tile, Gaussian) entries) in pgsag_bin_sort (not in
+ *     pgsag_bin_sort_async) and of the output counts in pgsag_densify_plan.
  *   - Return value: PGSAG_OK (0) or a negative PGSAG_E* code; the message is in
  *     pgsag_last_error() (thread-local).  No exception crosses the ABI.  On error
  *     nothing is guaranteed about the output buffers.
@@ -175,6 +175,15 @@ int pgsag_preprocess(const pgsag_gaussians *g, const pgsag_camera *cam, const ui
 int pgsag_bin_sort(const pgsag_projected *p, const pgsag_tilemask *tm, const pgsag_camera *cam, int32_t n,
                    pgsag_bins *bins, void *ws, size_t ws_bytes, void *stream);
 
+/* A2-A5 without any host synchronisation (same outputs as pgsag_bin_sort when M <= capacity): every
+ * grid is bounded by bins->capacity and the kernels read M on the device.  bins->n_dup is set to -1.
+ * If m_out is non-NULL (pinned host or device memory) M is copied there, stream-ordered, after the
+ * sort; the caller must check it once the stream has passed this point: if M > capacity the lists
+ * are incomplete and the view must be re-sorted with capacity >= M (nothing is written past the
+ * capacity). */
+int pgsag_bin_sort_async(const pgsag_projected *p, const pgsag_tilemask *tm, const pgsag_camera *cam, int32_t n,
+                         pgsag_bins *bins, unsigned long long *m_out, void *ws, size_t ws_bytes, void *stream);
+
 /* A6: per active tile, per masked pixel, front-to-back compositing over the tile's
  * sorted list (Eq. 1-3; alpha = min(0.99, o exp(power)), skip alpha < 1/255,
  * stop when T would drop below 1e-4 — the crossing entry is not blended, R6), then
@@ -320,6 +329,9 @@ const char *pgsag_version(void);
  * returns the kernel name (static storage), the summed milliseconds and the number
  * of launches.  Returns PGSAG_EINVAL for k out of range. */
 void pgsag_timing_enable(int on);
+/* Restrict the timing to kernels whose name starts with prefix (NULL or "" = all), e.g. only
+ * the dominant kernel inside a timed region, so the other launches carry no event records. */
+void pgsag_timing_filter(const char *prefix);
 int pgsag_timing_collect(void);
 int pgsag_timing_get(int k, const char **name, double *ms, long long *launches);
 

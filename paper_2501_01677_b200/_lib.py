@@ -14,8 +14,8 @@ LIB_PATH = os.path.join(HERE, "libpgsag.so")
 PGSAG_OK, PGSAG_EINVAL, PGSAG_ECAPACITY, PGSAG_ECUDA, PGSAG_EWORKSPACE = 0, -1, -2, -3, -4
 F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT, F_LIVE = 1, 2, 4, 8, 15
 
-SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd",
-           "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable",
+SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_bin_sort_async", "pgsag_render_fwd",
+           "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable", "pgsag_timing_filter",
            "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights", "pgsag_boundary_band",
            "pgsag_ban_loss", "pgsag_rgb_loss_workspace_size", "pgsag_rgb_loss", "pgsag_adam_step",
            "pgsag_densify_workspace_size", "pgsag_densify_plan", "pgsag_densify_apply", "pgsag_opacity_reset", "pgsag_microbench_fp32")
@@ -108,12 +108,17 @@ def lib():
             L.pgsag_render_bwd.argtypes = [P(Gaussians), P(Camera), P(Projected), P(Bins), P(TileMask), _vp,
                                            P(C.c_float * 3), P(Image), P(ImageGrad), P(GaussianGrad), _vp,
                                            C.c_size_t, _vp]
-            for nm in ("pgsag_preprocess", "pgsag_bin_sort", "pgsag_render_fwd", "pgsag_render_bwd"):
+            L.pgsag_bin_sort_async.argtypes = [P(Projected), P(TileMask), P(Camera), C.c_int32, P(Bins), _vp, _vp,
+                                               C.c_size_t, _vp]
+            for nm in ("pgsag_preprocess", "pgsag_bin_sort", "pgsag_bin_sort_async", "pgsag_render_fwd",
+                       "pgsag_render_bwd"):
                 getattr(L, nm).restype = C.c_int
             L.pgsag_last_error.restype = C.c_char_p
             L.pgsag_version.restype = C.c_char_p
             L.pgsag_timing_enable.argtypes = [C.c_int]
             L.pgsag_timing_enable.restype = None
+            L.pgsag_timing_filter.argtypes = [C.c_char_p]
+            L.pgsag_timing_filter.restype = None
             L.pgsag_timing_collect.argtypes = []
             L.pgsag_timing_collect.restype = C.c_int
             L.pgsag_timing_get.argtypes = [C.c_int, P(C.c_char_p), P(C.c_double), P(C.c_longlong)]
@@ -153,6 +158,10 @@ def timing_enable(on=True):
     lib().pgsag_timing_enable(1 if on else 0)
 
 
+def timing_filter(prefix=None):
+    lib().pgsag_timing_filter(prefix.encode() if prefix else None)
+
+
 def timing_collect():
     """{kernel name: (total ms, launches)} since the last collect (synchronises on the events)."""
     L = lib()
@@ -183,6 +192,11 @@ def workspace_size(n, W, H, cap):
 def preprocess(g, cam, mask, tm, proj, ws, ws_bytes, stream):
     return check(lib().pgsag_preprocess(C.byref(g), C.byref(cam), mask, C.byref(tm), C.byref(proj), ws,
                                         ws_bytes, stream))
+
+
+def bin_sort_async(proj, tm, cam, n, bins, m_out, ws, ws_bytes, stream):
+    return check(lib().pgsag_bin_sort_async(C.byref(proj), C.byref(tm), C.byref(cam), int(n), C.byref(bins), m_out,
+                                            ws, ws_bytes, stream))
 
 
 def bin_sort(proj, tm, cam, n, bins, ws, ws_bytes, stream):

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <cstring>
 #include <string>
 
 #include "internal.cuh"
@@ -24,6 +25,7 @@ struct TimingRec {
 };
 std::mutex g_tmu;
 bool g_timing = false;
+std::string g_timing_prefix;  // only kernels whose name starts with it ("" = all)
 std::vector<TimingRec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 std::vector<std::pair<const char*, std::pair<double, long long>>> g_agg;
@@ -45,6 +47,7 @@ namespace pgsag {
 KTimer::KTimer(const char* name, cudaStream_t s) : slot(-1), st(s) {
   std::lock_guard<std::mutex> lk(g_tmu);
   if (!g_timing) return;
+  if (!g_timing_prefix.empty() && strncmp(name, g_timing_prefix.c_str(), g_timing_prefix.size()) != 0) return;
   TimingRec r{name, take_event(), take_event()};
   cudaEventRecord(r.a, st);
   g_recs.push_back(r);
@@ -126,6 +129,11 @@ const char* pgsag_version(void) { return "pgsag-b200 0.1 sm_100a"; }
 void pgsag_timing_enable(int on) {
   std::lock_guard<std::mutex> lk(g_tmu);
   g_timing = on != 0;
+}
+
+void pgsag_timing_filter(const char* prefix) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing_prefix = prefix ? prefix : "";
 }
 
 int pgsag_timing_collect(void) {
@@ -210,8 +218,42 @@ int pgsag_bin_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const pgs
   }
   bins->n_dup = (int64_t)M;
   if ((int64_t)M > bins->capacity) return fail(PGSAG_ECAPACITY, "bins capacity < M (bins->n_dup holds M)");
-  e = launch_duplicate_and_sort(p, tm, d, n, (uint32_t)M, ids_sorted, L, w, bins, st);
+  e = launch_duplicate_and_sort(p, tm, d, n, (uint32_t)M, true, ids_sorted, L, w, bins, st);
   if (e != cudaSuccess) return cuda_fail(e, "duplicate / tile sort / ranges");
+  return PGSAG_OK;
+}
+
+int pgsag_bin_sort_async(const pgsag_projected* p, const pgsag_tilemask* tm, const pgsag_camera* cam, int32_t n,
+                         pgsag_bins* bins, unsigned long long* m_out, void* ws, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_cam(cam)) || (rc = check_tm(tm))) return rc;
+  if (n < 0) return fail(PGSAG_EINVAL, "n < 0");
+  if (n > 0 && (rc = check_proj(p))) return rc;
+  if (!bins || !bins->ranges || (bins->capacity > 0 && (!bins->tile_keys || !bins->vals)))
+    return fail(PGSAG_EINVAL, "bins buffer is NULL");
+  if (bins->capacity < 0 || bins->capacity >= (int64_t)kLbMask)
+    return fail(PGSAG_EINVAL, "bins capacity must be in [0, 2^30)");
+  const WsLayout L = ws_layout(n, cam->width, cam->height, bins->capacity);
+  if ((rc = check_ws(ws, ws_bytes, L.total))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Dims d = make_dims(cam->width, cam->height);
+  char* w = static_cast<char*>(ws);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(w + L.counters);
+  cudaError_t e = cudaMemsetAsync(w + L.status1, 0, 4 * (size_t)kMaxSortPasses * L.tiles1 * kMaxRadix, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w + L.scan_status, 0, L.g2d - L.scan_status, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  const uint32_t* ids_sorted = nullptr;
+  if (n > 0) {
+    e = launch_bin_sort_stage1(p, n, L, w, st, &ids_sorted);
+    if (e != cudaSuccess) return cuda_fail(e, "depth sort / scan");
+  }
+  bins->n_dup = -1;  // unknown on the host until the stream reaches the copy below
+  e = launch_duplicate_and_sort(p, tm, d, n, 0u, false, ids_sorted, L, w, bins, st);
+  if (e != cudaSuccess) return cuda_fail(e, "duplicate / tile sort / ranges");
+  if (m_out) {
+    e = cudaMemcpyAsync(m_out, counters + CNT_M, sizeof(unsigned long long), cudaMemcpyDefault, st);
+    if (e != cudaSuccess) return cuda_fail(e, "M copy");
+  }
   return PGSAG_OK;
 }
 

@@ -62,6 +62,7 @@ enum : int {
   CNT_FWD = 9,     // A6 work counter
   CNT_BWD = 10,    // A7 work counter
   CNT_M = 12,      // 2 slots: M as u64 (A2 total)
+  CNT_MC = 14,     // min(M, capacity) as u32 (published by A3)
   CNT_N = 16
 };
 
@@ -82,8 +83,8 @@ cudaError_t launch_preprocess(const pgsag_gaussians* g, const pgsag_camera* cam,
 cudaError_t launch_bin_sort_stage1(const pgsag_projected* p, int n, const WsLayout& L, char* ws,
                                    cudaStream_t st, const uint32_t** ids_sorted);
 cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const Dims& d, int n,
-                                      uint32_t M, const uint32_t* ids_sorted, const WsLayout& L, char* ws,
-                                      pgsag_bins* bins, cudaStream_t st);
+                                      uint32_t M, bool M_known, const uint32_t* ids_sorted, const WsLayout& L,
+                                      char* ws, pgsag_bins* bins, cudaStream_t st);
 cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, const pgsag_tilemask* tm,
                               const Dims& d, const pgsag_camera* cam, const uint8_t* mask, const float bg[3],
                               pgsag_image* out, uint32_t* work_counter, cudaStream_t st);

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
                                                           const uint32_t* __restrict__ n_ptr, uint32_t n_fixed,
                                                           PassPlan plan, uint32_t* __restrict__ ghist) {
   __shared__ uint32_t sh[kMaxSortPasses][kMaxRadix];
-  const uint32_t n = n_ptr ? *n_ptr : n_fixed;
+  const uint32_t n = n_ptr ? min(*n_ptr, n_fixed) : n_fixed;
   for (int k = threadIdx.x; k < kMaxSortPasses * kMaxRadix; k += blockDim.x) (&sh[0][0])[k] = 0;
   __syncthreads();
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
   __shared__ uint32_t s_warp[NW];
   __shared__ uint32_t s_tile;
 
-  const uint32_t n = n_ptr ? *n_ptr : n_fixed;
+  const uint32_t n = n_ptr ? min(*n_ptr, n_fixed) : n_fixed;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   for (int k = tid; k < NW * R; k += kSortThreads) s_whist[k] = 0;
@@ -312,18 +312,24 @@ __global__ void __launch_bounds__(256) scan_kernel(int n, const uint32_t* __rest
 // ----------------------------------------------------------- A3 duplicate
 // Thread per Gaussian in depth order; emits (tile, id) for every active tile of
 // its rect in row-major order starting at offsets[k].
+// cap bounds the writes (sync-free path: M is not known on the host; if M > cap the
+// output is incomplete and the caller retries).  Thread 0 also publishes min(M, cap).
 __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* __restrict__ ids,
                                                          const uint32_t* __restrict__ offsets,
                                                          const uint32_t* __restrict__ touched,
                                                          const short4* __restrict__ rect,
                                                          const uint32_t* __restrict__ bitmap, Dims d,
-                                                         uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals) {
+                                                         uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
+                                                         uint32_t cap, const unsigned long long* __restrict__ M64,
+                                                         uint32_t* __restrict__ m_clamped) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 0) *m_clamped = (uint32_t)min(*M64, (unsigned long long)cap);
   if (k >= n) return;
   const uint32_t id = ids[k];
   if (touched[id] == 0) return;
-  const short4 r = rect[id];
   uint32_t o = offsets[k];
+  if (o + touched[id] > cap) return;
+  const short4 r = rect[id];
   for (int ty = r.y; ty <= r.w; ++ty) {
     const uint32_t* row = bitmap + ty * d.WPR;
     for (int tx = r.x; tx <= r.z; ++tx) {
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
 // -------------------------------------------------------------- A5 ranges
 __global__ void ranges_kernel(const uint32_t* __restrict__ tkeys, const uint32_t* __restrict__ M_ptr,
                               uint32_t* __restrict__ ranges) {
-  const uint32_t M = *M_ptr;
+  const uint32_t M = *M_ptr;  // min(M, capacity) published by A3
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < M; k += gridDim.x * blockDim.x) {
     const uint32_t t = tkeys[k];
     if (k == 0 || tkeys[k - 1] != t) ranges[2 * t] = k;
@@ -460,9 +466,11 @@ cudaError_t launch_bin_sort_stage1(const pgsag_projected* p, int n, const WsLayo
   return cudaGetLastError();
 }
 
+// M_known: the host read M (sync path; grids sized by M).  Otherwise M is only on the device
+// and every grid is bounded by the capacity (sync-free path).
 cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const Dims& d, int n,
-                                      uint32_t M, const uint32_t* ids_sorted, const WsLayout& L, char* ws,
-                                      pgsag_bins* bins, cudaStream_t st) {
+                                      uint32_t M, bool M_known, const uint32_t* ids_sorted, const WsLayout& L,
+                                      char* ws, pgsag_bins* bins, cudaStream_t st) {
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + L.counters);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist) + kMaxSortPasses * kMaxRadix;
   const int ntiles = d.TX * d.TY;
@@ -479,25 +487,29 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
     ok = bins->tile_keys; ov = bins->vals;
   }
   cudaMemsetAsync(bins->ranges, 0, sizeof(uint32_t) * 2 * (size_t)ntiles, st);
-  if (M == 0) return cudaGetLastError();
+  const uint32_t bound = M_known ? M : (uint32_t)bins->capacity;  // grid bound
+  if (bound == 0 || n == 0) return cudaGetLastError();
+  uint32_t* m_clamped = counters + CNT_MC;
   {
     KTimer kt_("A3_duplicate", st);
     duplicate_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, ids_sorted, reinterpret_cast<uint32_t*>(ws + L.offsets),
                                                       p->tiles_touched, reinterpret_cast<const short4*>(p->rect),
-                                                      tm->active_bits, d, ek, ev);
+                                                      tm->active_bits, d, ek, ev, (uint32_t)bins->capacity,
+                                                      reinterpret_cast<const unsigned long long*>(counters + CNT_M),
+                                                      m_clamped);
   }
   bool in_a = true;
-  // look-back state for exactly the tiles this M needs
-  const size_t stride = (size_t)((M + kSortTile - 1) / kSortTile) * kMaxRadix;
+  // look-back state for exactly the tiles the bound needs
+  const size_t stride = (size_t)((bound + kSortTile - 1) / kSortTile) * kMaxRadix;
   cudaMemsetAsync(ws + L.status2, 0, 4 * stride * (size_t)npass, st);
-  cudaError_t e = radix_sort(ek, ev, ok, ov, nullptr, M, M, tile_bits,
+  cudaError_t e = radix_sort(ek, ev, ok, ov, m_clamped, bound, bound, tile_bits,
                              reinterpret_cast<uint32_t*>(ws + L.status2), stride, hist,
                              counters + CNT_SORT2, st, &in_a);
   if (e != cudaSuccess) return e;
-  const int grid = min((int)((M + 255) / 256), num_sms() * 8);
+  const int grid = min((int)((bound + 255) / 256), num_sms() * 8);
   {
     KTimer kt_("A5_ranges", st);
-    ranges_kernel<<<grid, 256, 0, st>>>(bins->tile_keys, counters + CNT_M, bins->ranges);
+    ranges_kernel<<<grid, 256, 0, st>>>(bins->tile_keys, m_clamped, bins->ranges);
   }
   return cudaGetLastError();
 }

@@ -71,8 +71,12 @@ class Rasterizer:
     """Buffers for one (n, width, height, sh_degree) problem; reusable across views."""
 
     def __init__(self, n, width, height, sh_degree=3, capacity=None, device="cuda", counters=True, sat=True,
-                 absgrad=False):
+                 absgrad=False, sync_free=False):
+        """sync_free: use pgsag_bin_sort_async (no host synchronisation per view; M is read back
+        lazily and check_capacity() re-sorts a view whose M exceeded the capacity)."""
         self.want_sat = bool(sat)
+        self.sync_free = bool(sync_free)
+        self._m_host = torch.zeros(1, dtype=torch.int64, pin_memory=torch.cuda.is_available())
         self.want_absgrad = bool(absgrad)
         self.n, self.W, self.H, self.deg = int(n), int(width), int(height), int(sh_degree)
         self.device = torch.device(device)
@@ -213,6 +217,14 @@ class Rasterizer:
             self.counters.zero_()
         ws = C.c_void_p(self.ws.data_ptr())
         L.preprocess(self._g, cam, C.c_void_p(mask.data_ptr()), self._tm, self._proj, ws, self.ws_bytes, st)
+        if self.sync_free:
+            L.bin_sort_async(self._proj, self._tm, cam, self.n, self._bins, C.c_void_p(self._m_host.data_ptr()), ws,
+                             self.ws_bytes, st)
+            self.M = None  # known after the stream passes the sort: see check_capacity()
+            L.render_fwd(self._proj, self._bins, self._tm, cam, C.c_void_p(mask.data_ptr()), self._bg, self._img,
+                         ws, self.ws_bytes, st)
+            return dict(C=self.img_C, N=self.img_N, D=self.img_D, A=self.img_A, Dep=self.img_Dep, T=self.img_T,
+                        g=self.img_g, last=self.img_last)
         rc = L.bin_sort(self._proj, self._tm, cam, self.n, self._bins, ws, self.ws_bytes, st)
         if rc == L.PGSAG_ECAPACITY:
             self._alloc_bins(int(self._bins.n_dup * 1.25) + 1024)
@@ -244,6 +256,19 @@ class Rasterizer:
         if self._grad.grad2d:
             out["grad2d"] = self.grad2d
         return out
+
+    def check_capacity(self) -> bool:
+        """sync_free mode: after synchronising, True if the last view's M fitted the capacity; otherwise
+        grows the entry buffers (the caller re-runs that view)."""
+        if not self.sync_free:
+            return True
+        torch.cuda.current_stream().synchronize()
+        self.M = int(self._m_host.item())
+        if self.M <= self.capacity:
+            return True
+        self._alloc_bins(int(self.M * 1.25) + 1024)
+        self._build_structs()
+        return False
 
     def stats(self):
         c = self.counters.tolist() if self.counters is not None else [0, 0, 0, 0]

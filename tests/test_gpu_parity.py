@@ -223,3 +223,28 @@ def test_counting_and_timed_variants_agree():
         assert np.array_equal(a["img"][k], b["img"][k]), k
     ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=per)
     compare_grads(b["grads"], ora["grads"], sc.gaussians.sh_degree)
+
+
+def test_sync_free_bin_sort():
+    """pgsag_bin_sort_async (no host synchronisation) gives bitwise the same lists, ranges and images
+    as pgsag_bin_sort; with a too-small capacity the overflow is detected afterwards and the view
+    re-sorted after growing the buffers."""
+    from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+    sc = ragged_scene()
+    H, W = sc.mask.shape
+    g = GaussianTensors.from_numpy(sc.gaussians)
+    cam = camera_from(sc.camera)
+    mask = torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda()
+    ref = Rasterizer(g.n, W, H, g.sh_degree)
+    ref.forward(g, cam, mask)
+    fast = Rasterizer(g.n, W, H, g.sh_degree, capacity=16, sync_free=True)
+    fast.forward(g, cam, mask)
+    assert not fast.check_capacity() and fast.M == ref.M  # overflow detected, buffers grown
+    fast.forward(g, cam, mask)
+    assert fast.check_capacity() and fast.M == ref.M
+    torch.cuda.synchronize()
+    M = ref.M
+    assert torch.equal(fast.vals[:M], ref.vals[:M]) and torch.equal(fast.tile_keys[:M], ref.tile_keys[:M])
+    assert torch.equal(fast.ranges, ref.ranges)
+    for k in ("img_C", "img_N", "img_D", "img_T", "img_g", "img_last", "img_Dep"):
+        assert torch.equal(getattr(fast, k), getattr(ref, k)), k
