@@ -312,6 +312,12 @@ __global__ void __launch_bounds__(256) scan_kernel(int n, const uint32_t* __rest
 // ----------------------------------------------------------- A3 duplicate
 // Thread per Gaussian in depth order; emits (tile, id) for every active tile of
 // its rect in row-major order starting at offsets[k].
+constexpr int kDupSmall = 16;  // rect tiles a lane emits on its own
+
+// Warp-cooperative for large splats: a warp takes 32 consecutive Gaussians (depth order) and emits them one
+// after the other, its 32 lanes walking the Gaussian's rect in row-major chunks of 32 tiles and
+// compacting the active ones with a ballot, so every entry run is written coalesced and a
+// large splat is spread over 32 lanes instead of one thread.
 // cap bounds the writes (sync-free path: M is not known on the host; if M > cap the
 // output is incomplete and the caller retries).  Thread 0 also publishes min(M, cap).
 __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* __restrict__ ids,
@@ -323,21 +329,63 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
                                                          uint32_t cap, const unsigned long long* __restrict__ M64,
                                                          uint32_t* __restrict__ m_clamped) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
   if (k == 0) *m_clamped = (uint32_t)min(*M64, (unsigned long long)cap);
-  if (k >= n) return;
-  const uint32_t id = ids[k];
-  if (touched[id] == 0) return;
-  uint32_t o = offsets[k];
-  if (o + touched[id] > cap) return;
-  const short4 r = rect[id];
-  for (int ty = r.y; ty <= r.w; ++ty) {
-    const uint32_t* row = bitmap + ty * d.WPR;
-    for (int tx = r.x; tx <= r.z; ++tx) {
-      if ((__ldg(row + (tx >> 5)) >> (tx & 31)) & 1u) {
-        tkeys[o] = (uint32_t)(ty * d.TX + tx);
-        tvals[o] = id;
-        ++o;
+  uint32_t id = 0, cnt = 0, o = 0;
+  short4 r = make_short4(0, 0, -1, -1);
+  if (k < n) {
+    id = ids[k];
+    cnt = touched[id];
+    if (cnt) {
+      o = offsets[k];
+      if (o + cnt > cap) cnt = 0;  // would overflow: skip (the caller sees M > cap)
+      else r = rect[id];
+    }
+  }
+  // small rects (<= kDupSmall tiles): the lane emits its own entries
+  const int area0 = (r.z - r.x + 1) * (r.w - r.y + 1);
+  const bool big = cnt != 0 && area0 > kDupSmall;
+  if (cnt != 0 && !big) {
+    uint32_t oo = o;
+    for (int ty = r.y; ty <= r.w; ++ty) {
+      const uint32_t* row = bitmap + ty * d.WPR;
+      for (int tx = r.x; tx <= r.z; ++tx) {
+        if ((__ldg(row + (tx >> 5)) >> (tx & 31)) & 1u) {
+          tkeys[oo] = (uint32_t)(ty * d.TX + tx);
+          tvals[oo] = id;
+          ++oo;
+        }
       }
+    }
+  }
+  // large rects: the whole warp, one Gaussian at a time
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t todo = __ballot_sync(0xffffffffu, big);
+  while (todo) {
+    const int j = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t gid = __shfl_sync(0xffffffffu, id, j);
+    const uint32_t go = __shfl_sync(0xffffffffu, o, j);
+    const int x0 = __shfl_sync(0xffffffffu, (int)r.x, j), y0 = __shfl_sync(0xffffffffu, (int)r.y, j);
+    const int x1 = __shfl_sync(0xffffffffu, (int)r.z, j), y1 = __shfl_sync(0xffffffffu, (int)r.w, j);
+    const int w = x1 - x0 + 1, area = w * (y1 - y0 + 1);
+    uint32_t written = 0;
+    for (int t0 = 0; t0 < area; t0 += 32) {
+      const int t = t0 + lane;
+      bool act = false;
+      uint32_t tile = 0;
+      if (t < area) {
+        const int ty = y0 + t / w, tx = x0 + (t - (t / w) * w);
+        act = (__ldg(bitmap + ty * d.WPR + (tx >> 5)) >> (tx & 31)) & 1u;
+        tile = (uint32_t)(ty * d.TX + tx);
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        const uint32_t pos = go + written + __popc(bal & lt);
+        tkeys[pos] = tile;
+        tvals[pos] = gid;
+      }
+      written += __popc(bal);
     }
   }
 }
