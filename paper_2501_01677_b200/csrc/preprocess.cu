@@ -159,8 +159,9 @@ __device__ __forceinline__ float lnup(float y) {
   return (e * 0.6931471805599453f + (f * (6.0f + f)) / (6.0f + 4.0f * f)) + 3.814697265625e-06f;
 }
 
+template <int DEG>
 __global__ void __launch_bounds__(256) preprocess_kernel(
-    int n, int deg, const float* __restrict__ mean, const float* __restrict__ scale,
+    int n, const float* __restrict__ mean, const float* __restrict__ scale,
     const float* __restrict__ rot, const float* __restrict__ opac, const float* __restrict__ sh, CamK cam,
     Dims d, const uint32_t* __restrict__ bits, float2* __restrict__ mean2d, float4* __restrict__ conic_o,
     float* __restrict__ depth, short4* __restrict__ rect, uint32_t* __restrict__ tiles_touched,
@@ -276,10 +277,14 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         }
         // flattened-Gaussian normal (R4) and plane distance (Eq. 3, R2)
         int k = 0;
-        if (s[1] < s[k]) k = 1;
-        if (s[2] < s[k]) k = 2;
+        float smin = s[0];
+        if (s[1] < smin) { k = 1; smin = s[1]; }
+        if (s[2] < smin) k = 2;
         fl |= (uint32_t)k << PGSAG_F_AXIS_SHIFT;
-        float n0 = Rg[0][k], n1 = Rg[1][k], n2 = Rg[2][k];
+        // (selects, not a dynamic index: keeps Rg in registers)
+        float n0 = k == 0 ? Rg[0][0] : (k == 1 ? Rg[0][1] : Rg[0][2]);
+        float n1 = k == 0 ? Rg[1][0] : (k == 1 ? Rg[1][1] : Rg[1][2]);
+        float n2 = k == 0 ? Rg[2][0] : (k == 1 ? Rg[2][1] : Rg[2][2]);
         const float dotv = (n0 * t0 + n1 * t1) + n2 * t2;
         if (dotv > 0.0f) { n0 = -n0; n1 = -n1; n2 = -n2; fl |= PGSAG_F_NFLIP; }
         nc.x = (Rc[0] * n0 + Rc[1] * n1) + Rc[2] * n2;
@@ -307,12 +312,18 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         Y[13] = (kShC3[4] * dx) * ((4.0f * zz - xx) - yy);
         Y[14] = (kShC3[5] * dz) * (xx - yy);
         Y[15] = (kShC3[6] * dx) * (xx - 3.0f * yy);
-        const int K = (deg + 1) * (deg + 1);
+        constexpr int K = (DEG + 1) * (DEG + 1);
+        // SH coefficients: all loads issued up front (compile-time degree), then the same
+        // left-to-right sums as the oracle
+        float shv[3 * K];
+#pragma unroll
+        for (int q = 0; q < 3 * K; ++q) shv[q] = __ldg(sh + (size_t)q * n + i);
         float col[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          float acc = Y[0] * __ldg(sh + (size_t)c * n + i);
-          for (int l = 1; l < K; ++l) acc = acc + Y[l] * __ldg(sh + (size_t)(l * 3 + c) * n + i);
+          float acc = Y[0] * shv[c];
+#pragma unroll
+          for (int l = 1; l < K; ++l) acc = acc + Y[l] * shv[l * 3 + c];
           acc = acc + 0.5f;
           if (acc < 0.0f) { acc = 0.0f; fl |= PGSAG_F_RGB_CLAMP0 << c; }
           col[c] = acc;
@@ -372,11 +383,19 @@ cudaError_t launch_preprocess(const pgsag_gaussians* g, const pgsag_camera* c, c
   const int threads = 256;
   {
     KTimer kt_("A1_preprocess", st);
-    preprocess_kernel<<<(g->n + threads - 1) / threads, threads, 0, st>>>(
-        g->n, g->sh_degree, g->mean, g->scale, g->rot, g->opacity, g->sh, k, d, tm->active_bits,
-        reinterpret_cast<float2*>(out->mean2d), reinterpret_cast<float4*>(out->conic_o), out->depth,
-        reinterpret_cast<short4*>(out->rect), out->tiles_touched, reinterpret_cast<float4*>(out->rgb_d),
-        reinterpret_cast<float4*>(out->ncam), out->flags);
+#define PGSAG_A1(DEG)                                                                                      \
+  preprocess_kernel<DEG><<<(g->n + threads - 1) / threads, threads, 0, st>>>(                              \
+      g->n, g->mean, g->scale, g->rot, g->opacity, g->sh, k, d, tm->active_bits,                           \
+      reinterpret_cast<float2*>(out->mean2d), reinterpret_cast<float4*>(out->conic_o), out->depth,         \
+      reinterpret_cast<short4*>(out->rect), out->tiles_touched, reinterpret_cast<float4*>(out->rgb_d),     \
+      reinterpret_cast<float4*>(out->ncam), out->flags)
+    switch (g->sh_degree) {
+      case 0: PGSAG_A1(0); break;
+      case 1: PGSAG_A1(1); break;
+      case 2: PGSAG_A1(2); break;
+      default: PGSAG_A1(3); break;
+    }
+#undef PGSAG_A1
   }
   return cudaGetLastError();
 }
