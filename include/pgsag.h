@@ -141,6 +141,10 @@ typedef struct {
 typedef struct {
   const float *dC, *dN, *dD, *dA, *dDep;
   float gc_lambda;
+  /* optional device scalar: if non-NULL, dN and dDep are divided by *nd_div (multiplied by 0 when
+   * *nd_div <= 0), e.g. the term count of a mean loss whose sum-gradient was written in one pass
+   * (pgsag_ban_loss with mean = 0). */
+  const double *nd_div;
 } pgsag_image_grad;
 
 /* A8 output, same layouts as pgsag_gaussians; OVERWRITTEN (not accumulated).  Rows of dsh
@@ -222,7 +226,9 @@ int pgsag_boundary_band(const uint8_t *mask, int32_t width, int32_t height, int3
  * elsewhere in the mask.  loss (device, double[2], zeroed by the call) receives
  * (sum of terms, number of terms).  If dN ([3][H][W]) / dDep ([H][W]) are non-NULL the call
  * ADDS lambda * d(S)/dN, lambda * d(S)/dDep, with S = sum (mean = 0) or sum / count (mean = 1),
- * ready to be passed as upstream to pgsag_render_bwd.  N and Dep are A6 outputs. */
+ * ready to be passed as upstream to pgsag_render_bwd.  N and Dep are A6 outputs.  mean = 0 takes
+ * one pass over the image (mean = 1 two); the gradient of the mean is then obtained in A7 by
+ * pointing pgsag_image_grad.nd_div at loss + 1. */
 int pgsag_ban_loss(const pgsag_camera *cam, const uint8_t *mask, const uint8_t *band, const float *N,
                    const float *Dep, float boundary_w, float lambda, int32_t mean, double *loss, float *dN,
                    float *dDep, void *stream);

@@ -54,7 +54,8 @@ class Image(C.Structure):
 
 
 class ImageGrad(C.Structure):
-    _fields_ = [("dC", _vp), ("dN", _vp), ("dD", _vp), ("dA", _vp), ("dDep", _vp), ("gc_lambda", C.c_float)]
+    _fields_ = [("dC", _vp), ("dN", _vp), ("dD", _vp), ("dA", _vp), ("dDep", _vp), ("gc_lambda", C.c_float),
+                ("nd_div", _vp)]
 
 
 class GaussianGrad(C.Structure):

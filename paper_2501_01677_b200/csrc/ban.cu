@@ -91,41 +91,42 @@ __device__ __forceinline__ void ban_term(const BanArgs& A, int x, int y, BanTerm
   t.valid = true;
 }
 
-__global__ void __launch_bounds__(256) ban_loss_kernel(BanArgs A) {
+// kLoss: accumulate (sum of terms, count) into loss[0..1]; kGrad: scatter lambda s dL/d(N, Dep)
+// with s = 1 / loss[1] (mean, needs a finished loss pass) or 1 (sum).  mean = 0 runs both in
+// one pass.
+template <bool kLoss, bool kGrad>
+__global__ void __launch_bounds__(256) ban_kernel(BanArgs A) {
   __shared__ float s_r[8][2];
   const int x = blockIdx.x * 32 + (threadIdx.x & 31), y = blockIdx.y * 8 + (threadIdx.x >> 5);
   float sum = 0.f, cnt = 0.f;
-  if (x < A.W && y < A.H && __ldg(A.mask + (size_t)y * A.W + x)) {
-    BanTerm t;
-    ban_term(A, x, y, t);
+  BanTerm t;
+  t.valid = false;
+  if (x < A.W && y < A.H && __ldg(A.mask + (size_t)y * A.W + x)) ban_term(A, x, y, t);
+  if (kLoss) {
     if (t.valid) {
       sum = t.w * (t.e[0] * t.e[0] + t.e[1] * t.e[1] + t.e[2] * t.e[2]);
       cnt = 1.f;
     }
-  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if ((threadIdx.x & 31) == 0) { s_r[threadIdx.x >> 5][0] = sum; s_r[threadIdx.x >> 5][1] = cnt; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0, c = 0.0;
+      for (int k = 0; k < 8; ++k) { s += s_r[k][0]; c += s_r[k][1]; }
+      if (c > 0.0) { atomicAdd(A.loss, s); atomicAdd(A.loss + 1, c); }
+    }
   }
-  if ((threadIdx.x & 31) == 0) { s_r[threadIdx.x >> 5][0] = sum; s_r[threadIdx.x >> 5][1] = cnt; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0, c = 0.0;
-    for (int k = 0; k < 8; ++k) { s += s_r[k][0]; c += s_r[k][1]; }
-    if (c > 0.0) { atomicAdd(A.loss, s); atomicAdd(A.loss + 1, c); }
+  if (!kGrad || !t.valid) return;
+  float sc = A.lambda;
+  if (A.mean) {
+    const double c = A.loss[1];
+    if (c <= 0.0) return;
+    sc *= (float)(1.0 / c);
   }
-}
-
-__global__ void __launch_bounds__(256) ban_grad_kernel(BanArgs A) {
-  const int x = blockIdx.x * 32 + (threadIdx.x & 31), y = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (x >= A.W || y >= A.H || !__ldg(A.mask + (size_t)y * A.W + x)) return;
-  const double cnt = A.loss[1];
-  if (cnt <= 0.0) return;
-  BanTerm t;
-  ban_term(A, x, y, t);
-  if (!t.valid) return;
-  const float sc = A.lambda * (A.mean ? (float)(1.0 / cnt) : 1.0f);
   const size_t HW = (size_t)A.W * A.H, p = (size_t)y * A.W + x;
   float gnd[3];
 #pragma unroll
@@ -176,13 +177,19 @@ cudaError_t launch_ban_loss(const pgsag_camera* cam, const uint8_t* mask, const 
   A.loss = loss; A.dN = dN; A.dDep = dDep;
   cudaMemsetAsync(loss, 0, 2 * sizeof(double), st);
   const dim3 grid((A.W + 31) / 32, (A.H + 7) / 8);
+  const bool grads = dN || dDep;
+  if (grads && !mean) {  // sum: loss and gradients in one pass
+    KTimer kt_("N2_ban_fused", st);
+    ban_kernel<true, true><<<grid, 256, 0, st>>>(A);
+    return cudaGetLastError();
+  }
   {
     KTimer kt_("N2_ban_loss", st);
-    ban_loss_kernel<<<grid, 256, 0, st>>>(A);
+    ban_kernel<true, false><<<grid, 256, 0, st>>>(A);
   }
-  if (dN || dDep) {
+  if (grads) {  // mean: the gradient pass needs the finished count
     KTimer kt_("N2_ban_grad", st);
-    ban_grad_kernel<<<grid, 256, 0, st>>>(A);
+    ban_kernel<false, true><<<grid, 256, 0, st>>>(A);
   }
   return cudaGetLastError();
 }

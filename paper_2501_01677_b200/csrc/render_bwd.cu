@@ -59,6 +59,7 @@ struct BwdArgs {
   const float *N, *D, *T;
   const int32_t *g, *last;
   const float *dC, *dN, *dD, *dA, *dDep;
+  const double* nd_div;  // optional: dN, dDep divided by *nd_div
   double* g2d;  // [kG2][n]
   int n;
   unsigned long long* counters;
@@ -133,7 +134,13 @@ __device__ __forceinline__ void load_pixel(const BwdArgs& a, bool masked, size_t
   s.G[3] = ld_or0(a.dN, pix); s.G[4] = ld_or0(a.dN, HW + pix); s.G[5] = ld_or0(a.dN, 2 * HW + pix);
   s.G[6] = ld_or0(a.dD, pix);
   s.G[7] = ld_or0(a.dA, pix);
-  const float gDep = ld_or0(a.dDep, pix);
+  float gDep = ld_or0(a.dDep, pix);
+  if (a.nd_div) {  // sum-gradient of a mean loss: divide by its term count
+    const double dv = *a.nd_div;
+    const float sc = dv > 0.0 ? (float)(1.0 / dv) : 0.0f;
+    s.G[3] *= sc; s.G[4] *= sc; s.G[5] *= sc;
+    gDep *= sc;
+  }
   // Eq. 4 prologue: Dep = D / (N . r); validity re-derived exactly as A6 did
   const float N0 = a.N[pix], N1 = a.N[HW + pix], N2 = a.N[2 * HW + pix];
   const float r0 = __fdiv_rn(__fsub_rn(px, a.cx), a.fx), r1 = __fdiv_rn(__fsub_rn(py, a.cy), a.fy);
@@ -426,6 +433,7 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
   a.bg0 = bg[0]; a.bg1 = bg[1]; a.bg2 = bg[2];
   a.N = fwd->N; a.D = fwd->D; a.T = fwd->T; a.g = fwd->g; a.last = fwd->last;
   a.dC = dL->dC; a.dN = dL->dN; a.dD = dL->dD; a.dA = dL->dA; a.dDep = dL->dDep;
+  a.nd_div = dL->nd_div;
   a.g2d = g2d;
   a.n = n;
   a.counters = fwd->counters;

@@ -238,9 +238,11 @@ class Rasterizer:
         return dict(C=self.img_C, N=self.img_N, D=self.img_D, A=self.img_A, Dep=self.img_Dep, T=self.img_T,
                     g=self.img_g, last=self.img_last)
 
-    def backward(self, dC=None, dN=None, dD=None, dA=None, dDep=None, gc_lambda=0.0):
+    def backward(self, dC=None, dN=None, dD=None, dA=None, dDep=None, gc_lambda=0.0, nd_div=None):
+        """nd_div: optional device float64 scalar dividing dN and dDep (pgsag_image_grad.nd_div)."""
         ig = L.ImageGrad()
         ig.gc_lambda = float(gc_lambda)
+        ig.nd_div = None if nd_div is None else nd_div.data_ptr()
         for k, t in (("dC", dC), ("dN", dN), ("dD", dD), ("dA", dA), ("dDep", dDep)):
             if t is not None:
                 assert t.dtype == torch.float32 and t.is_contiguous() and t.device == self.device

@@ -109,13 +109,16 @@ class Trainer:
         if self.used_ban:
             self.dN.zero_()
             self.dDep.zero_()
-            L.ban_loss(cam, p(mask), p(band), p(r.img_N), p(r.img_Dep), self.bw, (1.0 - self.lam) * self.lam4, 1,
+            # one pass: loss sums + the gradient of the SUM; A7 divides dN / dDep by the term count
+            # (pgsag_image_grad.nd_div), which makes it the gradient of the mean (R27)
+            L.ban_loss(cam, p(mask), p(band), p(r.img_N), p(r.img_Dep), self.bw, (1.0 - self.lam) * self.lam4, 0,
                        p(self.loss_ban), p(self.dN), p(self.dDep), st)
         self.used_gc = gc_w is not None
         r._grad.densify_accum, r._grad.densify_count = self.accum.data_ptr(), self.count.data_ptr()
         try:
             r.backward(dC=self.dC, dN=self.dN if self.used_ban else None, dDep=self.dDep if self.used_ban else None,
-                       gc_lambda=self.lam if self.used_gc else 0.0)
+                       gc_lambda=self.lam if self.used_gc else 0.0,
+                       nd_div=self.loss_ban[1:] if self.used_ban else None)
         finally:
             r._grad.densify_accum = r._grad.densify_count = None
         if dp_group is not None:

@@ -63,17 +63,19 @@ def test_ban_loss_and_gradients(name):
 
 
 @pytest.mark.parametrize("name", list(SCENES))
-def test_ban_chained_into_backward(name):
+@pytest.mark.parametrize("one_pass", [False, True])
+def test_ban_chained_into_backward(name, one_pass):
     """lambda_4 L_ban as the whole loss: its dN, dDep as A7's upstream; parameter gradients vs the
     oracle backward fed with the oracle's own L_ban gradients (depth upstream dropped where Eq. 4
-    is ill-conditioned, R19)."""
+    is ill-conditioned, R19).  one_pass: the sum-gradient written in one pass (mean = 0) and
+    divided by the term count inside A7 (pgsag_image_grad.nd_div)."""
     sc = SCENES[name]()
     g, r, mask = _render(sc)
     band = r.boundary_band(mask, 1)
     H, W = sc.mask.shape
     dN = torch.zeros(3, H, W, device="cuda")
     dD = torch.zeros(H, W, device="cuda")
-    r.ban_loss(band, lam=0.01, dN=dN, dDep=dD)
+    loss = r.ban_loss(band, lam=0.01, mean=not one_pass, dN=dN, dDep=dD)
     torch.cuda.synchronize()
     pix = all_pixels(sc.mask)
     ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix)
@@ -89,7 +91,8 @@ def test_ban_chained_into_backward(name):
     rNf[:, pix[ora0["near"].astype(bool)]] = 0.0
     dNg = dN.reshape(3, -1)
     dNg[:, torch.from_numpy(pix[ora0["near"].astype(bool)]).cuda()] = 0.0
-    grads = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in r.backward(dN=dN, dDep=dD).items()}
+    out = r.backward(dN=dN, dDep=dD, nd_div=loss[1:] if one_pass else None)
+    grads = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in out.items()}
     up = np.zeros((len(pix), 10))
     up[:, 3:6] = rN.reshape(3, -1)[:, pix].T
     up[:, 8] = rD.reshape(-1)[pix]
