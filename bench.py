@@ -480,8 +480,10 @@ def main():
                      "last_loss": {k: round(float(x), 6) for k, x in lo.items()}}
             del extras
         if not args.no_e2e:
-            htgt = tgt.cpu().pin_memory()
+            # the photo as captured: 8-bit interleaved RGB (pgsag_unpack_rgb8 makes the float planes)
+            htgt = (tgt * 255.0).round().to(torch.uint8).permute(1, 2, 0).contiguous().cpu().pin_memory()
             hmask = [m.cpu().pin_memory() for m in masks]
+            dt8 = [torch.empty(H, W, 3, dtype=torch.uint8, device=dev) for _ in range(2)]
             dt = [torch.empty_like(tgt) for _ in range(2)]
             dm = [torch.empty_like(masks[0]) for _ in range(2)]
             hloss = torch.empty(kt, 6, dtype=torch.float64, pin_memory=True)
@@ -493,7 +495,7 @@ def main():
             def fetch(slot, v):
                 with torch.cuda.stream(cs):
                     cs.wait_event(free[slot])
-                    dt[slot].copy_(htgt, non_blocking=True)
+                    dt8[slot].copy_(htgt, non_blocking=True)
                     dm[slot].copy_(hmask[v], non_blocking=True)
                     ready[slot].record(cs)
 
@@ -510,6 +512,7 @@ def main():
                 if s_ + 1 < kt:
                     fetch(cur ^ 1, tviews[s_ + 1])
                 main.wait_event(ready[cur])
+                L.unpack_rgb8(dt8[cur].data_ptr(), W, H, dt[cur].data_ptr(), main.cuda_stream)
                 tr.step(ccam[v], dm[cur], dt[cur], gc_w=r.gc_weights(dt[cur], dm[cur]),
                         band=r.boundary_band(dm[cur], 1))
                 hloss[s_].copy_(tr.loss_rgb, non_blocking=True)
@@ -519,11 +522,12 @@ def main():
             ems = dmax(e0.elapsed_time(e1))
             epix = dsum(float(sum(npix[v] for v in tviews)))
             e2e = {"value": epix / 1e6 / (ems / 1e3), "unit": UNIT,
-                   "h2d_bytes_per_step": int(htgt.numel() * 4 + hmask[0].numel()),
+                   "h2d_bytes_per_step": int(htgt.numel() + hmask[0].numel()),
                    "d2h_bytes_per_step": int(hloss[0].numel() * 8), "steps": kt,
-                   "note": "train.Trainer.step per view: pinned host target photo (3xHxW f32) + building mask "
-                           "-> device (copy stream, prefetched), A0-A8 + L_rgb + L_ban + L_GC-load + L_s/Adam, "
-                           "loss terms -> host; Gaussians and optimiser state are resident model state"}
+                   "note": "train.Trainer.step per view: pinned host photo (8-bit HxWx3) + building mask -> device "
+                           "(copy stream, prefetched), pgsag_unpack_rgb8, Eq. 9 weights + boundary band, A0-A8 + "
+                           "L_rgb + L_ban + L_GC-load + L_s/Adam, loss terms -> host; Gaussians and optimiser state "
+                           "are resident model state"}
         del tr, gt_
 
     # ------------------------------------------------------------- CPU oracle baseline

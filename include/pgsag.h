@@ -239,6 +239,11 @@ int pgsag_ban_loss(const pgsag_camera *cam, const uint8_t *mask, const uint8_t *
  * are out of scope.  The driver composes: A0-A6 -> pgsag_rgb_loss (+ pgsag_ban_loss)
  * -> A7/A8 (gc_lambda = lambda) -> pgsag_adam_step. */
 
+/* The photo as captured: 8-bit interleaved RGB rgb8[H][W][3] -> image[3][H][W] float in [0, 1]
+ * (b / 255 correctly rounded), the layout pgsag_rgb_loss / pgsag_gc_weights take.  rgb8 4-byte and
+ * image 16-byte aligned, W*H a multiple of 4. */
+int pgsag_unpack_rgb8(const uint8_t *rgb8, int32_t width, int32_t height, float *image, void *stream);
+
 /* Scratch bytes for pgsag_rgb_loss on a width x height image (36 W H). */
 size_t pgsag_rgb_loss_workspace_size(int32_t width, int32_t height);
 

@@ -18,7 +18,7 @@ SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_
            "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable", "pgsag_timing_filter",
            "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights", "pgsag_boundary_band",
            "pgsag_ban_loss", "pgsag_rgb_loss_workspace_size", "pgsag_rgb_loss", "pgsag_adam_step",
-           "pgsag_densify_workspace_size", "pgsag_densify_plan", "pgsag_densify_apply", "pgsag_opacity_reset", "pgsag_microbench_fp32")
+           "pgsag_densify_workspace_size", "pgsag_densify_plan", "pgsag_densify_apply", "pgsag_opacity_reset", "pgsag_microbench_fp32", "pgsag_unpack_rgb8")
 
 _vp = C.c_void_p
 
@@ -151,6 +151,8 @@ def lib():
             L.pgsag_opacity_reset.restype = C.c_int
             L.pgsag_microbench_fp32.argtypes = [C.c_int32, C.c_int32, _vp, P(C.c_double), _vp]
             L.pgsag_microbench_fp32.restype = C.c_int
+            L.pgsag_unpack_rgb8.argtypes = [_vp, C.c_int32, C.c_int32, _vp, _vp]
+            L.pgsag_unpack_rgb8.restype = C.c_int
             _lib = L
     return _lib
 
@@ -275,3 +277,7 @@ def microbench_fp32(mode, iters, scratch, stream):
     out = C.c_double(0.0)
     check(lib().pgsag_microbench_fp32(int(mode), int(iters), scratch, C.byref(out), stream))
     return out.value
+
+
+def unpack_rgb8(rgb8, W, H, image, stream):
+    return check(lib().pgsag_unpack_rgb8(rgb8, int(W), int(H), image, stream))

@@ -427,4 +427,14 @@ int pgsag_microbench_fp32(int32_t mode, int32_t iters, float* scratch, double* t
   return PGSAG_OK;
 }
 
+int pgsag_unpack_rgb8(const uint8_t* rgb8, int32_t width, int32_t height, float* image, void* stream) {
+  if (!rgb8 || !image) return fail(PGSAG_EINVAL, "unpack_rgb8: NULL argument");
+  if (width <= 0 || height <= 0) return fail(PGSAG_EINVAL, "width/height must be > 0");
+  if (!aligned(rgb8, 4) || !aligned(image, 16) || (((size_t)width * height) % 4) != 0)
+    return fail(PGSAG_EINVAL, "unpack_rgb8: rgb8 4-byte and image 16-byte aligned, W*H a multiple of 4");
+  cudaError_t e = launch_unpack_rgb8(rgb8, width, height, image, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "unpack_rgb8");
+  return PGSAG_OK;
+}
+
 }  // extern "C"

@@ -105,6 +105,7 @@ cudaError_t launch_ban_loss(const pgsag_camera* cam, const uint8_t* mask, const 
 
 cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8_t* mask, int W, int H, float weight,
                             double* loss, float* dC, float* abc, cudaStream_t st);
+cudaError_t launch_unpack_rgb8(const uint8_t* rgb, int W, int H, float* chw, cudaStream_t st);
 cudaError_t launch_adam(int n, int sh_degree, const pgsag_gaussian_grad* gr, pgsag_adam_state* s,
                         const pgsag_adam_hparams* hp, double* flat, cudaStream_t st);
 

@@ -465,7 +465,42 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs A) {
   }
 }
 
+// 8-bit interleaved photo [H][W][3] -> planar float [3][H][W] in [0, 1] (b / 255, correctly
+// rounded); 4 pixels (12 bytes, three aligned words) per thread when W allows.
+__global__ void __launch_bounds__(256) unpack_rgb8_kernel(const uint8_t* __restrict__ rgb, size_t npix,
+                                                          float* __restrict__ chw) {
+  const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // group of 4 pixels
+  const size_t p0 = 4 * q;
+  if (p0 >= npix) return;
+  if (p0 + 4 <= npix) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(rgb + 3 * p0);
+    const uint32_t a = __ldg(w), b = __ldg(w + 1), c = __ldg(w + 2);
+    const uint32_t by[12] = {a & 255u, (a >> 8) & 255u, (a >> 16) & 255u, a >> 24, b & 255u, (b >> 8) & 255u,
+                             (b >> 16) & 255u, b >> 24, c & 255u, (c >> 8) & 255u, (c >> 16) & 255u, c >> 24};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      float4 v;
+      v.x = __fdiv_rn((float)by[ch], 255.0f);
+      v.y = __fdiv_rn((float)by[3 + ch], 255.0f);
+      v.z = __fdiv_rn((float)by[6 + ch], 255.0f);
+      v.w = __fdiv_rn((float)by[9 + ch], 255.0f);
+      *reinterpret_cast<float4*>(chw + ch * npix + p0) = v;
+    }
+  } else {
+    for (size_t p = p0; p < npix; ++p)
+      for (int ch = 0; ch < 3; ++ch) chw[ch * npix + p] = __fdiv_rn((float)rgb[3 * p + ch], 255.0f);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_unpack_rgb8(const uint8_t* rgb, int W, int H, float* chw, cudaStream_t st) {
+  const size_t npix = (size_t)W * H;
+  const size_t groups = (npix + 3) / 4;
+  KTimer kt_("N3_unpack_rgb8", st);
+  unpack_rgb8_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, st>>>(rgb, npix, chw);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8_t* mask, int W, int H, float weight,
                             double* loss, float* dC, float* abc, cudaStream_t st) {

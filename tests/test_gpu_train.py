@@ -330,3 +330,16 @@ def test_group_driver_single_rank():
     assert sorted(r["region"] for r in rep) == [0, 1]
     for r in rep:
         assert np.isfinite(r["final_loss"]["total"]) and r["n_gaussians"] > 0 and r["ms"] > 0
+
+
+def test_unpack_rgb8_exact():
+    """8-bit interleaved photo -> planar float: bit-exact with numpy's float32 b / 255."""
+    H, W = 37, 52  # W*H multiple of 4
+    rng = np.random.default_rng(99)
+    rgb = rng.integers(0, 256, (H, W, 3), dtype=np.uint8)
+    src = torch.from_numpy(rgb).cuda()
+    out = torch.empty(3, H, W, device="cuda")
+    L.unpack_rgb8(src.data_ptr(), W, H, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = (rgb.astype(np.float32) / np.float32(255.0)).transpose(2, 0, 1)
+    assert np.array_equal(out.cpu().numpy(), ref)
