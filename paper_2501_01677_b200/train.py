@@ -181,7 +181,8 @@ class Trainer:
                                               opacity=self.g.opacity, sh=self.g.sh, log_scale=self.log_scale,
                                               logit_opacity=self.logit_opacity, m=self.m, v=self.v))
         self.r = Rasterizer(n_out, r.W, r.H, g.sh_degree, capacity=max(1024, capacity_per_gaussian * n_out),
-                            device=dev, counters=r.counters is not None, sat=r.want_sat)
+                            device=dev, counters=r.counters is not None, sat=r.want_sat, absgrad=r.want_absgrad,
+                            sync_free=r.sync_free)
         self._alloc_stats(n_out)
         return tuple(counts)
 
