@@ -378,6 +378,41 @@ def main():
             pass
         roof["share_of_step"] = tot_ms / max(ms, 1e-9)
 
+    # every kernel of the step against its own roof: algorithmic bytes (HBM) or
+    # flops (FP32) per launch / its mean launch time in the split pass
+    rooflines_all = {}
+    if ksplit:
+        Mv = sum(per_view[v]["M"] for v in views) / len(views)
+        Ev = sum(per_view[v]["evaluated"] for v in views) / len(views)
+        Bv = sum(per_view[v]["blended"] for v in views) / len(views)
+        Vv = sum(per_view[v]["bwd_visited"] for v in views) / len(views)
+        n_, px_, tiles_ = g.n, W * H, ((W + 15) // 16) * ((H + 15) // 16)
+        tile_bits = max(1, (tiles_ - 1).bit_length())
+        alg = {  # (bound, units per view over all launches of the kernel)
+            "A0_tilemask_count": ("hbm", px_ + 4 * tiles_),
+            "A1_preprocess": ("hbm", BYTES_A1[g.sh_degree] * n_),
+            "A2_scan": ("hbm", 8 * n_),
+            "A3_duplicate": ("hbm", 8 * Mv + 20 * n_),
+            "A4_radix_onesweep": ("hbm", 4 * 16 * n_ + (2 if tile_bits > 9 else 1) * 16 * Mv),
+            "A4_radix_hist": ("hbm", 4 * n_ + 4 * Mv),
+            "A5_ranges": ("hbm", 4 * Mv + 8 * tiles_),
+            "A6_render_fwd": ("alu", FLOP_EVAL * Ev + FLOP_BLEND_FWD * Bv),
+            "A7_render_bwd": ("alu", FLOP_EVAL * Vv + FLOP_BLEND_BWD * Bv),
+            "A8_preprocess_bwd": ("hbm", 584 * n_),
+        }
+        hbm = float(peaks.get("hbm_gbs", 6551.4))
+        fp32 = SM_COUNT * FP32_LANES * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        for k, (b_, units) in alg.items():
+            if k not in ksteps:
+                continue
+            t_s = ksteps[k][0] / 1e3  # ms per step -> s
+            if b_ == "hbm":
+                a_ = units / t_s / 1e9
+                rooflines_all[k] = {"bound": "hbm", "achieved_gbs": round(a_, 1), "frac": round(a_ / hbm, 4)}
+            else:
+                a_ = units / t_s / 1e12
+                rooflines_all[k] = {"bound": "alu", "achieved_tflops": round(a_, 3), "frac": round(a_ / fp32, 4)}
+
     def dmax(x):  # max over ranks of a device time
         if world > 1:
             t = torch.tensor([x], device=cdev)
@@ -562,7 +597,7 @@ def main():
             "M_per_view": st0["M"], "evaluated_per_view": st0["evaluated"], "blended_per_view": st0["blended"],
             "bwd_visited_per_view": st0["bwd_visited"],
             "flop_per_unit": {"evaluated": FLOP_EVAL, "blended_fwd": FLOP_BLEND_FWD, "blended_bwd": FLOP_BLEND_BWD},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_raster": e2e_raster, "gpu_launches": launches,
+            "roofline": roof, "rooflines_all_kernels": rooflines_all, "cpu_baseline": cpu, "e2e": e2e, "e2e_raster": e2e_raster, "gpu_launches": launches,
             "train_step": train,
             "kernels_ms_per_step": {k: round(v[0], 4) for k, v in sorted(ksteps.items())},
             "kernels_split_source": "untimed pass over the same views with every kernel event-bracketed; inside "
