@@ -265,6 +265,11 @@ def main():
     tb = gt.reshape(gt.shape[0] // 16, 16, gt.shape[1] // 16, 16).sum(dim=(1, 3))
     act = tb[tb > 0]
     imbalance = float(act.max() / act.mean()) if act.numel() else 0.0
+    # SURVEY §8(d) C5 statistics, for every config: entries per active tile (p50 / p99 / max)
+    rl = (r.ranges.view(-1, 2)[:, 1] - r.ranges.view(-1, 2)[:, 0]).double()
+    rl = rl[rl > 0]
+    tile_entries = ([float(torch.quantile(rl, 0.5)), float(torch.quantile(rl, 0.99)), float(rl.max())]
+                    if rl.numel() else [0.0, 0.0, 0.0])
     r._img.counters = None  # timed steps run the non-counting kernels
     # timed steps use the sync-free sort (no host synchronisation inside a step); the counting pass
     # above read every view's M: size the entry buffers to the largest (+15 %), which also bounds the
@@ -594,6 +599,7 @@ def main():
             "blends_per_s": blends_all / (ms_max / 1e3),
             "masked_pixels_per_step": pix_all / args.steps,
             "tile_imbalance_max_over_mean": imbalance,
+            "tile_entries_p50_p99_max": tile_entries,
             "M_per_view": st0["M"], "evaluated_per_view": st0["evaluated"], "blended_per_view": st0["blended"],
             "bwd_visited_per_view": st0["bwd_visited"],
             "flop_per_unit": {"evaluated": FLOP_EVAL, "blended_fwd": FLOP_BLEND_FWD, "blended_bwd": FLOP_BLEND_BWD},
