@@ -113,6 +113,8 @@ typedef struct {
   uint32_t *ranges;    /* [2*TY*TX]  */
   int64_t capacity;    /* in: entries allocated            */
   int64_t n_dup;       /* out (host field): M              */
+  uint32_t *order;     /* optional [TY*TX]: work order for A6/A7 = the active tiles by decreasing list
+                          length (log2 classes), written by pgsag_bin_sort(_async); NULL = ascending ids */
 } pgsag_bins;
 
 /* A6 output (planar float32 [H][W] unless noted).  Only pixels with mask != 0 are

@@ -45,7 +45,7 @@ class TileMask(C.Structure):
 
 class Bins(C.Structure):
     _fields_ = [("tile_keys", _vp), ("vals", _vp), ("ranges", _vp), ("capacity", C.c_int64),
-                ("n_dup", C.c_int64)]
+                ("n_dup", C.c_int64), ("order", _vp)]
 
 
 class Image(C.Structure):

@@ -51,6 +51,7 @@ struct BwdArgs {
   const uint32_t* vals;
   const uint32_t* ranges;
   const uint32_t* active;
+  const uint32_t* order;  // optional LPT work order (pgsag_bins.order)
   const uint32_t* n_active;
   const uint8_t* mask;
   Dims d;
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
     __syncthreads();
     const uint32_t widx = s_tile;
     if (widx >= n_active) break;
-    const uint32_t tile = a.active[widx];
+    const uint32_t tile = a.order ? a.order[widx] : a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
     const int i = tx * kTile + w * 8 + (lane & 7);
     const int jb = ty * kTile + (lane >> 3);
@@ -426,6 +427,7 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
   a.vals = bins->vals;
   a.ranges = bins->ranges;
   a.active = tm->active;
+  a.order = bins->order;
   a.n_active = tm->n_active;
   a.mask = mask;
   a.d = d;

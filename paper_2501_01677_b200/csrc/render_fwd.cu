@@ -32,6 +32,7 @@ struct FwdArgs {
   const uint32_t* vals;
   const uint32_t* ranges;
   const uint32_t* active;
+  const uint32_t* order;  // optional LPT work order (pgsag_bins.order)
   const uint32_t* n_active;
   const uint8_t* mask;
   Dims d;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
     const uint32_t widx = s_tile;
     __syncthreads();
     if (widx >= n_active) break;
-    const uint32_t tile = a.active[widx];
+    const uint32_t tile = a.order ? a.order[widx] : a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
     const int i = tx * kTile + (w & 1) * 8 + (lane & 7);
     const int jb = ty * kTile + (w >> 1) * Cfg::BH + (lane >> 3);
@@ -270,6 +271,7 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
   a.vals = bins->vals;
   a.ranges = bins->ranges;
   a.active = tm->active;
+  a.order = bins->order;
   a.n_active = tm->n_active;
   a.mask = mask;
   a.d = d;

@@ -401,6 +401,36 @@ __global__ void ranges_kernel(const uint32_t* __restrict__ tkeys, const uint32_t
   }
 }
 
+// ------------------------------------------------------ A5b work order (LPT)
+// One CTA: the active tiles bucketed by floor(log2(list length)), emitted longest class first,
+// so the persistent A6/A7 grids start the heaviest tiles first (longest-processing-time order;
+// the order inside a class is arbitrary).
+__global__ void __launch_bounds__(1024) lpt_order_kernel(const uint32_t* __restrict__ active,
+                                                         const uint32_t* __restrict__ n_active,
+                                                         const uint2* __restrict__ ranges,
+                                                         uint32_t* __restrict__ order) {
+  __shared__ uint32_t s_cnt[33], s_pos[33];
+  const int tid = threadIdx.x;
+  const uint32_t na = *n_active;
+  if (tid < 33) s_cnt[tid] = 0;
+  __syncthreads();
+  auto cls = [&](uint32_t tile) {  // 32 - clz(len): 0 for an empty list, 1..32 otherwise
+    const uint2 r = __ldg(ranges + tile);
+    return 32 - __clz(r.y - r.x);
+  };
+  for (uint32_t k = tid; k < na; k += 1024) atomicAdd(&s_cnt[cls(__ldg(active + k))], 1u);
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (int c = 32; c >= 0; --c) { s_pos[c] = run; run += s_cnt[c]; }
+  }
+  __syncthreads();
+  for (uint32_t k = tid; k < na; k += 1024) {
+    const uint32_t t = __ldg(active + k);
+    order[atomicAdd(&s_pos[cls(t)], 1u)] = t;
+  }
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -535,8 +565,17 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
     ok = bins->tile_keys; ov = bins->vals;
   }
   cudaMemsetAsync(bins->ranges, 0, sizeof(uint32_t) * 2 * (size_t)ntiles, st);
+  auto order = [&]() {
+    if (!bins->order) return;
+    KTimer kt_("A5_lpt_order", st);
+    lpt_order_kernel<<<1, 1024, 0, st>>>(tm->active, tm->n_active, reinterpret_cast<const uint2*>(bins->ranges),
+                                         bins->order);
+  };
   const uint32_t bound = M_known ? M : (uint32_t)bins->capacity;  // grid bound
-  if (bound == 0 || n == 0) return cudaGetLastError();
+  if (bound == 0 || n == 0) {
+    order();
+    return cudaGetLastError();
+  }
   uint32_t* m_clamped = counters + CNT_MC;
   {
     KTimer kt_("A3_duplicate", st);
@@ -559,6 +598,7 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
     KTimer kt_("A5_ranges", st);
     ranges_kernel<<<grid, 256, 0, st>>>(bins->tile_keys, m_clamped, bins->ranges);
   }
+  order();
   return cudaGetLastError();
 }
 

@@ -125,6 +125,7 @@ class Rasterizer:
         self.absgrad = e(n)
         self.grad2d = e(14, n)
         self.ranges = e(2 * T, dtype=i32)
+        self.order = e(T, dtype=i32)  # LPT work order of the active tiles (pgsag_bins.order)
         self._alloc_bins(capacity if capacity is not None else max(1024, 8 * self.n))
         self.M = 0
         self._build_structs()
@@ -152,6 +153,7 @@ class Rasterizer:
         b = L.Bins()
         b.tile_keys, b.vals, b.ranges = self.tile_keys.data_ptr(), self.vals.data_ptr(), self.ranges.data_ptr()
         b.capacity, b.n_dup = self.capacity, 0
+        b.order = self.order.data_ptr()
         self._bins = b
         im = L.Image()
         im.C, im.N, im.D, im.A = self.img_C.data_ptr(), self.img_N.data_ptr(), self.img_D.data_ptr(), \
