@@ -57,7 +57,7 @@ def lib():
             L.oracle_keys.restype = i64
             for nm in ("oracle_render_f32", "oracle_render_f64"):
                 getattr(L, nm).argtypes = [P, P, P, P, P, i32, i32, P, i32, i32, P, P, P, i32, P, P, P, P,
-                                           P, i32, P, P, P]
+                                           P, i32, P, P, P, P]
                 getattr(L, nm).restype = None
             L.oracle_gc_weights.argtypes = [P, P, i32, i32, P]
             L.oracle_gc_weights.restype = None
@@ -139,7 +139,8 @@ def keys(proj, mask):
     return tiles, vals, ranges
 
 
-def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=False, upstream=None):
+def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=False, upstream=None,
+           bound=False):
     """O4 (and O5/O6 if upstream is given) for the listed flat pixel indices.
 
     upstream: (npix, 9) or (npix, 10) float64 = gC(3), gN(3), gD, gA, gDep[, gG] per listed pixel,
@@ -166,15 +167,18 @@ def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=F
         up[:, :u.shape[1]] = u
     grads = None if upstream is None else np.zeros((N_GRAD_ROWS, n), np.float64)
     gsoft = np.zeros(npix, np.float64)
+    bnd = np.zeros((59, n), np.float64) if (bound and upstream is not None) else None
     fn = lib().oracle_render_f32 if dtype == np.float32 else lib().oracle_render_f64
     ca = cam_array(cam)
     fn(*[_p(a) for a in prm], n, int(g.sh_degree), _p(ca), W, H, _p(m), _p(bgd), _p(pix), npix, _p(out),
-       _p(iout), _p(id_sum), _p(evaluated), _p(gsoft), int(bool(certify)), _p(cert), _p(up), _p(grads))
+       _p(iout), _p(id_sum), _p(evaluated), _p(gsoft), int(bool(certify)), _p(cert), _p(up), _p(grads), _p(bnd))
     res = dict(C=out[:, 0:3], N=out[:, 3:6], D=out[:, 6], A=out[:, 7], Dep=out[:, 8], T=out[:, 9],
                g=iout[:, 0], last=iout[:, 1], near=iout[:, 2], n_clamped=iout[:, 3], id_sum=id_sum,
                evaluated=evaluated, cert_bad=int(cert[0]), gsoft=gsoft)
     if grads is not None:
         res["grads"] = grads
+    if bnd is not None:
+        res["bound"] = bnd  # R19b: float32-accumulation bound on rows 0..58 of grads
     return res
 
 

@@ -434,6 +434,9 @@ template <typename R> struct Renderer {
 // -------------------------------------------------- per-Gaussian 2D grads
 struct G2 {
   double du, dv, dca, dcb, dcc, dop, drgb[3], dncam[3], ddist, absg;
+  // sums over pixels of |contribution| for the 13 values above (du .. ddist): the scale of the
+  // float32 rounding of a GPU that sums the same per-pixel terms (R19b)
+  double abs[13];
 };
 
 // O5: reverse-order backward of one pixel (exact reverse mode of Eq. 1-4,
@@ -475,24 +478,31 @@ void pixel_backward(const Renderer<R>& rd, int i, int j, const PixOut<R>& fw,
     }
     const double w = a * T;
     G2& o = g2[b.id];
-    for (int c = 0; c < 3; ++c) o.drgb[c] += w * G[c];
-    for (int c = 0; c < 3; ++c) o.dncam[c] += w * G[3 + c];
+    for (int c = 0; c < 3; ++c) { o.drgb[c] += w * G[c]; o.abs[6 + c] += std::fabs(w * G[c]); }
+    for (int c = 0; c < 3; ++c) { o.dncam[c] += w * G[3 + c]; o.abs[9 + c] += std::fabs(w * G[3 + c]); }
     o.ddist += w * G[6];
+    o.abs[12] += std::fabs(w * G[6]);
     for (int c = 0; c < 8; ++c) S[c] = a * F[c] + (1.0 - a) * S[c];
     Pp *= (1.0 - a);
     double dpow = 0.0;
     if (b.orho <= (R)0.99) {
       o.dop += (double)b.rho * dalpha;
+      o.abs[5] += std::fabs((double)b.rho * dalpha);
       dpow = a * dalpha;
     }
     const double dx = (double)b.dx, dy = (double)b.dy;
     o.dca += -0.5 * dx * dx * dpow;
     o.dcb += -dx * dy * dpow;
     o.dcc += -0.5 * dy * dy * dpow;
+    o.abs[2] += std::fabs(0.5 * dx * dx * dpow);
+    o.abs[3] += std::fabs(dx * dy * dpow);
+    o.abs[4] += std::fabs(0.5 * dy * dy * dpow);
     const double du = ((double)g.ca * dx + (double)g.cb * dy) * dpow;
     const double dv = ((double)g.cb * dx + (double)g.cc * dy) * dpow;
     o.du += du;
     o.dv += dv;
+    o.abs[0] += std::fabs(du);
+    o.abs[1] += std::fabs(dv);
     o.absg += std::fabs(du) + std::fabs(dv);  // densification statistic (sum over pixels)
   }
 }
@@ -673,7 +683,8 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
                    const int64_t* pix, int npix, R* out /* [npix][10]: C3 N3 D A Dep T */,
                    int32_t* iout /* [npix][4]: g last near_flag n_clamped */, double* id_sum, int64_t* evaluated,
                    double* gsoft /* [npix] soft counts (R24) or null */, int certify_flag, int64_t* cert_bad,
-                   const double* upstream /* [npix][10] or null */, double* grads /* 73 x n or null */) {
+                   const double* upstream /* [npix][10] or null */, double* grads /* 73 x n or null */,
+                   double* bound /* 59 x n or null: R19b accumulation bound of rows 0..58 */) {
   const Params<R> P = make_params(mean, scale, rot, opac, sh, n, deg);
   const Cam<R> cam = load_cam<R>(camf, W, H);
   const TileMask tm = make_tilemask(mask, W, H);
@@ -687,7 +698,7 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
   std::vector<int> cand;
   std::vector<Blend<R>> bl;
   std::vector<G2> g2;
-  if (grads) g2.assign(n, G2{0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, 0, 0});
+  if (grads) g2.assign(n, G2{0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, 0, 0, {0}});
   int cur_tile = -1;
   long long bad = 0;
   for (int k : order) {
@@ -729,6 +740,28 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
       const double v[14] = {q.du, q.dv, q.dca, q.dcb, q.dcc, q.dop, q.drgb[0], q.drgb[1], q.drgb[2],
                             q.dncam[0], q.dncam[1], q.dncam[2], q.ddist, q.absg};
       for (int c = 0; c < 14; ++c) grads[(size_t)(59 + c) * n + i] = v[c];
+    }
+    // R19b: bound on what float32 accumulation of the same per-pixel terms can cost each 3D
+    // gradient: sum_k |d g3D / d g2D_k| * kAccEps * sum_pixels |term_k|, the Jacobian columns
+    // being this oracle's own (linear) chain O6 applied to unit 2D gradients
+    if (bound) {
+      const double kAccEps = 16.0 * 5.9604644775390625e-08;  // 16 ulp(1) of float32
+      std::memset(bound, 0, sizeof(double) * (size_t)59 * n);
+      std::vector<double> tmp((size_t)59 * n, 0.0);
+      for (int i = 0; i < n; ++i) {
+        if ((rd.proj[i].flags & F_LIVE) != F_LIVE) continue;
+        for (int k = 0; k < 13; ++k) {
+          const double d = kAccEps * g2[i].abs[k];
+          if (d == 0.0) continue;
+          G2 e{0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, 0, 0, {0}};
+          double* ev[13] = {&e.du, &e.dv, &e.dca, &e.dcb, &e.dcc, &e.dop, &e.drgb[0], &e.drgb[1], &e.drgb[2],
+                            &e.dncam[0], &e.dncam[1], &e.dncam[2], &e.ddist};
+          *ev[k] = 1.0;
+          gaussian_backward(P, i, cam, rd.proj[i].flags, e, tmp.data(), tmp.data() + (size_t)3 * n,
+                            tmp.data() + (size_t)6 * n, tmp.data() + (size_t)10 * n, tmp.data() + (size_t)11 * n);
+          for (int j = 0; j < 59; ++j) bound[(size_t)j * n + i] += std::fabs(tmp[(size_t)j * n + i]) * d;
+        }
+      }
     }
   }
 }
@@ -803,17 +836,18 @@ int64_t oracle_keys(const float* depth, const int32_t* rect, const uint32_t* fla
 void oracle_render_f32(const float* mean, const float* scale, const float* rot, const float* opac, const float* sh,
                        int n, int deg, const double* cam, int W, int H, const uint8_t* mask, const double* bg,
                        const int64_t* pix, int npix, float* out, int32_t* iout, double* id_sum, int64_t* evaluated,
-                       double* gsoft, int certify, int64_t* cert_bad, const double* upstream, double* grads) {
+                       double* gsoft, int certify, int64_t* cert_bad, const double* upstream, double* grads,
+                       double* bound) {
   render_pixels<float>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, bg, pix, npix, out, iout, id_sum,
-                       evaluated, gsoft, certify, cert_bad, upstream, grads);
+                       evaluated, gsoft, certify, cert_bad, upstream, grads, bound);
 }
 void oracle_render_f64(const double* mean, const double* scale, const double* rot, const double* opac,
                        const double* sh, int n, int deg, const double* cam, int W, int H, const uint8_t* mask,
                        const double* bg, const int64_t* pix, int npix, double* out, int32_t* iout, double* id_sum,
                        int64_t* evaluated, double* gsoft, int certify, int64_t* cert_bad, const double* upstream,
-                       double* grads) {
+                       double* grads, double* bound) {
   render_pixels<double>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, bg, pix, npix, out, iout, id_sum,
-                        evaluated, gsoft, certify, cert_bad, upstream, grads);
+                        evaluated, gsoft, certify, cert_bad, upstream, grads, bound);
 }
 
 // ---------------------------------------------------- L_GC-load (NEXT-1)

@@ -120,17 +120,23 @@ def compare_pixels(gpu_img, ora, pix, W, vals, cam=None):
     return errs
 
 
-def compare_grads(gpu, ref, deg):
-    """Per-class gradient parity (reading R19)."""
+def compare_grads(gpu, ref, deg, bound=None):
+    """Per-class gradient parity (reading R19).  bound: the oracle's R19b bound (59, n) on
+    what float32 accumulation of the same per-pixel terms can cost each element; added to the
+    element tolerance when given."""
     K3 = (deg + 1) ** 2 * 3
     classes = {"dmean": (gpu["dmean"], ref[0:3]), "dscale": (gpu["dscale"], ref[3:6]),
                "drot": (gpu["drot"], ref[6:10]), "dopacity": (gpu["dopacity"], ref[10]),
                "dsh": (gpu["dsh"][:K3], ref[11:11 + K3])}
     report = {}
+    rows = {"dmean": slice(0, 3), "dscale": slice(3, 6), "drot": slice(6, 10), "dopacity": 10,
+            "dsh": slice(11, 11 + K3)}
     for k, (a, b) in classes.items():
         a = np.asarray(a, np.float64)
         scale = max(np.abs(b).max(), 1e-30)
         den = np.maximum(np.abs(b), 1e-2 * scale)
+        if bound is not None:  # R19b: the accumulation bound, in units of the relative tolerance
+            den = den + bound[rows[k]] / GRAD_REL
         el = float((np.abs(a - b) / den).max())
         nrm = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
         report[k] = (el, nrm)
