@@ -553,8 +553,7 @@ def main():
                     fetch(cur ^ 1, tviews[s_ + 1])
                 main.wait_event(ready[cur])
                 L.unpack_rgb8(dt8[cur].data_ptr(), W, H, dt[cur].data_ptr(), main.cuda_stream)
-                tr.step(ccam[v], dm[cur], dt[cur], gc_w=r.gc_weights(dt[cur], dm[cur]),
-                        band=r.boundary_band(dm[cur], 1))
+                tr.step_photo(ccam[v], dm[cur], dt[cur])
                 hloss[s_].copy_(tr.loss_rgb, non_blocking=True)
                 free[cur].record(main)
             e1.record(main)

@@ -203,7 +203,10 @@ class Rasterizer:
         mu = s1 / n if n else 0.0
         return (max(s2 / n - mu * mu, 0.0) ** 0.5 if n else 0.0), mu, n
 
-    def forward(self, g: GaussianTensors, cam: L.Camera, mask: torch.Tensor, bg=(0.0, 0.0, 0.0), gc_w=None):
+    def forward(self, g: GaussianTensors, cam: L.Camera, mask: torch.Tensor, bg=(0.0, 0.0, 0.0), gc_w=None,
+                wait_before_render=None):
+        """A0-A6.  wait_before_render: optional torch.cuda.Event the stream waits on between the
+        sort and A6 (e.g. gc_w computed concurrently on another stream)."""
         assert g.n == self.n and g.sh_degree == self.deg
         assert mask.dtype == torch.uint8 and tuple(mask.shape) == (self.H, self.W) and mask.is_contiguous()
         st = _stream()
@@ -223,6 +226,8 @@ class Rasterizer:
             L.bin_sort_async(self._proj, self._tm, cam, self.n, self._bins, C.c_void_p(self._m_host.data_ptr()), ws,
                              self.ws_bytes, st)
             self.M = None  # known after the stream passes the sort: see check_capacity()
+            if wait_before_render is not None:
+                torch.cuda.current_stream().wait_event(wait_before_render)
             L.render_fwd(self._proj, self._bins, self._tm, cam, C.c_void_p(mask.data_ptr()), self._bg, self._img,
                          ws, self.ws_bytes, st)
             return dict(C=self.img_C, N=self.img_N, D=self.img_D, A=self.img_A, Dep=self.img_Dep, T=self.img_T,
@@ -235,6 +240,8 @@ class Rasterizer:
             rc = L.bin_sort(self._proj, self._tm, cam, self.n, self._bins, ws, self.ws_bytes, st)
             L.check(rc)
         self.M = int(self._bins.n_dup)
+        if wait_before_render is not None:
+            torch.cuda.current_stream().wait_event(wait_before_render)
         L.render_fwd(self._proj, self._bins, self._tm, cam, C.c_void_p(mask.data_ptr()), self._bg, self._img, ws,
                      self.ws_bytes, st)
         return dict(C=self.img_C, N=self.img_N, D=self.img_D, A=self.img_A, Dep=self.img_Dep, T=self.img_T,

@@ -92,27 +92,44 @@ class Trainer:
         hp.step = self.t
         return hp
 
+    def _side(self):
+        if getattr(self, "_side_stream", None) is None:
+            self._side_stream = torch.cuda.Stream(device=self.r.device)
+        return self._side_stream
+
     def step(self, cam, mask: torch.Tensor, target: torch.Tensor, gc_w: torch.Tensor | None = None,
-             band: torch.Tensor | None = None, bg=(0.0, 0.0, 0.0), dp_group=None):
+             band: torch.Tensor | None = None, bg=(0.0, 0.0, 0.0), dp_group=None, gc_ready=None):
         """One iteration on one view; returns nothing (losses stay on the device, see losses()).
         dp_group: process group of the ranks training the same sub-region view-parallel (NEXT-4);
-        their parameter gradients are averaged before the (identical) Adam step."""
+        their parameter gradients are averaged before the (identical) Adam step.  L_ban runs on a
+        side stream concurrently with L_rgb (both only read A6's outputs).  gc_ready: event after
+        which gc_w / band are valid (A6 waits for it)."""
         r = self.r
         self.t += 1
         st = _stream()
+        main = torch.cuda.current_stream()
         p = lambda t: C.c_void_p(t.data_ptr())
-        r.forward(self.g, cam, mask, bg, gc_w=gc_w)
+        r.forward(self.g, cam, mask, bg, gc_w=gc_w, wait_before_render=gc_ready)
         assert target.dtype == torch.float32 and target.is_contiguous() and tuple(target.shape) == (3, r.H, r.W)
-        L.rgb_loss(p(r.img_C), p(target), p(mask), r.W, r.H, 1.0 - self.lam, p(self.loss_rgb), p(self.dC),
-                   p(self.rgb_ws), self.rgb_ws_bytes, st)
         self.used_ban = band is not None
         if self.used_ban:
-            self.dN.zero_()
-            self.dDep.zero_()
-            # one pass: loss sums + the gradient of the SUM; A7 divides dN / dDep by the term count
-            # (pgsag_image_grad.nd_div), which makes it the gradient of the mean (R27)
-            L.ban_loss(cam, p(mask), p(band), p(r.img_N), p(r.img_Dep), self.bw, (1.0 - self.lam) * self.lam4, 0,
-                       p(self.loss_ban), p(self.dN), p(self.dDep), st)
+            side = self._side()
+            ev_fwd = torch.cuda.Event()
+            ev_fwd.record(main)
+            with torch.cuda.stream(side):
+                side.wait_event(ev_fwd)
+                self.dN.zero_()
+                self.dDep.zero_()
+                # one pass: loss sums + the gradient of the SUM; A7 divides dN / dDep by the term
+                # count (pgsag_image_grad.nd_div), which makes it the gradient of the mean (R27)
+                L.ban_loss(cam, p(mask), p(band), p(r.img_N), p(r.img_Dep), self.bw, (1.0 - self.lam) * self.lam4,
+                           0, p(self.loss_ban), p(self.dN), p(self.dDep), C.c_void_p(side.cuda_stream))
+                ev_ban = torch.cuda.Event()
+                ev_ban.record(side)
+        L.rgb_loss(p(r.img_C), p(target), p(mask), r.W, r.H, 1.0 - self.lam, p(self.loss_rgb), p(self.dC),
+                   p(self.rgb_ws), self.rgb_ws_bytes, st)
+        if self.used_ban:
+            main.wait_event(ev_ban)
         self.used_gc = gc_w is not None
         r._grad.densify_accum, r._grad.densify_count = self.accum.data_ptr(), self.count.data_ptr()
         try:
@@ -125,6 +142,29 @@ class Trainer:
             K3 = (self.g.sh_degree + 1) ** 2 * 3
             shard.allreduce_mean([r.dmean, r.dscale, r.drot, r.dopacity, r.dsh[:K3]], dp_group)
         L.adam_step(self.g.n, self.g.sh_degree, r._grad, self._state, self.hparams(), p(self.loss_flat), st)
+
+    def step_photo(self, cam, mask: torch.Tensor, target: torch.Tensor, bg=(0.0, 0.0, 0.0), dp_group=None,
+                   band_radius=1):
+        """step() with the Eq. 9 weights and the boundary band derived from this view's photo and
+        mask on the side stream, concurrently with A0-A5 (A6 waits for them)."""
+        r, dev = self.r, self.r.device
+        if getattr(self, "_gc_w", None) is None:
+            self._gc_w = torch.empty(r.H, r.W, dtype=torch.float32, device=dev)
+            self._band = torch.empty(r.H, r.W, dtype=torch.uint8, device=dev)
+            self._gc_ws_bytes = L.workspace_size(0, r.W, r.H, 0)
+            self._gc_ws = torch.empty(max(self._gc_ws_bytes, 256), dtype=torch.uint8, device=dev)
+        side, main = self._side(), torch.cuda.current_stream()
+        p = lambda t: C.c_void_p(t.data_ptr())
+        ev_in = torch.cuda.Event()
+        ev_in.record(main)
+        with torch.cuda.stream(side):
+            side.wait_event(ev_in)
+            ss = C.c_void_p(side.cuda_stream)
+            L.gc_weights(p(target), p(mask), r.W, r.H, p(self._gc_w), p(self._gc_ws), self._gc_ws_bytes, ss)
+            L.boundary_band(p(mask), r.W, r.H, band_radius, p(self._band), ss)
+            ev_gc = torch.cuda.Event()
+            ev_gc.record(side)
+        self.step(cam, mask, target, gc_w=self._gc_w, band=self._band, bg=bg, dp_group=dp_group, gc_ready=ev_gc)
 
     def losses(self) -> dict:
         """Host read of the last iteration's terms and the Eq. 11 total."""

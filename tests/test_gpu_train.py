@@ -343,3 +343,28 @@ def test_unpack_rgb8_exact():
     torch.cuda.synchronize()
     ref = (rgb.astype(np.float32) / np.float32(255.0)).transpose(2, 0, 1)
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_step_photo_matches_step():
+    """step_photo (Eq. 9 weights and band on the side stream, overlapped with A0-A5) gives the same
+    iteration as step() with the weights and band computed up front."""
+    sc = S.config1(seed=97, n=600, W=96, H=64)
+    H, W = sc.mask.shape
+    cam = camera_from(sc.camera)
+    m_t = torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda()
+    tgt = torch.from_numpy(np.ascontiguousarray(S.reference_image(H, W, 97), np.float32)).cuda()
+    res = []
+    for photo in (False, True):
+        g = GaussianTensors.from_numpy(sc.gaussians)
+        r = Rasterizer(g.n, W, H, g.sh_degree)
+        tr = Trainer(r, g)
+        if photo:
+            tr.step_photo(cam, m_t, tgt)
+        else:
+            tr.step(cam, m_t, tgt, gc_w=r.gc_weights(tgt, m_t), band=r.boundary_band(m_t, 1))
+        torch.cuda.synchronize()
+        res.append((tr.losses(), g.mean.cpu().numpy(), tr.m.cpu().numpy()))
+    (la, ma, mma), (lb, mb, mmb) = res
+    for k in ("rgb", "ban", "gc_load", "flat"):
+        assert abs(la[k] - lb[k]) <= 1e-6 * max(1.0, abs(la[k])), k
+    assert np.allclose(mma, mmb, rtol=1e-4, atol=1e-9 * np.abs(mma).max())
