@@ -4,10 +4,9 @@ import collections, csv, io, subprocess, sys
 
 STAGE = {"tilemask_count_kernel": "A0", "tilemask_sat_kernel": "A0", "preprocess_kernel": "A1", "scan_kernel": "A2",
          "duplicate_kernel": "A3", "depth_keys_kernel": "A4", "radix_hist_kernel": "A4", "radix_pass_kernel": "A4",
-         "ranges_kernel": "A5", "render_fwd_kernel": "A6", "render_bwd_kernel": "A7", "preprocess_bwd_kernel": "A8",
-         "sobel_kernel": "N1", "gc_normalize_kernel": "N1", "band_kernel": "N2", "ban_loss_kernel": "N2",
-         "ban_grad_kernel": "N2", "rgb_fwd_kernel": "N3", "rgb_bwd_kernel": "N3", "rgb_finalize_kernel": "N3",
-         "adam_kernel": "N3", "densify_classify_kernel": "N3", "densify_scan_kernel": "N3",
+         "ranges_kernel": "A5", "lpt_order_kernel": "A5", "render_fwd_kernel": "A6", "render_bwd_kernel": "A7", "preprocess_bwd_kernel": "A8",
+         "sobel_kernel": "N1", "gc_normalize_kernel": "N1", "band_kernel": "N2", "ban_kernel": "N2", "rgb_fwd_kernel": "N3", "rgb_bwd_kernel": "N3", "rgb_finalize_kernel": "N3",
+         "adam_kernel": "N3", "unpack_rgb8_kernel": "N3", "densify_classify_kernel": "N3", "densify_scan_kernel": "N3",
          "densify_apply_kernel": "N3", "opacity_reset_kernel": "N3"}
 OURS = tuple(STAGE)
 
@@ -77,6 +76,6 @@ if __name__ == "__main__":
         "Per-launch times are cold-cache and serialised (ncu); compare SHARES with the bench's live CUDA-event "
         "split (`kernels_ms_per_step`), not absolutes.\n\n" + launches(launch_csv, 2) + "\n")
     open(f"profiles/{tag}_ncu.md", "w").write(
-        f"# {tag}: ncu --set full captures (C4 view)\n\nCommand: `{sys.argv[5] if len(sys.argv) > 5 else ''}`\n\n"
+        f"# {tag}: ncu --set full captures (C4 view)\n\nCommand: `{sys.argv[5] if len(sys.argv) > 5 else cmd}`\n\n"
         + "\n".join(ncu(x) for x in rep.split(",")) + "\n")
     print("ok")
