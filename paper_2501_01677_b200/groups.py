@@ -97,10 +97,16 @@ def main(argv=None):
     from . import shard
     world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("PGSAG_DIST_BACKEND", "nccl")  # gloo: smoke-test N ranks on one GPU
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     lay = shard.rank_layout(args.regions, world)
     groups = {}
     if world > args.regions:  # every rank creates every group, in the same order
