@@ -18,8 +18,11 @@ struct CamB {
   double fx, fy, C[3], R[9], lx, ly;
 };
 
+#ifndef PGSAG_A8_MINB
+#define PGSAG_A8_MINB 4
+#endif
 template <int DEG>
-__global__ void __launch_bounds__(128, 4) preprocess_bwd_kernel(
+__global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
     int n, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
     const float* __restrict__ sh, const uint32_t* __restrict__ flags, const double* __restrict__ g2d, CamB cam,
     float* __restrict__ dmean, float* __restrict__ dscale, float* __restrict__ drot, float* __restrict__ dopac,
