@@ -378,12 +378,17 @@ template <typename R> struct Renderer {
       o.evaluated += 1;
       const R dx = px - g.u, dy = py - g.v;
       const R power = (R)-0.5 * ((g.ca * dx) * dx + (g.cc * dy) * dy) - (g.cb * dx) * dy;
-      if (std::fabs((double)power) < 1e-5) o.near_flag = 1;
+      // R18: the decision band is 1e-5 plus the float32 rounding bound of the quadratic form,
+      // which grows with the magnitude of its terms where they cancel (thin, rotated ellipses).
+      const double band = 1e-5 + 1e-6 * (0.5 * (std::fabs((double)g.ca) * (double)dx * (double)dx +
+                                                 std::fabs((double)g.cc) * (double)dy * (double)dy) +
+                                          std::fabs((double)g.cb * (double)dx * (double)dy));
+      if (std::fabs((double)power) < band) o.near_flag = 1;
       if (power > (R)0) continue;
       const R rho = std::exp(power);
       const R orho = g.o * rho;
       const R alpha = std::min((R)0.99, orho);
-      if (near_rel(orho, a_min, 1e-5) || near_rel(orho, (R)0.99, 1e-5)) o.near_flag = 1;
+      if (near_rel(orho, a_min, band) || near_rel(orho, (R)0.99, band)) o.near_flag = 1;
       if (alpha < a_min) continue;
       const R Tn = T * ((R)1 - alpha);
       if (near_rel(Tn, t_min, 1e-3)) o.near_flag = 1;

@@ -41,12 +41,12 @@ def test_fuzz_forward_backward(seed):
     ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=bg)
     planes, per = upstream_at(pix, H, W, seed=seed, exclude=ora0["near"].astype(bool), ora=ora0, cam=sc.camera)
     res = run_gpu(sc, bg=bg, upstream=planes, counters=bool(seed % 2))
-    p = oracle.project(sc.gaussians, sc.camera, sc.mask)
+    p = oracle.project(sc.gaussians, sc.camera, sc.mask, np.float32)
     tl, vl, rg = oracle.keys(p, sc.mask)
     np.testing.assert_array_equal(res["vals"], vl)
     np.testing.assert_array_equal(res["tile_keys"], tl)
     np.testing.assert_array_equal(res["ranges"], rg)
-    compare_pixels(res["img"], ora0, pix, W, res["vals"], cam=sc.camera)
+    compare_pixels(res["img"], ora0, pix, W, res["vals"], cam=sc.camera, proj=p)
     ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=bg, upstream=per, bound=True)
     if np.abs(ora["grads"][:59]).max() > 0:
         compare_grads(res["grads"], ora["grads"], sc.gaussians.sh_degree, bound=ora["bound"])
