@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -517,7 +518,8 @@ def main():
                      "terms": "L_rgb (L1+SSIM) + L_s + L_ban + L_GC-load with P:179 weights; Adam on raw params",
                      "gpu_launches": int(sum(v[1] for v in tk.values())),
                      "kernels_ms_per_iter": {k: round(v[0] / kt, 4) for k, v in sorted(tk.items())},
-                     "last_loss": {k: round(float(x), 6) for k, x in lo.items()}}
+                     "last_loss": {k: round(float(x), 6) for k, x in lo.items()},
+                     "losses_finite": bool(all(math.isfinite(float(x)) for x in lo.values()))}
             del extras
         if not args.no_e2e:
             # the photo as captured: 8-bit interleaved RGB (pgsag_unpack_rgb8 makes the float planes)

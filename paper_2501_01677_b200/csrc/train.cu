@@ -231,9 +231,12 @@ __global__ void __launch_bounds__(256) rgb_fwd_kernel(RgbArgs A) {
       const float mx = cx + ax, my = cy + ay;
       const float n1 = 2.f * mx * my + kC1, n2 = 2.f * sxy_ + kC2;
       const float d1 = mx * mx + my * my + kC1, d2 = sxx + syy + kC2;
-      const float s = __fdividef(n1 * n2, d1 * d2);
-      const float dmx = s * (__fdividef(2.f * my, n1) - __fdividef(2.f * mx, d1));
-      const float dsxx = -__fdividef(s, d2), dsxy = __fdividef(2.f * s, n2);
+      // no division by n1 or n2 (n2 = 2 sigma_xy + C2 crosses zero for anti-correlated windows:
+      // s / n2 would be 0/0 there); d1 >= C1 and d2 >= C2 up to rounding
+      const float id = __fdividef(1.f, d1 * d2);
+      const float s = n1 * n2 * id;
+      const float dmx = 2.f * (my * n2 * id - __fdividef(mx * s, d1));
+      const float dsxx = -__fdividef(s, d2), dsxy = 2.f * n1 * id;
       const size_t p = (size_t)(y0 + h) * A.W + x;
       float* abc = A.abc + (size_t)ch * 3 * HW;
       abc[p] = dmx - 2.f * dsxx * (mx - kShift) - dsxy * (my - kShift);

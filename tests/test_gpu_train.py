@@ -65,6 +65,28 @@ def test_rgb_loss_parity(H, W, seed):
     assert (dC[~on] == -7.0).all()  # off-mask pixels untouched
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_rgb_loss_anticorrelated(seed):
+    """Windows whose covariance term n2 = 2 sigma_xy + C2 crosses zero (I ~ 1 - C with the
+    contrast sweeping through sqrt(3 C2 / 2) across the columns): SSIM's gradient is finite there
+    (dS/dsigma_xy = 2 n1 / (d1 d2)), so dC must be finite and match the oracle (R28).  A kernel
+    that forms it as 2 S / n2 returns 0/0 where n2 rounds to zero (seen once per ~5 C4 views)."""
+    rng = np.random.default_rng(50 + seed)
+    H, W = 96, 160
+    a = np.linspace(0.02, 0.06, W)[None, None, :]
+    u = rng.uniform(-1, 1, (3, H, W))
+    Cimg = (0.5 + a * u).astype(np.float32)
+    Iimg = (0.5 - a * u + rng.normal(0, 0.002, (3, H, W))).astype(np.float32)
+    mask = _blocky_mask(rng, H, W)
+    loss, dC = _rgb_gpu(Cimg, Iimg, mask)
+    Lr, L1, Sm, dref = oracle.rgb_loss(Cimg.astype(np.float64), Iimg.astype(np.float64), mask, grads=True)
+    on = np.broadcast_to(mask != 0, dC.shape)
+    assert np.isfinite(dC).all() and np.isfinite(loss).all()
+    assert abs(loss[2] - Sm) <= 1e-5
+    err = np.abs(dC - dref)[on] / np.maximum(np.abs(dref[on]), 1e-2 * np.abs(dref).max())
+    assert err.max() <= RGB_GRAD_REL, err.max()
+
+
 def test_rgb_loss_empty_mask():
     H, W = 40, 50
     rng = np.random.default_rng(4)
