@@ -297,7 +297,7 @@ int pgsag_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pg
   uint32_t* counters = reinterpret_cast<uint32_t*>(w + L.counters);
   cudaError_t e = cudaMemsetAsync(counters + CNT_BWD, 0, sizeof(uint32_t), st);
   if (e == cudaSuccess)
-    e = launch_render_bwd(g, cam, p, bins, tm, d, mask, bg, fwd, dL, out, reinterpret_cast<double*>(w + L.g2d),
+    e = launch_render_bwd(g, cam, p, bins, tm, d, mask, bg, fwd, dL, out, reinterpret_cast<float*>(w + L.g2d),
                           counters + CNT_BWD, st);
   if (e != cudaSuccess) return cuda_fail(e, "render_bwd");
   return PGSAG_OK;

@@ -47,7 +47,7 @@ struct WsLayout {
   size_t scan_status;            // A2 look-back [tilesN] u64
   size_t hist;                   // [2][kMaxSortPasses][256] u32
   size_t counters;               // [64] u32 (tile counters, M, misc)
-  size_t g2d;                    // [14][n] f64 per-Gaussian 2D gradients (A7 -> A8)
+  size_t g2d;                    // [n][16] f32 per-Gaussian 2D gradients (A7 -> A8; 14 used)
   size_t total;
   int tiles1, tiles2, tilesN;
 };
@@ -91,10 +91,10 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
 cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
                               const pgsag_bins* bins, const pgsag_tilemask* tm, const Dims& d,
                               const uint8_t* mask, const float bg[3], const pgsag_image* fwd,
-                              const pgsag_image_grad* dL, pgsag_gaussian_grad* out, double* g2d,
+                              const pgsag_image_grad* dL, pgsag_gaussian_grad* out, float* g2d,
                               uint32_t* work_counter, cudaStream_t st);
 cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
-                                  pgsag_gaussian_grad* out, const double* g2d, cudaStream_t st);
+                                  pgsag_gaussian_grad* out, const float* g2d, cudaStream_t st);
 cudaError_t launch_gc_weights(const float* image, const uint8_t* mask, int W, int H, float* w, double* acc,
                               cudaStream_t st);
 

@@ -24,7 +24,7 @@ struct CamB {
 template <int DEG>
 __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
     int n, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
-    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const double* __restrict__ g2d, CamB cam,
+    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const float4* __restrict__ g2d, CamB cam,
     float* __restrict__ dmean, float* __restrict__ dscale, float* __restrict__ drot, float* __restrict__ dopac,
     float* __restrict__ dsh, float* __restrict__ absgrad, float* __restrict__ grad2d,
     const uint32_t* __restrict__ tiles_touched, float* __restrict__ daccum, float* __restrict__ dcount, double hw,
@@ -46,9 +46,12 @@ __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
       for (int c = 0; c < kG2; ++c) grad2d[(size_t)c * n + i] = 0.f;
     return;
   }
-  double gg[kG2];
+  double gg[16];
 #pragma unroll
-  for (int c = 0; c < kG2; ++c) gg[c] = g2d[(size_t)c * n + i];
+  for (int c = 0; c < 4; ++c) {
+    const float4 q = g2d[(size_t)i * 4 + c];
+    gg[4 * c] = q.x; gg[4 * c + 1] = q.y; gg[4 * c + 2] = q.z; gg[4 * c + 3] = q.w;
+  }
   if (grad2d) {
 #pragma unroll
     for (int c = 0; c < kG2; ++c) grad2d[(size_t)c * n + i] = (float)gg[c];
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
 }  // namespace
 
 cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
-                                  pgsag_gaussian_grad* out, const double* g2d, cudaStream_t st) {
+                                  pgsag_gaussian_grad* out, const float* g2d, cudaStream_t st) {
   const int n = g->n;
   CamB cb;
   cb.fx = cam->fx; cb.fy = cam->fy;
@@ -249,8 +252,9 @@ cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* 
   {
     KTimer kt_("A8_preprocess_bwd", st);
     const int blocks = (n + 127) / 128;
+    const float4* g2d4 = reinterpret_cast<const float4*>(g2d);
 #define PGSAG_A8(DEG)                                                                                         \
-  preprocess_bwd_kernel<DEG><<<blocks, 128, 0, st>>>(n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d, cb, \
+  preprocess_bwd_kernel<DEG><<<blocks, 128, 0, st>>>(n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d4, cb, \
                                                       out->dmean, out->dscale, out->drot, out->dopacity,      \
                                                       out->dsh, out->absgrad2d, out->grad2d,                  \
                                                       p->tiles_touched, out->densify_accum, out->densify_count, \

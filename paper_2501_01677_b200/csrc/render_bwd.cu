@@ -23,7 +23,8 @@
 // lane sums its four pixels, the warp reduce-scatters the 14 partials (5 butterfly
 // levels, 16 shuffles) so that 14 lanes each hold one warp sum, those lanes add
 // into a padded shared accumulator of the batch, and after the batch the CTA
-// flushes one double-precision global atomic per (entry, value).
+// flushes each entry's nonzero groups of four with one vector reduction (red.add.v4.f32)
+// into the Gaussian's 64-byte line of the [n][16] accumulator.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -61,7 +62,7 @@ struct BwdArgs {
   const int32_t *g, *last;
   const float *dC, *dN, *dD, *dA, *dDep;
   const double* nd_div;  // optional: dN, dDep divided by *nd_div
-  double* g2d;  // [kG2][n]
+  float* g2d;  // [n][16] (kG2 used)
   int n;
   unsigned long long* counters;
   uint32_t* work;
@@ -209,10 +210,12 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 
 
 template <bool kCount, bool kGC, bool kAbs>
 __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs a) {
-  constexpr int kAccStride = 15;  // padded row: the 14 values of an entry sit in 14 distinct banks
+  // padded row of 16 values: the 14 values of an entry sit in 14 distinct banks, and the
+  // flush's 128-bit loads of 8 consecutive entries start in 8 distinct 4-bank groups
+  constexpr int kAccStride = 20;
   __shared__ Rec s_rec[kBBatch];
   __shared__ uint32_t s_id[kBBatch];
-  __shared__ float s_acc[kBBatch * kAccStride];
+  __shared__ __align__(16) float s_acc[kBBatch * kAccStride];
   __shared__ uint8_t s_list[kBNB * kBBatch];
   __shared__ uint32_t s_wc[kBEPT * (kBT / 32) * kBNB];
   __shared__ int s_nw[kBNB];
@@ -371,18 +374,21 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         if (writer && sum != 0.0f) atomicAdd(&s_acc[q * kAccStride + my_c], sum);
       }
       __syncthreads();
-      // flush the batch: one f64 atomic per (entry, value), then re-zero
+      // flush the batch: one vector reduction per nonzero group of four values, then re-zero
 #pragma unroll
       for (int e = 0; e < kBEPT; ++e) {
         const int slot = e * kBT + tid;
         if (slot < cnt) {
-          const uint32_t id = s_id[slot];
+          float* dst = a.g2d + (size_t)s_id[slot] * 16;
 #pragma unroll
-          for (int c = 0; c < kG2; ++c) {
-            const float x = s_acc[slot * kAccStride + c];
-            if (x != 0.0f) {
-              atomicAdd(a.g2d + (size_t)c * a.n + id, (double)x);
-              s_acc[slot * kAccStride + c] = 0.f;
+          for (int c = 0; c < 4; ++c) {
+            float4* sp = reinterpret_cast<float4*>(s_acc + slot * kAccStride + 4 * c);
+            const float4 x = *sp;
+            if (x.x != 0.0f || x.y != 0.0f || x.z != 0.0f || x.w != 0.0f) {
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c), "f"(x.x), "f"(x.y),
+                           "f"(x.z), "f"(x.w)
+                           : "memory");
+              *sp = make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
         }
@@ -414,11 +420,11 @@ int bwd_grid() {
 cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
                               const pgsag_bins* bins, const pgsag_tilemask* tm, const Dims& d,
                               const uint8_t* mask, const float bg[3], const pgsag_image* fwd,
-                              const pgsag_image_grad* dL, pgsag_gaussian_grad* out, double* g2d,
+                              const pgsag_image_grad* dL, pgsag_gaussian_grad* out, float* g2d,
                               uint32_t* work_counter, cudaStream_t st) {
   const int n = g->n;
   if (n == 0) return cudaSuccess;
-  cudaMemsetAsync(g2d, 0, sizeof(double) * kG2 * (size_t)n, st);
+  cudaMemsetAsync(g2d, 0, sizeof(float) * 16 * (size_t)n, st);
   BwdArgs a;
   a.mean2d = reinterpret_cast<const float2*>(p->mean2d);
   a.conic_o = reinterpret_cast<const float4*>(p->conic_o);

@@ -509,7 +509,7 @@ WsLayout ws_layout(int32_t n, int32_t W, int32_t H, int64_t cap) {
   L.scan_status = take(8 * (size_t)(L.tilesN > 0 ? L.tilesN : 1));
   L.hist = take(4 * 2 * kMaxSortPasses * kMaxRadix);
   L.counters = take(4 * 64);
-  L.g2d = take(8 * 14 * nn);
+  L.g2d = take(4 * 16 * nn);  // [n][16] f32 (14 used), one 64-byte line per Gaussian
   L.total = off;
   return L;
 }
