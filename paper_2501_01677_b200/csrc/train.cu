@@ -256,13 +256,15 @@ __global__ void __launch_bounds__(256) rgb_fwd_kernel(RgbArgs A) {
   }
 }
 
-__global__ void rgb_finalize_kernel(double* loss) {
+__device__ __forceinline__ void rgb_finalize(double* loss) {
   const double n = loss[5];
   const double L1 = n > 0 ? loss[3] / (3.0 * n) : 0.0, S = n > 0 ? loss[4] / (3.0 * n) : 1.0;
   loss[0] = 0.8 * L1 + 0.2 * (1.0 - S);
   loss[1] = L1;
   loss[2] = S;
 }
+
+__global__ void rgb_finalize_kernel(double* loss) { rgb_finalize(loss); }
 
 __global__ void __launch_bounds__(256) rgb_bwd_kernel(RgbArgs A) {
   extern __shared__ float4 smem_f4[];
@@ -273,6 +275,9 @@ __global__ void __launch_bounds__(256) rgb_bwd_kernel(RgbArgs A) {
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
   const int x = bx + tx, y0 = by + 2 * ty;
+  // the loss values (the sums are complete: rgb_fwd precedes on the stream); no separate
+  // one-thread launch that would queue behind concurrent side-stream work
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) rgb_finalize(A.loss);
   bool m0, m1;
   if (!tile_has_mask(A, x, y0, m0, m1)) return;
   const double n = A.loss[5];
@@ -523,13 +528,12 @@ cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8
     KTimer kt_("N3_rgb_fwd", st);
     rgb_fwd_kernel<<<grid, 256, kFwdSmem, st>>>(A);
   }
-  {
-    KTimer kt_("N3_rgb_finalize", st);
-    rgb_finalize_kernel<<<1, 1, 0, st>>>(loss);
-  }
   if (dC) {
     KTimer kt_("N3_rgb_bwd", st);
-    rgb_bwd_kernel<<<grid, 256, kBwdSmem, st>>>(A);
+    rgb_bwd_kernel<<<grid, 256, kBwdSmem, st>>>(A);  // also finalises the loss values
+  } else {
+    KTimer kt_("N3_rgb_finalize", st);
+    rgb_finalize_kernel<<<1, 1, 0, st>>>(loss);
   }
   return cudaGetLastError();
 }

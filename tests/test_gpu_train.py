@@ -63,6 +63,15 @@ def test_rgb_loss_parity(H, W, seed):
     err = np.abs(dC - dref)[on] / np.maximum(np.abs(dref[on]), 1e-2 * scale)
     assert err.max() <= RGB_GRAD_REL, err.max()
     assert (dC[~on] == -7.0).all()  # off-mask pixels untouched
+    # value only (dC = NULL): the same loss terms from the standalone finalisation
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    c, i, m = t(Cimg), t(Iimg), torch.from_numpy(np.ascontiguousarray(mask)).cuda()
+    lo2 = torch.zeros(6, dtype=torch.float64, device="cuda")
+    nb = L.rgb_loss_workspace_size(W, H)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    L.rgb_loss(c.data_ptr(), i.data_ptr(), m.data_ptr(), W, H, 0.59, lo2.data_ptr(), None, ws.data_ptr(), nb,
+               torch.cuda.current_stream().cuda_stream)
+    assert np.array_equal(lo2.cpu().numpy(), loss)
 
 
 @pytest.mark.parametrize("seed", range(4))
