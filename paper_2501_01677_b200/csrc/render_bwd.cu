@@ -159,7 +159,7 @@ __device__ __forceinline__ void load_pixel(const BwdArgs& a, bool masked, size_t
 // State of one packed pixel pair.
 struct Pair {
   float2 G[8];
-  float2 Pb, T, Sg, gG;
+  float2 Pb, T, Sg, gGk;  // gGk = k * dL/d(soft count)
   int last0, last1;
 };
 
@@ -167,7 +167,7 @@ __device__ __forceinline__ void make_pair(const PixState& a, const PixState& b, 
 #pragma unroll
   for (int c = 0; c < 8; ++c) p.G[c] = f2(a.G[c], b.G[c]);
   p.Pb = f2(a.Pb, b.Pb);
-  p.gG = f2(a.gG, b.gG);
+  p.gGk = f2(kGcK * a.gG, kGcK * b.gG);
   p.T = f2(a.T, b.T);
   p.Sg = f2(0.f, 0.f);
   p.last0 = a.last;
@@ -195,10 +195,11 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 
   const float2 sp = __fadd2_rn(p.Sg, p.Pb);
   float2 dal = __fmul2_rn(Ti, __fadd2_rn(GF, f2(-sp.x, -sp.y)));
   if (kGC) {  // + gG * d(sigmoid(k (alpha - 1/255)))/d alpha; only reaches the outputs through ac / rc
-    const float2 z = __fmul2_rn(bc(-kGcK * kLog2e), __fadd2_rn(al, bc(-kAlphaMin)));
-    const float2 s = f2(rcp_approx(1.0f + ex2_approx(z.x)), rcp_approx(1.0f + ex2_approx(z.y)));
-    const float2 ds = __fmul2_rn(__fmul2_rn(bc(kGcK), s), __fadd2_rn(bc(1.0f), f2(-s.x, -s.y)));
-    dal = __ffma2_rn(p.gG, ds, dal);
+    // z = -k log2(e) (alpha - 1/255), s = 1 / (1 + 2^z), 1 - s = 2^z s
+    const float2 z = __ffma2_rn(al, bc(-kGcK * kLog2e), bc(kGcK * kLog2e * kAlphaMin));
+    const float2 e = f2(ex2_approx(z.x), ex2_approx(z.y));
+    const float2 s = f2(rcp_approx(1.0f + e.x), rcp_approx(1.0f + e.y));
+    dal = __ffma2_rn(__fmul2_rn(p.gGk, s), __fmul2_rn(e, s), dal);
   }
   p.Sg = __ffma2_rn(al, GF, __fmul2_rn(om, p.Sg));
   p.Pb = __fmul2_rn(p.Pb, om);
