@@ -142,12 +142,17 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
           const uint32_t id = a.vals[k];
           Rec& r = s_rec[e * NT + tid];
           mk[e] = stage_gaussian<8, Cfg::BH>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
+          r.b.w = (float)(e * NT + tid);  // slot in the batch, for the blend's last index
           r.cd = a.rgb_d[id];
           r.n = a.ncam[id];
         }
       }
       build_lists<NT, EPT, NB>(mk, s_list, s_wc, s_nw);
       const int nw = s_nw[w];
+      // batch slot of each pixel's last blend in this batch (-1: none), kept on the FMA pipe
+      float2 lastf[NP];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) lastf[p] = f2(-1.f, -1.f);
       const uint32_t lbase = list_base + (uint32_t)(w * BATCH);
       for (int t = 0; t < nw; ++t) {
         if ((t & 7) == 0 && __all_sync(0xffffffffu, all_done())) break;
@@ -159,7 +164,6 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
         const float tA = __fmul_rn(ra.z, dx);
         const float4 cd = lds128(ra_addr + 32);
         const float4 nn = lds128(ra_addr + 48);
-        const int kq = (int)(b + q);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           // p2 for the pair (bit-identical to power2r per element)
@@ -176,8 +180,13 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
           const float2 Tn = __fmul2_rn(T[p], __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
           const bool st0 = ok0 && Tn.x < kTmin, st1 = ok1 && Tn.y < kTmin;
           ok0 &= !st0; ok1 &= !st1;
-          // branch-free blend (predicated weights): no loop-carried phi copies
-          const float2 wt = __fmul2_rn(f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f), T[p]);
+          // branch-free blend (predicated weights): no loop-carried phi copies.  The blend
+          // indicator (alpha >= 1/255 > 0 when blended) is formed by a saturating multiply on
+          // the FMA pipe and drives the blend count and the last slot (the ALU pipe is the
+          // limiter here)
+          const float2 als = f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f);
+          const float2 okf = f2(__saturatef(als.x * 1e30f), __saturatef(als.y * 1e30f));
+          const float2 wt = __fmul2_rn(als, T[p]);
           C0[p] = __ffma2_rn(wt, f2(cd.x, cd.x), C0[p]);
           C1[p] = __ffma2_rn(wt, f2(cd.y, cd.y), C1[p]);
           C2[p] = __ffma2_rn(wt, f2(cd.z, cd.z), C2[p]);
@@ -187,10 +196,15 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
           N2[p] = __ffma2_rn(wt, f2(nn.z, nn.z), N2[p]);
           T[p].x = ok0 ? Tn.x : (st0 ? -T[p].x : T[p].x);
           T[p].y = ok1 ? Tn.y : (st1 ? -T[p].y : T[p].y);
-          gc[p] = __fadd2_rn(gc[p], f2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f));  // blend counts (exact below 2^24)
-          last[p][0] = ok0 ? kq : last[p][0];
-          last[p][1] = ok1 ? kq : last[p][1];
+          gc[p] = __fadd2_rn(gc[p], okf);  // blend counts (exact below 2^24)
+          // lastf <- okf ? slot : lastf, exactly (small integers)
+          lastf[p] = __ffma2_rn(okf, __fadd2_rn(f2(rb.w, rb.w), f2(-lastf[p].x, -lastf[p].y)), lastf[p]);
         }
+      }
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        if (lastf[p].x >= 0.f) last[p][0] = (int)b + (int)lastf[p].x;
+        if (lastf[p].y >= 0.f) last[p][1] = (int)b + (int)lastf[p].y;
       }
     }
     float n = 0.f, s1 = 0.f, s2 = 0.f;
