@@ -230,6 +230,12 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   // value index this lane owns after the reduce-scatter: bit-reversed lane bits 1..4
   const int my_c = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
   const bool writer = ((lane & 1) == 0) && my_c < kG2;
+  // loop-invariant lane values pinned in registers (otherwise re-derived from S2R per candidate);
+  // not in the L_GC-load variant, whose extra live values would then spill inside the loop
+  const uint32_t lbits = kGC ? (uint32_t)lane : opaque((uint32_t)lane);
+  const uint32_t acc_lane0 = smem_u32(s_acc) + (uint32_t)my_c * 4u;
+  const uint32_t acc_lane = kGC ? acc_lane0 : opaque(acc_lane0);
+  const uint32_t wr = kGC ? (uint32_t)writer : opaque((uint32_t)writer);
   for (int k = tid; k < kBBatch * kAccStride; k += kBT) s_acc[k] = 0.f;
   for (;;) {
     if (tid == 0) { s_tile = atomicAdd(a.work, 1u); s_maxlast = -1; }
@@ -367,12 +373,15 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         v[15] = 0.f;
         // reduce-scatter 16 -> 1 value per lane pair
         float v8[8], v4[4], v2[2], v1[1];
-        rs_level<8>(v, v8, (lane & 16) != 0, 16);
-        rs_level<4>(v8, v4, (lane & 8) != 0, 8);
-        rs_level<2>(v4, v2, (lane & 4) != 0, 4);
-        rs_level<1>(v2, v1, (lane & 2) != 0, 2);
+        rs_level<8>(v, v8, (lbits & 16u) != 0u, 16);
+        rs_level<4>(v8, v4, (lbits & 8u) != 0u, 8);
+        rs_level<2>(v4, v2, (lbits & 4u) != 0u, 4);
+        rs_level<1>(v2, v1, (lbits & 2u) != 0u, 2);
         const float sum = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 1);
-        if (writer && sum != 0.0f) atomicAdd(&s_acc[q * kAccStride + my_c], sum);
+        if (wr && sum != 0.0f) {
+          const uint32_t addr = acc_lane + (uint32_t)q * (uint32_t)(kAccStride * 4);
+          asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(addr), "f"(sum) : "memory");
+        }
       }
       __syncthreads();
       // flush the batch: one vector reduction per nonzero group of four values, then re-zero
