@@ -237,8 +237,9 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   const uint32_t acc_lane = kGC ? acc_lane0 : opaque(acc_lane0);
   const uint32_t wr = kGC ? (uint32_t)writer : opaque((uint32_t)writer);
   for (int k = tid; k < kBBatch * kAccStride; k += kBT) s_acc[k] = 0.f;
+  if (tid == 0) s_tile = atomicAdd(a.work, 1u);
   for (;;) {
-    if (tid == 0) { s_tile = atomicAdd(a.work, 1u); s_maxlast = -1; }
+    if (tid == 0) s_maxlast = -1;
     __syncthreads();
     const uint32_t widx = s_tile;
     if (widx >= n_active) break;
@@ -269,6 +270,8 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
     const int wlast = __reduce_max_sync(0xffffffffu, mylast);
     __syncthreads();
     const int maxlast = s_maxlast;
+    // every thread has read s_tile: claim the next tile now (latency hidden behind this one)
+    if (tid == 0) s_tile = atomicAdd(a.work, 1u);
     for (int bhi = maxlast + 1; bhi > (int)rs; bhi -= kBBatch) {
       const int blo = max((int)rs, bhi - kBBatch);
       const int cnt = bhi - blo;

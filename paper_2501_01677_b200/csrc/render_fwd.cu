@@ -93,12 +93,14 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
   const size_t HW = (size_t)a.d.W * a.d.H;
   const uint32_t rec_base = smem_u32(s_rec), list_base = smem_u32(s_list);
   unsigned long long cntE = 0, cntB = 0;
+  if (tid == 0) s_tile = atomicAdd(a.work, 1u);
   for (;;) {
-    if (tid == 0) s_tile = atomicAdd(a.work, 1u);
-    __syncthreads();
+    __syncthreads();  // s_tile published
     const uint32_t widx = s_tile;
-    __syncthreads();
+    __syncthreads();  // read by every thread
     if (widx >= n_active) break;
+    // claim the next tile now: the atomic's latency hides behind this tile's work
+    if (tid == 0) s_tile = atomicAdd(a.work, 1u);
     const uint32_t tile = a.order ? a.order[widx] : a.active[widx];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
     const int i = tx * kTile + (w & 1) * 8 + (lane & 7);
