@@ -87,9 +87,12 @@ __device__ __forceinline__ bool ellipse_meets_rect(float2 mu, float4 co, float k
 // conservative cull of the warp blocks: every pixel with alpha >= 1/255 has
 // d^T conic d <= 2 ln(255 o), hence |dx| <= sqrt(2 ln(255 o) cov_xx) (R8), here
 // with a 5% + 0.5 px margin that dominates the float error of the conic inverse.
-template <int BW, int BH>
-__device__ __forceinline__ uint32_t stage_gaussian(float2 xy, float4 co, float tile_x0, float tile_y0, Rec& r) {
-  constexpr int NBX = 16 / BW, NB = NBX * (16 / BH);
+struct StageCull {
+  float rx, ry, k2m;  // bounding half-extents and the (margined) ellipse level of the cull
+};
+
+// The record of one staged Gaussian and its cull parameters.
+__device__ __forceinline__ StageCull stage_record(float2 xy, float4 co, Rec& r) {
   const float4 sc = scaled_conic(co);
   r.a = make_float4(xy.x, xy.y, sc.x, sc.y);
   const float o = co.w;
@@ -104,14 +107,28 @@ __device__ __forceinline__ uint32_t stage_gaussian(float2 xy, float4 co, float t
   const float rx = sqrtf(kd * co.z) + 0.5f;
   const float ry = sqrtf(kd * co.x) + 0.5f;
   const float k2m = k2 + 0.05f;
+  return StageCull{rx, ry, k2m};
+}
+
+// Can the Gaussian reach a pixel centre of the rectangle [xlo, xhi] x [ylo, yhi]?
+__device__ __forceinline__ bool block_hit(float2 xy, float4 co, const StageCull& c, float xlo, float xhi, float ylo,
+                                          float yhi) {
+  bool hit = (xy.x + c.rx >= xlo) && (xy.x - c.rx <= xhi) && (xy.y + c.ry >= ylo) && (xy.y - c.ry <= yhi);
+  if (hit) hit = ellipse_meets_rect(xy, co, c.k2m, xlo, xhi, ylo, yhi);
+  return hit;
+}
+
+// Record + bit mask of the warp blocks of the tile the Gaussian can reach.
+template <int BW, int BH>
+__device__ __forceinline__ uint32_t stage_gaussian(float2 xy, float4 co, float tile_x0, float tile_y0, Rec& r) {
+  constexpr int NBX = 16 / BW, NB = NBX * (16 / BH);
+  const StageCull c = stage_record(xy, co, r);
   uint32_t m = 0;
 #pragma unroll
   for (int k = 0; k < NB; ++k) {
     const float xlo = tile_x0 + (float)((k % NBX) * BW) + 0.5f, xhi = xlo + (float)(BW - 1);
     const float ylo = tile_y0 + (float)((k / NBX) * BH) + 0.5f, yhi = ylo + (float)(BH - 1);
-    bool hit = (xy.x + rx >= xlo) && (xy.x - rx <= xhi) && (xy.y + ry >= ylo) && (xy.y - ry <= yhi);
-    if (hit) hit = ellipse_meets_rect(xy, co, k2m, xlo, xhi, ylo, yhi);
-    m |= (hit ? 1u : 0u) << k;
+    m |= (block_hit(xy, co, c, xlo, xhi, ylo, yhi) ? 1u : 0u) << k;
   }
   return m;
 }

@@ -13,11 +13,11 @@
 // suffix is carried as one scalar (mathematically identical to the 8-vector
 // recurrence of the oracle).
 //
-// Mapping: per active tile one 64-thread CTA (2 warps); warp w owns the 8x16 pixel
-// block of columns 8w..8w+7; a lane owns the FOUR pixels (x, y + 4k), k = 0..3, of
-// its column, which share dx and every per-entry load and run as two packed FP32x2
-// pairs.  Batches of 128 entries are staged with the exact warp-block cull of A6
-// and walked in reverse through compacted per-warp candidate lists.  A pixel that
+// Mapping: per active tile two single-warp CTAs (PGSAG_BWD_WARPS below), the one of half h
+// owning the 8x16 pixel block of columns 8h..8h+7; a lane owns the FOUR pixels (x, y + 4k),
+// k = 0..3, of its column, which share dx and every per-entry load and run as two packed FP32x2
+// pairs.  Batches of 64 entries are staged with the exact block cull of A6 and walked in
+// reverse through a compacted candidate list.  A pixel that
 // does not contribute to an entry carries alpha = rho = 0, which zeroes all of its
 // terms and leaves its state unchanged without branches.  Reduction: per entry the
 // lane sums its four pixels, the warp reduce-scatters the 14 partials (5 butterfly
@@ -35,12 +35,20 @@ namespace pgsag {
 namespace {
 
 constexpr int kG2 = 14;  // du dv dca dcb dcc dop drgb3 dncam3 ddist absgrad
-constexpr int kBT = 64;
+// PGSAG_BWD_WARPS = 1 (default): one single-warp CTA per 8x16 half tile (the tile's entries
+// are staged by both halves' CTAs, each culling against its own half): no inter-warp barrier
+// and no shared atomics, at twice the record loads (L2 hits).  = 2: one CTA per tile whose two
+// warps share the staged batch (C4: A7 3.51 vs 3.41 ms; with the L_GC-load upstream 3.95 vs 3.68).
+#ifndef PGSAG_BWD_WARPS
+#define PGSAG_BWD_WARPS 1
+#endif
+constexpr int kBW = PGSAG_BWD_WARPS;
+constexpr int kBT = 32 * kBW;
 constexpr int kBEPT = 2;
 constexpr int kBBatch = kBT * kBEPT;
-constexpr int kBNB = 2;
+constexpr int kBNB = kBW;  // candidate lists per CTA
 #ifndef PGSAG_BWD_MINB
-#define PGSAG_BWD_MINB 10  // resident CTAs per SM the register budget is sized for
+#define PGSAG_BWD_MINB (20 / kBW)  // resident CTAs per SM the register budget is sized for
 #endif
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -230,22 +238,22 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   // value index this lane owns after the reduce-scatter: bit-reversed lane bits 1..4
   const int my_c = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
   const bool writer = ((lane & 1) == 0) && my_c < kG2;
-  // loop-invariant lane values pinned in registers (otherwise re-derived from S2R per candidate);
-  // not in the L_GC-load variant, whose extra live values would then spill inside the loop
-  const uint32_t lbits = kGC ? (uint32_t)lane : opaque((uint32_t)lane);
-  const uint32_t acc_lane0 = smem_u32(s_acc) + (uint32_t)my_c * 4u;
-  const uint32_t acc_lane = kGC ? acc_lane0 : opaque(acc_lane0);
-  const uint32_t wr = kGC ? (uint32_t)writer : opaque((uint32_t)writer);
+  // loop-invariant lane values pinned in registers (otherwise re-derived from S2R per candidate)
+  const uint32_t lbits = opaque((uint32_t)lane);
+  const uint32_t acc_lane = opaque(smem_u32(s_acc) + (uint32_t)my_c * 4u);
+  const uint32_t wr = opaque((uint32_t)writer);
   for (int k = tid; k < kBBatch * kAccStride; k += kBT) s_acc[k] = 0.f;
   if (tid == 0) s_tile = atomicAdd(a.work, 1u);
   for (;;) {
     if (tid == 0) s_maxlast = -1;
     __syncthreads();
     const uint32_t widx = s_tile;
-    if (widx >= n_active) break;
-    const uint32_t tile = a.order ? a.order[widx] : a.active[widx];
+    if (widx >= n_active * (uint32_t)(3 - kBW)) break;
+    const uint32_t titem = kBW == 1 ? widx >> 1 : widx;
+    const int half = kBW == 1 ? (int)(widx & 1u) : w;  // which 8-column half of the tile
+    const uint32_t tile = a.order ? a.order[titem] : a.active[titem];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
-    const int i = tx * kTile + w * 8 + (lane & 7);
+    const int i = tx * kTile + half * 8 + (lane & 7);
     const int jb = ty * kTile + (lane >> 3);
     const uint32_t rs = a.ranges[2 * tile];
     const float px = opaque((float)i + 0.5f);
@@ -266,10 +274,10 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       make_pair(s[2], s[3], P23);
     }
     const int mylast = max(max(P01.last0, P01.last1), max(P23.last0, P23.last1));
-    if (mylast >= 0) atomicMax(&s_maxlast, mylast);
+    if (kBW > 1 && mylast >= 0) atomicMax(&s_maxlast, mylast);
     const int wlast = __reduce_max_sync(0xffffffffu, mylast);
     __syncthreads();
-    const int maxlast = s_maxlast;
+    const int maxlast = kBW > 1 ? s_maxlast : wlast;
     // every thread has read s_tile: claim the next tile now (latency hidden behind this one)
     if (tid == 0) s_tile = atomicAdd(a.work, 1u);
     for (int bhi = maxlast + 1; bhi > (int)rs; bhi -= kBBatch) {
@@ -283,7 +291,15 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         if (slot < cnt) {
           const uint32_t id = a.vals[blo + slot];
           Rec& r = s_rec[slot];
-          mk[e] = stage_gaussian<8, 16>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
+          if (kBW > 1) {
+            mk[e] = stage_gaussian<8, 16>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
+          } else {  // this CTA's half only
+            const float2 xy = a.mean2d[id];
+            const float4 co = a.conic_o[id];
+            const StageCull c = stage_record(xy, co, r);
+            const float xlo = tx0 + (float)(half * 8) + 0.5f, ylo = ty0 + 0.5f;
+            mk[e] = block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 15.0f) ? 1u : 0u;
+          }
           r.cd = a.rgb_d[id];
           r.n = a.ncam[id];
           s_id[slot] = id;
@@ -291,8 +307,8 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       }
       build_lists<kBT, kBEPT, kBNB>(mk, s_list, s_wc, s_nw);
       const int qtop = wlast - blo;  // entries past the warp's last are never needed
-      const uint32_t lbase = list_base + (uint32_t)(w * kBBatch);
-      for (int t = s_nw[w] - 1; t >= 0; --t) {
+      const uint32_t lbase = list_base + (uint32_t)((kBW > 1 ? w : 0) * kBBatch);
+      for (int t = s_nw[kBW > 1 ? w : 0] - 1; t >= 0; --t) {
         const int q = (int)lds_u8(lbase + (uint32_t)t);
         if (q > qtop) continue;  // warp-uniform
         const int kk = blo + q;
@@ -383,7 +399,13 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float sum = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 1);
         if (wr && sum != 0.0f) {
           const uint32_t addr = acc_lane + (uint32_t)q * (uint32_t)(kAccStride * 4);
-          asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(addr), "f"(sum) : "memory");
+          if (kBW > 1) {  // the CTA's two warps may add to the same entry
+            asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(addr), "f"(sum) : "memory");
+          } else {  // one warp: (entry, value) has a single writer lane
+            float acc;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(acc) : "r"(addr));
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(acc + sum) : "memory");
+          }
         }
       }
       __syncthreads();
@@ -463,7 +485,7 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
   a.gc_w = gc ? fwd->gc_w : nullptr;
   a.gc_stats = fwd->gc_stats;
   a.gc_lambda = dL->gc_lambda;
-  const int grid = min(bwd_grid(), d.TX * d.TY);
+  const int grid = min(bwd_grid(), d.TX * d.TY * (3 - kBW));  // work items: tiles (kBW = 2) or half tiles
   {
     KTimer kt_("A7_render_bwd", st);
     const bool abs_ = out->absgrad2d || out->grad2d;
