@@ -22,6 +22,7 @@ namespace pgsag {
 namespace {
 
 constexpr int kTW = 32, kTH = 16, kR = 5, kIW = kTW + 2 * kR, kIH = kTH + 2 * kR;
+constexpr int kHalo = kIH * kIW, kHIt = (kHalo + 255) / 256;  // halo positions, per-thread share
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
 
 // Window weights g[k] = exp(-k^2 / 4.5) / sum (sigma 1.5), computed in double, rounded once.
@@ -137,27 +138,38 @@ __global__ void __launch_bounds__(256) rgb_fwd_kernel(RgbArgs A) {
   if (!tile_has_mask(A, x, y0, m0, m1)) return;
   const size_t HW = (size_t)A.W * A.H;
   float sums[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int r = ty; r < kIH; r += 8) {
-    const int gy = by - kR + r;
-    for (int c = tx; c < kIW; c += 32) {
-      const int gx = bx - kR + c;
-      float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (gx >= 0 && gy >= 0 && gx < A.W && gy < A.H) {
-        const size_t p = (size_t)gy * A.W + gx;
-        const uint8_t mk = __ldg(A.mask + p);
+  // halo: all loads of the thread's (up to 5) halo positions first, then the shared stores, so
+  // the global latencies overlap instead of serialising per position
+  float hv[kHIt][6];
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          v[2 * ch] = __ldg(A.C + ch * HW + p);
-          v[2 * ch + 1] = __ldg(A.I + ch * HW + p);
-        }
-        if (!mk)
+  for (int it = 0; it < kHIt; ++it) {
+    const int k = tid + 256 * it;
+    const int r = k / kIW, c = k - r * kIW;
+    const int gy = by - kR + r, gx = bx - kR + c;
 #pragma unroll
-          for (int k = 0; k < 6; ++k) v[k] = 0.f;
+    for (int q = 0; q < 6; ++q) hv[it][q] = 0.f;
+    if (k < kHalo && gx >= 0 && gy >= 0 && gx < A.W && gy < A.H) {
+      const size_t p = (size_t)gy * A.W + gx;
+      const uint8_t mk = __ldg(A.mask + p);
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        hv[it][2 * ch] = __ldg(A.C + ch * HW + p);
+        hv[it][2 * ch + 1] = __ldg(A.I + ch * HW + p);
       }
+      if (!mk)
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) s_in[ch * kPlane + r * kIWp + c] = f2(v[2 * ch], v[2 * ch + 1]);
+        for (int q = 0; q < 6; ++q) hv[it][q] = 0.f;
+    }
+  }
 #pragma unroll
-      for (int k = 0; k < 6; ++k) sums[k] += v[k];
+  for (int it = 0; it < kHIt; ++it) {
+    const int k = tid + 256 * it;
+    if (k < kHalo) {
+      const int r = k / kIW, c = k - r * kIW;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) s_in[ch * kPlane + r * kIWp + c] = f2(hv[it][2 * ch], hv[it][2 * ch + 1]);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) sums[q] += hv[it][q];
     }
   }
   block_sum<6>(sums, s_red);  // contains the barrier publishing s_in
