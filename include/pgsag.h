@@ -288,6 +288,20 @@ typedef struct {
 int pgsag_adam_step(int32_t n, int32_t sh_degree, const pgsag_gaussian_grad *grad, pgsag_adam_state *state,
                     const pgsag_adam_hparams *hp, double *flatten_loss, void *stream);
 
+/* A7 + A8 fused with the Adam step: the gradients pgsag_render_bwd computes, applied inside A8 by
+ * exactly pgsag_adam_step's update (same float32 gradients, same arithmetic: bitwise the same
+ * parameters, moments and L_s) instead of being written to memory (P:82 differentiable rendering +
+ * P:171-179 optimisation).  Arguments as pgsag_render_bwd and pgsag_adam_step; state
+ * must describe the same Gaussians as g (its mean / scale / rot / opacity / sh are g's arrays).  Of
+ * out only absgrad2d, grad2d, densify_accum and densify_count are used (all optional); its
+ * parameter-gradient pointers may be NULL.  For one optimiser per sub-region: ranks that average
+ * gradients first (NEXT-4) call pgsag_render_bwd, all-reduce, then pgsag_adam_step. */
+int pgsag_render_bwd_adam(const pgsag_gaussians *g, const pgsag_camera *cam, const pgsag_projected *p,
+                          const pgsag_bins *bins, const pgsag_tilemask *tm, const uint8_t *mask, const float bg[3],
+                          const pgsag_image *fwd, const pgsag_image_grad *dL, pgsag_gaussian_grad *out,
+                          pgsag_adam_state *state, const pgsag_adam_hparams *hp, double *flatten_loss, void *ws,
+                          size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------ NEXT-3: densification (R31)
  * 3DGS adaptive density control on a sub-region's optimiser state (the paper
  * trains every group with it, and gives no parameters: 3DGS's conventions). */

@@ -18,7 +18,8 @@ SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_
            "pgsag_render_bwd", "pgsag_last_error", "pgsag_version", "pgsag_timing_enable", "pgsag_timing_filter",
            "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights", "pgsag_boundary_band",
            "pgsag_ban_loss", "pgsag_rgb_loss_workspace_size", "pgsag_rgb_loss", "pgsag_adam_step",
-           "pgsag_densify_workspace_size", "pgsag_densify_plan", "pgsag_densify_apply", "pgsag_opacity_reset", "pgsag_microbench_fp32", "pgsag_unpack_rgb8")
+           "pgsag_densify_workspace_size", "pgsag_densify_plan", "pgsag_densify_apply", "pgsag_opacity_reset",
+           "pgsag_microbench_fp32", "pgsag_unpack_rgb8", "pgsag_render_bwd_adam")
 
 _vp = C.c_void_p
 
@@ -139,6 +140,10 @@ def lib():
             L.pgsag_adam_step.argtypes = [C.c_int32, C.c_int32, P(GaussianGrad), P(AdamState), P(AdamHparams), _vp,
                                           _vp]
             L.pgsag_adam_step.restype = C.c_int
+            L.pgsag_render_bwd_adam.argtypes = [P(Gaussians), P(Camera), P(Projected), P(Bins), P(TileMask), _vp,
+                                                P(C.c_float * 3), P(Image), P(ImageGrad), P(GaussianGrad),
+                                                P(AdamState), P(AdamHparams), _vp, _vp, C.c_size_t, _vp]
+            L.pgsag_render_bwd_adam.restype = C.c_int
             L.pgsag_densify_workspace_size.argtypes = [C.c_int32]
             L.pgsag_densify_workspace_size.restype = C.c_size_t
             L.pgsag_densify_plan.argtypes = [C.c_int32, _vp, _vp, _vp, _vp, P(DensifyParams), _vp, P(C.c_int64 * 3),
@@ -246,6 +251,12 @@ def rgb_loss_workspace_size(W, H):
 def rgb_loss(image, target, mask, W, H, weight, loss, dC, ws, ws_bytes, stream):
     return check(lib().pgsag_rgb_loss(image, target, mask, int(W), int(H), float(weight), loss, dC, ws, int(ws_bytes),
                                       stream))
+
+
+def render_bwd_adam(g, cam, proj, bins, tm, mask, bg, img, dimg, grad, state, hp, flat, ws, ws_bytes, stream):
+    return check(lib().pgsag_render_bwd_adam(C.byref(g), C.byref(cam), C.byref(proj), C.byref(bins), C.byref(tm),
+                                             mask, C.byref(bg), C.byref(img), C.byref(dimg), C.byref(grad),
+                                             C.byref(state), C.byref(hp), flat, ws, ws_bytes, stream))
 
 
 def adam_step(n, deg, grad, state, hp, flat, stream):

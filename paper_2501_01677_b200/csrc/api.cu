@@ -303,6 +303,38 @@ int pgsag_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pg
   return PGSAG_OK;
 }
 
+static int check_state(const pgsag_adam_state* s);
+
+int pgsag_render_bwd_adam(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
+                          const pgsag_bins* bins, const pgsag_tilemask* tm, const uint8_t* mask, const float bg[3],
+                          const pgsag_image* fwd, const pgsag_image_grad* dL, pgsag_gaussian_grad* out,
+                          pgsag_adam_state* state, const pgsag_adam_hparams* hp, double* flatten_loss, void* ws,
+                          size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_g(g)) || (rc = check_cam(cam)) || (rc = check_tm(tm))) return rc;
+  if (g->n > 0 && (rc = check_proj(p))) return rc;
+  if (!bins || !bins->vals || !bins->ranges) return fail(PGSAG_EINVAL, "bins buffer is NULL");
+  if (!mask || !bg || !fwd || !dL || !out || !state || !hp) return fail(PGSAG_EINVAL, "argument is NULL");
+  if (!fwd->N || !fwd->D || !fwd->T || !fwd->g || !fwd->last) return fail(PGSAG_EINVAL, "fwd image is NULL");
+  if (hp->step < 1) return fail(PGSAG_EINVAL, "adam: step must be >= 1");
+  if (g->n > 0 && (rc = check_state(state))) return rc;
+  if (g->n > 0 && (state->mean != g->mean || state->scale != g->scale || state->rot != g->rot ||
+                   state->opacity != g->opacity || state->sh != g->sh))
+    return fail(PGSAG_EINVAL, "render_bwd_adam: state does not hold g's parameter arrays");
+  const WsLayout L = ws_layout(g->n, cam->width, cam->height, 0);
+  if ((rc = check_ws(ws, ws_bytes, L.total))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Dims d = make_dims(cam->width, cam->height);
+  char* w = static_cast<char*>(ws);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(w + L.counters);
+  cudaError_t e = cudaMemsetAsync(counters + CNT_BWD, 0, sizeof(uint32_t), st);
+  if (e == cudaSuccess)
+    e = launch_render_bwd(g, cam, p, bins, tm, d, mask, bg, fwd, dL, out, reinterpret_cast<float*>(w + L.g2d),
+                          counters + CNT_BWD, st, state, hp, flatten_loss);
+  if (e != cudaSuccess) return cuda_fail(e, "render_bwd_adam");
+  return PGSAG_OK;
+}
+
 int pgsag_gc_weights(const float* image, const uint8_t* mask, int32_t width, int32_t height, float* w, void* ws,
                      size_t ws_bytes, void* stream) {
   if (!image || !mask || !w) return fail(PGSAG_EINVAL, "gc_weights: NULL argument");

@@ -92,9 +92,13 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
                               const pgsag_bins* bins, const pgsag_tilemask* tm, const Dims& d,
                               const uint8_t* mask, const float bg[3], const pgsag_image* fwd,
                               const pgsag_image_grad* dL, pgsag_gaussian_grad* out, float* g2d,
-                              uint32_t* work_counter, cudaStream_t st);
+                              uint32_t* work_counter, cudaStream_t st, pgsag_adam_state* adam = nullptr,
+                              const pgsag_adam_hparams* hp = nullptr, double* flat = nullptr);
+// adam != NULL: A8 applies the Adam step (hp, L_s into *flat) instead of writing the gradients
 cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
-                                  pgsag_gaussian_grad* out, const float* g2d, cudaStream_t st);
+                                  pgsag_gaussian_grad* out, const float* g2d, cudaStream_t st,
+                                  pgsag_adam_state* adam = nullptr, const pgsag_adam_hparams* hp = nullptr,
+                                  double* flat = nullptr);
 cudaError_t launch_gc_weights(const float* image, const uint8_t* mask, int W, int H, float* w, double* acc,
                               cudaStream_t st);
 

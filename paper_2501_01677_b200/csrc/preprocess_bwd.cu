@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "adam.cuh"
 #include "internal.cuh"
 
 namespace pgsag {
@@ -21,26 +22,90 @@ struct CamB {
 #ifndef PGSAG_A8_MINB
 #define PGSAG_A8_MINB 4
 #endif
-template <int DEG>
-__global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
-    int n, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
-    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const float4* __restrict__ g2d, CamB cam,
+
+// Fused A8 + Adam (pgsag_render_bwd_adam): the optimiser state; the gradients are applied where
+// A8 produces them (adam.cuh, bitwise the pgsag_adam_step update) instead of being written.
+struct AdamFused {
+  AdamP P;
+  float *mean, *scale, *rot, *op, *sh, *log_scale, *logit_op, *m, *v;
+  double* flat;  // L_s accumulator (zeroed by the launcher)
+};
+
+// The Adam step of Gaussian i from its float32 gradients staged in shared memory by A8 (sg: this
+// thread's column, row stride 128): rows in batches of 8, all loads of a batch before its stores.
+// Same arithmetic as adam_kernel (adam.cuh).
+template <int K3>
+__device__ __forceinline__ void adam_rows(const AdamFused& F, size_t n, size_t i, const float* sg, float gflat) {
+  constexpr int R = 11 + K3;
+  const AdamP& P = F.P;
+  int kmin;
+  const float s3[3] = {__ldg(F.scale + i), __ldg(F.scale + n + i), __ldg(F.scale + 2 * n + i)};
+  min_axis(s3[0], s3[1], s3[2], kmin);
+  const float o = __ldg(F.op + i);
+  auto raw_ptr = [&](int r) -> float* {
+    return r < 3 ? F.mean + r * n : r < 6 ? F.log_scale + (r - 3) * n : r < 10 ? F.rot + (r - 6) * n
+           : r == 10 ? F.logit_op : F.sh + (r - 11) * n;
+  };
+#pragma unroll
+  for (int r0 = 0; r0 < R; r0 += 8) {
+    float g[8], m[8], v[8], raw[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = r0 + q;
+      if (r < R) {
+        g[q] = sg[r * 128];
+        m[q] = __ldg(F.m + r * n + i);
+        v[q] = __ldg(F.v + r * n + i);
+        raw[q] = __ldg(raw_ptr(r) + i);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = r0 + q;
+      if (r < R) {
+        float gr = g[q], lr;
+        if (r < 3) lr = P.lr_mean;
+        else if (r < 6) { gr = dlog_scale(gr, r - 3 == kmin, gflat, s3[r - 3]); lr = P.lr_scale; }
+        else if (r < 10) lr = P.lr_rot;
+        else if (r == 10) { gr = dlogit_opacity(gr, o); lr = P.lr_op; }
+        else lr = r < 14 ? P.lr_dc : P.lr_rest;
+        const float nr = adam_elem(P, m[q], v[q], raw[q], gr, lr);
+        F.m[r * n + i] = m[q];
+        F.v[r * n + i] = v[q];
+        raw_ptr(r)[i] = nr;
+        if (r >= 3 && r < 6) F.scale[(r - 3) * n + i] = expf(nr);
+        if (r == 10) F.op[i] = 1.f / (1.f + expf(-nr));
+      }
+    }
+  }
+}
+
+// A8 for one Gaussian.  kAdam: the float32 parameter gradients go to this thread's column of the
+// block's shared staging area (sg, row stride 128) instead of global memory.
+template <int DEG, bool kAdam>
+__device__ __forceinline__ void a8_gaussian(
+    int n, int i, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
+    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const float4* __restrict__ g2d, const CamB& cam,
     float* __restrict__ dmean, float* __restrict__ dscale, float* __restrict__ drot, float* __restrict__ dopac,
     float* __restrict__ dsh, float* __restrict__ absgrad, float* __restrict__ grad2d,
     const uint32_t* __restrict__ tiles_touched, float* __restrict__ daccum, float* __restrict__ dcount, double hw,
-    double hh) {
+    double hh, float* gst) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t fl = flags[i];
   if ((fl & PGSAG_F_LIVE) != PGSAG_F_LIVE) {
+    if (kAdam) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { dmean[(size_t)k * n + i] = 0.f; dscale[(size_t)k * n + i] = 0.f; }
+      for (int r = 0; r < 11 + 3 * K; ++r) gst[r * 128] = 0.f;
+    } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) drot[(size_t)k * n + i] = 0.f;
-    dopac[i] = 0.f;
+      for (int k = 0; k < 3; ++k) { dmean[(size_t)k * n + i] = 0.f; dscale[(size_t)k * n + i] = 0.f; }
 #pragma unroll
-    for (int k = 0; k < 3 * K; ++k) dsh[(size_t)k * n + i] = 0.f;
+      for (int k = 0; k < 4; ++k) drot[(size_t)k * n + i] = 0.f;
+      dopac[i] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 3 * K; ++k) dsh[(size_t)k * n + i] = 0.f;
+    }
     if (absgrad) absgrad[i] = 0.f;
     if (grad2d)
       for (int c = 0; c < kG2; ++c) grad2d[(size_t)c * n + i] = 0.f;
@@ -174,7 +239,11 @@ __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
   const double qh[4] = {w, X, Y, Z};
   const double qdot = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) drot[(size_t)k * n + i] = (float)((dq[k] - qh[k] * qdot) / qn);
+  for (int k = 0; k < 4; ++k) {
+    const float gq = (float)((dq[k] - qh[k] * qdot) / qn);
+    if (kAdam) gst[(6 + k) * 128] = gq;
+    else drot[(size_t)k * n + i] = gq;
+  }
   // SH colour: rgb_c = max(0, sum_l Y_l(dir) sh_lc + 0.5)
   const double len = sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
   const double il = 1.0 / len;
@@ -192,8 +261,10 @@ __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const size_t k = (size_t)(l * 3 + c) * n + i;
-        dsh[k] = Yl * gcs[c];
-        const float f = __ldg(sh + k) * gcs[c];
+        const float shv = __ldg(sh + k), gsh = Yl * gcs[c];
+        if (kAdam) gst[(11 + l * 3 + c) * 128] = gsh;
+        else dsh[k] = gsh;
+        const float f = shv * gcs[c];
         dd0 += gx * f; dd1 += gy * f; dd2 += gz * f;
       }
     };
@@ -229,20 +300,73 @@ __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
   dt[0] += (dd0 - dx * ddot) * il;
   dt[1] += (dd1 - dy * ddot) * il;
   dt[2] += (dd2 - dz * ddot) * il;
+  if (kAdam) {
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    dmean[(size_t)k * n + i] = (float)dt[k];
-    dscale[(size_t)k * n + i] = (float)ds[k];
+    for (int k = 0; k < 3; ++k) {
+      gst[k * 128] = (float)dt[k];
+      gst[(3 + k) * 128] = (float)ds[k];
+    }
+    gst[10 * 128] = (float)gg[5];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      dmean[(size_t)k * n + i] = (float)dt[k];
+      dscale[(size_t)k * n + i] = (float)ds[k];
+    }
+    dopac[i] = (float)gg[5];
   }
-  dopac[i] = (float)gg[5];
   if (absgrad) absgrad[i] = (float)gg[13];
+}
+
+template <int DEG, bool kAdam>
+__global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
+    int n, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
+    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const float4* __restrict__ g2d, CamB cam,
+    float* __restrict__ dmean, float* __restrict__ dscale, float* __restrict__ drot, float* __restrict__ dopac,
+    float* __restrict__ dsh, float* __restrict__ absgrad, float* __restrict__ grad2d,
+    const uint32_t* __restrict__ tiles_touched, float* __restrict__ daccum, float* __restrict__ dcount, double hw,
+    double hh, AdamFused F) {
+  constexpr int K3 = 3 * (DEG + 1) * (DEG + 1);
+  __shared__ float s_g[kAdam ? (11 + K3) * 128 : 1];  // fused: the gradients, one column per thread
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const float gflat = kAdam ? F.P.flat_w / (float)n : 0.f;
+  if (kAdam) {  // L_s = mean of min(scale) before the update: block sum, one atomic per block
+    __shared__ float s_flat[4];
+    float sm = 0.f;
+    if (i < n) {
+      int km;
+      sm = min_axis(F.scale[i], F.scale[(size_t)n + i], F.scale[2 * (size_t)n + i], km);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    if ((threadIdx.x & 31) == 0) s_flat[threadIdx.x >> 5] = sm;
+    __syncthreads();
+    if (threadIdx.x == 0 && F.flat)
+      atomicAdd(F.flat, ((double)s_flat[0] + s_flat[1] + s_flat[2] + s_flat[3]) / (double)n);
+  }
+  a8_gaussian<DEG, kAdam>(n, i, mean, scale, rot, sh, flags, g2d, cam, dmean, dscale, drot, dopac, dsh, absgrad,
+                          grad2d, tiles_touched, daccum, dcount, hw, hh, s_g + threadIdx.x);
+  // each thread reads back only its own column: no barrier
+  if (kAdam && i < n) adam_rows<K3>(F, n, i, s_g + threadIdx.x, gflat);
 }
 
 }  // namespace
 
 cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
-                                  pgsag_gaussian_grad* out, const float* g2d, cudaStream_t st) {
+                                  pgsag_gaussian_grad* out, const float* g2d, cudaStream_t st,
+                                  pgsag_adam_state* adam, const pgsag_adam_hparams* hp, double* flat) {
   const int n = g->n;
+  AdamFused F{};
+  if (adam) {
+    F.P = adam_params(hp);
+    F.mean = adam->mean; F.scale = adam->scale; F.rot = adam->rot; F.op = adam->opacity; F.sh = adam->sh;
+    F.log_scale = adam->log_scale; F.logit_op = adam->logit_opacity; F.m = adam->m; F.v = adam->v;
+    F.flat = flat;
+    if (flat) {
+      cudaError_t e = cudaMemsetAsync(flat, 0, sizeof(double), st);
+      if (e != cudaSuccess) return e;
+    }
+  }
   CamB cb;
   cb.fx = cam->fx; cb.fy = cam->fy;
   for (int k = 0; k < 3; ++k) cb.C[k] = cam->C[k];
@@ -250,20 +374,24 @@ cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* 
   cb.lx = (double)(1.3f * ((0.5f * (float)cam->width) / cam->fx));
   cb.ly = (double)(1.3f * ((0.5f * (float)cam->height) / cam->fy));
   {
-    KTimer kt_("A8_preprocess_bwd", st);
+    KTimer kt_(adam ? "A8_preprocess_bwd_adam" : "A8_preprocess_bwd", st);
     const int blocks = (n + 127) / 128;
     const float4* g2d4 = reinterpret_cast<const float4*>(g2d);
-#define PGSAG_A8(DEG)                                                                                         \
-  preprocess_bwd_kernel<DEG><<<blocks, 128, 0, st>>>(n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d4, cb, \
-                                                      out->dmean, out->dscale, out->drot, out->dopacity,      \
-                                                      out->dsh, out->absgrad2d, out->grad2d,                  \
-                                                      p->tiles_touched, out->densify_accum, out->densify_count, \
-                                                      0.5 * cam->width, 0.5 * cam->height)
-    switch (g->sh_degree) {
-      case 0: PGSAG_A8(0); break;
-      case 1: PGSAG_A8(1); break;
-      case 2: PGSAG_A8(2); break;
-      default: PGSAG_A8(3); break;
+#define PGSAG_A8(DEG, AD)                                                                                    \
+  preprocess_bwd_kernel<DEG, AD><<<blocks, 128, 0, st>>>(                                                  \
+      n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d4, cb, out->dmean, out->dscale, out->drot,         \
+      out->dopacity, out->dsh, out->absgrad2d, out->grad2d, p->tiles_touched, out->densify_accum,          \
+      out->densify_count, 0.5 * cam->width, 0.5 * cam->height, F)
+    const int deg = g->sh_degree < 0 ? 0 : (g->sh_degree > 3 ? 3 : g->sh_degree);
+    switch (deg * 2 + (adam ? 1 : 0)) {
+      case 0: PGSAG_A8(0, false); break;
+      case 1: PGSAG_A8(0, true); break;
+      case 2: PGSAG_A8(1, false); break;
+      case 3: PGSAG_A8(1, true); break;
+      case 4: PGSAG_A8(2, false); break;
+      case 5: PGSAG_A8(2, true); break;
+      case 6: PGSAG_A8(3, false); break;
+      default: PGSAG_A8(3, true); break;
     }
 #undef PGSAG_A8
   }

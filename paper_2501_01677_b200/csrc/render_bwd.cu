@@ -456,7 +456,8 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
                               const pgsag_bins* bins, const pgsag_tilemask* tm, const Dims& d,
                               const uint8_t* mask, const float bg[3], const pgsag_image* fwd,
                               const pgsag_image_grad* dL, pgsag_gaussian_grad* out, float* g2d,
-                              uint32_t* work_counter, cudaStream_t st) {
+                              uint32_t* work_counter, cudaStream_t st, pgsag_adam_state* adam,
+                              const pgsag_adam_hparams* hp, double* flat) {
   const int n = g->n;
   if (n == 0) return cudaSuccess;
   cudaMemsetAsync(g2d, 0, sizeof(float) * 16 * (size_t)n, st);
@@ -504,7 +505,7 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
 #undef PGSAG_A7
     }
   }
-  return launch_preprocess_bwd(g, cam, p, out, g2d, st);
+  return launch_preprocess_bwd(g, cam, p, out, g2d, st, adam, hp, flat);
 }
 
 }  // namespace pgsag

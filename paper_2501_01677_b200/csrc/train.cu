@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "adam.cuh"
 #include "internal.cuh"
 
 namespace pgsag {
@@ -396,25 +397,9 @@ struct AdamArgs {
   const float *__restrict__ dmean, *__restrict__ dscale, *__restrict__ drot, *__restrict__ dop, *__restrict__ dsh;
   float *__restrict__ mean, *__restrict__ scale, *__restrict__ rot, *__restrict__ op, *__restrict__ sh;
   float *__restrict__ log_scale, *__restrict__ logit_op, *__restrict__ m, *__restrict__ v;
-  float lr_mean, lr_scale, lr_rot, lr_op, lr_dc, lr_rest;
-  float b1, b2, eps, flat_w, ibc1, isbc2;  // 1 / (1 - b1^t), 1 / sqrt(1 - b2^t)
+  AdamP P;  // adam.cuh: the update shared with the fused A8 + Adam
   double* flat;
 };
-
-__device__ __forceinline__ float sqrt_approx(float v) {  // MUFU; sqrt(0) = 0
-  float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
-  return r;
-}
-
-__device__ __forceinline__ float adam(const AdamArgs& A, int row, int i, float raw, float g, float lr) {
-  const size_t k = (size_t)row * A.n + i;
-  const float m = A.b1 * A.m[k] + (1.f - A.b1) * g;
-  const float v = A.b2 * A.v[k] + (1.f - A.b2) * g * g;
-  A.m[k] = m;
-  A.v[k] = v;
-  return raw - __fdividef(lr * A.ibc1 * m, sqrt_approx(v) * A.isbc2 + A.eps);
-}
 
 __global__ void __launch_bounds__(256) adam_kernel(AdamArgs A) {
   __shared__ float s_red[8];
@@ -422,28 +407,29 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs A) {
   float smin = 0.f;
   if (i < A.n) {
     const size_t n = A.n;
-    // L_s = mean_i min_k s_ik (ties -> lowest axis): d/ds = flat_w / n on the minimum axis
+    const AdamP& P = A.P;
+    // L_s = mean_i min_k s_ik: d/ds = flat_w / n on the minimum axis
     const float s0 = A.scale[i], s1 = A.scale[n + i], s2 = A.scale[2 * n + i];
-    int kmin = 0;
-    smin = s0;
-    if (s1 < smin) { smin = s1; kmin = 1; }
-    if (s2 < smin) { smin = s2; kmin = 2; }
-    const float gflat = A.flat_w / (float)A.n;
+    int kmin;
+    smin = min_axis(s0, s1, s2, kmin);
+    const float gflat = P.flat_w / (float)A.n;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) A.mean[c * n + i] = adam(A, c, i, A.mean[c * n + i], A.dmean[c * n + i], A.lr_mean);
+    for (int c = 0; c < 3; ++c)
+      A.mean[c * n + i] = adam_at(P, A.m, A.v, c, n, i, A.mean[c * n + i], A.dmean[c * n + i], P.lr_mean);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const float s = c == 0 ? s0 : (c == 1 ? s1 : s2);
-      const float gs = (A.dscale[c * n + i] + (c == kmin ? gflat : 0.f)) * s;  // d/dlog s = s d/ds
-      const float r = adam(A, 3 + c, i, A.log_scale[c * n + i], gs, A.lr_scale);
+      const float r = adam_at(P, A.m, A.v, 3 + c, n, i, A.log_scale[c * n + i],
+                              dlog_scale(A.dscale[c * n + i], c == kmin, gflat, s), P.lr_scale);
       A.log_scale[c * n + i] = r;
       A.scale[c * n + i] = expf(r);
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) A.rot[c * n + i] = adam(A, 6 + c, i, A.rot[c * n + i], A.drot[c * n + i], A.lr_rot);
+    for (int c = 0; c < 4; ++c)
+      A.rot[c * n + i] = adam_at(P, A.m, A.v, 6 + c, n, i, A.rot[c * n + i], A.drot[c * n + i], P.lr_rot);
     {
       const float o = A.op[i];
-      const float r = adam(A, 10, i, A.logit_op[i], A.dop[i] * o * (1.f - o), A.lr_op);  // d/dlogit = o(1-o) d/do
+      const float r = adam_at(P, A.m, A.v, 10, n, i, A.logit_op[i], dlogit_opacity(A.dop[i], o), P.lr_op);
       A.logit_op[i] = r;
       A.op[i] = 1.f / (1.f + expf(-r));
     }
@@ -463,15 +449,15 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs A) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const size_t k = (size_t)(11 + c + q) * n + i, e = (size_t)(c + q) * n + i;
-        const float m = A.b1 * mq[q] + (1.f - A.b1) * gq[q];
-        const float v = A.b2 * vq[q] + (1.f - A.b2) * gq[q] * gq[q];
-        A.m[k] = m;
-        A.v[k] = v;
-        A.sh[e] = rq[q] - __fdividef((c + q < 3 ? A.lr_dc : A.lr_rest) * A.ibc1 * m, sqrt_approx(v) * A.isbc2 + A.eps);
+        const float r = adam_elem(P, mq[q], vq[q], rq[q], gq[q], c + q < 3 ? P.lr_dc : P.lr_rest);
+        A.m[k] = mq[q];
+        A.v[k] = vq[q];
+        A.sh[e] = r;
       }
     }
     for (; c < A.K3; ++c)
-      A.sh[c * n + i] = adam(A, 11 + c, i, A.sh[c * n + i], A.dsh[c * n + i], c < 3 ? A.lr_dc : A.lr_rest);
+      A.sh[c * n + i] = adam_at(P, A.m, A.v, 11 + c, n, i, A.sh[c * n + i], A.dsh[c * n + i],
+                                c < 3 ? P.lr_dc : P.lr_rest);
   }
   float v = smin;
 #pragma unroll
@@ -557,11 +543,7 @@ cudaError_t launch_adam(int n, int sh_degree, const pgsag_gaussian_grad* gr, pgs
   A.dmean = gr->dmean; A.dscale = gr->dscale; A.drot = gr->drot; A.dop = gr->dopacity; A.dsh = gr->dsh;
   A.mean = s->mean; A.scale = s->scale; A.rot = s->rot; A.op = s->opacity; A.sh = s->sh;
   A.log_scale = s->log_scale; A.logit_op = s->logit_opacity; A.m = s->m; A.v = s->v;
-  A.lr_mean = hp->lr_mean; A.lr_scale = hp->lr_scale; A.lr_rot = hp->lr_rot; A.lr_op = hp->lr_opacity;
-  A.lr_dc = hp->lr_sh_dc; A.lr_rest = hp->lr_sh_rest;
-  A.b1 = hp->beta1; A.b2 = hp->beta2; A.eps = hp->eps; A.flat_w = hp->flatten_weight;
-  A.ibc1 = (float)(1.0 / (1.0 - pow((double)hp->beta1, (double)hp->step)));
-  A.isbc2 = (float)(1.0 / sqrt(1.0 - pow((double)hp->beta2, (double)hp->step)));
+  A.P = adam_params(hp);
   A.flat = flat;
   if (flat) {
     cudaError_t e = cudaMemsetAsync(flat, 0, sizeof(double), st);

@@ -247,8 +247,7 @@ class Rasterizer:
         return dict(C=self.img_C, N=self.img_N, D=self.img_D, A=self.img_A, Dep=self.img_Dep, T=self.img_T,
                     g=self.img_g, last=self.img_last)
 
-    def backward(self, dC=None, dN=None, dD=None, dA=None, dDep=None, gc_lambda=0.0, nd_div=None):
-        """nd_div: optional device float64 scalar dividing dN and dDep (pgsag_image_grad.nd_div)."""
+    def _image_grad(self, dC, dN, dD, dA, dDep, gc_lambda, nd_div):
         ig = L.ImageGrad()
         ig.gc_lambda = float(gc_lambda)
         ig.nd_div = None if nd_div is None else nd_div.data_ptr()
@@ -257,6 +256,20 @@ class Rasterizer:
                 assert t.dtype == torch.float32 and t.is_contiguous() and t.device == self.device
             setattr(ig, k, None if t is None else t.data_ptr())
         self._keep = (dC, dN, dD, dA, dDep)
+        return ig
+
+    def backward_adam(self, state, hparams, flat, dC=None, dN=None, dD=None, dA=None, dDep=None, gc_lambda=0.0,
+                      nd_div=None):
+        """A7 + A8 with the Adam step fused into A8 (pgsag_render_bwd_adam): state (L.AdamState over the
+        last forward's Gaussians) is updated in place; no parameter gradients are written."""
+        ig = self._image_grad(dC, dN, dD, dA, dDep, gc_lambda, nd_div)
+        L.render_bwd_adam(self._g, self._cam, self._proj, self._bins, self._tm, C.c_void_p(self._mask.data_ptr()),
+                          self._bg, self._img, ig, self._grad, state, hparams, flat,
+                          C.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream())
+
+    def backward(self, dC=None, dN=None, dD=None, dA=None, dDep=None, gc_lambda=0.0, nd_div=None):
+        """nd_div: optional device float64 scalar dividing dN and dDep (pgsag_image_grad.nd_div)."""
+        ig = self._image_grad(dC, dN, dD, dA, dDep, gc_lambda, nd_div)
         L.render_bwd(self._g, self._cam, self._proj, self._bins, self._tm, C.c_void_p(self._mask.data_ptr()),
                      self._bg, self._img, ig, self._grad, C.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream())
         K3 = (self.deg + 1) ** 2 * 3

@@ -51,8 +51,11 @@ class Trainer:
     """Owns the optimiser state of one sub-region's Gaussians (g is updated in place)."""
 
     def __init__(self, raster: Rasterizer, g: GaussianTensors, cfg: AdamConfig | None = None, lam=LAMBDA,
-                 lam3=LAMBDA3, lam4=LAMBDA4, boundary_w=0.1):
+                 lam3=LAMBDA3, lam4=LAMBDA4, boundary_w=0.1, fused=True):
+        """fused: single-rank steps apply Adam inside A8 (pgsag_render_bwd_adam); False runs A8 then
+        pgsag_adam_step (bitwise the same result; the gradients land in raster.dmean etc.)."""
         self.r, self.g, self.cfg = raster, g, cfg or AdamConfig()
+        self.fused = bool(fused)
         self.lam, self.lam3, self.lam4, self.bw = float(lam), float(lam3), float(lam4), float(boundary_w)
         dev, n, H, W = raster.device, g.n, raster.H, raster.W
         K3 = (g.sh_degree + 1) ** 2 * 3
@@ -132,16 +135,20 @@ class Trainer:
             main.wait_event(ev_ban)
         self.used_gc = gc_w is not None
         r._grad.densify_accum, r._grad.densify_count = self.accum.data_ptr(), self.count.data_ptr()
+        up = dict(dC=self.dC, dN=self.dN if self.used_ban else None, dDep=self.dDep if self.used_ban else None,
+                  gc_lambda=self.lam if self.used_gc else 0.0, nd_div=self.loss_ban[1:] if self.used_ban else None)
         try:
-            r.backward(dC=self.dC, dN=self.dN if self.used_ban else None, dDep=self.dDep if self.used_ban else None,
-                       gc_lambda=self.lam if self.used_gc else 0.0,
-                       nd_div=self.loss_ban[1:] if self.used_ban else None)
+            if dp_group is None and self.fused:  # A8 applies the Adam step: no gradient round trip
+                r.backward_adam(self._state, self.hparams(), p(self.loss_flat), **up)
+            else:
+                r.backward(**up)
         finally:
             r._grad.densify_accum = r._grad.densify_count = None
-        if dp_group is not None:
-            K3 = (self.g.sh_degree + 1) ** 2 * 3
-            shard.allreduce_mean([r.dmean, r.dscale, r.drot, r.dopacity, r.dsh[:K3]], dp_group)
-        L.adam_step(self.g.n, self.g.sh_degree, r._grad, self._state, self.hparams(), p(self.loss_flat), st)
+        if dp_group is not None or not self.fused:
+            if dp_group is not None:
+                K3 = (self.g.sh_degree + 1) ** 2 * 3
+                shard.allreduce_mean([r.dmean, r.dscale, r.drot, r.dopacity, r.dsh[:K3]], dp_group)
+            L.adam_step(self.g.n, self.g.sh_degree, r._grad, self._state, self.hparams(), p(self.loss_flat), st)
 
     def step_photo(self, cam, mask: torch.Tensor, target: torch.Tensor, bg=(0.0, 0.0, 0.0), dp_group=None,
                    band_radius=1):

@@ -174,7 +174,7 @@ def test_train_iteration_parity():
     # GPU iteration
     g = GaussianTensors.from_numpy(sc.gaussians)
     r = Rasterizer(g.n, W, H, g.sh_degree)
-    tr = Trainer(r, g, AdamConfig(), lam=lam, lam3=lam3)
+    tr = Trainer(r, g, AdamConfig(), lam=lam, lam3=lam3, fused=False)  # keeps the gradients for the check
     m_t = torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda()
     tgt = torch.from_numpy(np.ascontiguousarray(target, np.float32)).cuda()
     tr.step(camera_from(sc.camera), m_t, tgt)
@@ -399,3 +399,42 @@ def test_step_photo_matches_step():
     for k in ("rgb", "ban", "gc_load", "flat"):
         assert abs(la[k] - lb[k]) <= 1e-6 * max(1.0, abs(la[k])), k
     assert np.allclose(mma, mmb, rtol=1e-4, atol=1e-9 * np.abs(mma).max())
+
+
+@pytest.mark.parametrize("deg", [3, 1])
+def test_fused_adam_matches_separate_step(deg):
+    """pgsag_render_bwd_adam (Adam applied inside A8) against pgsag_render_bwd + pgsag_adam_step over
+    three iterations with every loss term (L_rgb, L_s, L_ban, L_GC-load) and the densification
+    statistic: the same update arithmetic (adam.cuh), so the only difference is the run-to-run order
+    of A7's float atomics (a few ulp in the gradients)."""
+    sc = S.config1(seed=60 + deg, n=900, W=96, H=64)
+    if deg != sc.gaussians.sh_degree:
+        import dataclasses
+        K = (deg + 1) ** 2
+        sc = dataclasses.replace(sc, gaussians=dataclasses.replace(
+            sc.gaussians, sh=np.ascontiguousarray(sc.gaussians.sh[:3 * K]), sh_degree=deg))
+    H, W = sc.mask.shape
+    m_t = torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda()
+    tgt = torch.from_numpy(S.reference_image(H, W, 61)).cuda()
+    runs = []
+    for fused in (True, False):
+        g = GaussianTensors.from_numpy(sc.gaussians)
+        r = Rasterizer(g.n, W, H, g.sh_degree)
+        tr = Trainer(r, g, AdamConfig(lr_mean=1e-3), fused=fused)
+        cam = camera_from(sc.camera)
+        gc_w, band = r.gc_weights(tgt, m_t), r.boundary_band(m_t, 1)
+        for _ in range(3):
+            tr.step(cam, m_t, tgt, gc_w=gc_w, band=band)
+        torch.cuda.synchronize()
+        runs.append(dict(mean=g.mean, scale=g.scale, rot=g.rot, opacity=g.opacity, sh=g.sh, log_scale=tr.log_scale,
+                         logit_opacity=tr.logit_opacity, m=tr.m, v=tr.v, accum=tr.accum, count=tr.count,
+                         flat=tr.loss_flat))
+    a, b = runs
+    for k in a:
+        x, y = a[k].double().cpu().numpy(), b[k].double().cpu().numpy()
+        x = x.reshape(x.shape[0], -1) if x.ndim > 1 else x[None]
+        y = y.reshape(y.shape[0], -1) if y.ndim > 1 else y[None]
+        sc_ = np.maximum(np.abs(y).max(axis=1, keepdims=True), 1e-30)
+        err = np.abs(x - y) / np.maximum(np.abs(y), 1e-3 * sc_)
+        assert err.max() <= 1e-4, (k, err.max())
+    assert torch.equal(a["count"], b["count"])
