@@ -143,3 +143,30 @@ def test_next_row_calls_validate_on_host(lib):
     # measurement aid: bad mode
     t = C.c_double()
     assert L.pgsag_microbench_fp32(7, 10, dummy, C.byref(t), None) == lib.PGSAG_EINVAL
+
+
+def test_render_bwd_adam_validates_on_host(lib):
+    """pgsag_render_bwd_adam: NULL optimiser arguments, step 0 and a state that does not hold the
+    Gaussians' own arrays are rejected before any device work."""
+    L = lib.lib()
+    d = C.c_void_p(256)  # never dereferenced: validation fails first
+    g = lib.Gaussians(10, 3, d, d, d, d, d)
+    cam = lib.Camera()
+    cam.width, cam.height, cam.fx, cam.fy = 64, 64, 64.0, 64.0
+    p = lib.Projected(*([d] * 8))
+    tm = lib.TileMask(d, None, d, d, d)
+    bins = lib.Bins(d, d, d, 1 << 20, 0, None)
+    fwd = lib.Image(*([d] * 8), None, None, None)
+    ig, out, st, hp = lib.ImageGrad(), lib.GaussianGrad(), lib.AdamState(*([d] * 9)), lib.AdamHparams()
+    bg = (C.c_float * 3)()
+    args = lambda st_, hp_: (C.byref(g), C.byref(cam), C.byref(p), C.byref(bins), C.byref(tm), d, C.byref(bg),
+                             C.byref(fwd), C.byref(ig), C.byref(out), st_, hp_, None, d, 1 << 40, None)
+    hp.step = 1
+    assert L.pgsag_render_bwd_adam(*args(None, C.byref(hp))) == lib.PGSAG_EINVAL
+    hp.step = 0
+    assert L.pgsag_render_bwd_adam(*args(C.byref(st), C.byref(hp))) == lib.PGSAG_EINVAL
+    assert b"step" in L.pgsag_last_error()
+    hp.step = 1
+    st.mean = C.c_void_p(512)  # not g's array
+    assert L.pgsag_render_bwd_adam(*args(C.byref(st), C.byref(hp))) == lib.PGSAG_EINVAL
+    assert b"state" in L.pgsag_last_error()
