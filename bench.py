@@ -491,7 +491,7 @@ def main():
         gt_ = GaussianTensors(*(getattr(g, k).clone() for k in ("mean", "scale", "rot", "opacity", "sh")),
                               g.sh_degree)
         tr = Trainer(r, gt_)
-        kt = min(args.steps, 5)
+        kt = args.steps  # the same K views as the timed rasterizer steps
         tviews = views[:kt]
         tgt = torch.rand(3, H, W, device=dev, generator=gen)  # synthetic target photo
         for v in tviews[:2]:  # warm-up
