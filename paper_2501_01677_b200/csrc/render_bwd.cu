@@ -236,8 +236,12 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   const uint32_t rec_base = opaque(smem_u32(s_rec)), list_base = opaque(smem_u32(s_list));
   unsigned long long cntV = 0;
   // value index this lane owns after the reduce-scatter: bit-reversed lane bits 1..4
-  const int my_c = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
-  const bool writer = ((lane & 1) == 0) && my_c < kG2;
+  // slot this lane owns after the reduce-scatter: bit-reversed lane bits 1..4.  Values 0..6 sit
+  // in slots 0..6 and values 7..13 in slots 8..14; slots 7 and 15 stay zero, so the first
+  // butterfly level has one all-zero pair the compiler drops.
+  const int my_s = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
+  const int my_c = my_s < 7 ? my_s : my_s - 1;  // value index of the slot
+  const bool writer = ((lane & 1) == 0) && my_s != 7 && my_s != 15;
   // loop-invariant lane values pinned in registers (otherwise re-derived from S2R per candidate)
   const uint32_t lbits = opaque((uint32_t)lane);
   const uint32_t acc_lane = opaque(smem_u32(s_acc) + (uint32_t)my_c * 4u);
@@ -359,10 +363,10 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
                   cd, nn, o01);
         pair_grad<kGC>(P23, f2(al2, al3), f2(u2 ? al2 : 0.f, u3 ? al3 : 0.f), f2(u2 ? rh23.x : 0.f, u3 ? rh23.y : 0.f),
                   cd, nn, o23);
-        float v[16];
+        float v[16];  // slot k holds value k (k < 7) or value k - 1 (8 <= k < 15); slots 7, 15 zero
 #pragma unroll
         for (int c = 0; c < 7; ++c)
-          v[6 + c] = hsum(__ffma2_rn(o23.wt, P23.G[c], __fmul2_rn(o01.wt, P01.G[c])));
+          v[c == 0 ? 6 : 7 + c] = hsum(__ffma2_rn(o23.wt, P23.G[c], __fmul2_rn(o01.wt, P01.G[c])));
         v[5] = hsum(__fadd2_rn(o01.dop, o23.dop));
         const float sdp = hsum(__fadd2_rn(o01.dpow, o23.dpow));
         const float2 dydp01 = __fmul2_rn(dy01, o01.dpow), dydp23 = __fmul2_rn(dy23, o23.dpow);
@@ -381,14 +385,14 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           const float2 dv23 = __fmul2_rn(__ffma2_rn(bc(twoC), dy23, bc(bdx)), kd23);
           v[0] = hsum(__fadd2_rn(du01, du23));
           v[1] = hsum(__fadd2_rn(dv01, dv23));
-          v[13] = ((fabsf(du01.x) + fabsf(dv01.x)) + (fabsf(du01.y) + fabsf(dv01.y))) +
+          v[14] = ((fabsf(du01.x) + fabsf(dv01.x)) + (fabsf(du01.y) + fabsf(dv01.y))) +
                   ((fabsf(du23.x) + fabsf(dv23.x)) + (fabsf(du23.y) + fabsf(dv23.y)));
         } else {  // sums only: du = -ln2 (B' dy + 2 A' dx) dpow, dv = -ln2 (2 C' dy + B' dx) dpow per pixel
           v[0] = -kLn2 * fmaf(ra.w, sdydp, twoA * sdp);
           v[1] = -kLn2 * fmaf(twoC, sdydp, bdx * sdp);
-          v[13] = 0.f;
+          v[14] = 0.f;
         }
-        v[14] = 0.f;
+        v[7] = 0.f;
         v[15] = 0.f;
         // reduce-scatter 16 -> 1 value per lane pair
         float v8[8], v4[4], v2[2], v1[1];
