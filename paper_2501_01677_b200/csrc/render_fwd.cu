@@ -156,8 +156,10 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
 #pragma unroll
       for (int p = 0; p < NP; ++p) lastf[p] = f2(-1.f, -1.f);
       const uint32_t lbase = list_base + (uint32_t)(w * BATCH);
-      for (int t = 0; t < nw; ++t) {
-        if ((t & 7) == 0 && __all_sync(0xffffffffu, all_done())) break;
+      for (int t0 = 0; t0 < nw; t0 += 8) {  // the warp's early-out test once per 8 candidates
+      if (__all_sync(0xffffffffu, all_done())) break;
+      const int tend = min(t0 + 8, nw);
+      for (int t = t0; t < tend; ++t) {
         const uint32_t q = lds_u8(lbase + (uint32_t)t);
         const uint32_t ra_addr = rec_base + q * (uint32_t)sizeof(Rec);
         const float4 ra = lds128(ra_addr);
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
           // lastf <- okf ? slot : lastf, exactly (small integers)
           lastf[p] = __ffma2_rn(okf, __fadd2_rn(f2(rb.w, rb.w), f2(-lastf[p].x, -lastf[p].y)), lastf[p]);
         }
+      }
       }
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
