@@ -312,9 +312,11 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       build_lists<kBT, kBEPT, kBNB>(mk, s_list, s_wc, s_nw);
       const int qtop = wlast - blo;  // entries past the warp's last are never needed
       const uint32_t lbase = list_base + (uint32_t)((kBW > 1 ? w : 0) * kBBatch);
-      for (int t = s_nw[kBW > 1 ? w : 0] - 1; t >= 0; --t) {
+      // the list is in ascending slot order: drop its tail past the warp's last entry up front
+      int t = s_nw[kBW > 1 ? w : 0] - 1;
+      while (t >= 0 && (int)lds_u8(lbase + (uint32_t)t) > qtop) --t;  // warp-uniform
+      for (; t >= 0; --t) {
         const int q = (int)lds_u8(lbase + (uint32_t)t);
-        if (q > qtop) continue;  // warp-uniform
         const int kk = blo + q;
         const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
         const float4 ra = lds128(ra_addr);
