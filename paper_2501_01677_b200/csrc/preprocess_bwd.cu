@@ -93,6 +93,13 @@ __device__ __forceinline__ void a8_gaussian(
   constexpr int K = (DEG + 1) * (DEG + 1);
   if (i >= n) return;
   const uint32_t fl = flags[i];
+  // every per-Gaussian load issued before the liveness branch: one memory latency, not two
+  float4 g2v[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) g2v[c] = g2d[(size_t)i * 4 + c];
+  const float mf[3] = {mean[i], mean[n + i], mean[2 * n + i]};
+  const float rf[4] = {rot[i], rot[n + i], rot[2 * n + i], rot[3 * n + i]};
+  const float sf[3] = {scale[i], scale[n + i], scale[2 * n + i]};
   if ((fl & PGSAG_F_LIVE) != PGSAG_F_LIVE) {
     if (kAdam) {
 #pragma unroll
@@ -114,7 +121,7 @@ __device__ __forceinline__ void a8_gaussian(
   double gg[16];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    const float4 q = g2d[(size_t)i * 4 + c];
+    const float4 q = g2v[c];
     gg[4 * c] = q.x; gg[4 * c + 1] = q.y; gg[4 * c + 2] = q.z; gg[4 * c + 3] = q.w;
   }
   if (grad2d) {
@@ -122,19 +129,19 @@ __device__ __forceinline__ void a8_gaussian(
     for (int c = 0; c < kG2; ++c) grad2d[(size_t)c * n + i] = (float)gg[c];
   }
   const double* Rc = cam.R;
-  const double t[3] = {(double)mean[i] - cam.C[0], (double)mean[n + i] - cam.C[1], (double)mean[2 * n + i] - cam.C[2]};
+  const double t[3] = {(double)mf[0] - cam.C[0], (double)mf[1] - cam.C[1], (double)mf[2] - cam.C[2]};
   double pc[3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) pc[r] = Rc[3 * r] * t[0] + Rc[3 * r + 1] * t[1] + Rc[3 * r + 2] * t[2];
   const double x = pc[0], y = pc[1], z = pc[2];
-  const double q0[4] = {rot[i], rot[n + i], rot[2 * n + i], rot[3 * n + i]};
+  const double q0[4] = {rf[0], rf[1], rf[2], rf[3]};
   const double qn = sqrt(q0[0] * q0[0] + q0[1] * q0[1] + q0[2] * q0[2] + q0[3] * q0[3]);
   const double w = q0[0] / qn, X = q0[1] / qn, Y = q0[2] / qn, Z = q0[3] / qn;
   double Rg[3][3];
   Rg[0][0] = 1. - 2. * (Y * Y + Z * Z); Rg[0][1] = 2. * (X * Y - w * Z); Rg[0][2] = 2. * (X * Z + w * Y);
   Rg[1][0] = 2. * (X * Y + w * Z); Rg[1][1] = 1. - 2. * (X * X + Z * Z); Rg[1][2] = 2. * (Y * Z - w * X);
   Rg[2][0] = 2. * (X * Z - w * Y); Rg[2][1] = 2. * (Y * Z + w * X); Rg[2][2] = 1. - 2. * (X * X + Y * Y);
-  const double s[3] = {scale[i], scale[n + i], scale[2 * n + i]};
+  const double s[3] = {sf[0], sf[1], sf[2]};
   double Mg[3][3], Sig[3][3];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
