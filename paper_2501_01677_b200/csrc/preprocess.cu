@@ -171,6 +171,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
   const float t0 = __ldg(mean + i) - cam.C[0];
   const float t1 = __ldg(mean + n + i) - cam.C[1];
   const float t2 = __ldg(mean + 2 * n + i) - cam.C[2];
+  // the other per-Gaussian loads issued before the visibility branch (one memory latency)
+  const float qw0 = __ldg(rot + i), qx0 = __ldg(rot + n + i), qy0 = __ldg(rot + 2 * n + i),
+              qz0 = __ldg(rot + 3 * n + i);
+  const float s[3] = {__ldg(scale + i), __ldg(scale + n + i), __ldg(scale + 2 * n + i)};
+  const float opv = __ldg(opac + i);
   const float* Rc = cam.R;
   const float x = (Rc[0] * t0 + Rc[1] * t1) + Rc[2] * t2;
   const float y = (Rc[3] * t0 + Rc[4] * t1) + Rc[5] * t2;
@@ -193,8 +198,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     uv.y = cam.fy * yz + cam.cy;
 
     // quaternion -> rotation (w,x,y,z), normalised
-    const float qw0 = __ldg(rot + i), qx0 = __ldg(rot + n + i), qy0 = __ldg(rot + 2 * n + i),
-                qz0 = __ldg(rot + 3 * n + i);
     const float qn = sqrtf(((qw0 * qw0 + qx0 * qx0) + qy0 * qy0) + qz0 * qz0);
     const float qw = qw0 / qn, qx = qx0 / qn, qy = qy0 / qn, qz = qz0 / qn;
     float Rg[3][3];
@@ -207,7 +210,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     Rg[2][0] = 2.0f * (qx * qz - qw * qy);
     Rg[2][1] = 2.0f * (qy * qz + qw * qx);
     Rg[2][2] = 1.0f - 2.0f * (qx * qx + qy * qy);
-    const float s[3] = {__ldg(scale + i), __ldg(scale + n + i), __ldg(scale + 2 * n + i)};
     float Mg[3][3], Sig[3][3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     const float det = A * Cc - B * B;
     if (det > 0.0f) {
       fl |= PGSAG_F_DET_OK;
-      const float o = __ldg(opac + i);
+      const float o = opv;
       co = make_float4(Cc / det, -B / det, A / det, o);
       if (!(o < 1.0f / 255.0f)) {
         fl |= PGSAG_F_OPAC_OK;
