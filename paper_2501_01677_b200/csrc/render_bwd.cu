@@ -123,45 +123,50 @@ struct PixState {
   int last;
 };
 
-__device__ __forceinline__ void load_pixel(const BwdArgs& a, bool masked, size_t pix, size_t HW, float px, float py,
+// inb: the pixel lies inside the image.  Every load is issued unconditionally (from pixel 0 when
+// outside) and the mask applied by selection afterwards, so the loads of the lane's pixels overlap
+// instead of waiting behind the mask test (one memory latency per tile).
+__device__ __forceinline__ void load_pixel(const BwdArgs& a, bool inb, size_t pix, size_t HW, float px, float py,
                                            PixState& s) {
-#pragma unroll
-  for (int c = 0; c < 8; ++c) s.G[c] = 0.f;
-  s.Pb = 0.f;
-  s.T = 1.f;
-  s.gG = 0.f;
-  s.last = -1;
-  if (!masked) return;
+  const size_t q = inb ? pix : 0;
+  const bool masked = inb && __ldg(a.mask + q) != 0;
+  const int last = __ldg(a.last + q), gcount = __ldg(a.g + q);
+  const float T = __ldg(a.T + q);
+  float G[8];
+  G[0] = ld_or0(a.dC, q); G[1] = ld_or0(a.dC, HW + q); G[2] = ld_or0(a.dC, 2 * HW + q);
+  G[3] = ld_or0(a.dN, q); G[4] = ld_or0(a.dN, HW + q); G[5] = ld_or0(a.dN, 2 * HW + q);
+  G[6] = ld_or0(a.dD, q);
+  G[7] = ld_or0(a.dA, q);
+  float gDep = ld_or0(a.dDep, q);
+  const float N0 = __ldg(a.N + q), N1 = __ldg(a.N + HW + q), N2 = __ldg(a.N + 2 * HW + q), D = __ldg(a.D + q);
+  const float w = a.gc_w ? __ldg(a.gc_w + q) : 1.0f;
+  float gG = 0.f;
   if (a.gc_w) {  // Eq. 9: L = std(r), r = g / w  ->  dL/dg = (r - mean) / (N L w)
-    const double N = a.gc_stats[0], mu = a.gc_stats[1] / N;
-    const double L = sqrt(fmax(a.gc_stats[2] / N - mu * mu, 0.0));
-    const float w = __ldg(a.gc_w + pix);
-    if (L > 0.0) s.gG = (float)((double)a.gc_lambda * ((double)a.g[pix] / w - mu) / (N * L * w));
+    const double Nn = a.gc_stats[0], mu = a.gc_stats[1] / Nn;
+    const double L = sqrt(fmax(a.gc_stats[2] / Nn - mu * mu, 0.0));
+    if (L > 0.0) gG = (float)((double)a.gc_lambda * ((double)gcount / w - mu) / (Nn * L * w));
   }
-  s.last = a.last[pix];
-  s.T = a.T[pix];
-  s.G[0] = ld_or0(a.dC, pix); s.G[1] = ld_or0(a.dC, HW + pix); s.G[2] = ld_or0(a.dC, 2 * HW + pix);
-  s.G[3] = ld_or0(a.dN, pix); s.G[4] = ld_or0(a.dN, HW + pix); s.G[5] = ld_or0(a.dN, 2 * HW + pix);
-  s.G[6] = ld_or0(a.dD, pix);
-  s.G[7] = ld_or0(a.dA, pix);
-  float gDep = ld_or0(a.dDep, pix);
   if (a.nd_div) {  // sum-gradient of a mean loss: divide by its term count
     const double dv = *a.nd_div;
     const float sc = dv > 0.0 ? (float)(1.0 / dv) : 0.0f;
-    s.G[3] *= sc; s.G[4] *= sc; s.G[5] *= sc;
+    G[3] *= sc; G[4] *= sc; G[5] *= sc;
     gDep *= sc;
   }
   // Eq. 4 prologue: Dep = D / (N . r); validity re-derived exactly as A6 did
-  const float N0 = a.N[pix], N1 = a.N[HW + pix], N2 = a.N[2 * HW + pix];
   const float r0 = __fdiv_rn(__fsub_rn(px, a.cx), a.fx), r1 = __fdiv_rn(__fsub_rn(py, a.cy), a.fy);
   const float den = __fadd_rn(__fadd_rn(__fmul_rn(N0, r0), __fmul_rn(N1, r1)), N2);
-  if (a.g[pix] > 0 && fabsf(den) > 1e-6f) {
+  if (gcount > 0 && fabsf(den) > 1e-6f) {
     const float inv = 1.0f / den;
-    s.G[6] += gDep * inv;
-    const float c = gDep * a.D[pix] * inv * inv;
-    s.G[3] -= c * r0; s.G[4] -= c * r1; s.G[5] -= c;
+    G[6] += gDep * inv;
+    const float c = gDep * D * inv * inv;
+    G[3] -= c * r0; G[4] -= c * r1; G[5] -= c;
   }
-  s.Pb = a.bg0 * s.G[0] + a.bg1 * s.G[1] + a.bg2 * s.G[2];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s.G[c] = masked ? G[c] : 0.f;
+  s.Pb = masked ? a.bg0 * G[0] + a.bg1 * G[1] + a.bg2 * G[2] : 0.f;
+  s.T = masked ? T : 1.f;
+  s.gG = masked ? gG : 0.f;
+  s.last = masked ? last : -1;
 }
 
 // State of one packed pixel pair.
@@ -271,8 +276,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       for (int k = 0; k < 4; ++k) {
         const int j = jb + 4 * k;
         const size_t pix = (size_t)j * a.d.W + i;
-        const bool m = i < a.d.W && j < a.d.H && a.mask[pix] != 0;
-        load_pixel(a, m, pix, HW, px, (float)j + 0.5f, s[k]);
+        load_pixel(a, i < a.d.W && j < a.d.H, pix, HW, px, (float)j + 0.5f, s[k]);
       }
       make_pair(s[0], s[1], P01);
       make_pair(s[2], s[3], P23);
