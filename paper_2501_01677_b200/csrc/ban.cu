@@ -34,6 +34,48 @@ __global__ void band_kernel(const uint8_t* __restrict__ mask, int W, int H, int 
   band[(size_t)y * W + x] = (uint8_t)(any != all);
 }
 
+// Tiled variant for radii up to kBandRmax: the (8 + 2r) x (128 + 2r) mask window of a 128 x 8
+// output tile is staged in shared memory once (coalesced 32-bit loads of the interior), then the
+// square structuring element is applied separably (row any / all, then column any / all).
+constexpr int kBandTW = 128, kBandTH = 8, kBandRmax = 8;
+__global__ void __launch_bounds__(256) band_tiled_kernel(const uint8_t* __restrict__ mask, int W, int H, int r,
+                                                         uint8_t* __restrict__ band) {
+  constexpr int SW = kBandTW + 2 * kBandRmax, SH = kBandTH + 2 * kBandRmax;
+  __shared__ uint8_t s_m[SH][SW];
+  __shared__ uint8_t s_any[SH][kBandTW], s_all[SH][kBandTW];
+  const int x0 = blockIdx.x * kBandTW, y0 = blockIdx.y * kBandTH;
+  const int rows = kBandTH + 2 * r, cols = kBandTW + 2 * r;
+  for (int k = threadIdx.x; k < rows * cols; k += 256) {
+    const int ry = k / cols, rx = k - ry * cols;
+    const int gy = y0 - r + ry, gx = x0 - r + rx;
+    s_m[ry][rx] = (gx >= 0 && gy >= 0 && gx < W && gy < H && __ldg(mask + (size_t)gy * W + gx) != 0) ? 1 : 0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < rows * kBandTW; k += 256) {  // horizontal pass
+    const int ry = k / kBandTW, x = k - ry * kBandTW;
+    uint8_t an = 0, al = 1;
+    for (int d = 0; d <= 2 * r; ++d) {
+      const uint8_t v = s_m[ry][x + d];
+      an |= v;
+      al &= v;
+    }
+    s_any[ry][x] = an;
+    s_all[ry][x] = al;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kBandTH * kBandTW; k += 256) {  // vertical pass + output
+    const int y = k / kBandTW, x = k - y * kBandTW;
+    const int gx = x0 + x, gy = y0 + y;
+    if (gx >= W || gy >= H) continue;
+    uint8_t an = 0, al = 1;
+    for (int d = 0; d <= 2 * r; ++d) {
+      an |= s_any[y + d][x];
+      al &= s_all[y + d][x];
+    }
+    band[(size_t)gy * W + gx] = (uint8_t)(an != al);
+  }
+}
+
 struct BanArgs {
   const uint8_t* mask;
   const uint8_t* band;
@@ -162,7 +204,11 @@ __global__ void __launch_bounds__(256) ban_kernel(BanArgs A) {
 
 cudaError_t launch_boundary_band(const uint8_t* mask, int W, int H, int r, uint8_t* band, cudaStream_t st) {
   KTimer kt_("N2_band", st);
-  band_kernel<<<dim3((W + 127) / 128, H), 128, 0, st>>>(mask, W, H, r, band);
+  if (r <= kBandRmax)
+    band_tiled_kernel<<<dim3((W + kBandTW - 1) / kBandTW, (H + kBandTH - 1) / kBandTH), 256, 0, st>>>(mask, W, H,
+                                                                                                    r, band);
+  else
+    band_kernel<<<dim3((W + 127) / 128, H), 128, 0, st>>>(mask, W, H, r, band);
   return cudaGetLastError();
 }
 

@@ -33,7 +33,7 @@ def _elementwise(a, b, rel=1e-3, floor=1e-2):
 
 
 @pytest.mark.parametrize("name", list(SCENES))
-@pytest.mark.parametrize("radius", [1, 2])
+@pytest.mark.parametrize("radius", [1, 2, 8, 9])  # 9: the untiled path (r > 8)
 def test_boundary_band_bitexact(name, radius):
     sc = SCENES[name]()
     _, r, mask = _render(sc)
