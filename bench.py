@@ -404,7 +404,7 @@ def main():
             "A5_ranges": ("hbm", 4 * Mv + 8 * tiles_),
             "A6_render_fwd": ("alu", FLOP_EVAL * Ev + FLOP_BLEND_FWD * Bv),
             "A7_render_bwd": ("alu", FLOP_EVAL * Vv + FLOP_BLEND_BWD * Bv),
-            "A8_preprocess_bwd": ("hbm", 584 * n_),
+            "A8_preprocess_bwd": ("hbm", 536 * n_),  # 236 B params + 64 B 2D gradients read, 236 B written
         }
         hbm = float(peaks.get("hbm_gbs", 6551.4))
         fp32 = SM_COUNT * FP32_LANES * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
