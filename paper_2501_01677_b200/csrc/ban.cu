@@ -42,37 +42,56 @@ __global__ void __launch_bounds__(256) band_tiled_kernel(const uint8_t* __restri
                                                          uint8_t* __restrict__ band) {
   constexpr int SW = kBandTW + 2 * kBandRmax, SH = kBandTH + 2 * kBandRmax;
   __shared__ uint8_t s_m[SH][SW];
-  __shared__ uint8_t s_any[SH][kBandTW], s_all[SH][kBandTW];
+  __shared__ __align__(4) uint8_t s_any[SH][kBandTW], s_all[SH][kBandTW];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int x0 = blockIdx.x * kBandTW, y0 = blockIdx.y * kBandTH;
   const int rows = kBandTH + 2 * r, cols = kBandTW + 2 * r;
-  for (int k = threadIdx.x; k < rows * cols; k += 256) {
-    const int ry = k / cols, rx = k - ry * cols;
-    const int gy = y0 - r + ry, gx = x0 - r + rx;
-    s_m[ry][rx] = (gx >= 0 && gy >= 0 && gx < W && gy < H && __ldg(mask + (size_t)gy * W + gx) != 0) ? 1 : 0;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < rows * kBandTW; k += 256) {  // horizontal pass
-    const int ry = k / kBandTW, x = k - ry * kBandTW;
-    uint8_t an = 0, al = 1;
-    for (int d = 0; d <= 2 * r; ++d) {
-      const uint8_t v = s_m[ry][x + d];
-      an |= v;
-      al &= v;
+  for (int ry = ty; ry < rows; ry += 8) {  // window staging: a warp per row, 32 consecutive bytes
+    const int gy = y0 - r + ry;
+    const bool rin = gy >= 0 && gy < H;
+    for (int rx = tx; rx < cols; rx += 32) {
+      const int gx = x0 - r + rx;
+      s_m[ry][rx] = (rin && gx >= 0 && gx < W && __ldg(mask + (size_t)gy * W + gx) != 0) ? 1 : 0;
     }
-    s_any[ry][x] = an;
-    s_all[ry][x] = al;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kBandTH * kBandTW; k += 256) {  // vertical pass + output
-    const int y = k / kBandTW, x = k - y * kBandTW;
+  for (int ry = ty; ry < rows; ry += 8) {  // horizontal any / all: 4 adjacent columns per thread
+    const int x = 4 * tx;
+    uint32_t an = 0, al = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t a = 0, b = 1;
+      for (int d = 0; d <= 2 * r; ++d) {
+        const uint32_t v = s_m[ry][x + q + d];
+        a |= v;
+        b &= v;
+      }
+      an |= a << (8 * q);
+      al |= b << (8 * q);
+    }
+    *reinterpret_cast<uint32_t*>(&s_any[ry][x]) = an;
+    *reinterpret_cast<uint32_t*>(&s_all[ry][x]) = al;
+  }
+  __syncthreads();
+  {  // vertical any / all on 4 columns at once (bytes are 0 / 1), band = any xor all
+    const int x = 4 * tx, y = ty;
+    uint32_t an = 0, al = 0x01010101u;
+    for (int d = 0; d <= 2 * r; ++d) {
+      an |= *reinterpret_cast<const uint32_t*>(&s_any[y + d][x]);
+      al &= *reinterpret_cast<const uint32_t*>(&s_all[y + d][x]);
+    }
+    const uint32_t out = an ^ al;
     const int gx = x0 + x, gy = y0 + y;
-    if (gx >= W || gy >= H) continue;
-    uint8_t an = 0, al = 1;
-    for (int d = 0; d <= 2 * r; ++d) {
-      an |= s_any[y + d][x];
-      al &= s_all[y + d][x];
+    if (gy < H) {
+      uint8_t* dst = band + (size_t)gy * W + gx;
+      if (gx + 3 < W && (((size_t)gy * W + gx) & 3) == 0) {
+        *reinterpret_cast<uint32_t*>(dst) = out;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (gx + q < W) dst[q] = (uint8_t)((out >> (8 * q)) & 0xffu);
+      }
     }
-    band[(size_t)gy * W + gx] = (uint8_t)(an != al);
   }
 }
 
