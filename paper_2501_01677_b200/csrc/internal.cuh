@@ -124,7 +124,7 @@ cudaError_t launch_opacity_reset(int n, pgsag_adam_state* s, float cap, cudaStre
 
 cudaError_t launch_fp32_microbench(int mode, int iters, float* scratch, float* ms, double* flops, cudaStream_t st);
 
-// counters[] slot (as 2 doubles at byte offset 4*CNT_GC) for pgsag_gc_weights
+// counters[] slots for pgsag_gc_weights: 8 (sum, count) double pairs at bytes 4*CNT_GC .. 4*CNT_GC + 127
 constexpr int CNT_GC = 32;
 
 }  // namespace pgsag
