@@ -179,9 +179,10 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
           const float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
           if (kCount) cntE += (unsigned long long)(T[p].x > 0.f) + (unsigned long long)(T[p].y > 0.f);
           // blend iff still compositing, power <= 0 and alpha >= 1/255 (R6)
-          // e = would blend; ok = blends (e and T stays >= 1e-4); e && !ok = terminates here (R6)
-          const bool e0 = T[p].x > 0.f && p2.x <= 0.0f && al0 >= kAlphaMin;
-          const bool e1 = T[p].y > 0.f && p2.y <= 0.0f && al1 >= kAlphaMin;
+          // e = alpha passes (R6); ok = blends (e and T stays >= 1e-4: a done pixel has T < 0, so
+          // Tn < 0 and it never blends); e && !ok = terminates here, T <- -|T| (idempotent once done)
+          const bool e0 = p2.x <= 0.0f && al0 >= kAlphaMin;
+          const bool e1 = p2.y <= 0.0f && al1 >= kAlphaMin;
           const float2 Tn = __fmul2_rn(T[p], __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
           const bool ok0 = e0 && Tn.x >= kTmin, ok1 = e1 && Tn.y >= kTmin;
           // branch-free blend (predicated weights): no loop-carried phi copies.  The blend
@@ -198,8 +199,8 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
           N0[p] = __ffma2_rn(wt, f2(nn.x, nn.x), N0[p]);
           N1[p] = __ffma2_rn(wt, f2(nn.y, nn.y), N1[p]);
           N2[p] = __ffma2_rn(wt, f2(nn.z, nn.z), N2[p]);
-          T[p].x = ok0 ? Tn.x : (e0 ? -T[p].x : T[p].x);
-          T[p].y = ok1 ? Tn.y : (e1 ? -T[p].y : T[p].y);
+          T[p].x = ok0 ? Tn.x : (e0 ? -fabsf(T[p].x) : T[p].x);
+          T[p].y = ok1 ? Tn.y : (e1 ? -fabsf(T[p].y) : T[p].y);
           gc[p] = __fadd2_rn(gc[p], okf);  // blend counts (exact below 2^24)
           // lastf <- okf ? slot : lastf, exactly (small integers)
           lastf[p] = __ffma2_rn(okf, __fadd2_rn(f2(rb.w, rb.w), f2(-lastf[p].x, -lastf[p].y)), lastf[p]);
