@@ -157,55 +157,54 @@ __global__ void __launch_bounds__(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
       for (int p = 0; p < NP; ++p) lastf[p] = f2(-1.f, -1.f);
       const uint32_t lbase = list_base + (uint32_t)(w * BATCH);
       for (int t0 = 0; t0 < nw; t0 += 8) {  // the warp's early-out test once per 8 candidates
-      if (__all_sync(0xffffffffu, all_done())) break;
-      const int tend = min(t0 + 8, nw);
-      for (int t = t0; t < tend; ++t) {
-        const uint32_t q = lds_u8(lbase + (uint32_t)t);
-        const uint32_t ra_addr = rec_base + q * (uint32_t)sizeof(Rec);
-        const float4 ra = lds128(ra_addr);
-        const float4 rb = lds128(ra_addr + 16);
-        const float dx = px - ra.x;
-        const float tA = __fmul_rn(ra.z, dx);
-        const float4 cd = lds128(ra_addr + 32);
-        const float4 nn = lds128(ra_addr + 48);
+        if (__all_sync(0xffffffffu, all_done())) break;
+        const int tend = min(t0 + 8, nw);
+        for (int t = t0; t < tend; ++t) {
+          const uint32_t q = lds_u8(lbase + (uint32_t)t);
+          const uint32_t ra_addr = rec_base + q * (uint32_t)sizeof(Rec);
+          const float4 ra = lds128(ra_addr);
+          const float4 rb = lds128(ra_addr + 16);
+          const float dx = px - ra.x;
+          const float tA = __fmul_rn(ra.z, dx);
+          const float4 cd = lds128(ra_addr + 32);
+          const float4 nn = lds128(ra_addr + 48);
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          // p2 for the pair (bit-identical to power2r per element)
-          const float2 dy = __fadd2_rn(py[p], f2(-ra.y, -ra.y));
-          const float2 u = __ffma2_rn(f2(ra.w, ra.w), dy, f2(tA, tA));
-          const float2 cq = __fmul2_rn(__fmul2_rn(f2(rb.x, rb.x), dy), dy);
-          const float2 p2 = __ffma2_rn(f2(dx, dx), u, cq);
-          const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(ex2_approx(p2.x), ex2_approx(p2.y)));
-          const float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
-          if (kCount) cntE += (unsigned long long)(T[p].x > 0.f) + (unsigned long long)(T[p].y > 0.f);
-          // blend iff still compositing, power <= 0 and alpha >= 1/255 (R6)
-          // e = alpha passes (R6); ok = blends (e and T stays >= 1e-4: a done pixel has T < 0, so
-          // Tn < 0 and it never blends); e && !ok = terminates here, T <- -|T| (idempotent once done)
-          const bool e0 = p2.x <= 0.0f && al0 >= kAlphaMin;
-          const bool e1 = p2.y <= 0.0f && al1 >= kAlphaMin;
-          const float2 Tn = __fmul2_rn(T[p], __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
-          const bool ok0 = e0 && Tn.x >= kTmin, ok1 = e1 && Tn.y >= kTmin;
-          // branch-free blend (predicated weights): no loop-carried phi copies.  The blend
-          // indicator (alpha >= 1/255 > 0 when blended) is formed by a saturating multiply on
-          // the FMA pipe and drives the blend count and the last slot (the ALU pipe is the
-          // limiter here)
-          const float2 als = f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f);
-          const float2 okf = f2(__saturatef(als.x * 1e30f), __saturatef(als.y * 1e30f));
-          const float2 wt = __fmul2_rn(als, T[p]);
-          C0[p] = __ffma2_rn(wt, f2(cd.x, cd.x), C0[p]);
-          C1[p] = __ffma2_rn(wt, f2(cd.y, cd.y), C1[p]);
-          C2[p] = __ffma2_rn(wt, f2(cd.z, cd.z), C2[p]);
-          D[p] = __ffma2_rn(wt, f2(cd.w, cd.w), D[p]);
-          N0[p] = __ffma2_rn(wt, f2(nn.x, nn.x), N0[p]);
-          N1[p] = __ffma2_rn(wt, f2(nn.y, nn.y), N1[p]);
-          N2[p] = __ffma2_rn(wt, f2(nn.z, nn.z), N2[p]);
-          T[p].x = ok0 ? Tn.x : (e0 ? -fabsf(T[p].x) : T[p].x);
-          T[p].y = ok1 ? Tn.y : (e1 ? -fabsf(T[p].y) : T[p].y);
-          gc[p] = __fadd2_rn(gc[p], okf);  // blend counts (exact below 2^24)
-          // lastf <- okf ? slot : lastf, exactly (small integers)
-          lastf[p] = __ffma2_rn(okf, __fadd2_rn(f2(rb.w, rb.w), f2(-lastf[p].x, -lastf[p].y)), lastf[p]);
+          for (int p = 0; p < NP; ++p) {
+            // p2 for the pair (bit-identical to power2r per element)
+            const float2 dy = __fadd2_rn(py[p], f2(-ra.y, -ra.y));
+            const float2 u = __ffma2_rn(f2(ra.w, ra.w), dy, f2(tA, tA));
+            const float2 cq = __fmul2_rn(__fmul2_rn(f2(rb.x, rb.x), dy), dy);
+            const float2 p2 = __ffma2_rn(f2(dx, dx), u, cq);
+            const float2 orho = __fmul2_rn(f2(rb.y, rb.y), f2(ex2_approx(p2.x), ex2_approx(p2.y)));
+            const float al0 = fminf(kAlphaMax, orho.x), al1 = fminf(kAlphaMax, orho.y);
+            if (kCount) cntE += (unsigned long long)(T[p].x > 0.f) + (unsigned long long)(T[p].y > 0.f);
+            // e = alpha passes (R6); ok = blends (e and T stays >= 1e-4: a done pixel has T < 0, so
+            // Tn < 0 and it never blends); e && !ok = terminates here, T <- -|T| (idempotent once done)
+            const bool e0 = p2.x <= 0.0f && al0 >= kAlphaMin;
+            const bool e1 = p2.y <= 0.0f && al1 >= kAlphaMin;
+            const float2 Tn = __fmul2_rn(T[p], __fadd2_rn(f2(1.f, 1.f), f2(-al0, -al1)));
+            const bool ok0 = e0 && Tn.x >= kTmin, ok1 = e1 && Tn.y >= kTmin;
+            // branch-free blend (predicated weights): no loop-carried phi copies.  The blend
+            // indicator (alpha >= 1/255 > 0 when blended) is formed by a saturating multiply on
+            // the FMA pipe and drives the blend count and the last slot (the ALU pipe is the
+            // limiter here)
+            const float2 als = f2(ok0 ? al0 : 0.f, ok1 ? al1 : 0.f);
+            const float2 okf = f2(__saturatef(als.x * 1e30f), __saturatef(als.y * 1e30f));
+            const float2 wt = __fmul2_rn(als, T[p]);
+            C0[p] = __ffma2_rn(wt, f2(cd.x, cd.x), C0[p]);
+            C1[p] = __ffma2_rn(wt, f2(cd.y, cd.y), C1[p]);
+            C2[p] = __ffma2_rn(wt, f2(cd.z, cd.z), C2[p]);
+            D[p] = __ffma2_rn(wt, f2(cd.w, cd.w), D[p]);
+            N0[p] = __ffma2_rn(wt, f2(nn.x, nn.x), N0[p]);
+            N1[p] = __ffma2_rn(wt, f2(nn.y, nn.y), N1[p]);
+            N2[p] = __ffma2_rn(wt, f2(nn.z, nn.z), N2[p]);
+            T[p].x = ok0 ? Tn.x : (e0 ? -fabsf(T[p].x) : T[p].x);
+            T[p].y = ok1 ? Tn.y : (e1 ? -fabsf(T[p].y) : T[p].y);
+            gc[p] = __fadd2_rn(gc[p], okf);  // blend counts (exact below 2^24)
+            // lastf <- okf ? slot : lastf, exactly (small integers)
+            lastf[p] = __ffma2_rn(okf, __fadd2_rn(f2(rb.w, rb.w), f2(-lastf[p].x, -lastf[p].y)), lastf[p]);
+          }
         }
-      }
       }
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
