@@ -186,7 +186,8 @@ int pgsag_bin_sort(const pgsag_projected *p, const pgsag_tilemask *tm, const pgs
  * If m_out is non-NULL (pinned host or device memory) M is copied there, stream-ordered, after the
  * sort; the caller must check it once the stream has passed this point: if M > capacity the lists
  * are incomplete and the view must be re-sorted with capacity >= M (nothing is written past the
- * capacity). */
+ * capacity; the device-side entry count is then 0, so the later stages see empty lists, and the
+ * workspace's overflow flag makes pgsag_render_bwd_adam skip its update). */
 int pgsag_bin_sort_async(const pgsag_projected *p, const pgsag_tilemask *tm, const pgsag_camera *cam, int32_t n,
                          pgsag_bins *bins, unsigned long long *m_out, void *ws, size_t ws_bytes, void *stream);
 
@@ -295,7 +296,11 @@ int pgsag_adam_step(int32_t n, int32_t sh_degree, const pgsag_gaussian_grad *gra
  * must describe the same Gaussians as g (its mean / scale / rot / opacity / sh are g's arrays).  Of
  * out only absgrad2d, grad2d, densify_accum and densify_count are used (all optional); its
  * parameter-gradient pointers may be NULL.  For one optimiser per sub-region: ranks that average
- * gradients first (NEXT-4) call pgsag_render_bwd, all-reduce, then pgsag_adam_step. */
+ * gradients first (NEXT-4) call pgsag_render_bwd, all-reduce, then pgsag_adam_step.
+ * ws must be the workspace this view's pgsag_bin_sort(_async) used: if that sort overflowed the
+ * capacity (M > capacity, pgsag_bin_sort_async; the lists are then empty) the Adam update is
+ * skipped on the device (parameters, moments untouched), so a sync-free caller can detect the
+ * overflow afterwards and re-run the view without having applied a step from incomplete lists. */
 int pgsag_render_bwd_adam(const pgsag_gaussians *g, const pgsag_camera *cam, const pgsag_projected *p,
                           const pgsag_bins *bins, const pgsag_tilemask *tm, const uint8_t *mask, const float bg[3],
                           const pgsag_image *fwd, const pgsag_image_grad *dL, pgsag_gaussian_grad *out,

@@ -55,7 +55,7 @@ def lib():
                 getattr(L, nm).restype = None
             L.oracle_keys.argtypes = [P, P, P, i32, P, i32, i32, i64, P, P, P]
             L.oracle_keys.restype = i64
-            for nm in ("oracle_render_f32", "oracle_render_f64"):
+            for nm in ("oracle_render_f32", "oracle_render_f64", "oracle_render_f64_fproj"):
                 getattr(L, nm).argtypes = [P, P, P, P, P, i32, i32, P, i32, i32, P, P, P, i32, P, P, P, P,
                                            P, i32, P, P, P, P]
                 getattr(L, nm).restype = None
@@ -69,6 +69,8 @@ def lib():
             L.oracle_ban_loss.restype = None
             L.oracle_rgb_loss.argtypes = [P, P, P, i32, i32, P, P]
             L.oracle_rgb_loss.restype = None
+            L.oracle_set_bound_eval.argtypes = [i32]
+            L.oracle_set_bound_eval.restype = None
             L.oracle_sh_basis.argtypes = [C.c_double, C.c_double, C.c_double, P]
             L.oracle_sh_basis.restype = None
             L.oracle_lnup_f32.argtypes = [C.c_float]
@@ -140,11 +142,16 @@ def keys(proj, mask):
 
 
 def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=False, upstream=None,
-           bound=False):
+           bound=False, fproj=False):
     """O4 (and O5/O6 if upstream is given) for the listed flat pixel indices.
 
     upstream: (npix, 9) or (npix, 10) float64 = gC(3), gN(3), gD, gA, gDep[, gG] per listed pixel,
     gG = dL/d(soft count) of the L_GC-load surrogate (R24).
+    certify: True/1 counts pairs outside the tile rect with alpha >= 1/255 (R8, must be 0); an
+    integer 1 + s first shrinks every rect by s tiles per side (the certificate's negative control).
+    bound: also return the R19b + R19c float32 accumulation / evaluation bound on rows 0..58
+    ("acc": the R19b accumulation part alone, the R19c negative control).
+    fproj (dtype float64 only): O2 in float32, Eq. 1-4 / O5 / O6 in double.
     Returns dict: C (npix,3) N (npix,3) D A Dep T (npix,), g, gsoft, last (Gaussian id), near, n_clamped,
     id_sum, evaluated, cert_bad, and grads (73, n) float64 if upstream was given.
     """
@@ -169,16 +176,20 @@ def render(g, cam, mask, pixels, bg=(0.0, 0.0, 0.0), dtype=np.float32, certify=F
     gsoft = np.zeros(npix, np.float64)
     bnd = np.zeros((59, n), np.float64) if (bound and upstream is not None) else None
     fn = lib().oracle_render_f32 if dtype == np.float32 else lib().oracle_render_f64
+    lib().oracle_set_bound_eval(0 if bound == "acc" else 1)
+    if fproj:
+        assert dtype == np.float64
+        fn = lib().oracle_render_f64_fproj
     ca = cam_array(cam)
     fn(*[_p(a) for a in prm], n, int(g.sh_degree), _p(ca), W, H, _p(m), _p(bgd), _p(pix), npix, _p(out),
-       _p(iout), _p(id_sum), _p(evaluated), _p(gsoft), int(bool(certify)), _p(cert), _p(up), _p(grads), _p(bnd))
+       _p(iout), _p(id_sum), _p(evaluated), _p(gsoft), int(certify), _p(cert), _p(up), _p(grads), _p(bnd))
     res = dict(C=out[:, 0:3], N=out[:, 3:6], D=out[:, 6], A=out[:, 7], Dep=out[:, 8], T=out[:, 9],
                g=iout[:, 0], last=iout[:, 1], near=iout[:, 2], n_clamped=iout[:, 3], id_sum=id_sum,
                evaluated=evaluated, cert_bad=int(cert[0]), gsoft=gsoft)
     if grads is not None:
         res["grads"] = grads
     if bnd is not None:
-        res["bound"] = bnd  # R19b: float32-accumulation bound on rows 0..58 of grads
+        res["bound"] = bnd  # R19b + R19c: float32 accumulation / evaluation bound on rows 0..58
     return res
 
 

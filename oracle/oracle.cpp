@@ -414,8 +414,10 @@ template <typename R> struct Renderer {
     return o;
   }
 
-  // Certificate: pairs excluded by the rect that would have alpha >= 1/255.
-  long long certify(int i, int j) const {
+  // Certificate: pairs excluded by the rect that would have alpha >= 1/255.  shrink > 0 (negative
+  // control of the certificate itself, tests only) first narrows every rect by that many tiles
+  // per side, which must then produce excluded pairs.
+  long long certify(int i, int j, int shrink = 0) const {
     long long bad = 0;
     const int tx = i / 16, ty = j / 16;
     const R px = (R)i + (R)0.5, py = (R)j + (R)0.5;
@@ -423,8 +425,8 @@ template <typename R> struct Renderer {
       const Proj<R>& g = proj[id];
       const uint32_t need = F_VISIBLE | F_DET_OK | F_OPAC_OK;
       if ((g.flags & need) != need) continue;
-      const bool inrect = (g.flags & F_RECT) && tx >= g.rect[0] && tx <= g.rect[2] &&
-                          ty >= g.rect[1] && ty <= g.rect[3];
+      const bool inrect = (g.flags & F_RECT) && tx >= g.rect[0] + shrink && tx <= g.rect[2] - shrink &&
+                          ty >= g.rect[1] + shrink && ty <= g.rect[3] - shrink;
       if (inrect) continue;
       const R dx = px - g.u, dy = py - g.v;
       const R power = (R)-0.5 * ((g.ca * dx) * dx + (g.cc * dy) * dy) - (g.cb * dx) * dy;
@@ -442,7 +444,93 @@ struct G2 {
   // sums over pixels of |contribution| for the 13 values above (du .. ddist): the scale of the
   // float32 rounding of a GPU that sums the same per-pixel terms (R19b)
   double abs[13];
+  // R19c: first-order bound on what float32 EVALUATION of alpha / rho / T (GPU and this oracle's
+  // float build each round them on their own) can move the same 13 sums; see eval_bound()
+  double ev[13];
 };
+
+// R19c: first-order bound on the change of one pixel's per-Gaussian 2D-gradient terms when every
+// blended alpha_k (and rho_k) carries a relative error e_k and every T_m a relative error E_m --
+// the size of the difference between two float32 evaluations of the same Eq. 2 / Eq. 1 chain
+// (the CUDA path's and this oracle's float build), which decide identically (R18 excludes
+// pixels near a threshold) but round differently.  Derivation (R19c):
+//  * e_k = 16 eps (mag_k + 1), eps = 2^-24, mag_k = |a|dx^2/2 + |c|dy^2/2 + |b dx dy| the
+//    magnitude of Eq. 2's terms: the GPU rounds 3 pre-scaled coefficients and 3 fused ops
+//    (<= 6 eps log2(e) mag in the base-2 exponent -> 6 eps mag in rho) plus ex2.approx
+//    (<= 2^-22 = 4 eps) and o*rho (eps); the float oracle rounds 7 products/sums of Eq. 2
+//    (<= 7 eps mag) plus expf (<= 2 eps) and o*rho (eps): 13 eps mag + 10 eps <= 16 eps (mag + 1).
+//    A clamped alpha (o rho > 0.99) is the exact 0.99 on both sides: e = 0.
+//  * T_m = prod_{k<m} (1 - alpha_k): a relative alpha error moves (1 - alpha_k) by
+//    alpha_k e_k / (1 - alpha_k), its rounding by <= 2 eps / (1 - alpha_k) (both sides); each
+//    side rounds the running product once per layer and the GPU's backward recovers T_m by one
+//    division per later layer: E_m = 2 eps (K + 1) + sum_{k<m} (alpha_k e_k + 2 eps)/(1 - alpha_k).
+// tests only: 0 drops the R19c part from the returned bound (its negative control)
+int g_bound_eval = 1;
+
+template <typename R>
+void alpha_errors(const Renderer<R>& rd, const std::vector<Blend<R>>& bl, std::vector<double>& e,
+                  std::vector<double>& E) {
+  const double eps = 5.9604644775390625e-08;  // 2^-24
+  const int K = (int)bl.size();
+  e.assign(K, 0.0);
+  E.assign(K, 0.0);
+  double acc = 2.0 * eps * (K + 1);
+  for (int k = 0; k < K; ++k) {
+    const Blend<R>& b = bl[k];
+    const Proj<R>& g = rd.proj[b.id];
+    const double dx = (double)b.dx, dy = (double)b.dy;
+    const double mag = 0.5 * (std::fabs((double)g.ca) * dx * dx + std::fabs((double)g.cc) * dy * dy) +
+                       std::fabs((double)g.cb * dx * dy);
+    e[k] = (b.orho > (R)0.99) ? 0.0 : 16.0 * eps * (mag + 1.0);
+    E[k] = acc;
+    acc += ((double)b.alpha * e[k] + 2.0 * eps) / (1.0 - (double)b.alpha);
+  }
+}
+
+// R19c (continued), given e, E and the per-layer dalpha (without the soft-count term, `dam`) and
+// dGa_m = T_m sum_c dG_c |F_mc - S_mc|, the part of dalpha_m moved by the error dG of Eq. 4's
+// upstream fold (see pixel_backward):
+//  * dalpha_m = T_m (G.(F_m - S_m) - P_m bg.G) depends on alpha_k, k > m, through the suffix:
+//    d dalpha_m / d alpha_k = -dalpha_k / (1 - alpha_m) (exact identity of the recursion), so a
+//    perturbation of the later layers moves it by sum_{k>m} alpha_k e_k |dalpha_k| / (1 - alpha_m).
+//  * then w = alpha T, d o = rho dalpha, dpow = alpha dalpha and the conic / mean terms
+//    (linear in dpow with coefficients both sides hold bit-identically) follow by the product rule.
+template <typename R>
+void eval_bound(const Renderer<R>& rd, const std::vector<Blend<R>>& bl, const double G[8], const double dG[8],
+                double gG, const std::vector<double>& e, const std::vector<double>& E,
+                const std::vector<double>& dam, const std::vector<double>& dGa, std::vector<G2>& g2) {
+  const int K = (int)bl.size();
+  if (K == 0) return;
+  std::vector<double> suf(K + 1, 0.0);
+  for (int k = K - 1; k >= 0; --k) suf[k] = suf[k + 1] + (double)bl[k].alpha * e[k] * std::fabs(dam[k]);
+  for (int m = 0; m < K; ++m) {
+    const Blend<R>& b = bl[m];
+    const Proj<R>& g = rd.proj[b.id];
+    const double a = (double)b.alpha, T = (double)b.T, rho = (double)b.rho;
+    G2& o = g2[b.id];
+    const double w = a * T, dw = w * (e[m] + E[m]);
+    for (int c = 0; c < 3; ++c) o.ev[6 + c] += dw * std::fabs(G[c]) + w * dG[c];
+    for (int c = 0; c < 3; ++c) o.ev[9 + c] += dw * std::fabs(G[3 + c]) + w * dG[3 + c];
+    o.ev[12] += dw * std::fabs(G[6]) + w * dG[6];
+    double da = dam[m], dda = std::fabs(dam[m]) * E[m] + suf[m + 1] / (1.0 - a) + dGa[m];
+    if (gG != 0.0) {
+      const double s = sigmoid(kGcK * (a - 1.0 / 255.0));
+      da += gG * kGcK * s * (1.0 - s);
+      dda += std::fabs(gG * kGcK * kGcK * s * (1.0 - s) * (1.0 - 2.0 * s)) * a * e[m];
+    }
+    if (b.orho <= (R)0.99) {
+      const double ddop = rho * (e[m] * std::fabs(da) + dda);
+      const double ddpow = a * (e[m] * std::fabs(da) + dda);
+      const double dx = (double)b.dx, dy = (double)b.dy;
+      o.ev[5] += ddop;
+      o.ev[2] += 0.5 * dx * dx * ddpow;
+      o.ev[3] += std::fabs(dx * dy) * ddpow;
+      o.ev[4] += 0.5 * dy * dy * ddpow;
+      o.ev[0] += std::fabs((double)g.ca * dx + (double)g.cb * dy) * ddpow;
+      o.ev[1] += std::fabs((double)g.cb * dx + (double)g.cc * dy) * ddpow;
+    }
+  }
+}
 
 // O5: reverse-order backward of one pixel (exact reverse mode of Eq. 1-4,
 // P:82; decisions frozen per R17; clamp gradient per R16).
@@ -465,9 +553,40 @@ void pixel_backward(const Renderer<R>& rd, int i, int j, const PixOut<R>& fw,
     G[6] += gDep / den;
     for (int c = 0; c < 3; ++c) G[3 + c] -= gDep * (double)fw.D / (den * den) * r[c];
   }
+  // R19c: the fold above uses the forward's float32 N and D, which the GPU and the float build
+  // accumulate with their own alpha / T errors (e_k + E_k relative per blended weight) and
+  // roundings (one per layer each side: 2 (K + 1) eps relative): dN_c, dD bound the difference;
+  // den = N.r adds 3 eps of |N0 r0| + |N1 r1| + |N2|, each division 2 eps.  dG bounds the
+  // resulting difference of the folded upstream.
+  const double eps = 5.9604644775390625e-08;
+  std::vector<double> ea, Ea;
+  alpha_errors(rd, bl, ea, Ea);
+  double dG[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (dep_valid && gDep != 0.0) {
+    const int K = (int)bl.size();
+    double dN[3] = {0, 0, 0}, dD = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const Proj<R>& g = rd.proj[bl[k].id];
+      const double w = (double)bl[k].alpha * (double)bl[k].T;
+      const double rel = ea[k] + Ea[k] + 2.0 * eps * (K + 1);
+      for (int c = 0; c < 3; ++c) dN[c] += std::fabs(w * (double)g.ncam[c]) * rel;
+      dD += std::fabs(w * (double)g.dist) * rel;
+    }
+    const double ad = std::fabs(den);
+    const double dden = std::fabs(r[0]) * dN[0] + std::fabs(r[1]) * dN[1] + dN[2] +
+                        3.0 * eps * (std::fabs((double)fw.N[0] * r[0]) + std::fabs((double)fw.N[1] * r[1]) +
+                                     std::fabs((double)fw.N[2]));
+    const double aD = std::fabs((double)fw.D);
+    dG[6] = std::fabs(gDep) * (dden / (ad * ad) + 2.0 * eps / ad);
+    for (int c = 0; c < 3; ++c)
+      dG[3 + c] = std::fabs(gDep * r[c]) * (dD / (ad * ad) + 2.0 * aD * dden / (ad * ad * ad) +
+                                            4.0 * eps * aD / (ad * ad));
+  }
+  std::vector<double> dGa(bl.size(), 0.0);
   const double bgdot = (double)bg[0] * G[0] + (double)bg[1] * G[1] + (double)bg[2] * G[2];
   double S[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double Pp = 1.0;
+  std::vector<double> dam(bl.size());  // dalpha without the soft-count term, per layer
   for (int k = (int)bl.size() - 1; k >= 0; --k) {
     const Blend<R>& b = bl[k];
     const Proj<R>& g = rd.proj[b.id];
@@ -477,6 +596,8 @@ void pixel_backward(const Renderer<R>& rd, int i, int j, const PixOut<R>& fw,
     double dot = 0.0;
     for (int c = 0; c < 8; ++c) dot += G[c] * (F[c] - S[c]);
     double dalpha = T * (dot - Pp * bgdot);
+    dam[k] = dalpha;  // S is still the suffix after layer k here
+    for (int c = 3; c < 7; ++c) dGa[k] += T * dG[c] * std::fabs(F[c] - S[c]);
     if (gG != 0.0) {  // d(soft count)/d alpha = k s (1 - s), s = sigmoid(k (alpha - 1/255))
       const double s = sigmoid(kGcK * (a - 1.0 / 255.0));
       dalpha += gG * kGcK * s * (1.0 - s);
@@ -510,6 +631,7 @@ void pixel_backward(const Renderer<R>& rd, int i, int j, const PixOut<R>& fw,
     o.abs[1] += std::fabs(dv);
     o.absg += std::fabs(du) + std::fabs(dv);  // densification statistic (sum over pixels)
   }
+  eval_bound(rd, bl, G, dG, gG, ea, Ea, dam, dGa, g2);
 }
 
 // O6: chain rule from the 2D/per-Gaussian gradients to the 3D parameters
@@ -689,11 +811,30 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
                    int32_t* iout /* [npix][4]: g last near_flag n_clamped */, double* id_sum, int64_t* evaluated,
                    double* gsoft /* [npix] soft counts (R24) or null */, int certify_flag, int64_t* cert_bad,
                    const double* upstream /* [npix][10] or null */, double* grads /* 73 x n or null */,
-                   double* bound /* 59 x n or null: R19b accumulation bound of rows 0..58 */) {
+                   double* bound /* 59 x n or null: R19b accumulation bound of rows 0..58 */,
+                   bool fproj = false /* R = double only: project in float32, evaluate Eq. 1-4 in R */) {
   const Params<R> P = make_params(mean, scale, rot, opac, sh, n, deg);
   const Cam<R> cam = load_cam<R>(camf, W, H);
   const TileMask tm = make_tilemask(mask, W, H);
   Renderer<R> rd(P, cam, tm);
+  if (fproj) {  // the float32 build's O2 output (bit-identical to the CUDA A1), widened exactly
+    const size_t K = (size_t)(deg + 1) * (deg + 1) * 3;
+    std::vector<float> fm(mean, mean + 3 * (size_t)n), fs(scale, scale + 3 * (size_t)n),
+        fr(rot, rot + 4 * (size_t)n), fo(opac, opac + (size_t)n), fsh(sh, sh + K * n);
+    const Params<float> PF = make_params<float>(fm.data(), fs.data(), fr.data(), fo.data(), fsh.data(), n, deg);
+    const Cam<float> camF = load_cam<float>(camf, W, H);
+    Renderer<float> rf(PF, camF, tm);
+    for (int i = 0; i < n; ++i) {
+      const Proj<float>& a = rf.proj[i];
+      Proj<R>& b = rd.proj[i];
+      b.u = a.u; b.v = a.v; b.ca = a.ca; b.cb = a.cb; b.cc = a.cc; b.o = a.o; b.depth = a.depth;
+      for (int k = 0; k < 4; ++k) b.rect[k] = a.rect[k];
+      b.tiles = a.tiles;
+      for (int c = 0; c < 3; ++c) { b.rgb[c] = a.rgb[c]; b.ncam[c] = a.ncam[c]; }
+      b.dist = a.dist;
+      b.flags = a.flags;
+    }
+  }
   const R bg[3] = {(R)bgd[0], (R)bgd[1], (R)bgd[2]};
   // group requested pixels by tile so each tile's candidate list is built once
   std::vector<int> order(npix);
@@ -726,7 +867,7 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
     if (id_sum) id_sum[k] = o.id_sum;
     if (evaluated) evaluated[k] = o.evaluated;
     if (gsoft) gsoft[k] = o.gsoft;
-    if (certify_flag) bad += rd.certify(i, j);
+    if (certify_flag) bad += rd.certify(i, j, certify_flag - 1);
     if (grads) pixel_backward(rd, i, j, o, bl, bg, upstream + (size_t)k * 10, g2);
   }
   if (cert_bad) *cert_bad = bad;
@@ -746,9 +887,10 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
                             q.dncam[0], q.dncam[1], q.dncam[2], q.ddist, q.absg};
       for (int c = 0; c < 14; ++c) grads[(size_t)(59 + c) * n + i] = v[c];
     }
-    // R19b: bound on what float32 accumulation of the same per-pixel terms can cost each 3D
-    // gradient: sum_k |d g3D / d g2D_k| * kAccEps * sum_pixels |term_k|, the Jacobian columns
-    // being this oracle's own (linear) chain O6 applied to unit 2D gradients
+    // R19b + R19c: bound on what float32 accumulation (kAccEps * sum_pixels |term_k|) and float32
+    // evaluation (ev_k, eval_bound) of the same per-pixel terms can cost each 3D gradient:
+    // sum_k |d g3D / d g2D_k| * (kAccEps * abs_k + ev_k), the Jacobian columns being this
+    // oracle's own (linear) chain O6 applied to unit 2D gradients
     if (bound) {
       const double kAccEps = 16.0 * 5.9604644775390625e-08;  // 16 ulp(1) of float32
       std::memset(bound, 0, sizeof(double) * (size_t)59 * n);
@@ -756,7 +898,7 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
       for (int i = 0; i < n; ++i) {
         if ((rd.proj[i].flags & F_LIVE) != F_LIVE) continue;
         for (int k = 0; k < 13; ++k) {
-          const double d = kAccEps * g2[i].abs[k];
+          const double d = kAccEps * g2[i].abs[k] + (g_bound_eval ? g2[i].ev[k] : 0.0);
           if (d == 0.0) continue;
           G2 e{0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, 0, 0, {0}};
           double* ev[13] = {&e.du, &e.dv, &e.dca, &e.dcb, &e.dcc, &e.dop, &e.drgb[0], &e.drgb[1], &e.drgb[2],
@@ -774,6 +916,8 @@ void render_pixels(const R* mean, const R* scale, const R* rot, const R* opac, c
 }  // namespace
 
 extern "C" {
+
+void oracle_set_bound_eval(int on) { g_bound_eval = on; }
 
 // O1: tile occupancy counts [TY*TX] and SAT [(TY+1)*(TX+1)].
 void oracle_tilemask(const uint8_t* mask, int W, int H, uint32_t* cnt, int32_t* sat) {
@@ -853,6 +997,17 @@ void oracle_render_f64(const double* mean, const double* scale, const double* ro
                        double* grads, double* bound) {
   render_pixels<double>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, bg, pix, npix, out, iout, id_sum,
                         evaluated, gsoft, certify, cert_bad, upstream, grads, bound);
+}
+// The same with O2 in float32 (the key path the CUDA A1 reproduces bit-exactly) and Eq. 1-4, O5,
+// O6 in double: the exact rendering of the float32 projection, against which the R19c
+// evaluation bound of the float build is checked.
+void oracle_render_f64_fproj(const double* mean, const double* scale, const double* rot, const double* opac,
+                             const double* sh, int n, int deg, const double* cam, int W, int H,
+                             const uint8_t* mask, const double* bg, const int64_t* pix, int npix, double* out,
+                             int32_t* iout, double* id_sum, int64_t* evaluated, double* gsoft, int certify,
+                             int64_t* cert_bad, const double* upstream, double* grads, double* bound) {
+  render_pixels<double>(mean, scale, rot, opac, sh, n, deg, cam, W, H, mask, bg, pix, npix, out, iout, id_sum,
+                        evaluated, gsoft, certify, cert_bad, upstream, grads, bound, true);
 }
 
 // ---------------------------------------------------- L_GC-load (NEXT-1)

@@ -204,8 +204,7 @@ int pgsag_bin_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const pgs
   uint32_t* counters = reinterpret_cast<uint32_t*>(w + L.counters);
   cudaError_t e;
   // zero the look-back / histogram / counter state of stage 1 and A2
-  e = cudaMemsetAsync(w + L.status1, 0, 4 * (size_t)kMaxSortPasses * L.tiles1 * kMaxRadix, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(w + L.scan_status, 0, L.g2d - L.scan_status, st);
+  e = cudaMemsetAsync(w + L.counters, 0, L.zero_end - L.counters, st);
   if (e != cudaSuccess) return cuda_fail(e, "memset");
   unsigned long long M = 0;
   const uint32_t* ids_sorted = nullptr;
@@ -239,8 +238,7 @@ int pgsag_bin_sort_async(const pgsag_projected* p, const pgsag_tilemask* tm, con
   const Dims d = make_dims(cam->width, cam->height);
   char* w = static_cast<char*>(ws);
   uint32_t* counters = reinterpret_cast<uint32_t*>(w + L.counters);
-  cudaError_t e = cudaMemsetAsync(w + L.status1, 0, 4 * (size_t)kMaxSortPasses * L.tiles1 * kMaxRadix, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(w + L.scan_status, 0, L.g2d - L.scan_status, st);
+  cudaError_t e = cudaMemsetAsync(w + L.counters, 0, L.zero_end - L.counters, st);
   if (e != cudaSuccess) return cuda_fail(e, "memset");
   const uint32_t* ids_sorted = nullptr;
   if (n > 0) {
@@ -330,7 +328,7 @@ int pgsag_render_bwd_adam(const pgsag_gaussians* g, const pgsag_camera* cam, con
   cudaError_t e = cudaMemsetAsync(counters + CNT_BWD, 0, sizeof(uint32_t), st);
   if (e == cudaSuccess)
     e = launch_render_bwd(g, cam, p, bins, tm, d, mask, bg, fwd, dL, out, reinterpret_cast<float*>(w + L.g2d),
-                          counters + CNT_BWD, st, state, hp, flatten_loss);
+                          counters + CNT_BWD, st, state, hp, flatten_loss, counters + CNT_OVF);
   if (e != cudaSuccess) return cuda_fail(e, "render_bwd_adam");
   return PGSAG_OK;
 }

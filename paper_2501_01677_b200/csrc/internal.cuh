@@ -37,6 +37,14 @@ inline Dims make_dims(int W, int H) {
   return d;
 }
 
+// Launch-configuration caches are kept per device (a process may drive several GPUs).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+
 // Workspace carve-up, identical for every call with the same sizes.
 struct WsLayout {
   size_t depth_keys[2], ids[2];  // stage-1 sort ping-pong [n]
@@ -46,7 +54,8 @@ struct WsLayout {
   size_t status2;                // stage-2 look-back [passes][tiles2][256] u32
   size_t scan_status;            // A2 look-back [tilesN] u64
   size_t hist;                   // [2][kMaxSortPasses][256] u32
-  size_t counters;               // [64] u32 (tile counters, M, misc)
+  size_t counters;               // [64] u32 (tile counters, M, misc); first: offset 0 for every size
+  size_t zero_end;               // end of the state a sort call zeroes: [counters, zero_end)
   size_t g2d;                    // [n][16] f32 per-Gaussian 2D gradients (A7 -> A8; 14 used)
   size_t total;
   int tiles1, tiles2, tilesN;
@@ -62,7 +71,8 @@ enum : int {
   CNT_FWD = 9,     // A6 work counter
   CNT_BWD = 10,    // A7 work counter
   CNT_M = 12,      // 2 slots: M as u64 (A2 total)
-  CNT_MC = 14,     // min(M, capacity) as u32 (published by A3)
+  CNT_MC = 14,     // M as u32 if M <= capacity, else 0 (published by A3: an overflowed view has empty lists)
+  CNT_OVF = 15,    // 1 if M > capacity (published by A3; the fused A8 + Adam step is then skipped)
   CNT_N = 16
 };
 
@@ -93,12 +103,14 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
                               const uint8_t* mask, const float bg[3], const pgsag_image* fwd,
                               const pgsag_image_grad* dL, pgsag_gaussian_grad* out, float* g2d,
                               uint32_t* work_counter, cudaStream_t st, pgsag_adam_state* adam = nullptr,
-                              const pgsag_adam_hparams* hp = nullptr, double* flat = nullptr);
-// adam != NULL: A8 applies the Adam step (hp, L_s into *flat) instead of writing the gradients
+                              const pgsag_adam_hparams* hp = nullptr, double* flat = nullptr,
+                              const uint32_t* skip = nullptr);
+// adam != NULL: A8 applies the Adam step (hp, L_s into *flat) instead of writing the gradients,
+// unless the device flag *skip (the sort's overflow flag) is set
 cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
                                   pgsag_gaussian_grad* out, const float* g2d, cudaStream_t st,
                                   pgsag_adam_state* adam = nullptr, const pgsag_adam_hparams* hp = nullptr,
-                                  double* flat = nullptr);
+                                  double* flat = nullptr, const uint32_t* skip = nullptr);
 cudaError_t launch_gc_weights(const float* image, const uint8_t* mask, int W, int H, float* w, double* acc,
                               cudaStream_t st);
 

@@ -29,6 +29,7 @@ struct AdamFused {
   AdamP P;
   float *mean, *scale, *rot, *op, *sh, *log_scale, *logit_op, *m, *v;
   double* flat;  // L_s accumulator (zeroed by the launcher)
+  const uint32_t* skip;  // optional device flag: nonzero = this view's sort overflowed, no update
 };
 
 // The Adam step of Gaussian i from its float32 gradients staged in shared memory by A8 (sg: this
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
     double hh, AdamFused F) {
   constexpr int K3 = 3 * (DEG + 1) * (DEG + 1);
   __shared__ float s_g[kAdam ? (11 + K3) * 128 : 1];  // fused: the gradients, one column per thread
+  if (kAdam && F.skip && *F.skip) return;  // overflowed view: its lists were empty, leave the state
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const float gflat = kAdam ? F.P.flat_w / (float)n : 0.f;
   if (kAdam) {  // L_s = mean of min(scale) before the update: block sum, one atomic per block
@@ -361,9 +363,11 @@ __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
 
 cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* cam, const pgsag_projected* p,
                                   pgsag_gaussian_grad* out, const float* g2d, cudaStream_t st,
-                                  pgsag_adam_state* adam, const pgsag_adam_hparams* hp, double* flat) {
+                                  pgsag_adam_state* adam, const pgsag_adam_hparams* hp, double* flat,
+                                  const uint32_t* skip) {
   const int n = g->n;
   AdamFused F{};
+  F.skip = skip;
   if (adam) {
     F.P = adam_params(hp);
     F.mean = adam->mean; F.scale = adam->scale; F.rot = adam->rot; F.op = adam->opacity; F.sh = adam->sh;

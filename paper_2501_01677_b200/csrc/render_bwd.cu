@@ -449,15 +449,15 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
 }
 
 int bwd_grid() {
-  static int grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
+  static int grid[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!grid[dev]) {
+    int sms = 148, occ = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_bwd_kernel<false, false, false>, kBT, 0);
-    grid = sms * (occ > 0 ? occ : 1);
+    grid[dev] = sms * (occ > 0 ? occ : 1);
   }
-  return grid;
+  return grid[dev];
 }
 
 }  // namespace
@@ -467,7 +467,7 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
                               const uint8_t* mask, const float bg[3], const pgsag_image* fwd,
                               const pgsag_image_grad* dL, pgsag_gaussian_grad* out, float* g2d,
                               uint32_t* work_counter, cudaStream_t st, pgsag_adam_state* adam,
-                              const pgsag_adam_hparams* hp, double* flat) {
+                              const pgsag_adam_hparams* hp, double* flat, const uint32_t* skip) {
   const int n = g->n;
   if (n == 0) return cudaSuccess;
   cudaMemsetAsync(g2d, 0, sizeof(float) * 16 * (size_t)n, st);
@@ -515,7 +515,7 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
 #undef PGSAG_A7
     }
   }
-  return launch_preprocess_bwd(g, cam, p, out, g2d, st, adam, hp, flat);
+  return launch_preprocess_bwd(g, cam, p, out, g2d, st, adam, hp, flat, skip);
 }
 
 }  // namespace pgsag

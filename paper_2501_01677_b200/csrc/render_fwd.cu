@@ -274,15 +274,15 @@ constexpr int kNP = PGSAG_FWD_NP;
 constexpr int kFT = FwdCfg<kNP>::NT;
 
 int fwd_grid() {
-  static int grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
+  static int grid[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!grid[dev]) {
+    int sms = 148, occ = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, render_fwd_kernel<false, kNP>, kFT, 0);
-    grid = sms * (occ > 0 ? occ : 1);
+    grid[dev] = sms * (occ > 0 ? occ : 1);
   }
-  return grid;
+  return grid[dev];
 }
 
 }  // namespace

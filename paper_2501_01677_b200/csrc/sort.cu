@@ -319,7 +319,9 @@ constexpr int kDupSmall = 16;  // rect tiles a lane emits on its own
 // compacting the active ones with a ballot, so every entry run is written coalesced and a
 // large splat is spread over 32 lanes instead of one thread.
 // cap bounds the writes (sync-free path: M is not known on the host; if M > cap the
-// output is incomplete and the caller retries).  Thread 0 also publishes min(M, cap).
+// output is incomplete and the caller retries).  Thread 0 also publishes the entry count the later
+// stages use: M if it fits, else 0 (an overflowed view gets EMPTY lists, never a partially written
+// prefix with stale entries), and the overflow flag.
 __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* __restrict__ ids,
                                                          const uint32_t* __restrict__ offsets,
                                                          const uint32_t* __restrict__ touched,
@@ -327,10 +329,15 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
                                                          const uint32_t* __restrict__ bitmap, Dims d,
                                                          uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
                                                          uint32_t cap, const unsigned long long* __restrict__ M64,
-                                                         uint32_t* __restrict__ m_clamped) {
+                                                         uint32_t* __restrict__ m_clamped,
+                                                         uint32_t* __restrict__ overflow) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  if (k == 0) *m_clamped = (uint32_t)min(*M64, (unsigned long long)cap);
+  if (k == 0) {
+    const unsigned long long M = *M64;
+    *m_clamped = M <= (unsigned long long)cap ? (uint32_t)M : 0u;
+    *overflow = M > (unsigned long long)cap ? 1u : 0u;
+  }
   uint32_t id = 0, cnt = 0, o = 0;
   short4 r = make_short4(0, 0, -1, -1);
   if (k < n) {
@@ -392,10 +399,11 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
 
 // -------------------------------------------------------------- A5 ranges
 __global__ void ranges_kernel(const uint32_t* __restrict__ tkeys, const uint32_t* __restrict__ M_ptr,
-                              uint32_t* __restrict__ ranges) {
-  const uint32_t M = *M_ptr;  // min(M, capacity) published by A3
+                              uint32_t ntiles, uint32_t* __restrict__ ranges) {
+  const uint32_t M = *M_ptr;  // the entry count published by A3 (0 after an overflow)
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < M; k += gridDim.x * blockDim.x) {
     const uint32_t t = tkeys[k];
+    if (t >= ntiles) continue;  // defensive: keys are tile ids < ntiles by construction
     if (k == 0 || tkeys[k - 1] != t) ranges[2 * t] = k;
     if (k == M - 1 || tkeys[k + 1] != t) ranges[2 * t + 1] = k + 1;
   }
@@ -432,14 +440,14 @@ __global__ void __launch_bounds__(1024) lpt_order_kernel(const uint32_t* __restr
 }
 
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  static int sms[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!sms[dev]) {
+    int s = 0;
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = s > 0 ? s : 148;
   }
-  return sms;
+  return sms[dev];
 }
 
 // LSD radix sort of (keys, vals) on bits [0, end_bit).  Ping-pongs between (a)
@@ -452,11 +460,12 @@ cudaError_t radix_sort(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, c
   const int npass = plan.n;
   *res_in_a = true;
   if (npass == 0 || grid_bound == 0) return cudaSuccess;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!attr_set[dev]) {
     cudaFuncSetAttribute(radix_pass_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem<8>());
     cudaFuncSetAttribute(radix_pass_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem<9>());
-    attr_set = true;
+    attr_set[dev] = true;
   }
   const int hist_grid = min((int)((grid_bound + 255) / 256), num_sms() * 4);
   {
@@ -500,22 +509,26 @@ WsLayout ws_layout(int32_t n, int32_t W, int32_t H, int64_t cap) {
   L.tiles2 = (int)((cc + kSortTile - 1) / kSortTile);
   L.tilesN = (int)((nn + kScanTile - 1) / kScanTile);
   (void)W; (void)H;
+  // counters first: their offset does not depend on n or the capacity, so a render call sees the
+  // flags the sort of the same view published in the same workspace
+  L.counters = take(4 * 64);
+  // the state a sort call zeroes, contiguous after the counters (one memset)
+  L.hist = take(4 * 2 * kMaxSortPasses * kMaxRadix);
+  L.scan_status = take(8 * (size_t)(L.tilesN > 0 ? L.tilesN : 1));
+  L.status1 = take(4 * (size_t)kMaxSortPasses * L.tiles1 * kMaxRadix);
+  L.zero_end = off;
   for (int k = 0; k < 2; ++k) { L.depth_keys[k] = take(4 * nn); L.ids[k] = take(4 * nn); }
   L.offsets = take(4 * nn);
   L.dup_keys = take(4 * cc);
   L.dup_vals = take(4 * cc);
-  L.status1 = take(4 * (size_t)kMaxSortPasses * L.tiles1 * kMaxRadix);
   L.status2 = take(4 * (size_t)kMaxSortPasses * L.tiles2 * kMaxRadix);
-  L.scan_status = take(8 * (size_t)(L.tilesN > 0 ? L.tilesN : 1));
-  L.hist = take(4 * 2 * kMaxSortPasses * kMaxRadix);
-  L.counters = take(4 * 64);
   L.g2d = take(4 * 16 * nn);  // [n][16] f32 (14 used), one 64-byte line per Gaussian
   L.total = off;
   return L;
 }
 
-// Stage 1 (depth sort of Gaussians) + A2 scan.  The zeroed region
-// [status1 .. counters] must have been cleared by the caller.
+// Stage 1 (depth sort of Gaussians) + A2 scan.  The region [counters, zero_end) (counters,
+// histograms, A2 and stage-1 look-back state) must have been cleared by the caller.
 cudaError_t launch_bin_sort_stage1(const pgsag_projected* p, int n, const WsLayout& L, char* ws,
                                    cudaStream_t st, const uint32_t** ids_sorted) {
   uint32_t* k0 = reinterpret_cast<uint32_t*>(ws + L.depth_keys[0]);
@@ -583,7 +596,7 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
                                                       p->tiles_touched, reinterpret_cast<const short4*>(p->rect),
                                                       tm->active_bits, d, ek, ev, (uint32_t)bins->capacity,
                                                       reinterpret_cast<const unsigned long long*>(counters + CNT_M),
-                                                      m_clamped);
+                                                      m_clamped, counters + CNT_OVF);
   }
   bool in_a = true;
   // look-back state for exactly the tiles the bound needs
@@ -596,7 +609,7 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
   const int grid = min((int)((bound + 255) / 256), num_sms() * 8);
   {
     KTimer kt_("A5_ranges", st);
-    ranges_kernel<<<grid, 256, 0, st>>>(bins->tile_keys, m_clamped, bins->ranges);
+    ranges_kernel<<<grid, 256, 0, st>>>(bins->tile_keys, m_clamped, (uint32_t)ntiles, bins->ranges);
   }
   order();
   return cudaGetLastError();

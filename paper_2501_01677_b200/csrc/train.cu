@@ -515,11 +515,12 @@ cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8
   A.abc = abc; A.loss = loss; A.dC = dC;
   cudaError_t e = cudaMemsetAsync(loss, 0, 6 * sizeof(double), st);
   if (e != cudaSuccess) return e;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!attr[dev]) {
     cudaFuncSetAttribute(rgb_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
     cudaFuncSetAttribute(rgb_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
-    attr = true;
+    attr[dev] = true;
   }
   const dim3 grid((W + kTW - 1) / kTW, (H + kTH - 1) / kTH);
   {

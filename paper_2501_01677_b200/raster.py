@@ -150,11 +150,7 @@ class Rasterizer:
         tm.sat = self.sat.data_ptr() if self.want_sat else None
         tm.n_active, tm.active_bits = self.n_active.data_ptr(), self.active_bits.data_ptr()
         self._tm = tm
-        b = L.Bins()
-        b.tile_keys, b.vals, b.ranges = self.tile_keys.data_ptr(), self.vals.data_ptr(), self.ranges.data_ptr()
-        b.capacity, b.n_dup = self.capacity, 0
-        b.order = self.order.data_ptr()
-        self._bins = b
+        self._build_bins()
         im = L.Image()
         im.C, im.N, im.D, im.A = self.img_C.data_ptr(), self.img_N.data_ptr(), self.img_D.data_ptr(), \
             self.img_A.data_ptr()
@@ -168,6 +164,15 @@ class Rasterizer:
         gg.absgrad2d = self.absgrad.data_ptr() if self.want_absgrad else None
         gg.grad2d = None
         self._grad = gg
+
+    def _build_bins(self):
+        """The pgsag_bins struct over the current entry buffers (the only struct a capacity change
+        touches: the image / gradient structs keep their per-call fields across a retry)."""
+        b = L.Bins()
+        b.tile_keys, b.vals, b.ranges = self.tile_keys.data_ptr(), self.vals.data_ptr(), self.ranges.data_ptr()
+        b.capacity, b.n_dup = self.capacity, 0
+        b.order = self.order.data_ptr()
+        self._bins = b
 
     def export_grad2d(self, on=True):
         """Also copy A7's per-Gaussian screen-space gradients into self.grad2d ([14][n])."""
@@ -235,7 +240,7 @@ class Rasterizer:
         rc = L.bin_sort(self._proj, self._tm, cam, self.n, self._bins, ws, self.ws_bytes, st)
         if rc == L.PGSAG_ECAPACITY:
             self._alloc_bins(int(self._bins.n_dup * 1.25) + 1024)
-            self._build_structs()
+            self._build_bins()
             ws = C.c_void_p(self.ws.data_ptr())
             rc = L.bin_sort(self._proj, self._tm, cam, self.n, self._bins, ws, self.ws_bytes, st)
             L.check(rc)
@@ -283,7 +288,9 @@ class Rasterizer:
 
     def check_capacity(self) -> bool:
         """sync_free mode: after synchronising, True if the last view's M fitted the capacity; otherwise
-        grows the entry buffers (the caller re-runs that view)."""
+        grows the entry buffers (the caller re-runs that view).  An overflowed view was rendered from
+        EMPTY lists (the device-side entry count is 0, never a partial prefix) and a fused
+        backward_adam of it skipped its update on the device."""
         if not self.sync_free:
             return True
         torch.cuda.current_stream().synchronize()
@@ -291,7 +298,7 @@ class Rasterizer:
         if self.M <= self.capacity:
             return True
         self._alloc_bins(int(self.M * 1.25) + 1024)
-        self._build_structs()
+        self._build_bins()
         return False
 
     def stats(self):

@@ -108,6 +108,9 @@ class Trainer:
         side stream concurrently with L_rgb (both only read A6's outputs).  gc_ready: event after
         which gc_w / band are valid (A6 waits for it)."""
         r = self.r
+        if (dp_group is not None or not self.fused) and r.sync_free:
+            # the separate pgsag_adam_step (averaged / unfused path) has no view-overflow guard
+            raise ValueError("dp_group / fused=False steps need a synchronising rasterizer (sync_free=False)")
         self.t += 1
         st = _stream()
         main = torch.cuda.current_stream()
@@ -174,14 +177,18 @@ class Trainer:
         self.step(cam, mask, target, gc_w=self._gc_w, band=self._band, bg=bg, dp_group=dp_group, gc_ready=ev_gc)
 
     def losses(self) -> dict:
-        """Host read of the last iteration's terms and the Eq. 11 total."""
+        """Host read of the last iteration's terms and the Eq. 11 total.  With a sync-free rasterizer
+        it also checks the last view's entry capacity: overflowed = True means that view was skipped
+        (empty lists, no Adam update, pgsag_render_bwd_adam) and the buffers have grown for a re-run."""
         rgb = self.loss_rgb.tolist()
+        overflowed = not self.r.check_capacity()
         Ls = float(self.loss_flat.item())
         ban = self.loss_ban.tolist()
         Lban = ban[0] / ban[1] if self.used_ban and ban[1] > 0 else 0.0
         Lgc = self.r.gc_load()[0] if self.used_gc else 0.0
         total = (1 - self.lam) * (rgb[0] + self.lam3 * Ls + self.lam4 * Lban) + self.lam * Lgc
-        return dict(total=total, rgb=rgb[0], l1=rgb[1], ssim=rgb[2], flat=Ls, ban=Lban, gc_load=Lgc)
+        return dict(total=total, rgb=rgb[0], l1=rgb[1], ssim=rgb[2], flat=Ls, ban=Lban, gc_load=Lgc,
+                    overflowed=overflowed)
 
     # ------------------------------------------------------------ densification (R31)
     def _state_tensors(self, n, K3, dev):

@@ -323,6 +323,29 @@ def random_gaussians(rng, n, lo, hi, s_lo=0.03, s_hi=0.3, o_lo=0.05, o_hi=0.99, 
     return _pack(P, sc, q, op, sh, deg)
 
 
+def fuzz_scene(seed):
+    """Randomised small scene of the parity sweep (tests/test_gpu_fuzz.py) and of the oracle's
+    R19c bound pin: image size (ragged, down to one partial tile), Gaussian count, SH degree,
+    scale / opacity ranges, mask density, background and focal length all vary with the seed.
+    Returns (Scene, bg)."""
+    rng = np.random.default_rng(1000 + seed)
+    W, H = int(rng.integers(5, 90)), int(rng.integers(5, 70))
+    n = int(rng.integers(1, 700))
+    deg = int(rng.integers(0, 4))
+    g = random_gaussians(rng, n, [-1.5, -1.2, 1.5], [1.5, 1.2, 7.0],
+                         s_lo=float(rng.uniform(0.005, 0.05)), s_hi=float(rng.uniform(0.1, 0.8)),
+                         o_lo=float(rng.uniform(0.0, 0.3)), o_hi=float(rng.uniform(0.5, 1.0)), deg=deg,
+                         sh_std=float(rng.uniform(0.1, 0.6)))
+    f = float(rng.uniform(0.6, 1.6)) * max(W, H)
+    cam = Camera(f, f * float(rng.uniform(0.8, 1.25)), W / 2.0 + float(rng.uniform(-3, 3)),
+                 H / 2.0 + float(rng.uniform(-3, 3)), W, H, np.eye(3, dtype=np.float32), np.zeros(3, np.float32))
+    mask = (rng.uniform(size=(H, W)) < float(rng.uniform(0.05, 1.0))).astype(np.uint8)
+    if not mask.any():
+        mask[H // 2, W // 2] = 1
+    bg = tuple(float(x) for x in rng.uniform(0, 1, 3)) if rng.uniform() < 0.5 else (0.0, 0.0, 0.0)
+    return Scene(f"fuzz{seed}", g, cam, mask, seed=seed), bg
+
+
 def config1(seed=None, n=1000, W=64, H=64, sh_degree=3, mask_p=0.5):
     """C1: 1000 random Gaussians, one 64x64 camera at the origin looking +z, 50% random mask."""
     seed = SEED_BASE + 1 if seed is None else seed

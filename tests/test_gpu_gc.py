@@ -46,7 +46,8 @@ def test_gc_weights_and_fused_stats(name):
 @pytest.mark.parametrize("name", ["C1", "ragged"])
 def test_gc_surrogate_gradient(name):
     """lambda * L_GC-load alone as the loss: A7/A8 vs the oracle backward with upstream
-    dL/d(soft count) = lambda * (r - mean) / (N L w) (R24)."""
+    dL/d(soft count) = lambda * (r - mean) / (N L w) (R24); the oracle side is an all-oracle chain
+    (its own Eq. 9 weights, its own render's counts g)."""
     sc = S.config1() if name == "C1" else ragged_scene()
     img, g, r, mask, w = _setup(sc, 32)
     lam = 0.41  # Eq. 11's lambda (P:179)
@@ -54,7 +55,7 @@ def test_gc_surrogate_gradient(name):
     grads = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in r.backward(gc_lambda=lam).items()}
     torch.cuda.synchronize()
     pix = all_pixels(sc.mask)
-    w_px = w.cpu().numpy().astype(np.float64).reshape(-1)[pix]
+    w_px = oracle.gc_weights(img, sc.mask).astype(np.float64).reshape(-1)[pix]  # all-oracle chain
     ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix)
     _, _, dLdg = oracle.gc_load(ora0["g"].astype(np.float64), w_px)
     up = np.zeros((len(pix), 10))

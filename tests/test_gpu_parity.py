@@ -248,3 +248,82 @@ def test_sync_free_bin_sort():
     assert torch.equal(fast.ranges, ref.ranges)
     for k in ("img_C", "img_N", "img_D", "img_T", "img_g", "img_last", "img_Dep"):
         assert torch.equal(getattr(fast, k), getattr(ref, k)), k
+
+
+@pytest.mark.parametrize("frac", [0.5, 0.97])
+def test_sync_free_overflow_gives_empty_lists(frac):
+    """when M exceeds the capacity in the sync-free sort, the device-side entry
+    count is 0 (no partially written prefix with stale entries), so A5 writes no range and A6
+    renders every mask pixel as empty (T = 1, g = 0, C = bg), even with the entry buffers
+    pre-filled with 0xFF (out-of-range tile ids); capacity = frac * M makes one splat's entry run
+    straddle the capacity."""
+    from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+    sc = ragged_scene()
+    H, W = sc.mask.shape
+    g = GaussianTensors.from_numpy(sc.gaussians)
+    cam = camera_from(sc.camera)
+    mask = torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda()
+    ref = Rasterizer(g.n, W, H, g.sh_degree)
+    ref.forward(g, cam, mask)
+    cap = max(1, int(frac * ref.M))
+    r = Rasterizer(g.n, W, H, g.sh_degree, capacity=cap, sync_free=True)
+    r.tile_keys.fill_(-1)
+    r.vals.fill_(-1)
+    bg = (0.25, 0.5, 0.75)
+    r.forward(g, cam, mask, bg)
+    torch.cuda.synchronize()
+    m = torch.from_numpy(sc.mask.astype(bool)).cuda()
+    assert int(r.ranges.abs().sum().item()) == 0
+    assert bool((r.img_T[m] == 1.0).all()) and bool((r.img_g[m] == 0).all()) and bool((r.img_last[m] == -1).all())
+    for c in range(3):
+        assert bool((r.img_C[c][m] == bg[c]).all())
+    assert not r.check_capacity() and r.M == ref.M
+
+
+def test_capacity_retry_keeps_gc_statistics():
+    """a PGSAG_ECAPACITY retry inside forward() keeps the per-call image fields
+    (the Eq. 9 weights / statistics): the statistics equal those of an ample-capacity run."""
+    from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+    sc = S.config1()
+    H, W = sc.mask.shape
+    g = GaussianTensors.from_numpy(sc.gaussians)
+    cam = camera_from(sc.camera)
+    mask = torch.from_numpy(sc.mask).cuda()
+    img = torch.from_numpy(S.reference_image(H, W, 5)).cuda()
+    out = []
+    for cap in (16, 1 << 20):
+        r = Rasterizer(g.n, W, H, g.sh_degree, capacity=cap)
+        w = r.gc_weights(img, mask)
+        r.forward(g, cam, mask, gc_w=w)
+        torch.cuda.synchronize()
+        out.append(r.gc_load())
+    assert out[0][2] == int(sc.mask.sum()) and out[0] == out[1]
+
+
+def test_trainer_skips_overflowed_view():
+    """a sync-free training step whose view overflows the entry capacity leaves
+    the parameters and Adam moments untouched (device-side skip in the fused A8 + Adam) and
+    reports the overflow; the re-run view then renders exactly like a synchronising trainer's."""
+    from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+    from paper_2501_01677_b200.train import Trainer
+    sc = S.config1()
+    H, W = sc.mask.shape
+    cam = camera_from(sc.camera)
+    mask = torch.from_numpy(sc.mask).cuda()
+    tgt = torch.from_numpy(S.reference_image(H, W, 9)).cuda()
+    ga, gb = GaussianTensors.from_numpy(sc.gaussians), GaussianTensors.from_numpy(sc.gaussians)
+    ta = Trainer(Rasterizer(ga.n, W, H, ga.sh_degree), ga)
+    tb = Trainer(Rasterizer(gb.n, W, H, gb.sh_degree, capacity=16, sync_free=True), gb)
+    before = [x.clone() for x in (gb.mean, gb.scale, gb.opacity, gb.sh, tb.m, tb.v)]
+    tb.step(cam, mask, tgt)
+    assert tb.losses()["overflowed"]
+    for x, y in zip(before, (gb.mean, gb.scale, gb.opacity, gb.sh, tb.m, tb.v)):
+        assert torch.equal(x, y)
+    tb.t -= 1  # the skipped step is re-run as the same step
+    tb.step(cam, mask, tgt)
+    lb = tb.losses()
+    assert not lb["overflowed"]
+    ta.step(cam, mask, tgt)
+    la = ta.losses()
+    assert la["rgb"] == lb["rgb"] and la["flat"] == lb["flat"]  # same render, same L_s
+    assert not torch.equal(before[0], gb.mean) and not torch.equal(before[4], tb.m)  # the re-run updated
