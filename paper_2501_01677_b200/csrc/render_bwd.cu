@@ -11,13 +11,16 @@
 //   G.S   <- alpha (G.F_i) + (1 - alpha) G.S,   P (bg.gC) <- (1 - alpha) P (bg.gC)
 // Only the projection G.S of the 8-channel suffix S is ever needed, so the
 // suffix is carried as one scalar (mathematically identical to the 8-vector
-// recurrence of the oracle).
+// recurrence of the oracle); the background term obeys the same
+// recursion, so Sg = G.S + P (bg.gC) is one scalar started at bg.gC.
 //
 // Mapping: per active tile two single-warp CTAs (PGSAG_BWD_WARPS below), the one of half h
 // owning the 8x16 pixel block of columns 8h..8h+7; a lane owns the FOUR pixels (x, y + 4k),
 // k = 0..3, of its column, which share dx and every per-entry load and run as two packed FP32x2
-// pairs.  Batches of 64 entries are staged with the exact block cull of A6 and walked in
-// reverse through a compacted candidate list.  A pixel that
+// pairs.  Batches of 64 entries are staged with the exact block cull of A6 (per 8x8 block of
+// the half: block p holds the lane's pair p) and walked in reverse through a compacted
+// candidate list; a pair whose block the entry misses, or none of whose 64 pixels blends it,
+// is skipped by a warp-uniform branch.  A pixel that
 // does not contribute to an entry carries alpha = rho = 0, which zeroes all of its
 // terms and leaves its state unchanged without branches.  Reduction: per entry the
 // lane sums its four pixels, the warp reduce-scatters the 14 partials (5 butterfly
@@ -51,6 +54,9 @@ constexpr int kBNB = kBW;  // candidate lists per CTA
 #define PGSAG_BWD_MINB (20 / kBW)  // resident CTAs per SM the register budget is sized for
 #endif
 constexpr float kLn2 = 0.6931471805599453f;
+#ifndef PGSAG_BWD_HSTRIPS
+#define PGSAG_BWD_HSTRIPS 1
+#endif
 
 struct BwdArgs {
   const float2* mean2d;
@@ -172,17 +178,16 @@ __device__ __forceinline__ void load_pixel(const BwdArgs& a, bool inb, size_t pi
 // State of one packed pixel pair.
 struct Pair {
   float2 G[8];
-  float2 Pb, T, Sg, gGk;  // gGk = k * dL/d(soft count)
+  float2 T, Sg, gGk;  // Sg = G.S + P (bg.gC) (one recursion for both, P' = (1 - alpha) P); gGk = k dL/d(soft count)
   int last0, last1;
 };
 
 __device__ __forceinline__ void make_pair(const PixState& a, const PixState& b, Pair& p) {
 #pragma unroll
   for (int c = 0; c < 8; ++c) p.G[c] = f2(a.G[c], b.G[c]);
-  p.Pb = f2(a.Pb, b.Pb);
   p.gGk = f2(kGcK * a.gG, kGcK * b.gG);
   p.T = f2(a.T, b.T);
-  p.Sg = f2(0.f, 0.f);
+  p.Sg = f2(a.Pb, b.Pb);
   p.last0 = a.last;
   p.last1 = b.last;
 }
@@ -193,7 +198,9 @@ struct PairOut {
 };
 
 template <bool kGC>
-__device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 rc, const float4& cd,
+// al: the blended alphas (0 where the pixel does not blend the entry); rh: rho; u0 / u1: the pixel
+// blends and its alpha is not clamped (R16: d opacity and d power are zero through the clamp)
+__device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 rh, bool u0, bool u1, const float4& cd,
                                           const float4& nn, PairOut& o) {
   const float2 om = __fadd2_rn(bc(1.f), f2(-al.x, -al.y));
   const float2 Ti = __fmul2_rn(p.T, f2(rcp_approx(om.x), rcp_approx(om.y)));
@@ -205,8 +212,7 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 
   GF = __ffma2_rn(p.G[4], bc(nn.y), GF);
   GF = __ffma2_rn(p.G[5], bc(nn.z), GF);
   GF = __ffma2_rn(p.G[6], bc(cd.w), GF);
-  const float2 sp = __fadd2_rn(p.Sg, p.Pb);
-  float2 dal = __fmul2_rn(Ti, __fadd2_rn(GF, f2(-sp.x, -sp.y)));
+  float2 dal = __fmul2_rn(Ti, __fadd2_rn(GF, f2(-p.Sg.x, -p.Sg.y)));
   if (kGC) {  // + gG * d(sigmoid(k (alpha - 1/255)))/d alpha; only reaches the outputs through ac / rc
     // z = -k log2(e) (alpha - 1/255), s = 1 / (1 + 2^z), 1 - s = 2^z s
     const float2 z = __ffma2_rn(al, bc(-kGcK * kLog2e), bc(kGcK * kLog2e * kAlphaMin));
@@ -215,11 +221,11 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 ac, float2 
     dal = __ffma2_rn(__fmul2_rn(p.gGk, s), __fmul2_rn(e, s), dal);
   }
   p.Sg = __ffma2_rn(al, GF, __fmul2_rn(om, p.Sg));
-  p.Pb = __fmul2_rn(p.Pb, om);
   p.T = Ti;
   o.wt = __fmul2_rn(al, Ti);
-  o.dpow = __fmul2_rn(ac, dal);
-  o.dop = __fmul2_rn(rc, dal);
+  const float2 dalu = f2(u0 ? dal.x : 0.f, u1 ? dal.y : 0.f);
+  o.dpow = __fmul2_rn(al, dalu);
+  o.dop = __fmul2_rn(rh, dalu);
 }
 
 template <bool kCount, bool kGC, bool kAbs>
@@ -306,7 +312,15 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
             const float4 co = a.conic_o[id];
             const StageCull c = stage_record(xy, co, r);
             const float xlo = tx0 + (float)(half * 8) + 0.5f, ylo = ty0 + 0.5f;
+#if PGSAG_BWD_HSTRIPS
+            // exact cull per 8x8 block of the half (block p = the rows of pixel pair p)
+            const uint32_t sm = (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 7.0f) ? 1u : 0u) |
+                                (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo + 8.0f, ylo + 15.0f) ? 2u : 0u);
+            mk[e] = sm != 0u ? 1u : 0u;
+            r.b.w = __uint_as_float(sm);
+#else
             mk[e] = block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 15.0f) ? 1u : 0u;
+#endif
           }
           r.cd = a.rgb_d[id];
           r.n = a.ncam[id];
@@ -325,6 +339,40 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
         const float4 ra = lds128(ra_addr);
         const float4 rb = lds128(ra_addr + 16);
+#if PGSAG_BWD_HSTRIPS
+        // per 8x8 block (pixel pair) of the half: skipped when the splat misses it (staging cull)
+        // or when none of its pixels blends the entry (a warp-uniform test after the alpha pass)
+        const uint32_t smask = __float_as_uint(rb.w);
+        const float dx = px - ra.x;
+        const float tA = __fmul_rn(ra.z, dx);
+        const float2 dy01 = __fadd2_rn(py01, bc(-ra.y));
+        const float2 dy23 = __fadd2_rn(py23, bc(-ra.y));
+        const float4 cd = lds128(ra_addr + 32);
+        const float4 nn = lds128(ra_addr + 48);
+        PairOut o01, o23;
+        o01.wt = o01.dpow = o01.dop = o23.wt = o23.dpow = o23.dop = f2(0.f, 0.f);
+        bool anyc = false;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (!((smask >> h) & 1u)) continue;
+          Pair& PP = h ? P23 : P01;
+          const float2 dy = h ? dy23 : dy01;
+          const float2 p2 = __ffma2_rn(bc(dx), __ffma2_rn(bc(ra.w), dy, bc(tA)), __fmul2_rn(__fmul2_rn(bc(rb.x), dy), dy));
+          const float2 rh = f2(ex2_approx(p2.x), ex2_approx(p2.y));
+          const float2 orh = __fmul2_rn(bc(rb.y), rh);
+          float al0 = fminf(kAlphaMax, orh.x), al1 = fminf(kAlphaMax, orh.y);
+          const bool c0 = kk <= PP.last0 && p2.x <= 0.0f && al0 >= kAlphaMin;
+          const bool c1 = kk <= PP.last1 && p2.y <= 0.0f && al1 >= kAlphaMin;
+          if (kCount) cntV += (unsigned long long)(kk <= PP.last0) + (kk <= PP.last1);
+          if (!__any_sync(0xffffffffu, c0 || c1)) continue;
+          anyc = true;
+          al0 = c0 ? al0 : 0.f;
+          al1 = c1 ? al1 : 0.f;
+          const bool u0 = c0 && orh.x <= kAlphaMax, u1 = c1 && orh.y <= kAlphaMax;
+          pair_grad<kGC>(PP, f2(al0, al1), rh, u0, u1, cd, nn, h ? o23 : o01);
+        }
+        if (!anyc) continue;
+#else
         // p2 for the four pixels (bit-identical to A6's evaluation per element)
         const float dx = px - ra.x;
         const float tA = __fmul_rn(ra.z, dx);
@@ -365,10 +413,11 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float4 cd = lds128(ra_addr + 32);
         const float4 nn = lds128(ra_addr + 48);
         PairOut o01, o23;
-        pair_grad<kGC>(P01, f2(al0, al1), f2(u0 ? al0 : 0.f, u1 ? al1 : 0.f), f2(u0 ? rh01.x : 0.f, u1 ? rh01.y : 0.f),
+        pair_grad<kGC>(P01, f2(al0, al1), rh01, u0, u1,
                   cd, nn, o01);
-        pair_grad<kGC>(P23, f2(al2, al3), f2(u2 ? al2 : 0.f, u3 ? al3 : 0.f), f2(u2 ? rh23.x : 0.f, u3 ? rh23.y : 0.f),
+        pair_grad<kGC>(P23, f2(al2, al3), rh23, u2, u3,
                   cd, nn, o23);
+#endif
         float v[16];  // slot k holds value k (k < 7) or value k - 1 (8 <= k < 15); slots 7, 15 zero
 #pragma unroll
         for (int c = 0; c < 7; ++c)

@@ -73,8 +73,13 @@ def train_region(k, args, dev, dp_group=None, dp_rank=0, dp_size=1):
     e1.record()
     torch.cuda.synchronize()
     last = tr.losses()
-    return {"region": k, "iters": args.iters, "dp_size": dp_size, "n_gaussians": tr.g.n,
-            "ms": e0.elapsed_time(e1), "first_loss": first, "final_loss": last}
+    import hashlib
+    h = hashlib.sha256()
+    for t in (tr.g.mean, tr.g.scale, tr.g.rot, tr.g.opacity, tr.g.sh, tr.m, tr.v):
+        h.update(t.detach().contiguous().cpu().numpy().tobytes())
+    return {"region": k, "iters": args.iters, "dp_size": dp_size, "dp_rank": dp_rank, "n_gaussians": tr.g.n,
+            "ms": e0.elapsed_time(e1), "first_loss": first, "final_loss": last,
+            "state_digest": h.hexdigest()[:24]}
 
 
 def main(argv=None):

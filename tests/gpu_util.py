@@ -15,12 +15,14 @@ GRAD_REL = 1e-3       # per element, relative to max(|ref|, 1e-2 * maxabs(class)
 GRAD_NORM = 1e-4      # per class ||d||/||ref|| (reading R19)
 
 
-def run_gpu(scene, bg=(0.0, 0.0, 0.0), capacity=None, upstream=None, counters=True):
+def run_gpu(scene, bg=(0.0, 0.0, 0.0), capacity=None, upstream=None, counters=True, sync_free=False):
+    """sync_free: the launch configuration bench.py times (pgsag_bin_sort_async, no host sync; the
+    capacity must then hold M, which is checked after the run)."""
     g = GaussianTensors.from_numpy(scene.gaussians)
     cam = camera_from(scene.camera)
     mask = torch.from_numpy(np.ascontiguousarray(scene.mask)).cuda()
     r = Rasterizer(g.n, scene.camera.width, scene.camera.height, g.sh_degree, capacity=capacity,
-                   counters=counters)
+                   counters=counters, sync_free=sync_free)
     # sentinel fill so unwritten (masked-out) pixels are detectable
     for t in (r.img_C, r.img_N, r.img_D, r.img_A, r.img_Dep, r.img_T):
         t.fill_(-7.0)
@@ -31,6 +33,8 @@ def run_gpu(scene, bg=(0.0, 0.0, 0.0), capacity=None, upstream=None, counters=Tr
         up = {k: torch.from_numpy(v).cuda() for k, v in upstream.items()}
         res["grads"] = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in r.backward(**up).items()}
     torch.cuda.synchronize()
+    if sync_free:
+        assert r.check_capacity(), "sync-free capacity exceeded"
     res["img"] = {k: v.detach().cpu().numpy() for k, v in dict(
         C=r.img_C, N=r.img_N, D=r.img_D, A=r.img_A, Dep=r.img_Dep, T=r.img_T, g=r.img_g, last=r.img_last).items()}
     res["vals"] = r.vals[:r.M].cpu().numpy().view(np.uint32)

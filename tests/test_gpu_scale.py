@@ -81,7 +81,7 @@ def test_scale_forward_sampled(name):
     assert errs["n_near"] <= max(3, len(pix) // 20)
 
 
-@pytest.mark.parametrize("name", ["C3", "C4v0"])
+@pytest.mark.parametrize("name", ["C3", "C5", "C4v0"])
 def test_scale_backward_sparse(name):
     sc = scene(name)
     H, W = sc.mask.shape
@@ -91,3 +91,26 @@ def test_scale_backward_sparse(name):
     res = run_gpu(sc, upstream=planes, counters=(name != "C4v0"))
     ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, upstream=per)
     compare_grads(res["grads"], ora["grads"], sc.gaussians.sh_degree)
+
+
+def test_c4_view_in_the_timed_configuration():
+    """Exactly what bench.py times: the non-counting kernels, pgsag_bin_sort_async with the bench's
+    capacity rule (1.15 x M + 4096, M from a counting pass), on a C4 view: lists, ranges and every
+    forward image bitwise equal to the synchronising path's; gradients (sparse upstream on sampled
+    pixels) vs the oracle with the R19 tolerances."""
+    sc = scene("C4v0")
+    H, W = sc.mask.shape
+    ref = run_gpu(sc, bg=(0.1, 0.2, 0.3), counters=False)
+    cap = int(1.15 * ref["r"].M) + 4096
+    pix = S.sample_pixels(sc.mask, 200, seed=21)
+    ora0 = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=(0.1, 0.2, 0.3))
+    planes, per = upstream_at(pix, H, W, seed=22, exclude=ora0["near"].astype(bool), ora=ora0, cam=sc.camera)
+    fast = run_gpu(sc, bg=(0.1, 0.2, 0.3), capacity=cap, upstream=planes, counters=False, sync_free=True)
+    assert fast["r"].M == ref["r"].M
+    np.testing.assert_array_equal(fast["vals"], ref["vals"])
+    np.testing.assert_array_equal(fast["ranges"], ref["ranges"])
+    for k in ("C", "N", "D", "A", "Dep", "T", "g", "last"):
+        np.testing.assert_array_equal(fast["img"][k], ref["img"][k])
+    compare_pixels(fast["img"], ora0, pix, W, fast["vals"], cam=sc.camera)
+    ora = oracle.render(sc.gaussians, sc.camera, sc.mask, pix, bg=(0.1, 0.2, 0.3), upstream=per, bound=True)
+    compare_grads(fast["grads"], ora["grads"], sc.gaussians.sh_degree, bound=ora["bound"])
