@@ -475,8 +475,12 @@ def main():
             "A1_preprocess": ("hbm", BYTES_A1[g0.sh_degree] * n_),
             "A2_scan": ("hbm", 8 * n_),
             "A3_duplicate": ("hbm", 8 * Mv + 20 * n_),
-            "A4_radix_onesweep": ("hbm", 4 * 16 * n_ + (2 if tile_bits > 9 else 1) * 16 * Mv),
-            "A4_radix_hist": ("hbm", 4 * n_ + 4 * Mv),
+            # stage 1 (depth, 32 bits, 4 passes over n) and stage 2 (tile, 2 passes over M): per pass
+            # key + value read and written (16 B per key)
+            "A4_radix_onesweep_s1": ("hbm", 4 * 16 * n_),
+            "A4_radix_onesweep_s2": ("hbm", (2 if tile_bits > 9 else 1) * 16 * Mv),
+            "A4_radix_hist_s1": ("hbm", 8 * n_ + 8 * n_),  # depth + tiles_touched read, keys + ids written
+            "A4_radix_hist_s2": ("hbm", 4 * Mv),
             "A5_ranges": ("hbm", 4 * Mv + 8 * tiles_),
             "A6_render_fwd": ("alu", INST_EVAL_FWD * Ev + INST_BLEND_FWD * Bv),
             "A7_render_bwd": ("alu", INST_VISIT_BWD * Vv + INST_BLEND_BWD * Bv),

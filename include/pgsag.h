@@ -41,7 +41,9 @@ enum {
   PGSAG_EINVAL = -1,    /* null pointer, n < 0, sh_degree > 3, width/height <= 0, misaligned buffer */
   PGSAG_ECAPACITY = -2, /* bins->capacity < M; bins->n_dup holds M, nothing else written */
   PGSAG_ECUDA = -3,     /* a CUDA launch/copy failed; message in pgsag_last_error() */
-  PGSAG_EWORKSPACE = -4 /* ws_bytes < pgsag_workspace_size(...) */
+  PGSAG_ENONFINITE = -4, /* a Gaussian parameter is NaN / inf (checked only with pgsag_set_checks(1):
+                            finiteness is a precondition; the check costs a host sync) */
+  PGSAG_EWORKSPACE = -5  /* ws_bytes < pgsag_workspace_size(...) */
 };
 
 /* Per-Gaussian flag bits written by pgsag_preprocess (A1). */
@@ -131,7 +133,9 @@ typedef struct {
   /* Optional fused L_GC-load statistics (NEXT-1, Eq. 9).  If gc_w (input, [H][W], the
    * weights of pgsag_gc_weights) is non-NULL, A6 accumulates over the mask pixels
    * gc_stats[0] = N, gc_stats[1] = sum r, gc_stats[2] = sum r^2 with r = g / w (gc_stats is
-   * zeroed by the call); L_GC-load = sqrt(sum r^2 / N - (sum r / N)^2). */
+   * zeroed by the call), and after the compositor gc_stats[3] = L_GC-load = the population std
+   * sqrt(sum r^2 / N - (sum r / N)^2) ("std over all pixels"), gc_stats[4] = sum r / N.
+   * gc_stats is double[5]. */
   const float *gc_w;
   double *gc_stats;
 } pgsag_image;
@@ -170,7 +174,9 @@ size_t pgsag_workspace_size(int32_t n, int32_t width, int32_t height, int64_t du
  * building pixel, the paper's RBM).  A1: per Gaussian, EWA projection
  * (P:78), culling, opacity-aware conservative tile rect (R8), active tiles touched,
  * flattened normal n_i (R4), d_i (Eq. 3, R2), SH colour (R12).  Key-path
- * arithmetic is IEEE float32 with no contraction (bit-exact with the oracle). */
+ * arithmetic is IEEE float32 with no contraction (bit-exact with the oracle).  ws: scratch of at least
+ * pgsag_workspace_size(n, width, height, 0) bytes (A0's word prefixes; the debug finiteness check),
+ * normally the workspace the view's pgsag_bin_sort uses. */
 int pgsag_preprocess(const pgsag_gaussians *g, const pgsag_camera *cam, const uint8_t *mask,
                      pgsag_tilemask *tm, pgsag_projected *out, void *ws, size_t ws_bytes, void *stream);
 
@@ -281,6 +287,20 @@ typedef struct {
   int32_t step;
 } pgsag_adam_hparams;
 
+/* The raw parameters the optimiser updates (R30, 3DGS's parameterisation) from the activated ones:
+ * state->log_scale = log(state->scale), state->logit_opacity = log(o / (1 - o)) (evaluated in
+ * double, stored as float), for n Gaussians.  Call once before the first pgsag_adam_step. */
+int pgsag_adam_init(int32_t n, pgsag_adam_state *state, void *stream);
+
+/* Eq. 11 on the device: total[0] = (1 - lambda) (rgb_loss[0] + lambda3 flatten_loss[0] +
+ * lambda4 L_ban) + lambda gc_stats[3], with L_ban = ban_loss[0] / ban_loss[1] (ban_mean = 1; 0 if
+ * the count is 0) or ban_loss[0] (ban_mean = 0).  rgb_loss is pgsag_rgb_loss's output, flatten_loss
+ * pgsag_adam_step's, ban_loss pgsag_ban_loss's, gc_stats pgsag_render_fwd's (pgsag_image.gc_stats);
+ * flatten_loss, ban_loss and gc_stats may be NULL (term absent).  All device pointers. */
+int pgsag_loss_total(const double *rgb_loss, const double *flatten_loss, const double *ban_loss, int32_t ban_mean,
+                     const double *gc_stats, float lambda, float lambda3, float lambda4, double *total,
+                     void *stream);
+
 /* One Adam step (Kingma & Ba) on the raw parameters with the gradients of pgsag_render_bwd (w.r.t.
  * the activated values, chained through exp / sigmoid here) plus flatten_weight * dL_s/dscale,
  * L_s = mean over the n Gaussians of min(scale) (PGSR flattening; R29; ties -> lowest
@@ -349,6 +369,12 @@ int pgsag_microbench_fp32(int32_t mode, int32_t iters, float *scratch, double *t
 
 /* Message for the last non-zero status on this thread ("" if none). */
 const char *pgsag_last_error(void);
+
+/* Debug checks: level 1 makes pgsag_preprocess verify that every Gaussian parameter is finite
+ * (SPEC S:289 makes finiteness a precondition) and return PGSAG_ENONFINITE otherwise; the check
+ * reads all parameters and synchronises the stream once (ws must hold >= 256 bytes).  0 (default)
+ * disables it.  Process-wide. */
+void pgsag_set_checks(int level);
 
 /* Library version string, e.g. "pgsag-b200 0.1 sm_100a". */
 const char *pgsag_version(void);

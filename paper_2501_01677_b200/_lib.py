@@ -11,7 +11,7 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpgsag.so")
 
-PGSAG_OK, PGSAG_EINVAL, PGSAG_ECAPACITY, PGSAG_ECUDA, PGSAG_EWORKSPACE = 0, -1, -2, -3, -4
+PGSAG_OK, PGSAG_EINVAL, PGSAG_ECAPACITY, PGSAG_ECUDA, PGSAG_ENONFINITE, PGSAG_EWORKSPACE = 0, -1, -2, -3, -4, -5
 F_VISIBLE, F_DET_OK, F_OPAC_OK, F_RECT, F_LIVE = 1, 2, 4, 8, 15
 
 SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_bin_sort_async", "pgsag_render_fwd",
@@ -19,7 +19,8 @@ SYMBOLS = ("pgsag_workspace_size", "pgsag_preprocess", "pgsag_bin_sort", "pgsag_
            "pgsag_timing_collect", "pgsag_timing_get", "pgsag_gc_weights", "pgsag_boundary_band",
            "pgsag_ban_loss", "pgsag_rgb_loss_workspace_size", "pgsag_rgb_loss", "pgsag_adam_step",
            "pgsag_densify_workspace_size", "pgsag_densify_plan", "pgsag_densify_apply", "pgsag_opacity_reset",
-           "pgsag_microbench_fp32", "pgsag_unpack_rgb8", "pgsag_render_bwd_adam")
+           "pgsag_microbench_fp32", "pgsag_unpack_rgb8", "pgsag_render_bwd_adam", "pgsag_set_checks",
+           "pgsag_adam_init", "pgsag_loss_total")
 
 _vp = C.c_void_p
 
@@ -158,6 +159,12 @@ def lib():
             L.pgsag_microbench_fp32.restype = C.c_int
             L.pgsag_unpack_rgb8.argtypes = [_vp, C.c_int32, C.c_int32, _vp, _vp]
             L.pgsag_unpack_rgb8.restype = C.c_int
+            L.pgsag_set_checks.argtypes = [C.c_int]
+            L.pgsag_set_checks.restype = None
+            L.pgsag_adam_init.argtypes = [C.c_int32, P(AdamState), _vp]
+            L.pgsag_adam_init.restype = C.c_int
+            L.pgsag_loss_total.argtypes = [_vp, _vp, _vp, C.c_int32, _vp, C.c_float, C.c_float, C.c_float, _vp, _vp]
+            L.pgsag_loss_total.restype = C.c_int
             _lib = L
     return _lib
 
@@ -292,3 +299,16 @@ def microbench_fp32(mode, iters, scratch, stream):
 
 def unpack_rgb8(rgb8, W, H, image, stream):
     return check(lib().pgsag_unpack_rgb8(rgb8, int(W), int(H), image, stream))
+
+
+def set_checks(level):
+    lib().pgsag_set_checks(int(level))
+
+
+def adam_init(n, state, stream):
+    return check(lib().pgsag_adam_init(int(n), C.byref(state), stream))
+
+
+def loss_total(rgb, flat, ban, ban_mean, gc_stats, lam, lam3, lam4, total, stream):
+    return check(lib().pgsag_loss_total(rgb, flat, ban, int(ban_mean), gc_stats, float(lam), float(lam3), float(lam4),
+                                        total, stream))

@@ -11,6 +11,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "dcheck.cuh"
+
 namespace pgsag {
 
 constexpr float kLog2e = 1.4426950408889634f;
@@ -188,7 +190,10 @@ __device__ __forceinline__ void build_lists(const uint32_t (&mk)[EPT], uint8_t* 
   for (int e = 0; e < EPT; ++e)
 #pragma unroll
     for (int b = 0; b < NB; ++b)
-      if ((mk[e] >> b) & 1u) s_list[b * (NT * EPT) + s_wc[(e * NW + sw) * NB + b] + pos[e][b]] = (uint8_t)(e * NT + tid);
+      if ((mk[e] >> b) & 1u) {
+        PGSAG_DCHECK(s_wc[(e * NW + sw) * NB + b] + pos[e][b] < (uint32_t)(NT * EPT));
+        s_list[b * (NT * EPT) + s_wc[(e * NW + sw) * NB + b] + pos[e][b]] = (uint8_t)(e * NT + tid);
+      }
   __syncthreads();
 }
 

@@ -11,6 +11,7 @@
 #include "internal.cuh"
 
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -102,6 +103,8 @@ int check_tm(const pgsag_tilemask* tm) {
   return PGSAG_OK;
 }
 
+std::atomic<int> g_checks{0};  // pgsag_set_checks: 1 = finiteness precondition of the Gaussians
+
 int check_g(const pgsag_gaussians* g) {
   if (!g) return fail(PGSAG_EINVAL, "gaussians is NULL");
   if (g->n < 0) return fail(PGSAG_EINVAL, "n < 0");
@@ -124,7 +127,9 @@ extern "C" {
 
 const char* pgsag_last_error(void) { return g_err.c_str(); }
 
-const char* pgsag_version(void) { return "pgsag-b200 0.1 sm_100a"; }
+const char* pgsag_version(void) { return "pgsag-b200 0.2 sm_100a"; }
+
+void pgsag_set_checks(int level) { g_checks.store(level); }
 
 void pgsag_timing_enable(int on) {
   std::lock_guard<std::mutex> lk(g_tmu);
@@ -172,14 +177,28 @@ size_t pgsag_workspace_size(int32_t n, int32_t width, int32_t height, int64_t du
 
 int pgsag_preprocess(const pgsag_gaussians* g, const pgsag_camera* cam, const uint8_t* mask, pgsag_tilemask* tm,
                      pgsag_projected* out, void* ws, size_t ws_bytes, void* stream) {
-  (void)ws; (void)ws_bytes;
   int rc;
   if ((rc = check_g(g)) || (rc = check_cam(cam)) || (rc = check_tm(tm))) return rc;
   if (!mask) return fail(PGSAG_EINVAL, "mask is NULL");
   if (g->n > 0 && (rc = check_proj(out))) return rc;
+  const WsLayout L = ws_layout(g->n, cam->width, cam->height, 0);
+  if ((rc = check_ws(ws, ws_bytes, L.a0 + 4 * (size_t)make_dims(cam->width, cam->height).TY *
+                                               make_dims(cam->width, cam->height).WPR)))
+    return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const Dims d = make_dims(cam->width, cam->height);
-  cudaError_t e = launch_tilemask(mask, d, tm, st);
+  cudaError_t e;
+  if (g_checks.load() && g->n > 0) {  // S:289 precondition, debug only (one host sync)
+    unsigned int* bad = static_cast<unsigned int*>(ws);
+    unsigned int nb = 0;
+    e = cudaMemsetAsync(bad, 0, sizeof(unsigned int), st);
+    if (e == cudaSuccess) e = launch_finite_check(g, bad, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&nb, bad, sizeof(nb), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "finite check");
+    if (nb) return fail(PGSAG_ENONFINITE, "non-finite Gaussian parameter (pgsag_set_checks)");
+  }
+  e = launch_tilemask(mask, d, tm, reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + L.a0), st);
   if (e != cudaSuccess) return cuda_fail(e, "tilemask");
   e = launch_preprocess(g, cam, d, tm, out, st);
   if (e != cudaSuccess) return cuda_fail(e, "preprocess");
@@ -394,6 +413,24 @@ int pgsag_adam_step(int32_t n, int32_t sh_degree, const pgsag_gaussian_grad* gra
     return fail(PGSAG_EINVAL, "adam: NULL buffer");
   cudaError_t e = launch_adam(n, sh_degree, grad, state, hp, flatten_loss, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "adam");
+  return PGSAG_OK;
+}
+
+int pgsag_adam_init(int32_t n, pgsag_adam_state* state, void* stream) {
+  if (n < 0 || !state) return fail(PGSAG_EINVAL, "adam_init: bad argument");
+  if (n > 0 && (!state->scale || !state->opacity || !state->log_scale || !state->logit_opacity))
+    return fail(PGSAG_EINVAL, "adam_init: NULL buffer");
+  cudaError_t e = launch_adam_init(n, state, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "adam_init");
+  return PGSAG_OK;
+}
+
+int pgsag_loss_total(const double* rgb_loss, const double* flatten_loss, const double* ban_loss, int32_t ban_mean,
+                     const double* gc_stats, float lambda, float lambda3, float lambda4, double* total, void* stream) {
+  if (!rgb_loss || !total) return fail(PGSAG_EINVAL, "loss_total: NULL argument");
+  cudaError_t e = launch_loss_total(rgb_loss, flatten_loss, ban_loss, gc_stats, lambda, lambda3, lambda4, ban_mean,
+                                    total, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "loss_total");
   return PGSAG_OK;
 }
 

@@ -1,6 +1,7 @@
 // Internal declarations shared by the libpgsag.so translation units.
 // Product code only: nothing here is shared with oracle/ (DESIGN.md §1).
 #pragma once
+#include "dcheck.cuh"
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -56,7 +57,9 @@ struct WsLayout {
   size_t hist;                   // [2][kMaxSortPasses][256] u32
   size_t counters;               // [64] u32 (tile counters, M, misc); first: offset 0 for every size
   size_t zero_end;               // end of the state a sort call zeroes: [counters, zero_end)
+  size_t a0;                     // [TY*WPR] u32 A0 scratch (bitmap word prefixes); offset depends on W, H only
   size_t g2d;                    // [n][16] f32 per-Gaussian 2D gradients (A7 -> A8; 14 used)
+  size_t lpt;                    // [TY*TX] u32 (length class, slot) of each active tile (A5b)
   size_t total;
   int tiles1, tiles2, tilesN;
 };
@@ -73,7 +76,9 @@ enum : int {
   CNT_M = 12,      // 2 slots: M as u64 (A2 total)
   CNT_MC = 14,     // M as u32 if M <= capacity, else 0 (published by A3: an overflowed view has empty lists)
   CNT_OVF = 15,    // 1 if M > capacity (published by A3; the fused A8 + Adam step is then skipped)
-  CNT_N = 16
+  CNT_NG = 16,     // n of the sorted view (published by A3; read by the debug bounds checks of A6)
+  CNT_LPT = 24,    // 33 slots: active tiles per LPT length class (A5b)
+  CNT_N = 57
 };
 
 // ------------------------------------------------------------- kernel timing
@@ -87,7 +92,8 @@ struct KTimer {
 };
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_tilemask(const uint8_t* mask, const Dims& d, pgsag_tilemask* tm, cudaStream_t st);
+cudaError_t launch_tilemask(const uint8_t* mask, const Dims& d, pgsag_tilemask* tm, uint32_t* scratch,
+                            cudaStream_t st);
 cudaError_t launch_preprocess(const pgsag_gaussians* g, const pgsag_camera* cam, const Dims& d,
                               const pgsag_tilemask* tm, pgsag_projected* out, cudaStream_t st);
 cudaError_t launch_bin_sort_stage1(const pgsag_projected* p, int n, const WsLayout& L, char* ws,
@@ -124,6 +130,10 @@ cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8
 cudaError_t launch_unpack_rgb8(const uint8_t* rgb, int W, int H, float* chw, cudaStream_t st);
 cudaError_t launch_adam(int n, int sh_degree, const pgsag_gaussian_grad* gr, pgsag_adam_state* s,
                         const pgsag_adam_hparams* hp, double* flat, cudaStream_t st);
+cudaError_t launch_adam_init(int n, pgsag_adam_state* s, cudaStream_t st);
+cudaError_t launch_loss_total(const double* rgb, const double* flat, const double* ban, const double* gc, double lam,
+                              double lam3, double lam4, int ban_mean, double* out, cudaStream_t st);
+cudaError_t launch_finite_check(const pgsag_gaussians* g, unsigned int* bad, cudaStream_t st);
 
 size_t densify_ws_bytes(int n);
 cudaError_t launch_densify_plan(int n, const float* scale, const float* op, const float* accum, const float* count,
@@ -137,6 +147,7 @@ cudaError_t launch_opacity_reset(int n, pgsag_adam_state* s, float cap, cudaStre
 cudaError_t launch_fp32_microbench(int mode, int iters, float* scratch, float* ms, double* flops, cudaStream_t st);
 
 // counters[] slots for pgsag_gc_weights: 8 (sum, count) double pairs at bytes 4*CNT_GC .. 4*CNT_GC + 127
-constexpr int CNT_GC = 32;
+constexpr int CNT_GC = 64;
+constexpr int kCounters = 128;  // u32 slots of the workspace counter block
 
 }  // namespace pgsag

@@ -9,6 +9,8 @@
 // viewing direction of each camera and then projected onto different image
 // tiles"; Eq. 2-3 (n_i, R_c n_i, d_i); P:243 masked pixels only.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "internal.cuh"
@@ -51,57 +53,54 @@ __global__ void __launch_bounds__(128) tilemask_count_kernel(const uint8_t* __re
   if (lane == 0 && wtx < d.TX) bitmap[ty * d.WPR + wtx / 32] = word;
 }
 
-// ------------------------------------------------------- A0 SAT + active list
-// Single CTA: the active-tile bitmap (TY x WPR words, 10 KB at 5472x3648) lives in
-// shared memory; one thread per SAT column accumulates down the rows.
-__global__ void __launch_bounds__(1024) tilemask_sat_kernel(Dims d, const uint32_t* __restrict__ bitmap_g,
-                                                              int32_t* __restrict__ sat,
-                                                              uint32_t* __restrict__ active,
-                                                              uint32_t* __restrict__ n_active) {
-  extern __shared__ uint32_t smem[];
-  uint32_t* bm = smem;                       // [TY][WPR]
-  uint32_t* rowpre = smem + d.TY * d.WPR;    // [TY+1] exclusive prefix of row totals
-  const int nt = blockDim.x, tid = threadIdx.x;
-  for (int k = tid; k < d.TY * d.WPR; k += nt) bm[k] = bitmap_g[k];
-  __syncthreads();
-  for (int y = tid; y < d.TY; y += nt) {
-    uint32_t c = 0;
-    for (int w = 0; w < d.WPR; ++w) c += __popc(bm[y * d.WPR + w]);
-    rowpre[y + 1] = c;
-  }
-  __syncthreads();
-  if (tid < 32) {  // warp-0 inclusive scan of rowpre[1..TY]
-    uint32_t carry = 0;
-    for (int base = 0; base < d.TY; base += 32) {
-      const int y = base + tid;
-      uint32_t v = y < d.TY ? rowpre[y + 1] : 0u;
+// ------------------------------------------------------------- A0 active list
+// (1) one CTA: exclusive prefix of the active-tile counts of the bitmap words (TY x WPR words,
+// row-major = tile order), 1024 threads with a few words each; (2) one warp per bitmap word, one
+// lane per bit: every active tile is written at its word's prefix + the set bits below it, so the
+// list is in ascending tile order.
+__global__ void __launch_bounds__(1024) tilemask_prefix_kernel(Dims d, const uint32_t* __restrict__ bitmap,
+                                                                 uint32_t* __restrict__ wpre,
+                                                                 uint32_t* __restrict__ n_active) {
+  constexpr int NT = 1024;
+  __shared__ uint32_t s_warp[NT / 32];
+  const int nw = d.TY * d.WPR, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int per = (nw + NT - 1) / NT;  // consecutive words per thread
+  const int k0 = tid * per;
+  uint32_t sum = 0;
+  for (int j = 0; j < per; ++j)
+    if (k0 + j < nw) sum += __popc(bitmap[k0 + j]);
+  uint32_t x = sum;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (tid >= o) v += u;
-      }
-      if (y < d.TY) rowpre[y + 1] = v + carry;
-      carry += __shfl_sync(0xffffffffu, v, 31);
-    }
-    if (tid == 0) rowpre[0] = 0;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += u;
   }
+  if (lane == 31) s_warp[w] = x;
   __syncthreads();
-  (void)sat;
-  // word-parallel active list: thread per bitmap word, set bits in ascending order
-  for (int k = tid; k < d.TY * d.WPR; k += nt) {
-    const int y = k / d.WPR, wq = k - y * d.WPR;
-    uint32_t bits = bm[k];
-    if (!bits) continue;
-    uint32_t pos = rowpre[y];
-    for (int w = 0; w < wq; ++w) pos += __popc(bm[y * d.WPR + w]);
-    const uint32_t t0 = (uint32_t)(y * d.TX + wq * 32);
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1u;
-      active[pos++] = t0 + (uint32_t)b;
-    }
+  uint32_t wb = 0, tot = 0;
+  for (int k = 0; k < NT / 32; ++k) {
+    const uint32_t t = s_warp[k];
+    if (k < w) wb += t;
+    tot += t;
   }
-  if (tid == 0) *n_active = rowpre[d.TY];
+  uint32_t run = wb + x - sum;
+  for (int j = 0; j < per; ++j)
+    if (k0 + j < nw) {
+      wpre[k0 + j] = run;
+      run += __popc(bitmap[k0 + j]);
+    }
+  if (tid == 0) *n_active = tot;
+}
+
+__global__ void __launch_bounds__(256) tilemask_list_kernel(Dims d, const uint32_t* __restrict__ bitmap,
+                                                              const uint32_t* __restrict__ wpre,
+                                                              uint32_t* __restrict__ active) {
+  const int k = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (k >= d.TY * d.WPR) return;
+  const uint32_t bits = bitmap[k];
+  if (!((bits >> lane) & 1u)) return;
+  const int y = k / d.WPR, x = (k - y * d.WPR) * 32 + lane;
+  active[wpre[k] + __popc(bits & ((1u << lane) - 1u))] = (uint32_t)(y * d.TX + x);
 }
 
 // SAT of the active flags, SAT[y][x] = #active tiles with ty < y, tx < x: one warp per
@@ -346,7 +345,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
 
 }  // namespace
 
-cudaError_t launch_tilemask(const uint8_t* mask, const Dims& d, pgsag_tilemask* tm, cudaStream_t st) {
+cudaError_t launch_tilemask(const uint8_t* mask, const Dims& d, pgsag_tilemask* tm, uint32_t* scratch,
+                            cudaStream_t st) {
   uint32_t* bitmap = tm->active_bits;
   const int vec16 = (d.W % 16 == 0) && ((reinterpret_cast<uintptr_t>(mask) & 15u) == 0);
   dim3 grid((d.TX + 127) / 128, d.TY);
@@ -354,17 +354,41 @@ cudaError_t launch_tilemask(const uint8_t* mask, const Dims& d, pgsag_tilemask* 
     KTimer kt_("A0_tilemask_count", st);
     tilemask_count_kernel<<<grid, 128, 0, st>>>(mask, d, tm->tile_cnt, bitmap, vec16);
   }
-  const size_t smem = sizeof(uint32_t) * ((size_t)d.TY * d.WPR + d.TY + 1);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(tilemask_sat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  uint32_t* wpre = scratch;  // [TY*WPR] word prefixes (workspace)
+  {
+    KTimer kt_("A0_tilemask_prefix", st);
+    tilemask_prefix_kernel<<<1, 1024, 0, st>>>(d, bitmap, wpre, tm->n_active);
+  }
   {
     KTimer kt_("A0_tilemask_list", st);
-    tilemask_sat_kernel<<<1, 1024, smem, st>>>(d, bitmap, tm->sat, tm->active, tm->n_active);
+    const int words = d.TY * d.WPR;
+    tilemask_list_kernel<<<(words * 32 + 255) / 256, 256, 0, st>>>(d, bitmap, wpre, tm->active);
   }
   if (tm->sat) {  // optional output (not needed by the path: A1 counts from the bitmap)
     KTimer kt_("A0_tilemask_sat", st);
     tilemask_satcol_kernel<<<(d.TX + 1 + 31) / 32, 32, sizeof(uint32_t) * d.TY, st>>>(d, bitmap, tm->sat);
+  }
+  return cudaGetLastError();
+}
+
+namespace {
+// Debug check (pgsag_set_checks): count non-finite Gaussian parameters (S:289 precondition).
+__global__ void finite_check_kernel(const float* __restrict__ a, size_t count, unsigned int* __restrict__ bad) {
+  unsigned int b = 0;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < count; k += (size_t)gridDim.x * blockDim.x)
+    b += !isfinite(a[k]);
+  b = __reduce_add_sync(0xffffffffu, b);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, b);
+}
+}  // namespace
+
+cudaError_t launch_finite_check(const pgsag_gaussians* g, unsigned int* bad, cudaStream_t st) {
+  const size_t n = (size_t)g->n, K3 = (size_t)(g->sh_degree + 1) * (g->sh_degree + 1) * 3;
+  const float* arr[5] = {g->mean, g->scale, g->rot, g->opacity, g->sh};
+  const size_t cnt[5] = {3 * n, 3 * n, 4 * n, n, K3 * n};
+  for (int k = 0; k < 5; ++k) {
+    if (!cnt[k]) continue;
+    finite_check_kernel<<<(unsigned)std::min<size_t>((cnt[k] + 255) / 256, 1184), 256, 0, st>>>(arr[k], cnt[k], bad);
   }
   return cudaGetLastError();
 }

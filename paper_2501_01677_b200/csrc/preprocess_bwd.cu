@@ -14,7 +14,7 @@ constexpr int kG2 = 14;
 // --------------------------------------------------------------------- A8
 // Per-Gaussian chain rule in float64 (FP64 on B200 is ample for ~600 ops per
 // Gaussian; the conic -> covariance -> Sigma chain amplifies rounding, so it is
-// done in double from the double-accumulated 2D gradients).
+// done in double from A7's float32-accumulated 2D gradients, widened exactly).
 struct CamB {
   double fx, fy, C[3], R[9], lx, ly;
 };

@@ -148,8 +148,7 @@ __device__ __forceinline__ void load_pixel(const BwdArgs& a, bool inb, size_t pi
   const float w = a.gc_w ? __ldg(a.gc_w + q) : 1.0f;
   float gG = 0.f;
   if (a.gc_w) {  // Eq. 9: L = std(r), r = g / w  ->  dL/dg = (r - mean) / (N L w)
-    const double Nn = a.gc_stats[0], mu = a.gc_stats[1] / Nn;
-    const double L = sqrt(fmax(a.gc_stats[2] / Nn - mu * mu, 0.0));
+    const double Nn = a.gc_stats[0], L = a.gc_stats[3], mu = a.gc_stats[4];  // finalised after A6
     if (L > 0.0) gG = (float)((double)a.gc_lambda * ((double)gcount / w - mu) / (Nn * L * w));
   }
   if (a.nd_div) {  // sum-gradient of a mean loss: divide by its term count
@@ -258,6 +257,13 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   const uint32_t acc_lane = opaque(smem_u32(s_acc) + (uint32_t)my_c * 4u);
   const uint32_t wr = opaque((uint32_t)writer);
   for (int k = tid; k < kBBatch * kAccStride; k += kBT) s_acc[k] = 0.f;
+#ifdef PGSAG_DEBUG_BOUNDS
+  // race-freedom of the shared accumulator (single warp: one writer lane per value slot)
+  if (kBW == 1) {
+    const uint32_t wm = __ballot_sync(0xffffffffu, writer);
+    if (writer) PGSAG_DCHECK(__match_any_sync(wm, my_c) == (1u << lane) && my_c >= 0 && my_c < 14);
+  }
+#endif
   if (tid == 0) s_tile = atomicAdd(a.work, 1u);
   for (;;) {
     if (tid == 0) s_maxlast = -1;
@@ -271,6 +277,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
     const int i = tx * kTile + half * 8 + (lane & 7);
     const int jb = ty * kTile + (lane >> 3);
     const uint32_t rs = a.ranges[2 * tile];
+    PGSAG_DCHECK(tile < (uint32_t)(a.d.TX * a.d.TY));
     const float px = opaque((float)i + 0.5f);
     const float2 py01 = f2(opaque((float)jb + 0.5f), opaque((float)(jb + 4) + 0.5f));
     const float2 py23 = f2(opaque((float)(jb + 8) + 0.5f), opaque((float)(jb + 12) + 0.5f));
@@ -304,6 +311,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         mk[e] = 0u;
         if (slot < cnt) {
           const uint32_t id = a.vals[blo + slot];
+          PGSAG_DCHECK(id < (uint32_t)a.n);
           Rec& r = s_rec[slot];
           if (kBW > 1) {
             mk[e] = stage_gaussian<8, 16>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
@@ -335,6 +343,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       while (t >= 0 && (int)lds_u8(lbase + (uint32_t)t) > qtop) --t;  // warp-uniform
       for (; t >= 0; --t) {
         const int q = (int)lds_u8(lbase + (uint32_t)t);
+        PGSAG_DCHECK(q < cnt);
         const int kk = blo + q;
         const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
         const float4 ra = lds128(ra_addr);

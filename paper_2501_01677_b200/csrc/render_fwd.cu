@@ -44,6 +44,7 @@ struct FwdArgs {
   uint32_t* work;
   const float* gc_w;   // optional L_GC-load weights (NEXT-1)
   double* gc_stats;    // N, sum r, sum r^2
+  const uint32_t* n_dev;  // Gaussians of the sorted view (A3's CNT_NG; debug bounds checks)
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -114,6 +115,7 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
     const int i = tx * kTile + (w & 1) * 8 + (lane & 7);
     const int jb = ty * kTile + (w >> 1) * Cfg::BH + (lane >> 3);
     const uint32_t rs = a.ranges[2 * tile], re = a.ranges[2 * tile + 1];
+    PGSAG_DCHECK(tile < (uint32_t)(a.d.TX * a.d.TY) && rs <= re);
     const float px = (float)i + 0.5f;
     const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
     // per pair p: rows jb + 8p and jb + 8p + 4.  T carries the pixel's "done" state in its
@@ -150,6 +152,7 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
         mk[e] = 0u;
         if (k < re) {
           const uint32_t id = a.vals[k];
+          PGSAG_DCHECK(id < *a.n_dev);
           Rec& r = s_rec[e * NT + tid];
           mk[e] = stage_gaussian<8, Cfg::BH>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
           r.b.w = (float)(e * NT + tid);  // slot in the batch, for the blend's last index
@@ -169,6 +172,7 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
         const int tend = min(t0 + 8, nw);
         for (int t = t0; t < tend; ++t) {
           const uint32_t q = lds_u8(lbase + (uint32_t)t);
+          PGSAG_DCHECK(b + q < re);
           const uint32_t ra_addr = rec_base + q * (uint32_t)sizeof(Rec);
           const float4 ra = lds128(ra_addr);
           const float4 rb = lds128(ra_addr + 16);
@@ -273,6 +277,14 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
 constexpr int kNP = PGSAG_FWD_NP;
 constexpr int kFT = FwdCfg<kNP>::NT;
 
+// Eq. 9 from the fused statistics: L_GC-load = population std of r = g / w over the mask pixels.
+__global__ void gc_finalize_kernel(double* st) {
+  const double n = st[0];
+  const double mu = n > 0.0 ? st[1] / n : 0.0;
+  st[3] = n > 0.0 ? sqrt(fmax(st[2] / n - mu * mu, 0.0)) : 0.0;
+  st[4] = mu;
+}
+
 int fwd_grid() {
   static int grid[kMaxDevices] = {};
   const int dev = current_device();
@@ -310,7 +322,8 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
   a.work = work_counter;
   a.gc_w = out->gc_w;
   a.gc_stats = out->gc_stats;
-  if (a.gc_w) cudaMemsetAsync(a.gc_stats, 0, 3 * sizeof(double), st);
+  a.n_dev = work_counter + (CNT_NG - CNT_FWD);
+  if (a.gc_w) cudaMemsetAsync(a.gc_stats, 0, 5 * sizeof(double), st);
   const int grid = min(fwd_grid(), d.TX * d.TY);
   {
     KTimer kt_("A6_render_fwd", st);
@@ -318,6 +331,10 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
       render_fwd_kernel<true, kNP><<<grid, kFT, 0, st>>>(a);
     else
       render_fwd_kernel<false, kNP><<<grid, kFT, 0, st>>>(a);
+  }
+  if (a.gc_w) {
+    KTimer kt_("N1_gc_finalize", st);
+    gc_finalize_kernel<<<1, 1, 0, st>>>(a.gc_stats);
   }
   return cudaGetLastError();
 }

@@ -60,19 +60,10 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
   return total;
 }
 
-// ----------------------------------------------------------------- keys
-// Stage-1 keys: depth bits for Gaussians that emit entries, else all-ones (last).
-__global__ void depth_keys_kernel(int n, const float* __restrict__ depth, const uint32_t* __restrict__ touched,
-                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ ids) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  keys[i] = touched[i] > 0 ? __float_as_uint(depth[i]) : 0xFFFFFFFFu;  // z > znear > 0: bit order = value order
-  ids[i] = (uint32_t)i;
-}
-
 // ------------------------------------------------------------ pass plan
 // Digit widths of an LSD sort over `bits` key bits: 8-bit digits, or 9-bit ones
-// where that saves a pass (17-18 bits: 2 passes instead of 3; 25-27: 3 instead of 4).
+// where that saves a pass (17-18 bits: 2 passes instead of 3; 25-27: 3 instead of 4).  At 17 bits the
+// 9-bit digit is the high one: its bins are the sparsely used ones (tile rows), which the pass skips.
 struct PassPlan {
   int n;
   int shift[kMaxSortPasses];
@@ -86,6 +77,7 @@ PassPlan make_plan(int bits) {
   if (bits <= 0) return p;
   if (bits <= 9) { w[0] = bits; p.n = 1; }
   else if (bits <= 16) { w[0] = 8; w[1] = bits - 8; p.n = 2; }
+  else if (bits <= 17) { w[0] = 8; w[1] = bits - 8; p.n = 2; }  // the wide digit on the sparse high bits
   else if (bits <= 18) { w[0] = 9; w[1] = bits - 9; p.n = 2; }
   else if (bits <= 24) { w[0] = 8; w[1] = 8; w[2] = bits - 16; p.n = 3; }
   else if (bits <= 27) { w[0] = 9; w[1] = 9; w[2] = bits - 18; p.n = 3; }
@@ -97,18 +89,38 @@ PassPlan make_plan(int bits) {
 
 // ------------------------------------------------------------ histogram
 // Digit histograms of all passes at once (onesweep's upfront pass); ghist is
-// [pass][kMaxRadix].
-__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys,
+// [pass][kMaxRadix].  (Warp-aggregating the shared-memory counts with match_any was measured 4x
+// slower.)  kFromDepth (stage 1): the keys are formed here from A1's outputs -- the depth bits of Gaussians
+// that emit entries, all-ones (sorted last) otherwise; z > znear > 0, so bit order is value order
+// -- and written out with the identity ids for the first pass.
+template <bool kFromDepth>
+__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys_in,
                                                           const uint32_t* __restrict__ n_ptr, uint32_t n_fixed,
-                                                          PassPlan plan, uint32_t* __restrict__ ghist) {
+                                                          PassPlan plan, uint32_t* __restrict__ ghist,
+                                                          const float* __restrict__ depth,
+                                                          const uint32_t* __restrict__ touched,
+                                                          uint32_t* __restrict__ keys_out,
+                                                          uint32_t* __restrict__ ids_out) {
   __shared__ uint32_t sh[kMaxSortPasses][kMaxRadix];
   const uint32_t n = n_ptr ? min(*n_ptr, n_fixed) : n_fixed;
   for (int k = threadIdx.x; k < kMaxSortPasses * kMaxRadix; k += blockDim.x) (&sh[0][0])[k] = 0;
   __syncthreads();
-  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-    const uint32_t key = keys[idx];
-    for (int p = 0; p < plan.n; ++p)
-      atomicAdd(&sh[p][(key >> plan.shift[p]) & ((1u << plan.width[p]) - 1u)], 1u);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {  // warp-uniform trip count
+    const uint32_t idx = base + threadIdx.x;
+    const bool live = idx < n;
+    uint32_t key = 0xFFFFFFFFu;
+    if (live) {
+      if (kFromDepth) {
+        key = touched[idx] > 0 ? __float_as_uint(depth[idx]) : 0xFFFFFFFFu;
+        keys_out[idx] = key;
+        ids_out[idx] = idx;
+      } else {
+        key = keys_in[idx];
+      }
+    }
+    if (live)
+      for (int p = 0; p < plan.n; ++p) atomicAdd(&sh[p][(key >> plan.shift[p]) & ((1u << plan.width[p]) - 1u)], 1u);
   }
   __syncthreads();
   for (int k = threadIdx.x; k < plan.n * kMaxRadix; k += blockDim.x) {
@@ -171,10 +183,12 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
     const uint32_t dg = idx < n ? ((key[k] >> shift) & mask) : (uint32_t)R;
     const uint32_t peers = __match_any_sync(0xffffffffu, dg);
     const uint32_t r = __popc(peers & lt);
-    const uint32_t prev = dg < (uint32_t)R ? s_whist[w * R + dg] : 0u;
-    __syncwarp();
-    if (r == 0 && dg < (uint32_t)R) s_whist[w * R + dg] = prev + __popc(peers);
-    __syncwarp();
+    // the peers' leader takes the group's counts with one shared atomic (in item order: a warp's
+    // shared-memory atomics on one address complete in issue order) and broadcasts the base
+    const int leader = __ffs(peers) - 1;
+    uint32_t prev = 0u;
+    if (r == 0 && dg < (uint32_t)R) prev = atomicAdd(&s_whist[w * R + dg], (uint32_t)__popc(peers));
+    prev = __shfl_sync(0xffffffffu, prev, leader);
     rank[k] = prev + r;
   }
   __syncthreads();
@@ -196,13 +210,14 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
     tsum += total;
     gh[j] = ghist[dgt];
     gsum += gh[j];
-    st_volatile(status + (size_t)tile * R + dgt, (tile == 0 ? kLbPrefix : kLbAgg) | total);
+    // a digit no key of the whole input has needs no look-back state (every CTA skips it alike)
+    if (gh[j]) st_volatile(status + (size_t)tile * R + dgt, (tile == 0 ? kLbPrefix : kLbAgg) | total);
   }
 #pragma unroll
   for (int j = 0; j < DPT; ++j) {
     const int dgt = tid * DPT + j;
     uint32_t ex = 0;
-    if (tile != 0) {
+    if (tile != 0 && gh[j] != 0) {
       int q = (int)tile - 1;
       while (q >= 0) {
         uint32_t s;
@@ -235,6 +250,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
     if (idx < n) {
       const uint32_t dg = (key[k] >> shift) & mask;
       const uint32_t pos = s_cta_start[dg] + s_whist[w * R + dg] + rank[k];
+      PGSAG_DCHECK(pos < (uint32_t)kSortTile);
       s_keys[pos] = key[k];
       s_vals[pos] = val[k];
     }
@@ -245,6 +261,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
     const uint32_t k = s_keys[p];
     const uint32_t dg = (k >> shift) & mask;
     const uint32_t dst = s_gbase[dg] + (p - s_cta_start[dg]);
+    PGSAG_DCHECK(dst < n);
     keys_out[dst] = k;
     vals_out[dst] = s_vals[p];
   }
@@ -260,21 +277,31 @@ __global__ void __launch_bounds__(256) scan_kernel(int n, const uint32_t* __rest
                                                     uint32_t* __restrict__ tile_counter,
                                                     unsigned long long* __restrict__ total) {
   constexpr int IT = kScanTile / 256;
+  constexpr int PAD = IT + 1;  // padded rows: the blocked reads of the transpose are conflict-free
   __shared__ uint32_t s_warp[8];
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_excl;
+  __shared__ uint32_t s_v[256 * PAD];
   const int tid = threadIdx.x;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint32_t base = tile * kScanTile;
   if (base >= (uint32_t)n) return;
+  // striped (coalesced) loads of the ids and their counts, transposed through shared memory so
+  // that each thread then owns IT consecutive items
+#pragma unroll
+  for (int k = 0; k < IT; ++k) {
+    const uint32_t j = (uint32_t)(k * 256 + tid);
+    const uint32_t idx = base + j;
+    s_v[(j / IT) * PAD + j % IT] = idx < (uint32_t)n ? __ldg(touched + ids[idx]) : 0u;
+  }
+  __syncthreads();
   uint32_t v[IT];
   uint32_t sum = 0;
 #pragma unroll
-  for (int k = 0; k < IT; ++k) {  // blocked: thread owns IT consecutive items
-    const uint32_t idx = base + tid * IT + k;
-    v[k] = idx < (uint32_t)n ? touched[ids[idx]] : 0u;
+  for (int k = 0; k < IT; ++k) {
+    v[k] = s_v[tid * PAD + k];
     sum += v[k];
   }
   uint32_t texcl;
@@ -302,10 +329,16 @@ __global__ void __launch_bounds__(256) scan_kernel(int n, const uint32_t* __rest
   __syncthreads();
   uint32_t run = (uint32_t)s_excl + texcl;
 #pragma unroll
-  for (int k = 0; k < IT; ++k) {
-    const uint32_t idx = base + tid * IT + k;
-    if (idx < (uint32_t)n) offsets[idx] = run;
+  for (int k = 0; k < IT; ++k) {  // exclusive offsets back into the blocked slots
+    s_v[tid * PAD + k] = run;
     run += v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < IT; ++k) {  // striped (coalesced) stores
+    const uint32_t j = (uint32_t)(k * 256 + tid);
+    const uint32_t idx = base + j;
+    if (idx < (uint32_t)n) offsets[idx] = s_v[(j / IT) * PAD + j % IT];
   }
 }
 
@@ -330,13 +363,15 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
                                                          uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
                                                          uint32_t cap, const unsigned long long* __restrict__ M64,
                                                          uint32_t* __restrict__ m_clamped,
-                                                         uint32_t* __restrict__ overflow) {
+                                                         uint32_t* __restrict__ overflow,
+                                                         uint32_t* __restrict__ n_out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if (k == 0) {
     const unsigned long long M = *M64;
     *m_clamped = M <= (unsigned long long)cap ? (uint32_t)M : 0u;
     *overflow = M > (unsigned long long)cap ? 1u : 0u;
+    *n_out = (uint32_t)n;
   }
   uint32_t id = 0, cnt = 0, o = 0;
   short4 r = make_short4(0, 0, -1, -1);
@@ -358,6 +393,7 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
       const uint32_t* row = bitmap + ty * d.WPR;
       for (int tx = r.x; tx <= r.z; ++tx) {
         if ((__ldg(row + (tx >> 5)) >> (tx & 31)) & 1u) {
+          PGSAG_DCHECK(oo < o + cnt && oo < cap);
           tkeys[oo] = (uint32_t)(ty * d.TX + tx);
           tvals[oo] = id;
           ++oo;
@@ -389,6 +425,7 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
       const uint32_t bal = __ballot_sync(0xffffffffu, act);
       if (act) {
         const uint32_t pos = go + written + __popc(bal & lt);
+        PGSAG_DCHECK(pos < cap);
         tkeys[pos] = tile;
         tvals[pos] = gid;
       }
@@ -410,33 +447,48 @@ __global__ void ranges_kernel(const uint32_t* __restrict__ tkeys, const uint32_t
 }
 
 // ------------------------------------------------------ A5b work order (LPT)
-// One CTA: the active tiles bucketed by floor(log2(list length)), emitted longest class first,
-// so the persistent A6/A7 grids start the heaviest tiles first (longest-processing-time order;
-// the order inside a class is arbitrary).
-__global__ void __launch_bounds__(1024) lpt_order_kernel(const uint32_t* __restrict__ active,
-                                                         const uint32_t* __restrict__ n_active,
-                                                         const uint2* __restrict__ ranges,
-                                                         uint32_t* __restrict__ order) {
-  __shared__ uint32_t s_cnt[33], s_pos[33];
-  const int tid = threadIdx.x;
+// The active tiles bucketed by floor(log2(list length)), emitted longest class first, so the
+// persistent A6/A7 grids start the heaviest tiles first (longest-processing-time order; the order
+// inside a class is arbitrary).  Two grid-wide kernels: (1) every active tile takes a slot in its
+// class (warp-aggregated atomics on the 33 class counters), (2) every tile is written at its
+// class's offset (classes longest first) + its slot.
+__device__ __forceinline__ uint32_t lpt_class(const uint2* __restrict__ ranges, uint32_t tile) {
+  const uint2 r = __ldg(ranges + tile);
+  return 32u - (uint32_t)__clz(r.y - r.x);  // 0 for an empty list, 1..32 otherwise
+}
+
+__global__ void __launch_bounds__(256) lpt_class_kernel(const uint32_t* __restrict__ active,
+                                                        const uint32_t* __restrict__ n_active,
+                                                        const uint2* __restrict__ ranges,
+                                                        uint32_t* __restrict__ cls_cnt, uint32_t* __restrict__ packed) {
   const uint32_t na = *n_active;
-  if (tid < 33) s_cnt[tid] = 0;
-  __syncthreads();
-  auto cls = [&](uint32_t tile) {  // 32 - clz(len): 0 for an empty list, 1..32 otherwise
-    const uint2 r = __ldg(ranges + tile);
-    return 32 - __clz(r.y - r.x);
-  };
-  for (uint32_t k = tid; k < na; k += 1024) atomicAdd(&s_cnt[cls(__ldg(active + k))], 1u);
-  __syncthreads();
-  if (tid == 0) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = k < na;
+  const uint32_t c = live ? lpt_class(ranges, __ldg(active + k)) : 63u;
+  const uint32_t peers = __match_any_sync(0xffffffffu, c);
+  const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == leader && live) base = atomicAdd(cls_cnt + c, (uint32_t)__popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (live) packed[k] = (c << 26) | (base + (uint32_t)__popc(peers & ((1u << lane) - 1u)));
+}
+
+__global__ void __launch_bounds__(256) lpt_scatter_kernel(const uint32_t* __restrict__ active,
+                                                          const uint32_t* __restrict__ n_active,
+                                                          const uint32_t* __restrict__ cls_cnt,
+                                                          const uint32_t* __restrict__ packed,
+                                                          uint32_t* __restrict__ order) {
+  __shared__ uint32_t s_pos[33];
+  if (threadIdx.x == 0) {
     uint32_t run = 0;
-    for (int c = 32; c >= 0; --c) { s_pos[c] = run; run += s_cnt[c]; }
+    for (int c = 32; c >= 0; --c) { s_pos[c] = run; run += cls_cnt[c]; }
   }
   __syncthreads();
-  for (uint32_t k = tid; k < na; k += 1024) {
-    const uint32_t t = __ldg(active + k);
-    order[atomicAdd(&s_pos[cls(t)], 1u)] = t;
-  }
+  const uint32_t na = *n_active;
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= na) return;
+  const uint32_t p = packed[k];
+  order[s_pos[p >> 26] + (p & 0x3FFFFFFu)] = __ldg(active + k);
 }
 
 int num_sms() {
@@ -455,7 +507,8 @@ int num_sms() {
 // pointer (n_dev) or a fixed count with a capacity bound for the grid size.
 cudaError_t radix_sort(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, const uint32_t* n_dev,
                        uint32_t n_fixed, uint32_t grid_bound, int end_bit, uint32_t* status, size_t status_stride,
-                       uint32_t* ghist, uint32_t* counters, cudaStream_t st, bool* res_in_a) {
+                       uint32_t* ghist, uint32_t* counters, cudaStream_t st, bool* res_in_a,
+                       const float* depth = nullptr, const uint32_t* touched = nullptr) {
   const PassPlan plan = make_plan(end_bit);
   const int npass = plan.n;
   *res_in_a = true;
@@ -469,14 +522,18 @@ cudaError_t radix_sort(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, c
   }
   const int hist_grid = min((int)((grid_bound + 255) / 256), num_sms() * 4);
   {
-    KTimer kt_("A4_radix_hist", st);
-    radix_hist_kernel<<<hist_grid, 256, 0, st>>>(ka, n_dev, n_fixed, plan, ghist);
+    KTimer kt_(depth ? "A4_radix_hist_s1" : "A4_radix_hist_s2", st);
+    if (depth)  // stage 1: the keys (and identity ids) are formed by the histogram pass itself
+      radix_hist_kernel<true><<<hist_grid, 256, 0, st>>>(nullptr, n_dev, n_fixed, plan, ghist, depth, touched, ka, va);
+    else
+      radix_hist_kernel<false><<<hist_grid, 256, 0, st>>>(ka, n_dev, n_fixed, plan, ghist, nullptr, nullptr, nullptr,
+                                                          nullptr);
   }
   const uint32_t tiles = (grid_bound + kSortTile - 1) / kSortTile;
   uint32_t *ki = ka, *vi = va, *ko = kb, *vo = vb;
   for (int p = 0; p < npass; ++p) {
     {
-      KTimer kt_("A4_radix_onesweep", st);
+      KTimer kt_(depth ? "A4_radix_onesweep_s1" : "A4_radix_onesweep_s2", st);
       if (plan.width[p] <= 8)
         radix_pass_kernel<8><<<tiles, kSortThreads, pass_smem<8>(), st>>>(
             ki, vi, ko, vo, n_dev, n_fixed, plan.shift[p], plan.width[p], ghist + p * kMaxRadix,
@@ -508,10 +565,11 @@ WsLayout ws_layout(int32_t n, int32_t W, int32_t H, int64_t cap) {
   L.tiles1 = (int)((nn + kSortTile - 1) / kSortTile);
   L.tiles2 = (int)((cc + kSortTile - 1) / kSortTile);
   L.tilesN = (int)((nn + kScanTile - 1) / kScanTile);
-  (void)W; (void)H;
   // counters first: their offset does not depend on n or the capacity, so a render call sees the
   // flags the sort of the same view published in the same workspace
-  L.counters = take(4 * 64);
+  L.counters = take(4 * kCounters);
+  L.a0 = take(4 * (size_t)(((H > 0 ? H : 0) + kTile - 1) / kTile) *
+              (size_t)((((W > 0 ? W : 0) + kTile - 1) / kTile + 31) / 32));
   // the state a sort call zeroes, contiguous after the counters (one memset)
   L.hist = take(4 * 2 * kMaxSortPasses * kMaxRadix);
   L.scan_status = take(8 * (size_t)(L.tilesN > 0 ? L.tilesN : 1));
@@ -523,6 +581,8 @@ WsLayout ws_layout(int32_t n, int32_t W, int32_t H, int64_t cap) {
   L.dup_vals = take(4 * cc);
   L.status2 = take(4 * (size_t)kMaxSortPasses * L.tiles2 * kMaxRadix);
   L.g2d = take(4 * 16 * nn);  // [n][16] f32 (14 used), one 64-byte line per Gaussian
+  const size_t ntiles = (size_t)((W > 0 ? W : 0) + kTile - 1) / kTile * (size_t)(((H > 0 ? H : 0) + kTile - 1) / kTile);
+  L.lpt = take(4 * ntiles);
   L.total = off;
   return L;
 }
@@ -537,14 +597,10 @@ cudaError_t launch_bin_sort_stage1(const pgsag_projected* p, int n, const WsLayo
   uint32_t* i1 = reinterpret_cast<uint32_t*>(ws + L.ids[1]);
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + L.counters);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
-  {
-    KTimer kt_("A4_depth_keys", st);
-    depth_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, p->depth, p->tiles_touched, k0, i0);
-  }
   bool in_a = true;
   cudaError_t e = radix_sort(k0, i0, k1, i1, nullptr, (uint32_t)n, (uint32_t)n, 32,
                              reinterpret_cast<uint32_t*>(ws + L.status1), (size_t)L.tiles1 * kMaxRadix, hist,
-                             counters + CNT_SORT1, st, &in_a);
+                             counters + CNT_SORT1, st, &in_a, p->depth, p->tiles_touched);
   if (e != cudaSuccess) return e;
   const uint32_t* ids = in_a ? i0 : i1;
   *ids_sorted = ids;
@@ -579,10 +635,16 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
   }
   cudaMemsetAsync(bins->ranges, 0, sizeof(uint32_t) * 2 * (size_t)ntiles, st);
   auto order = [&]() {
-    if (!bins->order) return;
-    KTimer kt_("A5_lpt_order", st);
-    lpt_order_kernel<<<1, 1024, 0, st>>>(tm->active, tm->n_active, reinterpret_cast<const uint2*>(bins->ranges),
-                                         bins->order);
+    if (!bins->order || ntiles == 0) return;
+    const int g = (ntiles + 255) / 256;
+    uint32_t* packed = reinterpret_cast<uint32_t*>(ws + L.lpt);
+    {
+      KTimer kt_("A5_lpt_class", st);
+      lpt_class_kernel<<<g, 256, 0, st>>>(tm->active, tm->n_active, reinterpret_cast<const uint2*>(bins->ranges),
+                                          counters + CNT_LPT, packed);
+    }
+    KTimer kt_("A5_lpt_scatter", st);
+    lpt_scatter_kernel<<<g, 256, 0, st>>>(tm->active, tm->n_active, counters + CNT_LPT, packed, bins->order);
   };
   const uint32_t bound = M_known ? M : (uint32_t)bins->capacity;  // grid bound
   if (bound == 0 || n == 0) {
@@ -596,7 +658,7 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
                                                       p->tiles_touched, reinterpret_cast<const short4*>(p->rect),
                                                       tm->active_bits, d, ek, ev, (uint32_t)bins->capacity,
                                                       reinterpret_cast<const unsigned long long*>(counters + CNT_M),
-                                                      m_clamped, counters + CNT_OVF);
+                                                      m_clamped, counters + CNT_OVF, counters + CNT_NG);
   }
   bool in_a = true;
   // look-back state for exactly the tiles the bound needs

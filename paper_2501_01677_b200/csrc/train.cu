@@ -537,6 +537,42 @@ cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8
   return cudaGetLastError();
 }
 
+namespace {
+// R30: the raw parameters of 3DGS's optimiser from the activated ones: log scale, logit opacity
+// (the logit in double: o near 1 loses its low bits in float32's 1 - o).
+__global__ void adam_init_kernel(int n, const float* __restrict__ scale, const float* __restrict__ op,
+                                 float* __restrict__ log_scale, float* __restrict__ logit_op) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) log_scale[(size_t)k * n + i] = logf(scale[(size_t)k * n + i]);
+  const double o = (double)op[i];
+  logit_op[i] = (float)log(o / (1.0 - o));
+}
+
+// Eq. 10-11: L = (1 - lambda) (L_rgb + lambda3 L_s + lambda4 L_ban) + lambda L_GC-load.
+__global__ void loss_total_kernel(const double* rgb, const double* flat, const double* ban, const double* gc,
+                                  double lam, double lam3, double lam4, int ban_mean, double* out) {
+  double Lban = 0.0;
+  if (ban) Lban = ban_mean ? (ban[1] > 0.0 ? ban[0] / ban[1] : 0.0) : ban[0];
+  const double Ls = flat ? flat[0] : 0.0;
+  const double Lgc = gc ? gc[3] : 0.0;
+  out[0] = (1.0 - lam) * (rgb[0] + lam3 * Ls + lam4 * Lban) + lam * Lgc;
+}
+}  // namespace
+
+cudaError_t launch_adam_init(int n, pgsag_adam_state* s, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  adam_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, s->scale, s->opacity, s->log_scale, s->logit_opacity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loss_total(const double* rgb, const double* flat, const double* ban, const double* gc, double lam,
+                              double lam3, double lam4, int ban_mean, double* out, cudaStream_t st) {
+  loss_total_kernel<<<1, 1, 0, st>>>(rgb, flat, ban, gc, lam, lam3, lam4, ban_mean, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_adam(int n, int sh_degree, const pgsag_gaussian_grad* gr, pgsag_adam_state* s,
                         const pgsag_adam_hparams* hp, double* flat, cudaStream_t st) {
   AdamArgs A;

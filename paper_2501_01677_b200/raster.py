@@ -113,7 +113,7 @@ class Rasterizer:
         self.img_g = torch.zeros(self.H, self.W, dtype=i32, device=dev)
         self.img_last = torch.full((self.H, self.W), -1, dtype=i32, device=dev)
         self.counters = torch.zeros(4, dtype=torch.int64, device=dev) if counters else None
-        self.gc_stats = torch.zeros(3, dtype=torch.float64, device=dev)  # NEXT-1: N, sum r, sum r^2
+        self.gc_stats = torch.zeros(5, dtype=torch.float64, device=dev)  # NEXT-1: N, sum r, sum r^2, L, mean r
         self.gc_w = None
         # A8 outputs
         K3 = (self.deg + 1) ** 2 * 3
@@ -203,10 +203,10 @@ class Rasterizer:
         return loss
 
     def gc_load(self):
-        """(L_GC-load, mean ratio, N) from the last forward with gc_w (fused A6 statistics)."""
-        n, s1, s2 = self.gc_stats.tolist()
-        mu = s1 / n if n else 0.0
-        return (max(s2 / n - mu * mu, 0.0) ** 0.5 if n else 0.0), mu, n
+        """(L_GC-load, mean ratio, N) from the last forward with gc_w (A6's fused statistics, Eq. 9
+        evaluated on the device: pgsag_image.gc_stats[3], [4])."""
+        n, _, _, L_, mu = self.gc_stats.tolist()
+        return L_, mu, n
 
     def forward(self, g: GaussianTensors, cam: L.Camera, mask: torch.Tensor, bg=(0.0, 0.0, 0.0), gc_w=None,
                 wait_before_render=None):

@@ -59,9 +59,9 @@ class Trainer:
         self.lam, self.lam3, self.lam4, self.bw = float(lam), float(lam3), float(lam4), float(boundary_w)
         dev, n, H, W = raster.device, g.n, raster.H, raster.W
         K3 = (g.sh_degree + 1) ** 2 * 3
-        # raw parameters (one-time initialisation from the activated values)
-        self.log_scale = torch.log(g.scale).contiguous()
-        self.logit_opacity = torch.logit(g.opacity.double()).float().contiguous()
+        # raw parameters (one-time initialisation from the activated values, pgsag_adam_init)
+        self.log_scale = torch.empty(3, max(n, 1), dtype=torch.float32, device=dev)
+        self.logit_opacity = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.m = torch.zeros(11 + K3, max(n, 1), dtype=torch.float32, device=dev)
         self.v = torch.zeros_like(self.m)
         self.dC = torch.zeros(3, H, W, dtype=torch.float32, device=dev)
@@ -78,6 +78,8 @@ class Trainer:
         st.log_scale, st.logit_opacity = self.log_scale.data_ptr(), self.logit_opacity.data_ptr()
         st.m, st.v = self.m.data_ptr(), self.v.data_ptr()
         self._state = st
+        L.adam_init(n, st, _stream())
+        self.loss_all = torch.zeros(1, dtype=torch.float64, device=dev)  # Eq. 11's total (pgsag_loss_total)
         self.t = 0
         self.used_ban = self.used_gc = False
         self._alloc_stats(n)
@@ -180,13 +182,17 @@ class Trainer:
         """Host read of the last iteration's terms and the Eq. 11 total.  With a sync-free rasterizer
         it also checks the last view's entry capacity: overflowed = True means that view was skipped
         (empty lists, no Adam update, pgsag_render_bwd_adam) and the buffers have grown for a re-run."""
+        p = lambda t: C.c_void_p(t.data_ptr())
+        L.loss_total(p(self.loss_rgb), p(self.loss_flat), p(self.loss_ban) if self.used_ban else None, 1,
+                     p(self.r.gc_stats) if self.used_gc else None, self.lam, self.lam3, self.lam4, p(self.loss_all),
+                     _stream())
         rgb = self.loss_rgb.tolist()
         overflowed = not self.r.check_capacity()
         Ls = float(self.loss_flat.item())
         ban = self.loss_ban.tolist()
         Lban = ban[0] / ban[1] if self.used_ban and ban[1] > 0 else 0.0
-        Lgc = self.r.gc_load()[0] if self.used_gc else 0.0
-        total = (1 - self.lam) * (rgb[0] + self.lam3 * Ls + self.lam4 * Lban) + self.lam * Lgc
+        Lgc = float(self.r.gc_stats[3].item()) if self.used_gc else 0.0
+        total = float(self.loss_all.item())
         return dict(total=total, rgb=rgb[0], l1=rgb[1], ssim=rgb[2], flat=Ls, ban=Lban, gc_load=Lgc,
                     overflowed=overflowed)
 

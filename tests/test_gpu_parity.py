@@ -325,5 +325,6 @@ def test_trainer_skips_overflowed_view():
     assert not lb["overflowed"]
     ta.step(cam, mask, tgt)
     la = ta.losses()
-    assert la["rgb"] == lb["rgb"] and la["flat"] == lb["flat"]  # same render, same L_s
+    # same render, same L_s (a sum of per-block atomics in double: equal up to its last bits)
+    assert la["rgb"] == lb["rgb"] and abs(la["flat"] - lb["flat"]) <= 1e-12 * abs(la["flat"])
     assert not torch.equal(before[0], gb.mean) and not torch.equal(before[4], tb.m)  # the re-run updated

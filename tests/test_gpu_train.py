@@ -438,3 +438,52 @@ def test_fused_adam_matches_separate_step(deg):
         err = np.abs(x - y) / np.maximum(np.abs(y), 1e-3 * sc_)
         assert err.max() <= 1e-4, (k, err.max())
     assert torch.equal(a["count"], b["count"])
+
+
+def test_adam_init_loss_total_and_checks():
+    """Boundary calls: pgsag_adam_init (R30 raw parameters: log scale, logit opacity in double),
+    pgsag_loss_total (Eq. 11, on the device) against the formulas evaluated here in float64,
+    and the debug finiteness check of pgsag_preprocess (PGSAG_ENONFINITE)."""
+    import ctypes as C
+    import torch
+    from paper_2501_01677_b200 import _lib as L
+    from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+    rng = np.random.default_rng(5)
+    n = 1000
+    sc = np.exp(rng.uniform(-4, 1, (3, n))).astype(np.float32)
+    op = rng.uniform(1e-3, 0.9999, n).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    st = L.AdamState()
+    s_, o_ = t(sc), t(op)
+    ls, lo = torch.empty(3, n, device="cuda"), torch.empty(n, device="cuda")
+    st.scale, st.opacity, st.log_scale, st.logit_opacity = s_.data_ptr(), o_.data_ptr(), ls.data_ptr(), lo.data_ptr()
+    L.adam_init(n, st, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(ls.cpu().numpy(), np.log(sc.astype(np.float64)), rtol=0, atol=4e-7)
+    ref = np.log(op.astype(np.float64) / (1 - op.astype(np.float64)))
+    np.testing.assert_allclose(lo.cpu().numpy(), ref, rtol=2e-7, atol=2e-7)
+    # Eq. 11 total
+    d = lambda *v: t(np.array(v, np.float64))
+    rgb, flat, ban, gc, out = d(0.3, 0, 0, 0, 0, 0), d(0.02), d(5.0, 20.0), d(10, 2, 3, 0.7, 0.2), d(0.0)
+    p = lambda x: C.c_void_p(x.data_ptr())
+    L.loss_total(p(rgb), p(flat), p(ban), 1, p(gc), 0.41, 100.0, 0.01, p(out), torch.cuda.current_stream().cuda_stream)
+    lam, lam3, lam4 = float(np.float32(0.41)), 100.0, float(np.float32(0.01))
+    want = (1 - lam) * (0.3 + lam3 * 0.02 + lam4 * 5.0 / 20.0) + lam * 0.7
+    assert abs(float(out.item()) - want) <= 1e-12
+    L.loss_total(p(rgb), None, None, 1, None, 0.41, 100.0, 0.01, p(out), torch.cuda.current_stream().cuda_stream)
+    assert abs(float(out.item()) - (1 - lam) * 0.3) <= 1e-12
+    # debug finiteness check
+    scn = S.config1(n=50)
+    g = GaussianTensors.from_numpy(scn.gaussians)
+    g.mean[1, 7] = float("nan")
+    r = Rasterizer(g.n, 64, 64, g.sh_degree)
+    mask = t(scn.mask)
+    L.set_checks(1)
+    try:
+        with pytest.raises(L.PgsagError) as ei:
+            r.forward(g, camera_from(scn.camera), mask)
+        assert ei.value.code == L.PGSAG_ENONFINITE
+        g.mean[1, 7] = 0.5
+        r.forward(g, camera_from(scn.camera), mask)
+    finally:
+        L.set_checks(0)
