@@ -136,7 +136,7 @@ constexpr size_t pass_smem() {
 }
 
 template <int RB>
-__global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
+__global__ void __launch_bounds__(kSortThreads, 3) radix_pass_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ n_ptr, uint32_t n_fixed, int shift, int nbits,
     const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   for (int k = tid; k < NW * R; k += kSortThreads) s_whist[k] = 0;
+  for (int k = tid; k < R; k += kSortThreads) s_cta_start[k] = 0;  // the CTA's digit counts first
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint32_t base = tile * (uint32_t)kSortTile;
@@ -174,6 +175,20 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
       key[k] = 0xFFFFFFFFu;
       val[k] = 0u;
     }
+  }
+  // the CTA's digit counts (cheap shared atomics), published for the successors' look-back
+  // BEFORE the expensive stable ranking: a CTA's successors then never wait on its ranking
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const uint32_t idx = wbase + (uint32_t)k * 32u + lane;
+    if (idx < n) atomicAdd(&s_cta_start[(key[k] >> shift) & mask], 1u);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int dgt = tid * DPT + j;
+    if (ghist[dgt])  // a digit no key of the whole input has needs no look-back state
+      st_volatile(status + (size_t)tile * R + dgt, (tile == 0 ? kLbPrefix : kLbAgg) | s_cta_start[dgt]);
   }
   const uint32_t lt = lanemask_lt();
   // stable warp-local ranking: item-major, lane-minor == input order
@@ -210,8 +225,6 @@ __global__ void __launch_bounds__(kSortThreads) radix_pass_kernel(
     tsum += total;
     gh[j] = ghist[dgt];
     gsum += gh[j];
-    // a digit no key of the whole input has needs no look-back state (every CTA skips it alike)
-    if (gh[j]) st_volatile(status + (size_t)tile * R + dgt, (tile == 0 ? kLbPrefix : kLbAgg) | total);
   }
 #pragma unroll
   for (int j = 0; j < DPT; ++j) {
