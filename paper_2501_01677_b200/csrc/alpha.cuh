@@ -74,16 +74,19 @@ __device__ __forceinline__ float edge_min(float ca, float cb, float cc, float df
   return a + b + c;
 }
 
+// Only the two edges nearer the centre are evaluated: with the centre mu outside the rectangle the
+// minimiser d* of the convex q lies on a face whose outer side contains mu (else q would decrease
+// from d* towards mu, inside the rectangle), i.e. on the nearer x-edge or the nearer y-edge; an
+// extra edge checked where mu is inside that coordinate's range only adds a valid upper bound.
 __device__ __forceinline__ bool ellipse_meets_rect(float2 mu, float4 co, float k2, float xlo, float xhi, float ylo,
                                                    float yhi) {
   if (mu.x >= xlo && mu.x <= xhi && mu.y >= ylo && mu.y <= yhi) return true;
   const float ca = co.x, cb = co.y, cc = co.z;
-  float e0, e1, e2, e3;
-  const float q0 = edge_min(ca, cb, cc, xlo - mu.x, ylo - mu.y, yhi - mu.y, true, e0);
-  const float q1 = edge_min(ca, cb, cc, xhi - mu.x, ylo - mu.y, yhi - mu.y, true, e1);
-  const float q2 = edge_min(ca, cb, cc, ylo - mu.y, xlo - mu.x, xhi - mu.x, false, e2);
-  const float q3 = edge_min(ca, cb, cc, yhi - mu.y, xlo - mu.x, xhi - mu.x, false, e3);
-  return (q0 - 1e-5f * e0 <= k2) || (q1 - 1e-5f * e1 <= k2) || (q2 - 1e-5f * e2 <= k2) || (q3 - 1e-5f * e3 <= k2);
+  const float ex = (mu.x < xlo ? xlo : xhi) - mu.x, ey = (mu.y < ylo ? ylo : yhi) - mu.y;
+  float e0, e2;
+  const float q0 = edge_min(ca, cb, cc, ex, ylo - mu.y, yhi - mu.y, true, e0);
+  const float q2 = edge_min(ca, cb, cc, ey, xlo - mu.x, xhi - mu.x, false, e2);
+  return (q0 - 1e-5f * e0 <= k2) || (q2 - 1e-5f * e2 <= k2);
 }
 
 // Per staged Gaussian: the scaled conic, a p2 threshold below which alpha < 1/255

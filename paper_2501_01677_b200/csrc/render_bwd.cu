@@ -57,9 +57,7 @@ constexpr float kLn2 = 0.6931471805599453f;
 #ifndef PGSAG_BWD_HSTRIPS
 #define PGSAG_BWD_HSTRIPS 1
 #endif
-#ifndef PGSAG_BWD_PREFETCH
-#define PGSAG_BWD_PREFETCH 0
-#endif
+
 
 struct BwdArgs {
   const float2* mean2d;
@@ -344,29 +342,11 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       // the list is in ascending slot order: drop its tail past the warp's last entry up front
       int t = s_nw[kBW > 1 ? w : 0] - 1;
       while (t >= 0 && (int)lds_u8(lbase + (uint32_t)t) > qtop) --t;  // warp-uniform
-#if PGSAG_BWD_PREFETCH
-      // the next candidate's list slot and first two record quads are loaded one iteration ahead
-      int qn = t >= 0 ? (int)lds_u8(lbase + (uint32_t)t) : 0;
-      float4 ran = lds128(rec_base + (uint32_t)qn * (uint32_t)sizeof(Rec));
-      float4 rbn = lds128(rec_base + (uint32_t)qn * (uint32_t)sizeof(Rec) + 16);
-#endif
       for (; t >= 0; --t) {
-#if PGSAG_BWD_PREFETCH
-        const int q = qn;
-        const float4 ra = ran, rb = rbn;
-        const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
-        if (t > 0) {
-          qn = (int)lds_u8(lbase + (uint32_t)(t - 1));
-          const uint32_t na = rec_base + (uint32_t)qn * (uint32_t)sizeof(Rec);
-          ran = lds128(na);
-          rbn = lds128(na + 16);
-        }
-#else
         const int q = (int)lds_u8(lbase + (uint32_t)t);
         const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
         const float4 ra = lds128(ra_addr);
         const float4 rb = lds128(ra_addr + 16);
-#endif
         PGSAG_DCHECK(q < cnt);
         const int kk = blo + q;
 #if PGSAG_BWD_HSTRIPS
