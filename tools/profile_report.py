@@ -2,9 +2,12 @@
 and profiles/<tag>_ncu.md (key counters of the full captures) from gpurun_out/ files."""
 import collections, csv, io, subprocess, sys
 
-STAGE = {"tilemask_count_kernel": "A0", "tilemask_sat_kernel": "A0", "preprocess_kernel": "A1", "scan_kernel": "A2",
-         "duplicate_kernel": "A3", "depth_keys_kernel": "A4", "radix_hist_kernel": "A4", "radix_pass_kernel": "A4",
-         "ranges_kernel": "A5", "lpt_order_kernel": "A5", "render_fwd_kernel": "A6", "render_bwd_kernel": "A7", "preprocess_bwd_kernel": "A8",
+STAGE = {"tilemask_count_kernel": "A0", "tilemask_prefix_kernel": "A0", "tilemask_list_kernel": "A0",
+         "tilemask_satcol_kernel": "A0", "preprocess_kernel": "A1", "scan_kernel": "A2",
+         "duplicate_kernel": "A3", "radix_hist_kernel": "A4", "radix_pass_kernel": "A4",
+         "ranges_kernel": "A5", "lpt_class_kernel": "A5", "lpt_scatter_kernel": "A5", "render_fwd_kernel": "A6",
+         "gc_finalize_kernel": "N1", "render_bwd_kernel": "A7", "preprocess_bwd_kernel": "A8",
+         "finite_check_kernel": "A1", "adam_init_kernel": "N3", "loss_total_kernel": "N3",
          "sobel_kernel": "N1", "gc_normalize_kernel": "N1", "band_kernel": "N2", "band_tiled_kernel": "N2", "ban_kernel": "N2", "rgb_fwd_kernel": "N3", "rgb_bwd_kernel": "N3", "rgb_finalize_kernel": "N3",
          "adam_kernel": "N3", "unpack_rgb8_kernel": "N3", "densify_classify_kernel": "N3", "densify_scan_kernel": "N3",
          "densify_apply_kernel": "N3", "opacity_reset_kernel": "N3"}
