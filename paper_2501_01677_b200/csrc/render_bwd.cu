@@ -14,7 +14,7 @@
 // recurrence of the oracle); the background term obeys the same
 // recursion, so Sg = G.S + P (bg.gC) is one scalar started at bg.gC.
 //
-// Mapping: per active tile two single-warp CTAs (PGSAG_BWD_WARPS below), the one of half h
+// Mapping: per active tile two single-warp CTAs, the one of half h
 // owning the 8x16 pixel block of columns 8h..8h+7; a lane owns the FOUR pixels (x, y + 4k),
 // k = 0..3, of its column, which share dx and every per-entry load and run as two packed FP32x2
 // pairs.  Batches of 64 entries are staged with the exact block cull of A6 (per 8x8 block of
@@ -37,26 +37,17 @@
 namespace pgsag {
 namespace {
 
-constexpr int kG2 = 14;  // du dv dca dcb dcc dop drgb3 dncam3 ddist absgrad
-// PGSAG_BWD_WARPS = 1 (default): one single-warp CTA per 8x16 half tile (the tile's entries
-// are staged by both halves' CTAs, each culling against its own half): no inter-warp barrier
-// and no shared atomics, at twice the record loads (L2 hits).  = 2: one CTA per tile whose two
-// warps share the staged batch (C4: A7 3.51 vs 3.41 ms; with the L_GC-load upstream 3.95 vs 3.68).
-#ifndef PGSAG_BWD_WARPS
-#define PGSAG_BWD_WARPS 1
-#endif
-constexpr int kBW = PGSAG_BWD_WARPS;
-constexpr int kBT = 32 * kBW;
+// One single-warp CTA per 8x16 half tile: the tile's entries are staged by both halves' CTAs,
+// each culling against its own half, so there is no inter-warp barrier and no shared atomics, at
+// twice the record loads (L2 hits).  (A two-warp CTA per tile sharing the staged batch measured
+// slower in round 1: C4 A7 3.51 vs 3.41 ms.)
+constexpr int kBT = 32;
 constexpr int kBEPT = 2;
 constexpr int kBBatch = kBT * kBEPT;
-constexpr int kBNB = kBW;  // candidate lists per CTA
 #ifndef PGSAG_BWD_MINB
-#define PGSAG_BWD_MINB (20 / kBW)  // resident CTAs per SM the register budget is sized for
+#define PGSAG_BWD_MINB 20  // resident CTAs per SM the register budget is sized for
 #endif
 constexpr float kLn2 = 0.6931471805599453f;
-#ifndef PGSAG_BWD_HSTRIPS
-#define PGSAG_BWD_HSTRIPS 1
-#endif
 
 
 struct BwdArgs {
@@ -198,9 +189,10 @@ struct PairOut {
 };
 
 template <bool kGC>
-// al: the blended alphas (0 where the pixel does not blend the entry); rh: rho; u0 / u1: the pixel
-// blends and its alpha is not clamped (R16: d opacity and d power are zero through the clamp)
-__device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 rh, bool u0, bool u1, const float4& cd,
+// al: the blended alphas (0 where the pixel does not blend the entry, which zeroes its d power and
+// d opacity too); inv_o = 1 / o of the entry; u0 / u1: the pixel's alpha is not clamped (R16: d
+// opacity and d power are zero through the clamp).  d opacity = rho dalpha = (alpha / o) dalpha.
+__device__ __forceinline__ void pair_grad(Pair& p, float2 al, float inv_o, bool u0, bool u1, const float4& cd,
                                           const float4& nn, PairOut& o) {
   const float2 om = __fadd2_rn(bc(1.f), f2(-al.x, -al.y));
   const float2 Ti = __fmul2_rn(p.T, f2(rcp_approx(om.x), rcp_approx(om.y)));
@@ -225,7 +217,7 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float2 rh, bool u0
   o.wt = __fmul2_rn(al, Ti);
   const float2 dalu = f2(u0 ? dal.x : 0.f, u1 ? dal.y : 0.f);
   o.dpow = __fmul2_rn(al, dalu);
-  o.dop = __fmul2_rn(rh, dalu);
+  o.dop = __fmul2_rn(o.dpow, bc(inv_o));
 }
 
 template <bool kCount, bool kGC, bool kAbs>
@@ -236,12 +228,11 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   __shared__ Rec s_rec[kBBatch];
   __shared__ uint32_t s_id[kBBatch];
   __shared__ __align__(16) float s_acc[kBBatch * kAccStride];
-  __shared__ uint8_t s_list[kBNB * kBBatch];
-  __shared__ uint32_t s_wc[kBEPT * (kBT / 32) * kBNB];
-  __shared__ int s_nw[kBNB];
+  __shared__ uint8_t s_list[kBBatch];
+  __shared__ uint32_t s_wc[kBEPT];
+  __shared__ int s_nw[1];
   __shared__ uint32_t s_tile;
-  __shared__ int s_maxlast;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
   const uint32_t rec_base = opaque(smem_u32(s_rec)), list_base = opaque(smem_u32(s_list));
@@ -260,19 +251,18 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   for (int k = tid; k < kBBatch * kAccStride; k += kBT) s_acc[k] = 0.f;
 #ifdef PGSAG_DEBUG_BOUNDS
   // race-freedom of the shared accumulator (single warp: one writer lane per value slot)
-  if (kBW == 1) {
+  {
     const uint32_t wm = __ballot_sync(0xffffffffu, writer);
     if (writer) PGSAG_DCHECK(__match_any_sync(wm, my_c) == (1u << lane) && my_c >= 0 && my_c < 14);
   }
 #endif
   if (tid == 0) s_tile = atomicAdd(a.work, 1u);
   for (;;) {
-    if (tid == 0) s_maxlast = -1;
     __syncthreads();
     const uint32_t widx = s_tile;
-    if (widx >= n_active * (uint32_t)(3 - kBW)) break;
-    const uint32_t titem = kBW == 1 ? widx >> 1 : widx;
-    const int half = kBW == 1 ? (int)(widx & 1u) : w;  // which 8-column half of the tile
+    if (widx >= 2u * n_active) break;
+    const uint32_t titem = widx >> 1;
+    const int half = (int)(widx & 1u);  // which 8-column half of the tile
     const uint32_t tile = a.order ? a.order[titem] : a.active[titem];
     const int ty = tile / a.d.TX, tx = tile - ty * a.d.TX;
     const int i = tx * kTile + half * 8 + (lane & 7);
@@ -296,10 +286,9 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       make_pair(s[2], s[3], P23);
     }
     const int mylast = max(max(P01.last0, P01.last1), max(P23.last0, P23.last1));
-    if (kBW > 1 && mylast >= 0) atomicMax(&s_maxlast, mylast);
     const int wlast = __reduce_max_sync(0xffffffffu, mylast);
     __syncthreads();
-    const int maxlast = kBW > 1 ? s_maxlast : wlast;
+    const int maxlast = wlast;
     // every thread has read s_tile: claim the next tile now (latency hidden behind this one)
     if (tid == 0) s_tile = atomicAdd(a.work, 1u);
     for (int bhi = maxlast + 1; bhi > (int)rs; bhi -= kBBatch) {
@@ -314,33 +303,28 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           const uint32_t id = a.vals[blo + slot];
           PGSAG_DCHECK(id < (uint32_t)a.n);
           Rec& r = s_rec[slot];
-          if (kBW > 1) {
-            mk[e] = stage_gaussian<8, 16>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
-          } else {  // this CTA's half only
+          {  // this CTA's half only
             const float2 xy = a.mean2d[id];
             const float4 co = a.conic_o[id];
             const StageCull c = stage_record(xy, co, r);
             const float xlo = tx0 + (float)(half * 8) + 0.5f, ylo = ty0 + 0.5f;
-#if PGSAG_BWD_HSTRIPS
             // exact cull per 8x8 block of the half (block p = the rows of pixel pair p)
             const uint32_t sm = (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 7.0f) ? 1u : 0u) |
                                 (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo + 8.0f, ylo + 15.0f) ? 2u : 0u);
             mk[e] = sm != 0u ? 1u : 0u;
+            r.b.z = __frcp_rn(co.w);  // d opacity = (alpha / o) d alpha
             r.b.w = __uint_as_float(sm);
-#else
-            mk[e] = block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 15.0f) ? 1u : 0u;
-#endif
           }
           r.cd = a.rgb_d[id];
           r.n = a.ncam[id];
           s_id[slot] = id;
         }
       }
-      build_lists<kBT, kBEPT, kBNB>(mk, s_list, s_wc, s_nw);
+      build_lists<kBT, kBEPT, 1>(mk, s_list, s_wc, s_nw);
       const int qtop = wlast - blo;  // entries past the warp's last are never needed
-      const uint32_t lbase = list_base + (uint32_t)((kBW > 1 ? w : 0) * kBBatch);
+      const uint32_t lbase = list_base;
       // the list is in ascending slot order: drop its tail past the warp's last entry up front
-      int t = s_nw[kBW > 1 ? w : 0] - 1;
+      int t = s_nw[0] - 1;
       while (t >= 0 && (int)lds_u8(lbase + (uint32_t)t) > qtop) --t;  // warp-uniform
       for (; t >= 0; --t) {
         const int q = (int)lds_u8(lbase + (uint32_t)t);
@@ -349,7 +333,6 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float4 rb = lds128(ra_addr + 16);
         PGSAG_DCHECK(q < cnt);
         const int kk = blo + q;
-#if PGSAG_BWD_HSTRIPS
         // per 8x8 block (pixel pair) of the half: skipped when the splat misses it (staging cull)
         // or when none of its pixels blends the entry (a warp-uniform test after the alpha pass)
         const uint32_t smask = __float_as_uint(rb.w);
@@ -378,56 +361,9 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           anyc = true;
           al0 = c0 ? al0 : 0.f;
           al1 = c1 ? al1 : 0.f;
-          const bool u0 = c0 && orh.x <= kAlphaMax, u1 = c1 && orh.y <= kAlphaMax;
-          pair_grad<kGC>(PP, f2(al0, al1), rh, u0, u1, cd, nn, h ? o23 : o01);
+          pair_grad<kGC>(PP, f2(al0, al1), rb.z, orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, h ? o23 : o01);
         }
         if (!anyc) continue;
-#else
-        // p2 for the four pixels (bit-identical to A6's evaluation per element)
-        const float dx = px - ra.x;
-        const float tA = __fmul_rn(ra.z, dx);
-        const float2 dy01 = __fadd2_rn(py01, bc(-ra.y));
-        const float2 dy23 = __fadd2_rn(py23, bc(-ra.y));
-        const float2 p01 = __ffma2_rn(bc(dx), __ffma2_rn(bc(ra.w), dy01, bc(tA)),
-                                      __fmul2_rn(__fmul2_rn(bc(rb.x), dy01), dy01));
-        const float2 p23 = __ffma2_rn(bc(dx), __ffma2_rn(bc(ra.w), dy23, bc(tA)),
-                                      __fmul2_rn(__fmul2_rn(bc(rb.x), dy23), dy23));
-        const float2 rh01 = f2(ex2_approx(p01.x), ex2_approx(p01.y));
-        const float2 rh23 = f2(ex2_approx(p23.x), ex2_approx(p23.y));
-        const float2 or01 = __fmul2_rn(bc(rb.y), rh01);
-        const float2 or23 = __fmul2_rn(bc(rb.y), rh23);
-        float al0 = fminf(kAlphaMax, or01.x), al1 = fminf(kAlphaMax, or01.y);
-        float al2 = fminf(kAlphaMax, or23.x), al3 = fminf(kAlphaMax, or23.y);
-        // exactly A6's blend decision (R6); entries past the pixel's last were not blended
-        const bool c0 = kk <= P01.last0 && p01.x <= 0.0f && al0 >= kAlphaMin;
-        const bool c1 = kk <= P01.last1 && p01.y <= 0.0f && al1 >= kAlphaMin;
-        const bool c2 = kk <= P23.last0 && p23.x <= 0.0f && al2 >= kAlphaMin;
-        const bool c3 = kk <= P23.last1 && p23.y <= 0.0f && al3 >= kAlphaMin;
-        if (kCount)
-          cntV += (unsigned long long)(kk <= P01.last0) + (kk <= P01.last1) + (kk <= P23.last0) + (kk <= P23.last1);
-        if (!__any_sync(0xffffffffu, c0 || c1 || c2 || c3)) continue;
-#ifdef PGSAG_HIST
-        if (kCount) {  // experiment: histogram of contributing lanes / pixels per (warp, candidate)
-          const uint32_t bl = __ballot_sync(0xffffffffu, c0 || c1 || c2 || c3);
-          const int npx = __reduce_add_sync(0xffffffffu, (int)c0 + (int)c1 + (int)c2 + (int)c3);
-          if (lane == 0) {
-            atomicAdd(a.counters + 4 + __popc(bl), 1ull);
-            atomicAdd(a.counters + 40 + min(npx / 4, 32), 1ull);
-          }
-        }
-#endif
-        al0 = c0 ? al0 : 0.f; al1 = c1 ? al1 : 0.f; al2 = c2 ? al2 : 0.f; al3 = c3 ? al3 : 0.f;
-        // rho and alpha as they enter d(opacity) and d(power): zero when clamped at 0.99 (R16)
-        const bool u0 = c0 && or01.x <= kAlphaMax, u1 = c1 && or01.y <= kAlphaMax;
-        const bool u2 = c2 && or23.x <= kAlphaMax, u3 = c3 && or23.y <= kAlphaMax;
-        const float4 cd = lds128(ra_addr + 32);
-        const float4 nn = lds128(ra_addr + 48);
-        PairOut o01, o23;
-        pair_grad<kGC>(P01, f2(al0, al1), rh01, u0, u1,
-                  cd, nn, o01);
-        pair_grad<kGC>(P23, f2(al2, al3), rh23, u2, u3,
-                  cd, nn, o23);
-#endif
         float v[16];  // slot k holds value k (k < 7) or value k - 1 (8 <= k < 15); slots 7, 15 zero
 #pragma unroll
         for (int c = 0; c < 7; ++c)
@@ -468,13 +404,10 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float sum = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 1);
         if (wr && sum != 0.0f) {
           const uint32_t addr = acc_lane + (uint32_t)q * (uint32_t)(kAccStride * 4);
-          if (kBW > 1) {  // the CTA's two warps may add to the same entry
-            asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(addr), "f"(sum) : "memory");
-          } else {  // one warp: (entry, value) has a single writer lane
-            float acc;
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(acc) : "r"(addr));
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(acc + sum) : "memory");
-          }
+          // one warp: (entry, value) has a single writer lane
+          float acc;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(acc) : "r"(addr));
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(acc + sum) : "memory");
         }
       }
       __syncthreads();
@@ -555,7 +488,7 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
   a.gc_w = gc ? fwd->gc_w : nullptr;
   a.gc_stats = fwd->gc_stats;
   a.gc_lambda = dL->gc_lambda;
-  const int grid = min(bwd_grid(), d.TX * d.TY * (3 - kBW));  // work items: tiles (kBW = 2) or half tiles
+  const int grid = min(bwd_grid(), d.TX * d.TY * 2);  // work items: half tiles
   {
     KTimer kt_("A7_render_bwd", st);
     const bool abs_ = out->absgrad2d || out->grad2d;
