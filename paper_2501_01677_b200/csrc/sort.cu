@@ -129,6 +129,52 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
   }
 }
 
+// Stage 2 (the tile keys of A3): a thread counts one contiguous span of the keys, run-length
+// aggregated per pass in registers -- A3 emits each splat's tiles in row-major runs, so the high
+// digit (the tile row) is constant over long runs that would otherwise hit one shared counter with
+// 32-way conflicts (heavy-tailed C5 facades) -- and adds each run with one shared atomic.
+__global__ void __launch_bounds__(256) radix_hist_runs_kernel(const uint32_t* __restrict__ keys,
+                                                               const uint32_t* __restrict__ n_ptr, uint32_t n_fixed,
+                                                               PassPlan plan, uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t sh[kMaxSortPasses][kMaxRadix];
+  const uint32_t n = n_ptr ? min(*n_ptr, n_fixed) : n_fixed;
+  for (int k = threadIdx.x; k < kMaxSortPasses * kMaxRadix; k += blockDim.x) (&sh[0][0])[k] = 0;
+  __syncthreads();
+  const uint32_t nt = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t span = ((n + nt - 1) / nt + 3u) & ~3u;  // multiple of 4: aligned uint4 loads
+  const uint32_t k0 = t * span, k1 = min(n, k0 + span);
+  uint32_t cur[kMaxSortPasses], run[kMaxSortPasses];
+#pragma unroll
+  for (int p = 0; p < kMaxSortPasses; ++p) { cur[p] = 0xFFFFFFFFu; run[p] = 0u; }
+  auto add = [&](uint32_t key) {
+#pragma unroll
+    for (int p = 0; p < kMaxSortPasses; ++p) {
+      if (p >= plan.n) break;
+      const uint32_t dg = (key >> plan.shift[p]) & ((1u << plan.width[p]) - 1u);
+      if (dg != cur[p]) {
+        if (run[p]) atomicAdd(&sh[p][cur[p]], run[p]);
+        cur[p] = dg;
+        run[p] = 0u;
+      }
+      ++run[p];
+    }
+  };
+  uint32_t k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(keys + k);
+    add(v.x); add(v.y); add(v.z); add(v.w);
+  }
+  for (; k < k1; ++k) add(keys[k]);
+#pragma unroll
+  for (int p = 0; p < kMaxSortPasses; ++p)
+    if (p < plan.n && run[p]) atomicAdd(&sh[p][cur[p]], run[p]);
+  __syncthreads();
+  for (int q = threadIdx.x; q < plan.n * kMaxRadix; q += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[q];
+    if (v) atomicAdd(ghist + q, v);
+  }
+}
+
 // ------------------------------------------------------------ onesweep pass
 template <int RB>
 constexpr size_t pass_smem() {
@@ -539,8 +585,7 @@ cudaError_t radix_sort(uint32_t* ka, uint32_t* va, uint32_t* kb, uint32_t* vb, c
     if (depth)  // stage 1: the keys (and identity ids) are formed by the histogram pass itself
       radix_hist_kernel<true><<<hist_grid, 256, 0, st>>>(nullptr, n_dev, n_fixed, plan, ghist, depth, touched, ka, va);
     else
-      radix_hist_kernel<false><<<hist_grid, 256, 0, st>>>(ka, n_dev, n_fixed, plan, ghist, nullptr, nullptr, nullptr,
-                                                          nullptr);
+      radix_hist_runs_kernel<<<hist_grid, 256, 0, st>>>(ka, n_dev, n_fixed, plan, ghist);
   }
   const uint32_t tiles = (grid_bound + kSortTile - 1) / kSortTile;
   uint32_t *ki = ka, *vi = va, *ko = kb, *vo = vb;
