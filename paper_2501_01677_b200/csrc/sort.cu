@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(256) scan_kernel(int n, const uint32_t* __rest
 // Thread per Gaussian in depth order; emits (tile, id) for every active tile of
 // its rect in row-major order starting at offsets[k].
 constexpr int kDupSmall = 16;  // rect tiles a lane emits on its own
+constexpr int kDupStage = 512;  // entries of a warp's output range staged in shared memory
 
 // Warp-cooperative for large splats: a warp takes 32 consecutive Gaussians (depth order) and emits them one
 // after the other, its 32 lanes walking the Gaussian's rect in row-major chunks of 32 tiles and
@@ -424,6 +425,7 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
                                                          uint32_t* __restrict__ m_clamped,
                                                          uint32_t* __restrict__ overflow,
                                                          uint32_t* __restrict__ n_out) {
+  __shared__ uint32_t s_dk[8][kDupStage], s_dv[8][kDupStage];  // per-warp output staging
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if (k == 0) {
@@ -443,9 +445,20 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
       else r = rect[id];
     }
   }
-  // small rects (<= kDupSmall tiles): the lane emits its own entries
+  // small rects (<= kDupSmall tiles): the lane emits its own entries.  The warp's 32 Gaussians are
+  // consecutive in depth order, so their entries form ONE contiguous output range: if it fits the
+  // warp's shared buffer the lanes stage their entries there and the warp writes the range out
+  // coalesced (positions of the cooperative large splats stay untouched), else they write directly.
   const int area0 = (r.z - r.x + 1) * (r.w - r.y + 1);
   const bool big = cnt != 0 && area0 > kDupSmall;
+  const int w = threadIdx.x >> 5;
+  const uint32_t lo = __reduce_min_sync(0xffffffffu, cnt ? o : 0xFFFFFFFFu);
+  const uint32_t hi = __reduce_max_sync(0xffffffffu, cnt ? o + cnt : 0u);
+  const bool staged = hi > lo && hi - lo <= (uint32_t)kDupStage;  // warp-uniform
+  if (staged) {
+    for (uint32_t j = lane; j < hi - lo; j += 32) s_dk[w][j] = 0xFFFFFFFFu;
+    __syncwarp();
+  }
   if (cnt != 0 && !big) {
     uint32_t oo = o;
     for (int ty = r.y; ty <= r.w; ++ty) {
@@ -453,10 +466,25 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
       for (int tx = r.x; tx <= r.z; ++tx) {
         if ((__ldg(row + (tx >> 5)) >> (tx & 31)) & 1u) {
           PGSAG_DCHECK(oo < o + cnt && oo < cap);
-          tkeys[oo] = (uint32_t)(ty * d.TX + tx);
-          tvals[oo] = id;
+          if (staged) {
+            s_dk[w][oo - lo] = (uint32_t)(ty * d.TX + tx);
+            s_dv[w][oo - lo] = id;
+          } else {
+            tkeys[oo] = (uint32_t)(ty * d.TX + tx);
+            tvals[oo] = id;
+          }
           ++oo;
         }
+      }
+    }
+  }
+  if (staged) {
+    __syncwarp();
+    for (uint32_t j = lane; j < hi - lo; j += 32) {
+      const uint32_t key = s_dk[w][j];
+      if (key != 0xFFFFFFFFu) {
+        tkeys[lo + j] = key;
+        tvals[lo + j] = s_dv[w][j];
       }
     }
   }
