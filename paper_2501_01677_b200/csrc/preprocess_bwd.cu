@@ -86,7 +86,8 @@ __device__ __forceinline__ void adam_rows(const AdamFused& F, size_t n, size_t i
 template <int DEG, bool kAdam>
 __device__ __forceinline__ void a8_gaussian(
     int n, int i, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
-    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const float4* __restrict__ g2d, const CamB& cam,
+    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const float4* __restrict__ g2d,
+    const float4* __restrict__ conic_o, const CamB& cam,
     float* __restrict__ dmean, float* __restrict__ dscale, float* __restrict__ drot, float* __restrict__ dopac,
     float* __restrict__ dsh, float* __restrict__ absgrad, float* __restrict__ grad2d,
     const uint32_t* __restrict__ tiles_touched, float* __restrict__ daccum, float* __restrict__ dcount, double hw,
@@ -98,6 +99,7 @@ __device__ __forceinline__ void a8_gaussian(
   float4 g2v[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) g2v[c] = g2d[(size_t)i * 4 + c];
+  const float4 co = conic_o[i];
   const float mf[3] = {mean[i], mean[n + i], mean[2 * n + i]};
   const float rf[4] = {rot[i], rot[n + i], rot[2 * n + i], rot[3 * n + i]};
   const float sf[3] = {scale[i], scale[n + i], scale[2 * n + i]};
@@ -124,6 +126,18 @@ __device__ __forceinline__ void a8_gaussian(
   for (int c = 0; c < 4; ++c) {
     const float4 q = g2v[c];
     gg[4 * c] = q.x; gg[4 * c + 1] = q.y; gg[4 * c + 2] = q.z; gg[4 * c + 3] = q.w;
+  }
+  {  // A7's moments of dpow = alpha dalpha -> the screen-space gradients, with the conic (ca, cb, cc) and
+     // o the forward blended with (A1's float values): alpha = o 2^p, p = -log2(e)/2 (ca dx^2 + 2 cb dx dy
+     // + cc dy^2), dx = px - u: du = ca S1 + cb Sy, dv = cb S1 + cc Sy, dca = -S2 / 2, dcb = -Sxy,
+     // dcc = -Syy / 2, do = S0 / o
+    const double S1 = gg[0], Sy = gg[1], S2 = gg[2], Sxy = gg[3], Syy = gg[4], S0 = gg[5];
+    gg[0] = (double)co.x * S1 + (double)co.y * Sy;
+    gg[1] = (double)co.y * S1 + (double)co.z * Sy;
+    gg[2] = -0.5 * S2;
+    gg[3] = -Sxy;
+    gg[4] = -0.5 * Syy;
+    gg[5] = S0 / (double)co.w;
   }
   if (grad2d) {
 #pragma unroll
@@ -329,7 +343,8 @@ __device__ __forceinline__ void a8_gaussian(
 template <int DEG, bool kAdam>
 __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
     int n, const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ rot,
-    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const float4* __restrict__ g2d, CamB cam,
+    const float* __restrict__ sh, const uint32_t* __restrict__ flags, const float4* __restrict__ g2d,
+    const float4* __restrict__ conic_o, CamB cam,
     float* __restrict__ dmean, float* __restrict__ dscale, float* __restrict__ drot, float* __restrict__ dopac,
     float* __restrict__ dsh, float* __restrict__ absgrad, float* __restrict__ grad2d,
     const uint32_t* __restrict__ tiles_touched, float* __restrict__ daccum, float* __restrict__ dcount, double hw,
@@ -353,7 +368,7 @@ __global__ void __launch_bounds__(128, PGSAG_A8_MINB) preprocess_bwd_kernel(
     if (threadIdx.x == 0 && F.flat)
       atomicAdd(F.flat, ((double)s_flat[0] + s_flat[1] + s_flat[2] + s_flat[3]) / (double)n);
   }
-  a8_gaussian<DEG, kAdam>(n, i, mean, scale, rot, sh, flags, g2d, cam, dmean, dscale, drot, dopac, dsh, absgrad,
+  a8_gaussian<DEG, kAdam>(n, i, mean, scale, rot, sh, flags, g2d, conic_o, cam, dmean, dscale, drot, dopac, dsh, absgrad,
                           grad2d, tiles_touched, daccum, dcount, hw, hh, s_g + threadIdx.x);
   // each thread reads back only its own column: no barrier
   if (kAdam && i < n) adam_rows<K3>(F, n, i, s_g + threadIdx.x, gflat);
@@ -390,7 +405,8 @@ cudaError_t launch_preprocess_bwd(const pgsag_gaussians* g, const pgsag_camera* 
     const float4* g2d4 = reinterpret_cast<const float4*>(g2d);
 #define PGSAG_A8(DEG, AD)                                                                                    \
   preprocess_bwd_kernel<DEG, AD><<<blocks, 128, 0, st>>>(                                                  \
-      n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d4, cb, out->dmean, out->dscale, out->drot,         \
+      n, g->mean, g->scale, g->rot, g->sh, p->flags, g2d4, reinterpret_cast<const float4*>(p->conic_o), cb,   \
+      out->dmean, out->dscale, out->drot,         \
       out->dopacity, out->dsh, out->absgrad2d, out->grad2d, p->tiles_touched, out->densify_accum,          \
       out->densify_count, 0.5 * cam->width, 0.5 * cam->height, F)
     const int deg = g->sh_degree < 0 ? 0 : (g->sh_degree > 3 ? 3 : g->sh_degree);

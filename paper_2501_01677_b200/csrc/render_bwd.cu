@@ -23,11 +23,13 @@
 // is skipped by a warp-uniform branch.  A pixel that
 // does not contribute to an entry carries alpha = rho = 0, which zeroes all of its
 // terms and leaves its state unchanged without branches.  Reduction: per entry the
-// lane sums its four pixels, the warp reduce-scatters the 14 partials (5 butterfly
-// levels, 16 shuffles) so that 14 lanes each hold one warp sum, those lanes add
-// into a padded shared accumulator of the batch, and after the batch the CTA
-// flushes each entry's nonzero groups of four with one vector reduction (red.add.v4.f32)
-// into the Gaussian's 64-byte line of the [n][16] accumulator.
+// lane sums its four pixels into 13 raw sums (the seven feature gradients sum alpha T G_c and the
+// moments sum dpow {1, dx, dx^2, dy, dx dy, dy^2} of dpow = alpha dalpha; A8 turns the moments
+// into the mean, conic and opacity gradients with the entry's conic and o), the warp transposes
+// them through a 13 x 32 shared buffer and sums each row (lane r and r + 16 add half a row each,
+// one shuffle joins the halves), and lane r stores row r's total in the batch accumulator.  After
+// the batch the CTA flushes each entry's nonzero groups of four with one vector reduction
+// (red.add.v4.f32) into the Gaussian's 64-byte line of the [n][16] accumulator.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -79,6 +81,11 @@ struct BwdArgs {
 
 constexpr float kGcK = 100.0f;  // soft-count sharpness (R24)
 
+#ifdef PGSAG_A7_STATS
+// diagnostic build only: per entry-warp work statistics of the candidate loop
+__device__ unsigned long long g_a7_stats[32];
+#endif
+
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float hsum(float2 a) { return a.x + a.y; }
@@ -99,17 +106,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-
-// one butterfly level: keep half of the values, exchange the other half with lane ^ m
-template <int H>
-__device__ __forceinline__ void rs_level(float (&v)[2 * H], float (&o)[H], bool upper, int m) {
-#pragma unroll
-  for (int k = 0; k < H; ++k) {
-    const float send = upper ? v[k] : v[k + H];
-    const float keep = upper ? v[k + H] : v[k];
-    o[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-  }
 }
 
 // Per-pixel prologue: upstream G (Eq. 4 folded in), P*(bg.gC), last index, T.
@@ -183,17 +179,17 @@ __device__ __forceinline__ void make_pair(const PixState& a, const PixState& b, 
   p.last1 = b.last;
 }
 
-// Per-entry per-pair screen-space partials (summed over the pair's two pixels into v).
+// Per-entry per-pair partials: alpha T and dpow = alpha dalpha of the pair's two pixels.
 struct PairOut {
-  float2 wt, dpow, dop, du, dv, dydp;
+  float2 wt, dpow;
 };
 
 template <bool kGC>
-// al: the blended alphas (0 where the pixel does not blend the entry, which zeroes its d power and
-// d opacity too); inv_o = 1 / o of the entry; u0 / u1: the pixel's alpha is not clamped (R16: d
-// opacity and d power are zero through the clamp).  d opacity = rho dalpha = (alpha / o) dalpha.
-__device__ __forceinline__ void pair_grad(Pair& p, float2 al, float inv_o, bool u0, bool u1, const float4& cd,
-                                          const float4& nn, PairOut& o) {
+// al: the blended alphas (0 where the pixel does not blend the entry, which zeroes its d power
+// too); u0 / u1: the pixel's alpha is not clamped (R16: d opacity and d power are zero through the
+// clamp).  d opacity = rho dalpha = (alpha / o) dalpha is formed by A8 from sum dpow.
+__device__ __forceinline__ void pair_grad(Pair& p, float2 al, bool u0, bool u1, const float4& cd, const float4& nn,
+                                          PairOut& o) {
   const float2 om = __fadd2_rn(bc(1.f), f2(-al.x, -al.y));
   const float2 Ti = __fmul2_rn(p.T, f2(rcp_approx(om.x), rcp_approx(om.y)));
   float2 GF = p.G[7];
@@ -217,17 +213,17 @@ __device__ __forceinline__ void pair_grad(Pair& p, float2 al, float inv_o, bool 
   o.wt = __fmul2_rn(al, Ti);
   const float2 dalu = f2(u0 ? dal.x : 0.f, u1 ? dal.y : 0.f);
   o.dpow = __fmul2_rn(al, dalu);
-  o.dop = __fmul2_rn(o.dpow, bc(inv_o));
 }
 
 template <bool kCount, bool kGC, bool kAbs>
 __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs a) {
-  // padded row of 16 values: the 14 values of an entry sit in 14 distinct banks, and the
-  // flush's 128-bit loads of 8 consecutive entries start in 8 distinct 4-bank groups
-  constexpr int kAccStride = 20;
+  constexpr int kNV = kAbs ? 14 : 13;  // raw sums per entry (g2d slots 0..kNV-1)
+  constexpr int kAccStride = 16;       // one 64-byte row per entry: the flush's line
+  constexpr int kRedStride = 36;       // transpose rows 4 banks apart: a lane's 128-bit loads of rows 0..7 do not collide
   __shared__ Rec s_rec[kBBatch];
   __shared__ uint32_t s_id[kBBatch];
   __shared__ __align__(16) float s_acc[kBBatch * kAccStride];
+  __shared__ __align__(16) float s_red[14 * kRedStride];
   __shared__ uint8_t s_list[kBBatch];
   __shared__ uint32_t s_wc[kBEPT];
   __shared__ int s_nw[1];
@@ -237,25 +233,14 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   const size_t HW = (size_t)a.d.W * a.d.H;
   const uint32_t rec_base = opaque(smem_u32(s_rec)), list_base = opaque(smem_u32(s_list));
   unsigned long long cntV = 0;
-  // value index this lane owns after the reduce-scatter: bit-reversed lane bits 1..4
-  // slot this lane owns after the reduce-scatter: bit-reversed lane bits 1..4.  Values 0..6 sit
-  // in slots 0..6 and values 7..13 in slots 8..14; slots 7 and 15 stay zero, so the first
-  // butterfly level has one all-zero pair the compiler drops.
-  const int my_s = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) | ((lane >> 1) & 1);
-  const int my_c = my_s < 7 ? my_s : my_s - 1;  // value index of the slot
-  const bool writer = ((lane & 1) == 0) && my_s != 7 && my_s != 15;
-  // loop-invariant lane values pinned in registers (otherwise re-derived from S2R per candidate)
-  const uint32_t lbits = opaque((uint32_t)lane);
-  const uint32_t acc_lane = opaque(smem_u32(s_acc) + (uint32_t)my_c * 4u);
-  const uint32_t wr = opaque((uint32_t)writer);
+  // transpose: lane l writes column l of every row; lane l then sums half (l >> 4) of row l & 15
+  // (rows past kNV-1 read row 0 and are discarded) and, for l < kNV, stores the row's total
+  const uint32_t red_w = opaque(smem_u32(s_red) + 4u * (uint32_t)lane);
+  const int my_row = (lane & 15) < kNV ? (lane & 15) : 0;
+  const uint32_t red_r = opaque(smem_u32(s_red) + 4u * (uint32_t)(my_row * kRedStride + 16 * (lane >> 4)));
+  const uint32_t acc_lane = opaque(smem_u32(s_acc) + 4u * (uint32_t)lane);
+  const uint32_t wr = opaque((uint32_t)(lane < kNV));
   for (int k = tid; k < kBBatch * kAccStride; k += kBT) s_acc[k] = 0.f;
-#ifdef PGSAG_DEBUG_BOUNDS
-  // race-freedom of the shared accumulator (single warp: one writer lane per value slot)
-  {
-    const uint32_t wm = __ballot_sync(0xffffffffu, writer);
-    if (writer) PGSAG_DCHECK(__match_any_sync(wm, my_c) == (1u << lane) && my_c >= 0 && my_c < 14);
-  }
-#endif
   if (tid == 0) s_tile = atomicAdd(a.work, 1u);
   for (;;) {
     __syncthreads();
@@ -312,7 +297,6 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
             const uint32_t sm = (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 7.0f) ? 1u : 0u) |
                                 (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo + 8.0f, ylo + 15.0f) ? 2u : 0u);
             mk[e] = sm != 0u ? 1u : 0u;
-            r.b.z = __frcp_rn(co.w);  // d opacity = (alpha / o) d alpha
             r.b.w = __uint_as_float(sm);
           }
           r.cd = a.rgb_d[id];
@@ -343,8 +327,13 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float4 cd = lds128(ra_addr + 32);
         const float4 nn = lds128(ra_addr + 48);
         PairOut o01, o23;
-        o01.wt = o01.dpow = o01.dop = o23.wt = o23.dpow = o23.dop = f2(0.f, 0.f);
+        o01.wt = o01.dpow = o23.wt = o23.dpow = f2(0.f, 0.f);
         bool anyc = false;
+#ifdef PGSAG_A7_STATS
+        st[0]++;
+        uint32_t stc = 0u;
+        const uint32_t stb0 = st[4];
+#endif
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (!((smask >> h) & 1u)) continue;
@@ -357,57 +346,66 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           const bool c0 = kk <= PP.last0 && p2.x <= 0.0f && al0 >= kAlphaMin;
           const bool c1 = kk <= PP.last1 && p2.y <= 0.0f && al1 >= kAlphaMin;
           if (kCount) cntV += (unsigned long long)(kk <= PP.last0) + (kk <= PP.last1);
+#ifdef PGSAG_A7_STATS
+          st[2]++;
+#endif
           if (!__any_sync(0xffffffffu, c0 || c1)) continue;
+#ifdef PGSAG_A7_STATS
+          st[3]++;
+          st[4] += __popc(__ballot_sync(0xffffffffu, c0)) + __popc(__ballot_sync(0xffffffffu, c1));
+          stc |= __ballot_sync(0xffffffffu, c0 || c1);
+#endif
           anyc = true;
           al0 = c0 ? al0 : 0.f;
           al1 = c1 ? al1 : 0.f;
-          pair_grad<kGC>(PP, f2(al0, al1), rb.z, orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, h ? o23 : o01);
+          pair_grad<kGC>(PP, f2(al0, al1), orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, h ? o23 : o01);
         }
         if (!anyc) continue;
-        float v[16];  // slot k holds value k (k < 7) or value k - 1 (8 <= k < 15); slots 7, 15 zero
+#ifdef PGSAG_A7_STATS
+        {
+          st[1]++;
+          const int nl = __popc(stc), nb = (int)(st[4] - stb0);
+          st[8 + (nl <= 1 ? 0 : nl <= 2 ? 1 : nl <= 4 ? 2 : nl <= 8 ? 3 : nl <= 16 ? 4 : 5)]++;
+          st[16 + (nb <= 2 ? 0 : nb <= 4 ? 1 : nb <= 8 ? 2 : nb <= 16 ? 3 : nb <= 32 ? 4 : nb <= 64 ? 5 : 6)]++;
+        }
+#endif
+        // the lane's raw sums (g2d slots): 0 S1 = sum dx dpow, 1 Sy = sum dy dpow, 2 S2 = sum dx^2 dpow,
+        // 3 Sxy, 4 Syy, 5 S0 = sum dpow, 6..12 sum alpha T G_c, 13 (kAbs) sum |du| + |dv| per pixel;
+        // dx is the lane's column offset, common to its four pixels
+        float v[kNV];
 #pragma unroll
-        for (int c = 0; c < 7; ++c)
-          v[c == 0 ? 6 : 7 + c] = hsum(__ffma2_rn(o23.wt, P23.G[c], __fmul2_rn(o01.wt, P01.G[c])));
-        v[5] = hsum(__fadd2_rn(o01.dop, o23.dop));
-        const float sdp = hsum(__fadd2_rn(o01.dpow, o23.dpow));
+        for (int c = 0; c < 7; ++c) v[6 + c] = hsum(__ffma2_rn(o23.wt, P23.G[c], __fmul2_rn(o01.wt, P01.G[c])));
         const float2 dydp01 = __fmul2_rn(dy01, o01.dpow), dydp23 = __fmul2_rn(dy23, o23.dpow);
-        const float sdydp = hsum(__fadd2_rn(dydp01, dydp23));
-        const float sdy2dp = hsum(__ffma2_rn(dy23, dydp23, __fmul2_rn(dy01, dydp01)));
-        v[2] = (-0.5f * dx) * dx * sdp;
-        v[3] = -dx * sdydp;
-        v[4] = -0.5f * sdy2dp;
-        // per-pixel screen-space mean gradient: (ca, cb, cc) = -ln2 (2A', B', 2C')
-        const float twoA = 2.0f * tA, bdx = ra.w * dx, twoC = 2.0f * rb.x;
-        if (kAbs) {  // per-pixel du, dv: needed for the absgrad statistic sum |du| + |dv|
+        v[5] = hsum(__fadd2_rn(o01.dpow, o23.dpow));
+        v[1] = hsum(__fadd2_rn(dydp01, dydp23));
+        v[4] = hsum(__ffma2_rn(dy23, dydp23, __fmul2_rn(dy01, dydp01)));
+        v[0] = dx * v[5];
+        v[2] = dx * v[0];
+        v[3] = dx * v[1];
+        if (kAbs) {  // per-pixel du = -ln2 (B' dy + 2 A' dx) dpow, dv = -ln2 (2 C' dy + B' dx) dpow
+          const float twoA = 2.0f * tA, bdx = ra.w * dx, twoC = 2.0f * rb.x;
           const float2 kd01 = __fmul2_rn(bc(-kLn2), o01.dpow), kd23 = __fmul2_rn(bc(-kLn2), o23.dpow);
           const float2 du01 = __fmul2_rn(__ffma2_rn(bc(ra.w), dy01, bc(twoA)), kd01);
           const float2 du23 = __fmul2_rn(__ffma2_rn(bc(ra.w), dy23, bc(twoA)), kd23);
           const float2 dv01 = __fmul2_rn(__ffma2_rn(bc(twoC), dy01, bc(bdx)), kd01);
           const float2 dv23 = __fmul2_rn(__ffma2_rn(bc(twoC), dy23, bc(bdx)), kd23);
-          v[0] = hsum(__fadd2_rn(du01, du23));
-          v[1] = hsum(__fadd2_rn(dv01, dv23));
-          v[14] = ((fabsf(du01.x) + fabsf(dv01.x)) + (fabsf(du01.y) + fabsf(dv01.y))) +
-                  ((fabsf(du23.x) + fabsf(dv23.x)) + (fabsf(du23.y) + fabsf(dv23.y)));
-        } else {  // sums only: du = -ln2 (B' dy + 2 A' dx) dpow, dv = -ln2 (2 C' dy + B' dx) dpow per pixel
-          v[0] = -kLn2 * fmaf(ra.w, sdydp, twoA * sdp);
-          v[1] = -kLn2 * fmaf(twoC, sdydp, bdx * sdp);
-          v[14] = 0.f;
+          v[kNV - 1] = ((fabsf(du01.x) + fabsf(dv01.x)) + (fabsf(du01.y) + fabsf(dv01.y))) +
+                       ((fabsf(du23.x) + fabsf(dv23.x)) + (fabsf(du23.y) + fabsf(dv23.y)));
         }
-        v[7] = 0.f;
-        v[15] = 0.f;
-        // reduce-scatter 16 -> 1 value per lane pair
-        float v8[8], v4[4], v2[2], v1[1];
-        rs_level<8>(v, v8, (lbits & 16u) != 0u, 16);
-        rs_level<4>(v8, v4, (lbits & 8u) != 0u, 8);
-        rs_level<2>(v4, v2, (lbits & 4u) != 0u, 4);
-        rs_level<1>(v2, v1, (lbits & 2u) != 0u, 2);
-        const float sum = v1[0] + __shfl_xor_sync(0xffffffffu, v1[0], 1);
-        if (wr && sum != 0.0f) {
+        // warp sums by a transpose through shared memory (single warp: __syncwarp orders it)
+        __syncwarp();  // the previous entry's row reads are done
+#pragma unroll
+        for (int r = 0; r < kNV; ++r)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(red_w + (uint32_t)(4 * r * kRedStride)), "f"(v[r]) : "memory");
+        __syncwarp();
+        const float4 h0 = lds128(red_r), h1 = lds128(red_r + 16), h2 = lds128(red_r + 32), h3 = lds128(red_r + 48);
+        const float2 t0 = __fadd2_rn(__fadd2_rn(f2(h0.x, h0.y), f2(h1.x, h1.y)), __fadd2_rn(f2(h0.z, h0.w), f2(h1.z, h1.w)));
+        const float2 t1 = __fadd2_rn(__fadd2_rn(f2(h2.x, h2.y), f2(h3.x, h3.y)), __fadd2_rn(f2(h2.z, h2.w), f2(h3.z, h3.w)));
+        float sum = hsum(__fadd2_rn(t0, t1));
+        sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+        if (wr) {  // one warp: (entry, row) has a single writer lane
           const uint32_t addr = acc_lane + (uint32_t)q * (uint32_t)(kAccStride * 4);
-          // one warp: (entry, value) has a single writer lane
-          float acc;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(acc) : "r"(addr));
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(acc + sum) : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(sum) : "memory");
         }
       }
       __syncthreads();
@@ -433,6 +431,11 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       __syncthreads();
     }
   }
+#ifdef PGSAG_A7_STATS
+  if (lane == 0)
+    for (int k = 0; k < 32; ++k)
+      if (st[k]) atomicAdd(&g_a7_stats[k], st[k]);
+#endif
   if (kCount) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cntV += __shfl_xor_sync(0xffffffffu, cntV, o);
@@ -511,3 +514,15 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
 }
 
 }  // namespace pgsag
+
+#ifdef PGSAG_A7_STATS
+extern "C" int pgsag_debug_a7_stats(unsigned long long* host, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host, pgsag::g_a7_stats, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(pgsag::g_a7_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
