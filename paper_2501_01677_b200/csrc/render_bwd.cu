@@ -310,8 +310,15 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       // the list is in ascending slot order: drop its tail past the warp's last entry up front
       int t = s_nw[0] - 1;
       while (t >= 0 && (int)lds_u8(lbase + (uint32_t)t) > qtop) --t;  // warp-uniform
+      // software pipeline over the candidates: the shuffle joining an entry's half-row sums is issued
+      // at the top of the next candidate and its total stored after that candidate's alpha pass, and
+      // the next list byte is loaded a candidate ahead
+      int pq = -1;  // entry whose transposed rows await their sums (warp-uniform)
+      float hs = 0.f;  // this lane's half-row sum of entry pq
+      uint32_t qn = t >= 0 ? lds_u8(lbase + (uint32_t)t) : 0u;
       for (; t >= 0; --t) {
-        const int q = (int)lds_u8(lbase + (uint32_t)t);
+        const int q = (int)qn;
+        if (t > 0) qn = lds_u8(lbase + (uint32_t)(t - 1));
         const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
         const float4 ra = lds128(ra_addr);
         const float4 rb = lds128(ra_addr + 16);
@@ -326,6 +333,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float2 dy23 = __fadd2_rn(py23, bc(-ra.y));
         const float4 cd = lds128(ra_addr + 32);
         const float4 nn = lds128(ra_addr + 48);
+        const float ho = pq >= 0 ? __shfl_xor_sync(0xffffffffu, hs, 16) : 0.f;
         PairOut o01, o23;
         o01.wt = o01.dpow = o23.wt = o23.dpow = f2(0.f, 0.f);
         bool anyc = false;
@@ -359,6 +367,13 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           al0 = c0 ? al0 : 0.f;
           al1 = c1 ? al1 : 0.f;
           pair_grad<kGC>(PP, f2(al0, al1), orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, h ? o23 : o01);
+        }
+        if (pq >= 0) {  // one warp: (entry, row) has a single writer lane
+          if (wr) {
+            const uint32_t addr = acc_lane + (uint32_t)pq * (uint32_t)(kAccStride * 4);
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(hs + ho) : "memory");
+          }
+          pq = -1;
         }
         if (!anyc) continue;
 #ifdef PGSAG_A7_STATS
@@ -397,14 +412,18 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
 #pragma unroll
         for (int r = 0; r < kNV; ++r)
           asm volatile("st.shared.f32 [%0], %1;" ::"r"(red_w + (uint32_t)(4 * r * kRedStride)), "f"(v[r]) : "memory");
+        pq = q;
         __syncwarp();
         const float4 h0 = lds128(red_r), h1 = lds128(red_r + 16), h2 = lds128(red_r + 32), h3 = lds128(red_r + 48);
         const float2 t0 = __fadd2_rn(__fadd2_rn(f2(h0.x, h0.y), f2(h1.x, h1.y)), __fadd2_rn(f2(h0.z, h0.w), f2(h1.z, h1.w)));
         const float2 t1 = __fadd2_rn(__fadd2_rn(f2(h2.x, h2.y), f2(h3.x, h3.y)), __fadd2_rn(f2(h2.z, h2.w), f2(h3.z, h3.w)));
-        float sum = hsum(__fadd2_rn(t0, t1));
+        hs = hsum(__fadd2_rn(t0, t1));
+      }
+      if (pq >= 0) {  // the batch's last transposed entry
+        float sum = hs;
         sum += __shfl_xor_sync(0xffffffffu, sum, 16);
-        if (wr) {  // one warp: (entry, row) has a single writer lane
-          const uint32_t addr = acc_lane + (uint32_t)q * (uint32_t)(kAccStride * 4);
+        if (wr) {
+          const uint32_t addr = acc_lane + (uint32_t)pq * (uint32_t)(kAccStride * 4);
           asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(sum) : "memory");
         }
       }
