@@ -220,7 +220,9 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   constexpr int kNV = kAbs ? 14 : 13;  // raw sums per entry (g2d slots 0..kNV-1)
   constexpr int kAccStride = 16;       // one 64-byte row per entry: the flush's line
   constexpr int kRedStride = 36;       // transpose rows 4 banks apart: a lane's 128-bit loads of rows 0..7 do not collide
-  __shared__ Rec s_rec[kBBatch];
+  // staged records as four float4 planes (SoA): the staging stores of consecutive slots are consecutive
+  // 16-byte words (conflict-free), the candidate loop's broadcast loads take one address + offsets
+  __shared__ float4 s_rec[4 * kBBatch];
   __shared__ uint32_t s_id[kBBatch];
   __shared__ __align__(16) float s_acc[kBBatch * kAccStride];
   __shared__ __align__(16) float s_red[14 * kRedStride];
@@ -234,9 +236,10 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   const uint32_t rec_base = opaque(smem_u32(s_rec)), list_base = opaque(smem_u32(s_list));
   unsigned long long cntV = 0;
   // transpose: lane l writes column l of every row; lane l then sums half (l >> 4) of row l & 15
-  // (rows past kNV-1 read row 0 and are discarded) and, for l < kNV, stores the row's total
+  // and, for l < kNV, stores the row's total
   const uint32_t red_w = opaque(smem_u32(s_red) + 4u * (uint32_t)lane);
-  const int my_row = (lane & 15) < kNV ? (lane & 15) : 0;
+  // (lanes past the last row re-read row kNV-1 with its lane: same address, no extra bank wavefront)
+  const int my_row = (lane & 15) < kNV ? (lane & 15) : kNV - 1;
   const uint32_t red_r = opaque(smem_u32(s_red) + 4u * (uint32_t)(my_row * kRedStride + 16 * (lane >> 4)));
   const uint32_t acc_lane = opaque(smem_u32(s_acc) + 4u * (uint32_t)lane);
   const uint32_t wr = opaque((uint32_t)(lane < kNV));
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         if (slot < cnt) {
           const uint32_t id = a.vals[blo + slot];
           PGSAG_DCHECK(id < (uint32_t)a.n);
-          Rec& r = s_rec[slot];
+          Rec r;
           {  // this CTA's half only
             const float2 xy = a.mean2d[id];
             const float4 co = a.conic_o[id];
@@ -301,6 +304,10 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           }
           r.cd = a.rgb_d[id];
           r.n = a.ncam[id];
+          s_rec[slot] = r.a;
+          s_rec[kBBatch + slot] = r.b;
+          s_rec[2 * kBBatch + slot] = r.cd;
+          s_rec[3 * kBBatch + slot] = r.n;
           s_id[slot] = id;
         }
       }
@@ -319,9 +326,9 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       for (; t >= 0; --t) {
         const int q = (int)qn;
         if (t > 0) qn = lds_u8(lbase + (uint32_t)(t - 1));
-        const uint32_t ra_addr = rec_base + (uint32_t)q * (uint32_t)sizeof(Rec);
+        const uint32_t ra_addr = rec_base + (uint32_t)q * 16u;
         const float4 ra = lds128(ra_addr);
-        const float4 rb = lds128(ra_addr + 16);
+        const float4 rb = lds128(ra_addr + 16 * kBBatch);
         PGSAG_DCHECK(q < cnt);
         const int kk = blo + q;
         // per 8x8 block (pixel pair) of the half: skipped when the splat misses it (staging cull)
@@ -331,8 +338,8 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float tA = __fmul_rn(ra.z, dx);
         const float2 dy01 = __fadd2_rn(py01, bc(-ra.y));
         const float2 dy23 = __fadd2_rn(py23, bc(-ra.y));
-        const float4 cd = lds128(ra_addr + 32);
-        const float4 nn = lds128(ra_addr + 48);
+        const float4 cd = lds128(ra_addr + 32 * kBBatch);
+        const float4 nn = lds128(ra_addr + 48 * kBBatch);
         const float ho = pq >= 0 ? __shfl_xor_sync(0xffffffffu, hs, 16) : 0.f;
         PairOut o01, o23;
         o01.wt = o01.dpow = o23.wt = o23.dpow = f2(0.f, 0.f);

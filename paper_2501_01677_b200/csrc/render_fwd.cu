@@ -10,7 +10,7 @@
 // pixels (x, y) and (x, y + 4) of its column, which share dx and every per-entry
 // load; their arithmetic runs as packed FP32x2 (FFMA2/FMUL2/FADD2, one issue slot
 // for both pixels).  Masked-out pixels start "done".  Each batch of 256 sorted
-// entries is staged in shared memory (64-byte records) together with a 4-bit
+// entries is staged in shared memory (64-byte records, as four 16-byte planes) together with a 4-bit
 // warp-block mask (exact conservative cull, alpha.cuh), from which every warp gets
 // a compacted depth-ordered candidate list.  Blending is branch-free (predicated
 // weights); the tile stops when every pixel is done.
@@ -92,7 +92,7 @@ template <bool kCount, int NP>
 __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
   using Cfg = FwdCfg<NP>;
   constexpr int NT = Cfg::NT, EPT = Cfg::EPT, NB = Cfg::NB, BATCH = Cfg::BATCH;
-  __shared__ Rec s_rec[BATCH];
+  __shared__ float4 s_rec[4 * BATCH];  // staged records as four float4 planes (conflict-free staging stores)
   __shared__ uint8_t s_list[NB * BATCH];
   __shared__ uint32_t s_wc[EPT * (NT / 32) * NB];
   __shared__ int s_nw[NB];
@@ -153,11 +153,14 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
         if (k < re) {
           const uint32_t id = a.vals[k];
           PGSAG_DCHECK(id < *a.n_dev);
-          Rec& r = s_rec[e * NT + tid];
+          Rec r;
           mk[e] = stage_gaussian<8, Cfg::BH>(a.mean2d[id], a.conic_o[id], tx0, ty0, r);
           r.b.w = (float)(e * NT + tid);  // slot in the batch, for the blend's last index
-          r.cd = a.rgb_d[id];
-          r.n = a.ncam[id];
+          const int slot = e * NT + tid;
+          s_rec[slot] = r.a;
+          s_rec[BATCH + slot] = r.b;
+          s_rec[2 * BATCH + slot] = a.rgb_d[id];
+          s_rec[3 * BATCH + slot] = a.ncam[id];
         }
       }
       build_lists<NT, EPT, NB>(mk, s_list, s_wc, s_nw);
@@ -173,13 +176,13 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
         for (int t = t0; t < tend; ++t) {
           const uint32_t q = lds_u8(lbase + (uint32_t)t);
           PGSAG_DCHECK(b + q < re);
-          const uint32_t ra_addr = rec_base + q * (uint32_t)sizeof(Rec);
+          const uint32_t ra_addr = rec_base + q * 16u;
           const float4 ra = lds128(ra_addr);
-          const float4 rb = lds128(ra_addr + 16);
+          const float4 rb = lds128(ra_addr + 16 * BATCH);
           const float dx = px - ra.x;
           const float tA = __fmul_rn(ra.z, dx);
-          const float4 cd = lds128(ra_addr + 32);
-          const float4 nn = lds128(ra_addr + 48);
+          const float4 cd = lds128(ra_addr + 32 * BATCH);
+          const float4 nn = lds128(ra_addr + 48 * BATCH);
 #pragma unroll
           for (int p = 0; p < NP; ++p) {
             // p2 for the pair (bit-identical to power2r per element)
