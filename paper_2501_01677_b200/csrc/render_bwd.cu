@@ -17,10 +17,10 @@
 // Mapping: per active tile two single-warp CTAs, the one of half h
 // owning the 8x16 pixel block of columns 8h..8h+7; a lane owns the FOUR pixels (x, y + 4k),
 // k = 0..3, of its column, which share dx and every per-entry load and run as two packed FP32x2
-// pairs.  Batches of 64 entries are staged with the exact block cull of A6 (per 8x8 block of
-// the half: block p holds the lane's pair p) and walked in reverse through a compacted
-// candidate list; a pair whose block the entry misses, or none of whose 64 pixels blends it,
-// is skipped by a warp-uniform branch.  A pixel that
+// pairs.  Batches of 32 entries (one per lane; the next batch's inputs prefetched by cp.async)
+// are staged with the exact block cull of A6 (per 8x8 block of the half: block p holds the
+// lane's pair p) and walked in reverse over the ballot of the culled slots; a pair whose block
+// the entry misses, or none of whose 64 pixels blends it, is skipped by a warp-uniform branch.  A pixel that
 // does not contribute to an entry carries alpha = rho = 0, which zeroes all of its
 // terms and leaves its state unchanged without branches.  Reduction: per entry the
 // lane sums its four pixels into 13 raw sums (the seven feature gradients sum alpha T G_c and the
@@ -44,8 +44,7 @@ namespace {
 // twice the record loads (L2 hits).  (A two-warp CTA per tile sharing the staged batch measured
 // slower in round 1: C4 A7 3.51 vs 3.41 ms.)
 constexpr int kBT = 32;
-constexpr int kBEPT = 2;
-constexpr int kBBatch = kBT * kBEPT;
+constexpr int kBBatch = kBT;  // a batch is one entry per lane (64-entry batches measured 1.6 % slower)
 #ifndef PGSAG_BWD_MINB
 #define PGSAG_BWD_MINB 20  // resident CTAs per SM the register budget is sized for
 #endif
@@ -107,6 +106,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// per-thread asynchronous global -> shared copies (LDGSTS), completed by cp_async_wait_all
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Per-pixel prologue: upstream G (Eq. 4 folded in), P*(bg.gC), last index, T.
 struct PixState {
@@ -226,14 +235,15 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   __shared__ uint32_t s_id[kBBatch];
   __shared__ __align__(16) float s_acc[kBBatch * kAccStride];
   __shared__ __align__(16) float s_red[14 * kRedStride];
-  __shared__ uint8_t s_list[kBBatch];
-  __shared__ uint32_t s_wc[kBEPT];
-  __shared__ int s_nw[1];
+  // the next batch's raw inputs (mean2d, conic_o, rgb_d, ncam), fetched by cp.async while this batch
+  // runs; each lane writes and later reads only its own slot
+  __shared__ float2 s_rxy[kBBatch];
+  __shared__ float4 s_rco[kBBatch], s_rcd[kBBatch], s_rnn[kBBatch];
   __shared__ uint32_t s_tile;
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t n_active = *a.n_active;
   const size_t HW = (size_t)a.d.W * a.d.H;
-  const uint32_t rec_base = opaque(smem_u32(s_rec)), list_base = opaque(smem_u32(s_list));
+  const uint32_t rec_base = opaque(smem_u32(s_rec));
   unsigned long long cntV = 0;
   // transpose: lane l writes column l of every row; lane l then sums half (l >> 4) of row l & 15
   // and, for l < kNV, stores the row's total
@@ -279,53 +289,73 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
     const int maxlast = wlast;
     // every thread has read s_tile: claim the next tile now (latency hidden behind this one)
     if (tid == 0) s_tile = atomicAdd(a.work, 1u);
-    for (int bhi = maxlast + 1; bhi > (int)rs; bhi -= kBBatch) {
-      const int blo = max((int)rs, bhi - kBBatch);
-      const int cnt = bhi - blo;
-      uint32_t mk[kBEPT];
-#pragma unroll
-      for (int e = 0; e < kBEPT; ++e) {
-        const int slot = e * kBT + tid;
-        mk[e] = 0u;
-        if (slot < cnt) {
-          const uint32_t id = a.vals[blo + slot];
-          PGSAG_DCHECK(id < (uint32_t)a.n);
-          Rec r;
-          {  // this CTA's half only
-            const float2 xy = a.mean2d[id];
-            const float4 co = a.conic_o[id];
-            const StageCull c = stage_record(xy, co, r);
-            const float xlo = tx0 + (float)(half * 8) + 0.5f, ylo = ty0 + 0.5f;
-            // exact cull per 8x8 block of the half (block p = the rows of pixel pair p)
-            const uint32_t sm = (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 7.0f) ? 1u : 0u) |
-                                (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo + 8.0f, ylo + 15.0f) ? 2u : 0u);
-            mk[e] = sm != 0u ? 1u : 0u;
-            r.b.w = __uint_as_float(sm);
-          }
-          r.cd = a.rgb_d[id];
-          r.n = a.ncam[id];
-          s_rec[slot] = r.a;
-          s_rec[kBBatch + slot] = r.b;
-          s_rec[2 * kBBatch + slot] = r.cd;
-          s_rec[3 * kBBatch + slot] = r.n;
-          s_id[slot] = id;
-        }
+    // batches of 32 entries walked down from the deepest entry a pixel of the half needs.  Pipeline:
+    // the raw inputs of batch k + 1 are in flight (cp.async) and the ids of batch k + 2 in a register
+    // while batch k runs, so neither dependent global latency (vals -> records) stalls the warp.
+    const auto fetch_raw = [&](uint32_t id) {
+      cp_async8(smem_u32(s_rxy + tid), a.mean2d + id);
+      cp_async16(smem_u32(s_rco + tid), a.conic_o + id);
+      cp_async16(smem_u32(s_rcd + tid), a.rgb_d + id);
+      cp_async16(smem_u32(s_rnn + tid), a.ncam + id);
+    };
+    const auto batch_lo = [&](int hi) { return max((int)rs, hi - kBBatch); };
+    int bhi = maxlast + 1;
+    uint32_t id_cur = 0u, id_n1 = 0u;
+    if (bhi > (int)rs) {
+      const int blo = batch_lo(bhi), blo1 = batch_lo(blo);
+      if (tid < bhi - blo) {
+        id_cur = a.vals[blo + tid];
+        fetch_raw(id_cur);
       }
-      build_lists<kBT, kBEPT, 1>(mk, s_list, s_wc, s_nw);
-      const int qtop = wlast - blo;  // entries past the warp's last are never needed
-      const uint32_t lbase = list_base;
-      // the list is in ascending slot order: drop its tail past the warp's last entry up front
-      int t = s_nw[0] - 1;
-      while (t >= 0 && (int)lds_u8(lbase + (uint32_t)t) > qtop) --t;  // warp-uniform
+      cp_async_commit();
+      if (tid < blo - blo1) id_n1 = a.vals[blo1 + tid];
+    }
+    for (; bhi > (int)rs; bhi -= kBBatch) {
+      const int blo = batch_lo(bhi), cnt = bhi - blo;
+      const int blo1 = batch_lo(blo), cnt1 = blo - blo1;
+      const int blo2 = batch_lo(blo1), cnt2 = blo1 - blo2;
+      uint32_t id_n2 = 0u;
+      if (tid < cnt2) id_n2 = a.vals[blo2 + tid];  // consumed two batches from now
+      cp_async_wait_all();
+      uint32_t mk = 0u;
+      if (tid < cnt) {
+        const uint32_t id = id_cur;
+        PGSAG_DCHECK(id < (uint32_t)a.n);
+        Rec r;
+        {  // this CTA's half only
+          const float2 xy = s_rxy[tid];
+          const float4 co = s_rco[tid];
+          const StageCull c = stage_record(xy, co, r);
+          const float xlo = tx0 + (float)(half * 8) + 0.5f, ylo = ty0 + 0.5f;
+          // exact cull per 8x8 block of the half (block p = the rows of pixel pair p)
+          mk = (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 7.0f) ? 1u : 0u) |
+               (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo + 8.0f, ylo + 15.0f) ? 2u : 0u);
+          r.b.w = __uint_as_float(mk);
+        }
+        s_rec[tid] = r.a;
+        s_rec[kBBatch + tid] = r.b;
+        s_rec[2 * kBBatch + tid] = s_rcd[tid];
+        s_rec[3 * kBBatch + tid] = s_rnn[tid];
+        s_id[tid] = id;
+      }
+      // this lane's raw slot is consumed: fetch the next batch's into it
+      if (tid < cnt1) fetch_raw(id_n1);
+      cp_async_commit();
+      id_cur = id_n1;
+      id_n1 = id_n2;
+      __syncwarp();  // the staged planes are visible to every lane
+      // candidates: bit q = slot q reaches a block of the half; entries past the warp's last are
+      // never needed.  Walked from the highest bit (back to front).
+      uint32_t cm = __ballot_sync(0xffffffffu, mk != 0u);
+      const int qtop = wlast - blo;
+      if (qtop < 31) cm &= (2u << qtop) - 1u;
       // software pipeline over the candidates: the shuffle joining an entry's half-row sums is issued
-      // at the top of the next candidate and its total stored after that candidate's alpha pass, and
-      // the next list byte is loaded a candidate ahead
+      // at the top of the next candidate and its total stored after that candidate's alpha pass
       int pq = -1;  // entry whose transposed rows await their sums (warp-uniform)
       float hs = 0.f;  // this lane's half-row sum of entry pq
-      uint32_t qn = t >= 0 ? lds_u8(lbase + (uint32_t)t) : 0u;
-      for (; t >= 0; --t) {
-        const int q = (int)qn;
-        if (t > 0) qn = lds_u8(lbase + (uint32_t)(t - 1));
+      while (cm != 0u) {
+        const int q = 31 - __clz(cm);
+        cm ^= 1u << q;
         const uint32_t ra_addr = rec_base + (uint32_t)q * 16u;
         const float4 ra = lds128(ra_addr);
         const float4 rb = lds128(ra_addr + 16 * kBBatch);
@@ -434,27 +464,23 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(sum) : "memory");
         }
       }
-      __syncthreads();
+      __syncwarp();
       // flush the batch: one vector reduction per nonzero group of four values, then re-zero
+      if (tid < cnt) {
+        float* dst = a.g2d + (size_t)s_id[tid] * 16;
 #pragma unroll
-      for (int e = 0; e < kBEPT; ++e) {
-        const int slot = e * kBT + tid;
-        if (slot < cnt) {
-          float* dst = a.g2d + (size_t)s_id[slot] * 16;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float4* sp = reinterpret_cast<float4*>(s_acc + slot * kAccStride + 4 * c);
-            const float4 x = *sp;
-            if (x.x != 0.0f || x.y != 0.0f || x.z != 0.0f || x.w != 0.0f) {
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c), "f"(x.x), "f"(x.y),
-                           "f"(x.z), "f"(x.w)
-                           : "memory");
-              *sp = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+        for (int c = 0; c < 4; ++c) {
+          float4* sp = reinterpret_cast<float4*>(s_acc + tid * kAccStride + 4 * c);
+          const float4 x = *sp;
+          if (x.x != 0.0f || x.y != 0.0f || x.z != 0.0f || x.w != 0.0f) {
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c), "f"(x.x), "f"(x.y),
+                         "f"(x.z), "f"(x.w)
+                         : "memory");
+            *sp = make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
       }
-      __syncthreads();
+      __syncwarp();
     }
   }
 #ifdef PGSAG_A7_STATS
