@@ -107,16 +107,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// per-thread asynchronous global -> shared copies (LDGSTS), completed by cp_async_wait_all
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
 // Per-pixel prologue: upstream G (Eq. 4 folded in), P*(bg.gC), last index, T.
 struct PixState {
   float G[8];
