@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float2 dy23 = __fadd2_rn(py23, bc(-ra.y));
         const float4 cd = lds128(ra_addr + 32 * kBBatch);
         const float4 nn = lds128(ra_addr + 48 * kBBatch);
-        const float ho = pq >= 0 ? __shfl_xor_sync(0xffffffffu, hs, 16) : 0.f;
+        const float ho = __shfl_xor_sync(0xffffffffu, hs, 16);  // (unused when no entry is pending)
         PairOut o01, o23;
         o01.wt = o01.dpow = o23.wt = o23.dpow = f2(0.f, 0.f);
         bool anyc = false;
