@@ -17,7 +17,10 @@ constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kMaxRadix = 512;  // 9-bit digits where they save a pass
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+#ifndef PGSAG_SORT_ITEMS
+#define PGSAG_SORT_ITEMS 16
+#endif
+constexpr int kSortItems = PGSAG_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per CTA
 constexpr uint32_t kLbAgg = 1u << 30;                 // look-back flags (top 2 bits)
 constexpr uint32_t kLbPrefix = 2u << 30;
