@@ -151,6 +151,10 @@ cudaError_t launch_fp32_microbench(int mode, int iters, float* scratch, float* m
 
 // counters[] slots for pgsag_gc_weights: 8 (sum, count) double pairs at bytes 4*CNT_GC .. 4*CNT_GC + 127
 constexpr int CNT_GC = 64;
-constexpr int kCounters = 128;  // u32 slots of the workspace counter block
+constexpr int kCounters = 256;  // u32 slots of the workspace counter block
+// A6's fused Eq. 9 statistics: kGcSlots (N, sum r, sum r^2) double triples at bytes 4*CNT_GCF.. (the
+// warps of CTA b add into slot b % kGcSlots: 16x less contention than three global addresses)
+constexpr int CNT_GCF = 128;
+constexpr int kGcSlots = 16;
 
 }  // namespace pgsag

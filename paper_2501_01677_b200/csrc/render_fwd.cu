@@ -43,7 +43,8 @@ struct FwdArgs {
   unsigned long long* counters;
   uint32_t* work;
   const float* gc_w;   // optional L_GC-load weights (NEXT-1)
-  double* gc_stats;    // N, sum r, sum r^2
+  double* gc_stats;    // N, sum r, sum r^2, L, mean (written by gc_finalize_kernel)
+  double* gc_part;     // [kGcSlots][3] partial sums (workspace counter block)
   const uint32_t* n_dev;  // Gaussians of the sorted view (A3's CNT_NG; debug bounds checks)
 };
 
@@ -255,9 +256,10 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
       if (lane == 0 && n > 0.f) {
-        atomicAdd(a.gc_stats, (double)n);
-        atomicAdd(a.gc_stats + 1, (double)s1);
-        atomicAdd(a.gc_stats + 2, (double)s2);
+        double* slot = a.gc_part + 3 * (blockIdx.x % kGcSlots);
+        atomicAdd(slot, (double)n);
+        atomicAdd(slot + 1, (double)s1);
+        atomicAdd(slot + 2, (double)s2);
       }
     }
   }
@@ -281,7 +283,13 @@ constexpr int kNP = PGSAG_FWD_NP;
 constexpr int kFT = FwdCfg<kNP>::NT;
 
 // Eq. 9 from the fused statistics: L_GC-load = population std of r = g / w over the mask pixels.
-__global__ void gc_finalize_kernel(double* st) {
+__global__ void gc_finalize_kernel(double* st, const double* part) {
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < kGcSlots; ++k)
+    for (int c = 0; c < 3; ++c) acc[c] += part[3 * k + c];
+  st[0] = acc[0];
+  st[1] = acc[1];
+  st[2] = acc[2];
   const double n = st[0];
   const double mu = n > 0.0 ? st[1] / n : 0.0;
   st[3] = n > 0.0 ? sqrt(fmax(st[2] / n - mu * mu, 0.0)) : 0.0;
@@ -326,7 +334,8 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
   a.gc_w = out->gc_w;
   a.gc_stats = out->gc_stats;
   a.n_dev = work_counter + (CNT_NG - CNT_FWD);
-  if (a.gc_w) cudaMemsetAsync(a.gc_stats, 0, 5 * sizeof(double), st);
+  a.gc_part = reinterpret_cast<double*>(work_counter + (CNT_GCF - CNT_FWD));
+  if (a.gc_w) cudaMemsetAsync(a.gc_part, 0, 3 * kGcSlots * sizeof(double), st);
   const int grid = min(fwd_grid(), d.TX * d.TY);
   {
     KTimer kt_("A6_render_fwd", st);
@@ -337,7 +346,7 @@ cudaError_t launch_render_fwd(const pgsag_projected* p, const pgsag_bins* bins, 
   }
   if (a.gc_w) {
     KTimer kt_("N1_gc_finalize", st);
-    gc_finalize_kernel<<<1, 1, 0, st>>>(a.gc_stats);
+    gc_finalize_kernel<<<1, 1, 0, st>>>(a.gc_stats, a.gc_part);
   }
   return cudaGetLastError();
 }
