@@ -273,8 +273,10 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       make_pair(s[0], s[1], P01);
       make_pair(s[2], s[3], P23);
     }
-    const int mylast = max(max(P01.last0, P01.last1), max(P23.last0, P23.last1));
-    const int wlast = __reduce_max_sync(0xffffffffu, mylast);
+    // the deepest entry each 8x8 block (pixel pair) needs: an entry past it skips the block's pair
+    const int blast0 = __reduce_max_sync(0xffffffffu, max(P01.last0, P01.last1));
+    const int blast1 = __reduce_max_sync(0xffffffffu, max(P23.last0, P23.last1));
+    const int wlast = max(blast0, blast1);
     __syncthreads();
     const int maxlast = wlast;
     // every thread has read s_tile: claim the next tile now (latency hidden behind this one)
@@ -318,8 +320,9 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           const StageCull c = stage_record(xy, co, r);
           const float xlo = tx0 + (float)(half * 8) + 0.5f, ylo = ty0 + 0.5f;
           // exact cull per 8x8 block of the half (block p = the rows of pixel pair p)
-          mk = (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 7.0f) ? 1u : 0u) |
-               (block_hit(xy, co, c, xlo, xlo + 7.0f, ylo + 8.0f, ylo + 15.0f) ? 2u : 0u);
+          const int kq = blo + tid;
+          mk = (kq <= blast0 && block_hit(xy, co, c, xlo, xlo + 7.0f, ylo, ylo + 7.0f) ? 1u : 0u) |
+               (kq <= blast1 && block_hit(xy, co, c, xlo, xlo + 7.0f, ylo + 8.0f, ylo + 15.0f) ? 2u : 0u);
           r.b.w = __uint_as_float(mk);
         }
         s_rec[tid] = r.a;
