@@ -528,11 +528,29 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
 __global__ void ranges_kernel(const uint32_t* __restrict__ tkeys, const uint32_t* __restrict__ M_ptr,
                               uint32_t ntiles, uint32_t* __restrict__ ranges) {
   const uint32_t M = *M_ptr;  // the entry count published by A3 (0 after an overflow)
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < M; k += gridDim.x * blockDim.x) {
-    const uint32_t t = tkeys[k];
-    if (t >= ntiles) continue;  // defensive: keys are tile ids < ntiles by construction
-    if (k == 0 || tkeys[k - 1] != t) ranges[2 * t] = k;
-    if (k == M - 1 || tkeys[k + 1] != t) ranges[2 * t + 1] = k + 1;
+  // four consecutive keys per thread (one 128-bit load) and their two outer neighbours; keys past
+  // M read as the all-ones sentinel (never a tile id), so the ends of the array close their ranges
+  const uint32_t ng = (M + 3u) / 4u;
+  const bool vec = (reinterpret_cast<uintptr_t>(tkeys) & 15u) == 0u;  // caller buffer: 16-byte aligned?
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ng; gi += gridDim.x * blockDim.x) {
+    const uint32_t k0 = gi * 4u;
+    uint32_t t[6];
+    if (vec && k0 + 4u <= M) {
+      const uint4 v = reinterpret_cast<const uint4*>(tkeys)[gi];
+      t[1] = v.x; t[2] = v.y; t[3] = v.z; t[4] = v.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[1 + j] = k0 + j < M ? tkeys[k0 + j] : 0xFFFFFFFFu;
+    }
+    t[0] = k0 > 0u ? tkeys[k0 - 1u] : 0xFFFFFFFFu;
+    t[5] = k0 + 4u < M ? tkeys[k0 + 4u] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t c = t[1 + j], k = k0 + (uint32_t)j;
+      if (k >= M || c >= ntiles) continue;  // (keys are tile ids < ntiles by construction)
+      if (t[j] != c) ranges[2 * c] = k;
+      if (t[j + 2] != c) ranges[2 * c + 1] = k + 1u;
+    }
   }
 }
 
@@ -757,7 +775,7 @@ cudaError_t launch_duplicate_and_sort(const pgsag_projected* p, const pgsag_tile
                              reinterpret_cast<uint32_t*>(ws + L.status2), stride, hist,
                              counters + CNT_SORT2, st, &in_a);
   if (e != cudaSuccess) return e;
-  const int grid = min((int)((bound + 255) / 256), num_sms() * 8);
+  const int grid = min((int)(((bound + 3) / 4 + 255) / 256), num_sms() * 8);
   {
     KTimer kt_("A5_ranges", st);
     ranges_kernel<<<grid, 256, 0, st>>>(bins->tile_keys, m_clamped, (uint32_t)ntiles, bins->ranges);
