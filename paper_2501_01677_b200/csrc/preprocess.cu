@@ -33,14 +33,20 @@ __global__ void __launch_bounds__(128) tilemask_count_kernel(const uint8_t* __re
     const int i1 = min(i0 + kTile, d.W);
     const int j0 = ty * kTile;
     const int j1 = min(j0 + kTile, d.H);
-    if (vec16 && i1 - i0 == kTile) {
-#pragma unroll 4
-      for (int j = j0; j < j1; ++j) {
-        const uint4 w = __ldg(reinterpret_cast<const uint4*>(mask + (size_t)j * d.W + i0));
-        // bytes != 0 -> 0xFF per byte; popc / 8 = number of nonzero bytes
-        cnt += (__popc(__vcmpne4(w.x, 0u)) + __popc(__vcmpne4(w.y, 0u)) + __popc(__vcmpne4(w.z, 0u)) +
-                __popc(__vcmpne4(w.w, 0u))) >> 3;
-      }
+    // bytes != 0 -> 0xFF per byte; popc / 8 = number of nonzero bytes
+    const auto row16 = [&](int j) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(mask + (size_t)j * d.W + i0));
+      return (uint32_t)(__popc(__vcmpne4(w.x, 0u)) + __popc(__vcmpne4(w.y, 0u)) + __popc(__vcmpne4(w.z, 0u)) +
+                        __popc(__vcmpne4(w.w, 0u))) >> 3;
+    };
+    if (vec16 && i1 - i0 == kTile && j1 - j0 == kTile) {
+      uint32_t c[kTile];  // the tile's 16 row loads all in flight
+#pragma unroll
+      for (int r = 0; r < kTile; ++r) c[r] = row16(j0 + r);
+#pragma unroll
+      for (int r = 0; r < kTile; ++r) cnt += c[r];
+    } else if (vec16 && i1 - i0 == kTile) {
+      for (int j = j0; j < j1; ++j) cnt += row16(j);
     } else {
       for (int j = j0; j < j1; ++j)
         for (int i = i0; i < i1; ++i) cnt += mask[(size_t)j * d.W + i] != 0;
