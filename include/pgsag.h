@@ -110,8 +110,8 @@ typedef struct {
  * (tile, depth bits, id).  ranges[2t], ranges[2t+1] = [start, end) of tile t
  * (empty tiles [0, 0)). */
 typedef struct {
-  uint32_t *tile_keys; /* [capacity] */
-  uint32_t *vals;      /* [capacity] */
+  uint32_t *tile_keys; /* [capacity], 16-byte aligned (the sort reads it with 128-bit loads) */
+  uint32_t *vals;      /* [capacity], 16-byte aligned */
   uint32_t *ranges;    /* [2*TY*TX]  */
   int64_t capacity;    /* in: entries allocated            */
   int64_t n_dup;       /* out (host field): M              */

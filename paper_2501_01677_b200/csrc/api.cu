@@ -213,6 +213,8 @@ int pgsag_bin_sort(const pgsag_projected* p, const pgsag_tilemask* tm, const pgs
   if (n > 0 && (rc = check_proj(p))) return rc;
   if (!bins || !bins->ranges || (bins->capacity > 0 && (!bins->tile_keys || !bins->vals)))
     return fail(PGSAG_EINVAL, "bins buffer is NULL");
+  if (!aligned(bins->tile_keys, 16) || !aligned(bins->vals, 16))
+    return fail(PGSAG_EINVAL, "bins tile_keys / vals must be 16-byte aligned");
   if (bins->capacity < 0 || bins->capacity >= (int64_t)kLbMask)
     return fail(PGSAG_EINVAL, "bins capacity must be in [0, 2^30)");
   const WsLayout L = ws_layout(n, cam->width, cam->height, bins->capacity);
@@ -249,6 +251,8 @@ int pgsag_bin_sort_async(const pgsag_projected* p, const pgsag_tilemask* tm, con
   if (n > 0 && (rc = check_proj(p))) return rc;
   if (!bins || !bins->ranges || (bins->capacity > 0 && (!bins->tile_keys || !bins->vals)))
     return fail(PGSAG_EINVAL, "bins buffer is NULL");
+  if (!aligned(bins->tile_keys, 16) || !aligned(bins->vals, 16))
+    return fail(PGSAG_EINVAL, "bins tile_keys / vals must be 16-byte aligned");
   if (bins->capacity < 0 || bins->capacity >= (int64_t)kLbMask)
     return fail(PGSAG_EINVAL, "bins capacity must be in [0, 2^30)");
   const WsLayout L = ws_layout(n, cam->width, cam->height, bins->capacity);

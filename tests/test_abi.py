@@ -99,6 +99,13 @@ def test_invalid_arguments_rejected_on_host(lib):
     bad = lib.Camera()
     rc = L.pgsag_preprocess(C.byref(g), C.byref(bad), None, None, None, None, 0, None)
     assert rc == lib.PGSAG_EINVAL and b"width" in L.pgsag_last_error()
+    # entry buffers off a 16-byte boundary are rejected before any launch (the sort's 128-bit loads);
+    # the pointers are never dereferenced
+    tm, b = lib.TileMask(), lib.Bins()
+    tm.tile_cnt = tm.active = tm.n_active = tm.active_bits = 0x1000
+    b.tile_keys, b.vals, b.ranges, b.capacity = 0x2004, 0x3000, 0x4000, 16
+    rc = L.pgsag_bin_sort(C.byref(lib.Projected()), C.byref(tm), C.byref(cam), 0, C.byref(b), None, 0, None)
+    assert rc == lib.PGSAG_EINVAL and b"16-byte aligned" in L.pgsag_last_error()
     assert lib.version().startswith("pgsag-b200")
 
 

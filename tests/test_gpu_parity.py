@@ -328,3 +328,23 @@ def test_trainer_skips_overflowed_view():
     # same render, same L_s (a sum of per-block atomics in double: equal up to its last bits)
     assert la["rgb"] == lb["rgb"] and abs(la["flat"] - lb["flat"]) <= 1e-12 * abs(la["flat"])
     assert not torch.equal(before[0], gb.mean) and not torch.equal(before[4], tb.m)  # the re-run updated
+
+
+def test_unaligned_tile_key_buffer():
+    """pgsag_bins.tile_keys / vals must be 16-byte aligned (the sort reads them with 128-bit loads):
+    a buffer 4 bytes off a 16-byte boundary is rejected with PGSAG_EINVAL before any launch."""
+    from paper_2501_01677_b200 import _lib as L
+    from paper_2501_01677_b200.raster import GaussianTensors, Rasterizer, camera_from
+    sc = ragged_scene(seed=5)
+    H, W = sc.mask.shape
+    g = GaussianTensors.from_numpy(sc.gaussians)
+    cam = camera_from(sc.camera)
+    mask = torch.from_numpy(np.ascontiguousarray(sc.mask)).cuda()
+    odd = Rasterizer(g.n, W, H, g.sh_degree, capacity=4096)
+    base = torch.empty(odd.capacity + 4, dtype=torch.int32, device="cuda")
+    odd.tile_keys = base[1:1 + odd.capacity]
+    assert odd.tile_keys.data_ptr() % 16 == 4
+    odd._build_bins()
+    with pytest.raises(L.PgsagError) as ei:
+        odd.forward(g, cam, mask)
+    assert ei.value.code == L.PGSAG_EINVAL and "16-byte aligned" in str(ei.value)
