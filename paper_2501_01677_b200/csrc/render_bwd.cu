@@ -83,6 +83,12 @@ constexpr float kGcK = 100.0f;  // soft-count sharpness (R24)
 #ifdef PGSAG_A7_STATS
 // diagnostic build only: per entry-warp work statistics of the candidate loop
 __device__ unsigned long long g_a7_stats[32];
+__device__ unsigned long long g_a7_t0 = ~0ull, g_a7_end[8192];  // kernel start, per-CTA end (globaltimer ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #endif
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -235,6 +241,9 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   const size_t HW = (size_t)a.d.W * a.d.H;
   const uint32_t rec_base = opaque(smem_u32(s_rec));
   unsigned long long cntV = 0;
+#ifdef PGSAG_A7_STATS
+  unsigned long long st[32] = {};
+#endif
   // transpose: lane l writes column l of every row; lane l then sums half (l >> 4) of row l & 15
   // and, for l < kNV, stores the row's total
   const uint32_t red_w = opaque(smem_u32(s_red) + 4u * (uint32_t)lane);
@@ -244,6 +253,9 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   const uint32_t acc_lane = opaque(smem_u32(s_acc) + 4u * (uint32_t)lane);
   const uint32_t wr = opaque((uint32_t)(lane < kNV));
   for (int k = tid; k < kBBatch * kAccStride; k += kBT) s_acc[k] = 0.f;
+#ifdef PGSAG_A7_STATS
+  if (tid == 0) atomicMin(&g_a7_t0, gtimer());
+#endif
   if (tid == 0) s_tile = atomicAdd(a.work, 1u);
   for (;;) {
     __syncthreads();
@@ -477,9 +489,11 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
     }
   }
 #ifdef PGSAG_A7_STATS
-  if (lane == 0)
+  if (lane == 0) {
     for (int k = 0; k < 32; ++k)
       if (st[k]) atomicAdd(&g_a7_stats[k], st[k]);
+    if (blockIdx.x < 8192) g_a7_end[blockIdx.x] = gtimer();
+  }
 #endif
   if (kCount) {
 #pragma unroll
@@ -561,6 +575,14 @@ cudaError_t launch_render_bwd(const pgsag_gaussians* g, const pgsag_camera* cam,
 }  // namespace pgsag
 
 #ifdef PGSAG_A7_STATS
+extern "C" int pgsag_debug_a7_times(unsigned long long* t0, unsigned long long* ends, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(t0, pgsag::g_a7_t0, sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(ends, pgsag::g_a7_end, sizeof(unsigned long long) * (n < 8192 ? n : 8192));
+  const unsigned long long big = ~0ull;
+  cudaMemcpyToSymbol(pgsag::g_a7_t0, &big, sizeof(big));
+  return 0;
+}
 extern "C" int pgsag_debug_a7_stats(unsigned long long* host, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(host, pgsag::g_a7_stats, sizeof(unsigned long long) * 32);
