@@ -19,10 +19,11 @@
 // k = 0..3, of its column, which share dx and every per-entry load and run as two packed FP32x2
 // pairs.  Batches of 32 entries (one per lane; the next batch's inputs prefetched by cp.async)
 // are staged with the exact block cull of A6 (per 8x8 block of the half: block p holds the
-// lane's pair p) and walked in reverse over the ballot of the culled slots; a pair whose block
-// the entry misses, or none of whose 64 pixels blends it, is skipped by a warp-uniform branch.  A pixel that
-// does not contribute to an entry carries alpha = rho = 0, which zeroes all of its
-// terms and leaves its state unchanged without branches.  Reduction: per entry the
+// lane's pair p; an entry past the block's deepest needed entry is culled for it too) and walked
+// in reverse over the ballot of the culled slots; a pair whose block the entry misses, or none of
+// whose 64 pixels blends it, is skipped by a warp-uniform branch.  A pixel that does not
+// contribute to an entry carries alpha = rho = 0, which zeroes all of its terms and leaves its
+// state unchanged without branches.  Reduction: per entry the
 // lane sums its four pixels into 13 raw sums (the seven feature gradients sum alpha T G_c and the
 // moments sum dpow {1, dx, dx^2, dy, dx dy, dy^2} of dpow = alpha dalpha; A8 turns the moments
 // into the mean, conic and opacity gradients with the entry's conic and o), the warp transposes
