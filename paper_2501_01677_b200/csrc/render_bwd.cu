@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
   // 16-byte words (conflict-free), the candidate loop's broadcast loads take one address + offsets
   __shared__ float4 s_rec[4 * kBBatch];
   __shared__ uint32_t s_id[kBBatch];
-  __shared__ __align__(16) float s_acc[kBBatch * kAccStride];
+  __shared__ __align__(16) float s_acc[(kBBatch + 1) * kAccStride];  // + a dummy row (no entry pending)
   __shared__ __align__(16) float s_red[14 * kRedStride];
   // the next batch's raw inputs (mean2d, conic_o, rgb_d, ncam), fetched by cp.async while this batch
   // runs; each lane writes and later reads only its own slot
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       if (qtop < 31) cm &= (2u << qtop) - 1u;
       // software pipeline over the candidates: the shuffle joining an entry's half-row sums is issued
       // at the top of the next candidate and its total stored after that candidate's alpha pass
-      int pq = -1;  // entry whose transposed rows await their sums (warp-uniform)
+      int pq = kBBatch;  // entry whose transposed rows await their sums (kBBatch: none, the dummy row)
       float hs = 0.f;  // this lane's half-row sum of entry pq
       while (cm != 0u) {
         const int q = 31 - __clz(cm);
@@ -411,13 +411,11 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           al1 = c1 ? al1 : 0.f;
           pair_grad<kGC>(PP, f2(al0, al1), orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, h ? o23 : o01);
         }
-        if (pq >= 0) {  // one warp: (entry, row) has a single writer lane
-          if (wr) {
-            const uint32_t addr = acc_lane + (uint32_t)pq * (uint32_t)(kAccStride * 4);
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(hs + ho) : "memory");
-          }
-          pq = -1;
+        if (wr) {  // one warp: (entry, row) has a single writer lane (none pending: the dummy row)
+          const uint32_t addr = acc_lane + (uint32_t)pq * (uint32_t)(kAccStride * 4);
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(hs + ho) : "memory");
         }
+        pq = kBBatch;
         if (!anyc) continue;
 #ifdef PGSAG_A7_STATS
         {
@@ -462,7 +460,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float2 t1 = __fadd2_rn(__fadd2_rn(f2(h2.x, h2.y), f2(h3.x, h3.y)), __fadd2_rn(f2(h2.z, h2.w), f2(h3.z, h3.w)));
         hs = hsum(__fadd2_rn(t0, t1));
       }
-      if (pq >= 0) {  // the batch's last transposed entry
+      if (pq < kBBatch) {  // the batch's last transposed entry
         float sum = hs;
         sum += __shfl_xor_sync(0xffffffffu, sum, 16);
         if (wr) {
