@@ -379,8 +379,8 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float ho = __shfl_xor_sync(0xffffffffu, hs, 16);  // (unused when no entry is pending)
         PairOut o01, o23;
         o01.wt = o01.dpow = o23.wt = o23.dpow = f2(0.f, 0.f);
-        bool anyc = false;
 #ifdef PGSAG_A7_STATS
+        bool anyc = false;
         st[0]++;
         uint32_t stc = 0u;
         const uint32_t stb0 = st[4];
@@ -405,8 +405,8 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           st[3]++;
           st[4] += __popc(__ballot_sync(0xffffffffu, c0)) + __popc(__ballot_sync(0xffffffffu, c1));
           stc |= __ballot_sync(0xffffffffu, c0 || c1);
-#endif
           anyc = true;
+#endif
           al0 = c0 ? al0 : 0.f;
           al1 = c1 ? al1 : 0.f;
           pair_grad<kGC>(PP, f2(al0, al1), orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, h ? o23 : o01);
@@ -416,9 +416,10 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(hs + ho) : "memory");
         }
         pq = kBBatch;
-        if (!anyc) continue;
+        // every candidate is summed (the ~7 % that no pixel blends transpose zeros): measured cheaper than
+        // a branch on "any pair blended" per candidate
 #ifdef PGSAG_A7_STATS
-        {
+        if (anyc) {
           st[1]++;
           const int nl = __popc(stc), nb = (int)(st[4] - stb0);
           st[8 + (nl <= 1 ? 0 : nl <= 2 ? 1 : nl <= 4 ? 2 : nl <= 8 ? 3 : nl <= 16 ? 4 : 5)]++;
