@@ -158,8 +158,9 @@ typedef struct {
  * |dL/du_p| + |dL/dv_p| (densification statistic).  Non-LIVE Gaussians get 0. */
 typedef struct {
   float *dmean, *dscale, *drot, *dopacity, *dsh, *absgrad2d;
-  float *grad2d; /* optional [14][n]: A7's per-Gaussian screen-space gradients du, dv, d(ca,cb,cc), d o,
-                    d rgb[3], d n_cam[3], d d_i, absgrad (the A7 -> A8 interface) */
+  float *grad2d; /* optional [14][n]: the per-Gaussian screen-space gradients du, dv, d(ca,cb,cc), d o,
+                    d rgb[3], d n_cam[3], d d_i, absgrad (A7 sums moments of alpha*dalpha per
+                    Gaussian; A8 forms du, dv, the conic and opacity gradients from them) */
   /* Optional densification statistic (NEXT-3, R31), ACCUMULATED across calls: for every Gaussian with
    * tiles_touched > 0, densify_accum[i] += |(du W/2, dv H/2)| (3DGS's view-space positional gradient
    * norm) and densify_count[i] += 1.  Both NULL or both [n]. */
