@@ -11,8 +11,8 @@
 // k ((G*A')_q + 2 x_q (G*B)_q + y_q (G*Cc)_q) — three more separable blurs.
 // Float32 throughout, with two shifts that keep the cancellations small (see the kernels):
 // error bound and tolerance in DESIGN.md (R28).
-// Tiles: 32 x 16 outputs per CTA (256 threads, 2 px each), 42 x 26 input halo in shared
-// memory, separable passes (horizontal into shared memory, then vertical).
+// Tiles: forward 32 x 32 outputs per CTA (42 x 42 halo), backward 32 x 16 (42 x 26 halo), 256
+// threads; separable passes (horizontal into shared memory, then vertical).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -23,7 +23,6 @@ namespace pgsag {
 namespace {
 
 constexpr int kTW = 32, kTH = 16, kR = 5, kIW = kTW + 2 * kR, kIH = kTH + 2 * kR;
-constexpr int kHalo = kIH * kIW, kHIt = (kHalo + 255) / 256;  // halo positions, per-thread share
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
 
 // Window weights g[k] = exp(-k^2 / 4.5) / sum (sigma 1.5), computed in double, rounded once.
@@ -88,7 +87,6 @@ __device__ __forceinline__ void block_sum(float (&v)[K], float (*s_red)[K]) {
 // of one column (12 samples).
 constexpr int kIWp = 44;
 constexpr int kPlane = kIH * kIWp, kHPlane = kIH * kTW;
-constexpr int kFwdSmem = (3 * 2 * kPlane + 2 * 2 * kHPlane + kHPlane) * 4;
 constexpr int kBwdSmem = (3 * 3 * kPlane + 2 * kHPlane + kHPlane) * 4;
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -119,75 +117,81 @@ __device__ __forceinline__ void store4(float* row, const float (&v)[4]) {
   *reinterpret_cast<float4*>(row) = make_float4(v[0], v[1], v[2], v[3]);
 }
 
-// Forward: window statistics in float32 on values shifted by the CTA's mean (every sample of
-// the zero-padded, zero-masked input is shifted, so mu = c + G*(x - c) and the (co)variances are
-// the shifted second moments minus the shifted means' products — the cancellation in
-// sigma^2 = E[x^2] - mu^2 is taken relative to the local mean instead of to 0).
-// One CTA = one 32x16 output tile, all three channels: the halo planes are fetched with
-// independent loads (mask applied by selection afterwards), one warp per row, then the
-// channels are filtered one after the other through the same horizontal-pass planes.
-__global__ void __launch_bounds__(256) rgb_fwd_kernel(RgbArgs A) {
+// Forward: window statistics in float32 on values shifted by the CTA's mean (every sample of the
+// zero-padded, zero-masked input is shifted, so mu = c + G*(x - c) and the (co)variances are the
+// shifted second moments minus the shifted means' products -- the cancellation in
+// sigma^2 = E[x^2] - mu^2 is taken relative to the local mean instead of to 0).  One CTA = one 32x32
+// output tile (the 42x42 halo: 1.72 input positions per output; a 32x16 tile measured 0.47 vs 0.44 ms
+// on a C4 view), the channels one after the other, each loading its own halo (41.7 KB of shared
+// memory); horizontal pass into shared memory, then a vertical pass of four output rows per thread
+// from 14 rows.  The window weights come from the host (kernel parameters).
+constexpr int kTW2 = 32, kTH2 = 32, kIW2 = kTW2 + 2 * kR, kIH2 = kTH2 + 2 * kR, kIWp2 = 44;
+constexpr int kHalo2 = kIH2 * kIW2, kHIt2 = (kHalo2 + 255) / 256;
+constexpr int kPlane2 = kIH2 * kIWp2, kHPlane2 = kIH2 * kTW2;
+constexpr int kFwdSmem2 = (2 * kPlane2 + 2 * 2 * kHPlane2 + kHPlane2) * 4;
+
+struct Win {
+  float g[2 * kR + 1];
+};
+
+__global__ void __launch_bounds__(256, 4) rgb_fwd2_kernel(RgbArgs A, Win win) {
   extern __shared__ float4 smem_f4[];
-  float2* s_in = reinterpret_cast<float2*>(smem_f4);  // [3] planes of (x, y)
-  float2* s_h2 = s_in + 3 * kPlane;                   // [2] planes: (mu_x, mu_y), (E x^2, E y^2)
-  float* s_h1 = reinterpret_cast<float*>(s_h2 + 2 * kHPlane);  // E xy
+  float2* s_in = reinterpret_cast<float2*>(smem_f4);            // (x, y) of the current channel
+  float2* s_h2 = s_in + kPlane2;                                // [2]: (mu_x, mu_y), (E x^2, E y^2)
+  float* s_h1 = reinterpret_cast<float*>(s_h2 + 2 * kHPlane2);  // E xy
   __shared__ float s_red[8][6];
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  const int bx = blockIdx.x * kTW, by = blockIdx.y * kTH;
-  const int x = bx + tx, y0 = by + 2 * ty;
-  bool m0, m1;
-  if (!tile_has_mask(A, x, y0, m0, m1)) return;
+  const int bx = blockIdx.x * kTW2, by = blockIdx.y * kTH2;
+  const int x = bx + tx, y0 = by + 4 * ty;
+  bool m[4], any = false;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    m[h] = x < A.W && y0 + h < A.H && __ldg(A.mask + (size_t)(y0 + h) * A.W + x);
+    any = any || m[h];
+  }
+  if (!__syncthreads_or(any)) return;
   const size_t HW = (size_t)A.W * A.H;
-  float sums[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  // halo: all loads of the thread's (up to 5) halo positions first, then the shared stores, so
-  // the global latencies overlap instead of serialising per position
-  float hv[kHIt][6];
-#pragma unroll
-  for (int it = 0; it < kHIt; ++it) {
-    const int k = tid + 256 * it;
-    const int r = k / kIW, c = k - r * kIW;
-    const int gy = by - kR + r, gx = bx - kR + c;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) hv[it][q] = 0.f;
-    if (k < kHalo && gx >= 0 && gy >= 0 && gx < A.W && gy < A.H) {
-      const size_t p = (size_t)gy * A.W + gx;
-      const uint8_t mk = __ldg(A.mask + p);
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        hv[it][2 * ch] = __ldg(A.C + ch * HW + p);
-        hv[it][2 * ch + 1] = __ldg(A.I + ch * HW + p);
-      }
-      if (!mk)
-#pragma unroll
-        for (int q = 0; q < 6; ++q) hv[it][q] = 0.f;
-    }
-  }
-#pragma unroll
-  for (int it = 0; it < kHIt; ++it) {
-    const int k = tid + 256 * it;
-    if (k < kHalo) {
-      const int r = k / kIW, c = k - r * kIW;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) s_in[ch * kPlane + r * kIWp + c] = f2(hv[it][2 * ch], hv[it][2 * ch + 1]);
-#pragma unroll
-      for (int q = 0; q < 6; ++q) sums[q] += hv[it][q];
-    }
-  }
-  block_sum<6>(sums, s_red);  // contains the barrier publishing s_in
   float g[2 * kR + 1];
-  window(g);
+#pragma unroll
+  for (int k = 0; k <= 2 * kR; ++k) g[k] = win.g[k];
   float acc[3] = {0.f, 0.f, 0.f};  // sum |C - I|, sum S, count
 #pragma unroll 1
   for (int ch = 0; ch < 3; ++ch) {
-    const float cx = (ch == 0 ? sums[0] : (ch == 1 ? sums[2] : sums[4])) * (1.0f / (kIH * kIW));
-    const float cy = (ch == 0 ? sums[1] : (ch == 1 ? sums[3] : sums[5])) * (1.0f / (kIH * kIW));
-    const float2* sxy = s_in + ch * kPlane;
-    if (ch) __syncthreads();  // previous channel's vertical pass is done with the s_h planes
-    if (tid < kIH * (kTW / 4)) {
-      const int r = tid >> 3, c0 = 4 * (tid & 7);
+    // this channel's halo: every load first, then the shared stores and the sums for the shift
+    float2 hv[kHIt2];
+#pragma unroll
+    for (int it = 0; it < kHIt2; ++it) {
+      const int k = tid + 256 * it;
+      const int r = k / kIW2, c = k - r * kIW2;
+      const int gy = by - kR + r, gx = bx - kR + c;
+      hv[it] = f2(0.f, 0.f);
+      if (k < kHalo2 && gx >= 0 && gy >= 0 && gx < A.W && gy < A.H) {
+        const size_t p = (size_t)gy * A.W + gx;
+        const uint8_t mk = __ldg(A.mask + p);
+        const float cv = __ldg(A.C + ch * HW + p), iv = __ldg(A.I + ch * HW + p);
+        if (mk) hv[it] = f2(cv, iv);
+      }
+    }
+    float sums[2] = {0.f, 0.f};
+    if (ch) __syncthreads();  // the previous channel's passes are done with s_in / s_h
+#pragma unroll
+    for (int it = 0; it < kHIt2; ++it) {
+      const int k = tid + 256 * it;
+      if (k < kHalo2) {
+        const int r = k / kIW2, c = k - r * kIW2;
+        s_in[r * kIWp2 + c] = hv[it];
+        sums[0] += hv[it].x;
+        sums[1] += hv[it].y;
+      }
+    }
+    block_sum<2>(sums, reinterpret_cast<float (*)[2]>(s_red));  // contains the barrier publishing s_in
+    const float cx = sums[0] * (1.0f / (kIH2 * kIW2)), cy = sums[1] * (1.0f / (kIH2 * kIW2));
+    // horizontal pass: 42 rows x 8 tasks of 4 adjacent output columns
+    for (int t = tid; t < kIH2 * (kTW2 / 4); t += 256) {
+      const int r = t >> 3, c0 = 4 * (t & 7);
       float2 v[16], sq[14];
       float pr[14];
-      load16x2(sxy + r * kIWp + c0, v);
+      load16x2(s_in + r * kIWp2 + c0, v);
 #pragma unroll
       for (int k = 0; k < 14; ++k) {
         v[k] = __fadd2_rn(v[k], f2(-cx, -cy));
@@ -207,45 +211,50 @@ __global__ void __launch_bounds__(256) rgb_fwd_kernel(RgbArgs A) {
           xy[o] = fmaf(g[k], pr[o + k], xy[o]);
         }
       }
-      store4x2(s_h2 + r * kTW + c0, ab);
-      store4x2(s_h2 + kHPlane + r * kTW + c0, q2);
-      store4(s_h1 + r * kTW + c0, xy);
+      store4x2(s_h2 + r * kTW2 + c0, ab);
+      store4x2(s_h2 + kHPlane2 + r * kTW2 + c0, q2);
+      store4(s_h1 + r * kTW2 + c0, xy);
     }
     __syncthreads();
-    float2 ab[2], q2[2];
-    float exy[2];
+    // vertical pass: four output rows per thread from 14 rows, one quantity group at a time
+    float2 ab[4], q2[4];
+    float exy[4];
     {
-      float2 ca[12], cq[12];
-      float cxy[12];
+      float2 col[14];
 #pragma unroll
-      for (int k = 0; k < 12; ++k) {
-        const int o = (2 * ty + k) * kTW + tx;
-        ca[k] = s_h2[o];
-        cq[k] = s_h2[kHPlane + o];
-        cxy[k] = s_h1[o];
+      for (int k = 0; k < 14; ++k) col[k] = s_h2[(4 * ty + k) * kTW2 + tx];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        ab[h] = f2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k <= 2 * kR; ++k) ab[h] = __ffma2_rn(f2(g[k], g[k]), col[k + h], ab[h]);
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        ab[h] = q2[h] = f2(0.f, 0.f);
+      for (int k = 0; k < 14; ++k) col[k] = s_h2[kHPlane2 + (4 * ty + k) * kTW2 + tx];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        q2[h] = f2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k <= 2 * kR; ++k) q2[h] = __ffma2_rn(f2(g[k], g[k]), col[k + h], q2[h]);
+      }
+      float cxy[14];
+#pragma unroll
+      for (int k = 0; k < 14; ++k) cxy[k] = s_h1[(4 * ty + k) * kTW2 + tx];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
         exy[h] = 0.f;
 #pragma unroll
-        for (int k = 0; k <= 2 * kR; ++k) {
-          ab[h] = __ffma2_rn(f2(g[k], g[k]), ca[k + h], ab[h]);
-          q2[h] = __ffma2_rn(f2(g[k], g[k]), cq[k + h], q2[h]);
-          exy[h] = fmaf(g[k], cxy[k + h], exy[h]);
-        }
+        for (int k = 0; k <= 2 * kR; ++k) exy[h] = fmaf(g[k], cxy[k + h], exy[h]);
       }
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (!(h ? m1 : m0)) continue;
+    for (int h = 0; h < 4; ++h) {
+      if (!m[h]) continue;
       const float ax = ab[h].x, ay = ab[h].y;
       const float sxx = fmaf(-ax, ax, q2[h].x), syy = fmaf(-ay, ay, q2[h].y), sxy_ = fmaf(-ax, ay, exy[h]);
       const float mx = cx + ax, my = cy + ay;
       const float n1 = 2.f * mx * my + kC1, n2 = 2.f * sxy_ + kC2;
       const float d1 = mx * mx + my * my + kC1, d2 = sxx + syy + kC2;
-      // no division by n1 or n2 (n2 = 2 sigma_xy + C2 crosses zero for anti-correlated windows:
-      // s / n2 would be 0/0 there); d1 >= C1 and d2 >= C2 up to rounding
       const float id = __fdividef(1.f, d1 * d2);
       const float s = n1 * n2 * id;
       const float dmx = 2.f * (my * n2 * id - __fdividef(mx * s, d1));
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(256) rgb_fwd_kernel(RgbArgs A) {
       abc[p] = dmx - 2.f * dsxx * (mx - kShift) - dsxy * (my - kShift);
       abc[HW + p] = dsxx;
       abc[2 * HW + p] = dsxy;
-      const float2 xy0 = sxy[(2 * ty + h + kR) * kIWp + tx + kR];
+      const float2 xy0 = s_in[(4 * ty + h + kR) * kIWp2 + tx + kR];
       acc[0] += fabsf(xy0.x - xy0.y);
       acc[1] += s;
       if (ch == 0) acc[2] += 1.f;
@@ -518,14 +527,24 @@ cudaError_t launch_rgb_loss(const float* image, const float* target, const uint8
   static bool attr[kMaxDevices] = {};
   const int dev = current_device();
   if (!attr[dev]) {
-    cudaFuncSetAttribute(rgb_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
+    cudaFuncSetAttribute(rgb_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem2);
     cudaFuncSetAttribute(rgb_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
     attr[dev] = true;
   }
+  static const Win kWin = [] {  // g[k] = exp(-k^2 / 4.5) / sum in double, rounded once (as window())
+    Win w;
+    double v[2 * kR + 1], sum = 0.0;
+    for (int k = -kR; k <= kR; ++k) {
+      v[k + kR] = exp(-(double)(k * k) / 4.5);
+      sum += v[k + kR];
+    }
+    for (int k = 0; k <= 2 * kR; ++k) w.g[k] = (float)(v[k] / sum);
+    return w;
+  }();
   const dim3 grid((W + kTW - 1) / kTW, (H + kTH - 1) / kTH);
   {
     KTimer kt_("N3_rgb_fwd", st);
-    rgb_fwd_kernel<<<grid, 256, kFwdSmem, st>>>(A);
+    rgb_fwd2_kernel<<<dim3((W + kTW2 - 1) / kTW2, (H + kTH2 - 1) / kTH2), 256, kFwdSmem2, st>>>(A, kWin);
   }
   if (dC) {
     KTimer kt_("N3_rgb_bwd", st);
