@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
       uint32_t mk = 0u;
       if (tid < cnt) {
         const uint32_t id = id_cur;
-        PGSAG_DCHECK(id < (uint32_t)a.n);
+        // the prefetched id is this batch's entry (the pipeline's bookkeeping) and a valid Gaussian
+        PGSAG_DCHECK(id < (uint32_t)a.n && id == a.vals[blo + tid] && blo >= (int)rs && cnt <= kBBatch);
         Rec r;
         {  // this CTA's half only
           const float2 xy = s_rxy[tid];
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
           al1 = c1 ? al1 : 0.f;
           pair_grad<kGC>(PP, f2(al0, al1), orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, h ? o23 : o01);
         }
+        PGSAG_DCHECK(pq <= kBBatch);
         if (wr) {  // one warp: (entry, row) has a single writer lane (none pending: the dummy row)
           const uint32_t addr = acc_lane + (uint32_t)pq * (uint32_t)(kAccStride * 4);
           asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(hs + ho) : "memory");
