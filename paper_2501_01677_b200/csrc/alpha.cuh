@@ -171,12 +171,13 @@ __device__ __forceinline__ uint32_t lanemask_lt_() {
 }
 
 // Per-warp candidate lists of a staged batch of NT*EPT slots (slot e*NT + tid is
-// thread tid's e-th entry, mask mk[e]): s_list[b*NT*EPT + ..] = ascending slots
-// whose mask has bit b, s_nw[b] = their count.  s_wc is [EPT*NW*NB] scratch.
+// thread tid's e-th entry, mask mk[e]): s_list[b*NT*EPT + ..] = the shared addresses
+// rec_base + 16 slot of the ascending slots whose mask has bit b (the record planes' first
+// plane; the loop reads a candidate's record with no address arithmetic), s_nw[b] = their count.  s_wc is [EPT*NW*NB] scratch.
 // Contains the barriers that publish the staged records and the lists.
 template <int NT, int EPT, int NB>
-__device__ __forceinline__ void build_lists(const uint32_t (&mk)[EPT], uint8_t* s_list, uint32_t* s_wc,
-                                            int* s_nw) {
+__device__ __forceinline__ void build_lists(const uint32_t (&mk)[EPT], uint32_t* s_list, uint32_t* s_wc,
+                                            int* s_nw, uint32_t rec_base) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, sw = tid >> 5;
   const uint32_t lt = lanemask_lt_();
@@ -207,7 +208,7 @@ __device__ __forceinline__ void build_lists(const uint32_t (&mk)[EPT], uint8_t* 
     for (int b = 0; b < NB; ++b)
       if ((mk[e] >> b) & 1u) {
         PGSAG_DCHECK(s_wc[(e * NW + sw) * NB + b] + pos[e][b] < (uint32_t)(NT * EPT));
-        s_list[b * (NT * EPT) + s_wc[(e * NW + sw) * NB + b] + pos[e][b]] = (uint8_t)(e * NT + tid);
+        s_list[b * (NT * EPT) + s_wc[(e * NW + sw) * NB + b] + pos[e][b]] = rec_base + 16u * (uint32_t)(e * NT + tid);
       }
   __syncthreads();
 }

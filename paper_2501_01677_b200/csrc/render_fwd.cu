@@ -98,7 +98,7 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
   using Cfg = FwdCfg<NP>;
   constexpr int NT = Cfg::NT, EPT = Cfg::EPT, NB = Cfg::NB, BATCH = Cfg::BATCH;
   __shared__ float4 s_rec[4 * BATCH];  // staged records as four float4 planes (conflict-free staging stores)
-  __shared__ uint8_t s_list[NB * BATCH];
+  __shared__ uint32_t s_list[NB * BATCH];  // candidate record addresses per warp block
   __shared__ uint32_t s_wc[EPT * (NT / 32) * NB];
   __shared__ int s_nw[NB];
   __shared__ uint32_t s_tile;
@@ -168,20 +168,20 @@ __global__ void PGSAG_FWD_BOUNDS(FwdCfg<NP>::NT) render_fwd_kernel(FwdArgs a) {
           s_rec[3 * BATCH + slot] = a.ncam[id];
         }
       }
-      build_lists<NT, EPT, NB>(mk, s_list, s_wc, s_nw);
+      build_lists<NT, EPT, NB>(mk, s_list, s_wc, s_nw, rec_base);
       const int nw = s_nw[w];
       // batch slot of each pixel's last blend in this batch (-1: none), kept on the FMA pipe
       float2 lastf[NP];
 #pragma unroll
       for (int p = 0; p < NP; ++p) lastf[p] = f2(-1.f, -1.f);
-      const uint32_t lbase = list_base + (uint32_t)(w * BATCH);
-      for (int t0 = 0; t0 < nw; t0 += kFwdDoneEvery) {  // the warp's early-out test once per kFwdDoneEvery candidates
+      const uint32_t lbase = list_base + (uint32_t)(4 * w * BATCH), lend = lbase + 4u * (uint32_t)nw;
+      for (uint32_t l0 = lbase; l0 < lend; l0 += 4u * kFwdDoneEvery) {  // the warp's early-out test once per kFwdDoneEvery candidates
         if (__all_sync(0xffffffffu, all_done())) break;
-        const int tend = min(t0 + kFwdDoneEvery, nw);
-        for (int t = t0; t < tend; ++t) {
-          const uint32_t q = lds_u8(lbase + (uint32_t)t);
-          PGSAG_DCHECK(b + q < re);
-          const uint32_t ra_addr = rec_base + q * 16u;
+        const uint32_t l1 = min(l0 + 4u * kFwdDoneEvery, lend);
+        for (uint32_t la = l0; la < l1; la += 4u) {
+          uint32_t ra_addr;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ra_addr) : "r"(la));
+          PGSAG_DCHECK(b + (ra_addr - rec_base) / 16u < re);
           const float4 ra = lds128(ra_addr);
           const float4 rb = lds128(ra_addr + 16 * BATCH);
           const float dx = px - ra.x;
