@@ -378,8 +378,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
         const float4 cd = lds128(ra_addr + 32 * kBBatch);
         const float4 nn = lds128(ra_addr + 48 * kBBatch);
         const float ho = __shfl_xor_sync(0xffffffffu, hs, 16);  // (unused when no entry is pending)
-        PairOut o01, o23;
-        o01.wt = o01.dpow = o23.wt = o23.dpow = f2(0.f, 0.f);
+        PairOut o01, o23;  // zeroed where a pair is skipped (below)
 #ifdef PGSAG_A7_STATS
         bool anyc = false;
         st[0]++;
@@ -388,7 +387,11 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
 #endif
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          if (!((smask >> h) & 1u)) continue;
+          PairOut& OO = h ? o23 : o01;
+          if (!((smask >> h) & 1u)) {
+            OO.wt = OO.dpow = f2(0.f, 0.f);
+            continue;
+          }
           Pair& PP = h ? P23 : P01;
           const float2 dy = h ? dy23 : dy01;
           const float2 p2 = __ffma2_rn(bc(dx), __ffma2_rn(bc(ra.w), dy, bc(tA)), __fmul2_rn(__fmul2_rn(bc(rb.x), dy), dy));
@@ -401,7 +404,10 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
 #ifdef PGSAG_A7_STATS
           st[2]++;
 #endif
-          if (!__any_sync(0xffffffffu, c0 || c1)) continue;
+          if (!__any_sync(0xffffffffu, c0 || c1)) {
+            OO.wt = OO.dpow = f2(0.f, 0.f);
+            continue;
+          }
 #ifdef PGSAG_A7_STATS
           st[3]++;
           st[4] += __popc(__ballot_sync(0xffffffffu, c0)) + __popc(__ballot_sync(0xffffffffu, c1));
@@ -410,7 +416,7 @@ __global__ void __launch_bounds__(kBT, PGSAG_BWD_MINB) render_bwd_kernel(BwdArgs
 #endif
           al0 = c0 ? al0 : 0.f;
           al1 = c1 ? al1 : 0.f;
-          pair_grad<kGC>(PP, f2(al0, al1), orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, h ? o23 : o01);
+          pair_grad<kGC>(PP, f2(al0, al1), orh.x <= kAlphaMax, orh.y <= kAlphaMax, cd, nn, OO);
         }
         PGSAG_DCHECK(pq <= kBBatch);
         if (wr) {  // one warp: (entry, row) has a single writer lane (none pending: the dummy row)
