@@ -148,11 +148,6 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
-  uint16_t v;
-  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
-  return (uint32_t)v;
-}
 
 // per-thread asynchronous global -> shared copies (LDGSTS), completed by cp_async_wait_all
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {

@@ -12,8 +12,9 @@
 // for both pixels).  Masked-out pixels start "done".  Each batch of 256 sorted
 // entries is staged in shared memory (64-byte records, as four 16-byte planes) together with a 4-bit
 // warp-block mask (exact conservative cull, alpha.cuh), from which every warp gets
-// a compacted depth-ordered candidate list.  Blending is branch-free (predicated
-// weights); the tile stops when every pixel is done.
+// a compacted depth-ordered list of its candidates' record addresses (walked by pointer).
+// Blending is branch-free (predicated weights); a warp stops when its pixels are done (tested
+// every 16 candidates), the tile when every pixel is.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
