@@ -463,11 +463,17 @@ __global__ void __launch_bounds__(256) duplicate_kernel(int n, const uint32_t* _
     __syncwarp();
   }
   if (cnt != 0 && !big) {
+    // row by row, the rect's active tiles are the set bits of the row's bitmap words masked to
+    // [x0, x1]: one load per word, one iteration per emitted entry (ascending tx, as the oracle)
     uint32_t oo = o;
     for (int ty = r.y; ty <= r.w; ++ty) {
       const uint32_t* row = bitmap + ty * d.WPR;
-      for (int tx = r.x; tx <= r.z; ++tx) {
-        if ((__ldg(row + (tx >> 5)) >> (tx & 31)) & 1u) {
+      for (int wx = r.x >> 5; wx <= (r.z >> 5); ++wx) {
+        const int b0 = max(r.x - 32 * wx, 0), b1 = min(r.z - 32 * wx, 31);
+        uint32_t bits = __ldg(row + wx) & (0xFFFFFFFFu << b0) & (0xFFFFFFFFu >> (31 - b1));
+        while (bits) {
+          const int tx = 32 * wx + __ffs(bits) - 1;
+          bits &= bits - 1u;
           PGSAG_DCHECK(oo < o + cnt && oo < cap);
           if (staged) {
             s_dk[w][oo - lo] = (uint32_t)(ty * d.TX + tx);
